@@ -1,0 +1,216 @@
+/*
+ * minplus.h -- C ABI of the B200 (sm_100a) hot path of arXiv 2409.17688,
+ * "HPC acceleration of large (min,+) matrix products to compute domination-type
+ * parameters in graphs".
+ *
+ * Citations: "P:L" = the paper's PAPER.md line L (section / equation / algorithm named
+ * beside it); "S:L" = SPEC.md line L; "G<k>" = a reading of the paper listed in DESIGN.md.
+ * Notation (G1): n = order of the path P_n (the paper's m), m = length of the cycle C_m
+ * (the paper's n), N = |C_n| = number of correct n-words = order of A(D_n).
+ *
+ * Conventions shared by every entry point
+ *   - Tropical values are uint16_t.  MP_INF = 0xFFFF is +inf; finite values are
+ *     0..MP_FINITE_MAX.  s(a,b) = a+b if both are finite and a+b <= MP_FINITE_MAX, else
+ *     +inf (G6; P:53 defines the semiring, P:250 fixes 16-bit storage).
+ *   - Matrices are row-major; "ld" is the row pitch in elements.
+ *   - No exception crosses the ABI.  Every call returns an mp_status; on a non-OK status
+ *     the outputs are left untouched and mp_last_error() returns a thread-local message.
+ *   - Calls serialise on a process-wide mutex.  GPU work runs on the calling thread's
+ *     current CUDA device (cudaSetDevice / torch.cuda.set_device before the call).
+ *   - There is no CPU fallback: if no sm_100 device is present, calls that compute
+ *     return MP_ERR_CUDA.
+ */
+#ifndef MINPLUS_H
+#define MINPLUS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_INF 0xFFFFu        /* +inf at the boundary                  */
+#define MP_FINITE_MAX 0x7FFEu /* largest finite input; a finite sum above it is +inf (G6) */
+#define MP_MAX_K 256          /* largest power index a periodic result can describe        */
+#define MP_MAX_N 12           /* largest path order n (n=13 exceeded 32 GB)         */
+
+typedef enum {
+    MP_OK = 0,
+    MP_ERR_DOMAIN = 1,       /* n < 2 or n > MP_MAX_N, cycle m < 3 (G17), dims <= 0, NULL
+                                pointers, ld < cols, C aliasing A or B */
+    MP_ERR_RANGE = 2,        /* an input entry in (MP_FINITE_MAX, MP_INF)                   */
+    MP_ERR_RESOURCE = 3,     /* device or host memory budget exceeded; mp_last_error()
+                                names the byte count                                 */
+    MP_ERR_NOT_PERIODIC = 4, /* no repeat A^k = c (x) A^j with k <= max_k (G20)             */
+    MP_ERR_CUDA = 5,         /* a CUDA runtime error, or no sm_100 device                   */
+    MP_ERR_COMM = 6          /* the registered all-reduce callback failed                   */
+} mp_status;
+
+/* ----------------------------------------------------------------------------------------
+ * a1  State enumeration and transition matrix (host, deterministic)
+ * ------------------------------------------------------------------------------------- */
+
+/* |C_n|, the number of correct n-words (Table 1).  No allocation.
+ * Errors: MP_ERR_DOMAIN if n < 2 or n > 13 (n = 13 is countable, not buildable here). */
+mp_status mp_count_words(int n, int64_t *N_out);
+
+/* A(D_n) by Algorithm 1: rows are the words q, columns the words p, both in
+ * lexicographic order 0 < 1 < 2 with the first letter (top row of the column) most
+ * significant (G5); A_qp = number of zeros of p if p can follow q (P:141-147,
+ * readings G2-G4), else MP_INF.
+ * The library allocates *A_out (N*N uint16_t, row-major, host memory); the caller
+ * releases it with mp_free().  Errors: MP_ERR_DOMAIN (n outside [2, MP_MAX_N], NULL),
+ * MP_ERR_RESOURCE (host allocation of 2*N*N bytes failed). */
+mp_status build_transition_matrix(int n, uint16_t **A_out, int64_t *N_out);
+
+/* Same matrix written into a caller-owned host buffer of exactly N*N entries (N from
+ * mp_count_words).  Errors as above, plus MP_ERR_DOMAIN if N does not match. */
+mp_status build_transition_matrix_into(int n, uint16_t *A, int64_t N);
+
+/* Releases memory returned by the library (NULL is a no-op). */
+void mp_free(void *p);
+
+/* ----------------------------------------------------------------------------------------
+ * a3  (min,+) product ((A x B)_ij = min_k (a_ik + b_kj))
+ * ------------------------------------------------------------------------------------- */
+
+/* C = A x B with A M x K, B K x N, C M x N; contiguous row-major HOST buffers, caller
+ * owned.  The library stages A and B to the current device, runs the sm_100a DPX kernel,
+ * and copies C back.  Errors: MP_ERR_DOMAIN (dims <= 0, NULL, C overlapping A or B),
+ * MP_ERR_RANGE, MP_ERR_RESOURCE, MP_ERR_CUDA. */
+mp_status minplus_mul(const uint16_t *A, const uint16_t *B, uint16_t *C, int64_t M,
+                      int64_t K, int64_t N);
+
+/* Device-pointer variant (e.g. torch tensors' data_ptr()): dA (M x K, pitch lda),
+ * dB (K x N, pitch ldb), dC (M x N, pitch ldc) live on the current device, in the
+ * boundary encoding above.  Asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ * default stream) except that a range violation is reported synchronously (the call
+ * synchronises `stream` once to read the range flag).  Scratch buffers are owned by the
+ * library and reused across calls.  Errors as minplus_mul. */
+mp_status minplus_mul_device(const uint16_t *dA, int64_t lda, const uint16_t *dB, int64_t ldb,
+                             uint16_t *dC, int64_t ldc, int64_t M, int64_t K, int64_t N,
+                             void *stream);
+
+/* ----------------------------------------------------------------------------------------
+ * a3-a5  Power sequence until it is quasi-periodic
+ * ------------------------------------------------------------------------------------- */
+
+typedef struct {
+    int32_t mu;         /* A^{mu+lambda} = offset (x) A^{mu}: mu = the paper's minimal n0   */
+    int32_t lambda;     /*   (Alg. 4), lambda = a, offset = b (Theorem 3) */
+    int32_t offset;     /*   first repeat up to a constant (G9); 0 if both are all-inf     */
+    int32_t k_last;     /* = mu + lambda: the number of powers computed                    */
+    int32_t dense_from; /* first k with no +inf entry (0 if none up to k_last)     */
+    uint16_t diag_min[MP_MAX_K + 1];    /* diag_min[k] = min_i (A^k)_ii, 1 <= k <= k_last
+                                           (Algorithm 5); MP_INF if none     */
+    uint64_t fingerprint[MP_MAX_K + 1]; /* H(A^k) = sum_t splitmix64(t) * x_t mod 2^64,
+                                           t = i*N + j, +inf as 0xFFFF      */
+} mp_periodic_result;
+
+/* A^1 = A, A^k = A x A^{k-1} (Algorithm 2, left multiplication G8) for
+ * k = 2, 3, ... until the first k with some j < k such that A^k - A^j is constant on the
+ * finite entries with an identical +inf pattern (Algorithm 3/4 collapsed into forward
+ * first-repeat detection; SURVEY.md section 8(c) "Why first-repeat detection equals
+ * Algs. 3/4").  A is an N x N HOST matrix in the boundary encoding.  The power store,
+ * products, fingerprints and exact comparisons run on the device; if a distributed
+ * context is set (mp_dist_set) every rank passes the same A and owns the column shard
+ * mp_shard_range(N, world, rank), and the result is identical on every rank.
+ * `out` is caller-owned.  Errors: MP_ERR_DOMAIN (N <= 0, max_k outside [2, MP_MAX_K],
+ * NULL), MP_ERR_RANGE, MP_ERR_RESOURCE, MP_ERR_NOT_PERIODIC (out untouched),
+ * MP_ERR_CUDA, MP_ERR_COMM. */
+mp_status minplus_power_until_periodic(const uint16_t *A, int64_t N, int max_k,
+                                       mp_periodic_result *out);
+
+/* ----------------------------------------------------------------------------------------
+ * a6  gamma_2(P_n x C_m) (Theorem 2; Theorem 3; solving procedure P:219-222)
+ * ------------------------------------------------------------------------------------- */
+
+/* gamma_2 of the cylinder with path order n (2..MP_MAX_N) and cycle length m >= 3.
+ * Builds A(D_n), runs minplus_power_until_periodic (max_k = 64) once per n per process
+ * (the (mu, lambda, b, diag_min) record is cached), and reads gamma_2 off: diag_min[m] if
+ * m <= k_last, else diag_min[m - t*lambda] + t*b with the least t that lands in
+ * [mu, k_last].  Errors: MP_ERR_DOMAIN, and those of minplus_power_until_periodic. */
+mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out);
+
+/* Read-off only (host, no device): applies the a6 rule to a result. */
+mp_status mp_gamma2_readoff(const mp_periodic_result *r, int64_t m, int64_t *gamma2_out);
+
+/* ----------------------------------------------------------------------------------------
+ * Multi-GPU: one process per GPU (torchrun), column shards, a tiny all-reduce per power
+ * ------------------------------------------------------------------------------------- */
+
+/* The all-reduce the driver calls once or twice per power on `count` int64 values living
+ * in DEVICE memory at dev_buf (already ordered after the library's work on `stream`, which
+ * the library synchronises before the call).  op: 0 = SUM (wrapping mod 2^64), 1 = MIN.
+ * Returns 0 on success.  The Python binding implements it with torch.distributed over
+ * NCCL (NVLink); any MPI-like runtime works. */
+typedef int (*mp_allreduce_fn)(void *ctx, int op, int64_t *dev_buf, int64_t count,
+                               void *stream);
+
+/* Registers (fn != NULL, world >= 1, 0 <= rank < world) or clears (fn == NULL) the
+ * process-wide distributed context used by minplus_power_until_periodic.
+ * Errors: MP_ERR_DOMAIN. */
+mp_status mp_dist_set(int rank, int world, mp_allreduce_fn fn, void *ctx);
+
+/* Column shard [*c0, *c1) of rank `rank` among `world` for an N x N power: width
+ * w = roundup(ceil(N / world), 8), c0 = min(N, rank*w), c1 = min(N, c0 + w) (the last
+ * shard takes the remainder; a shard may be empty when N is tiny).  Pure host function.
+ * Errors: MP_ERR_DOMAIN. */
+mp_status mp_shard_range(int64_t N, int world, int rank, int64_t *c0, int64_t *c1);
+
+/* ----------------------------------------------------------------------------------------
+ * Periodicity bookkeeping (pure host functions; exported so the multi-rank logic is
+ * testable without a GPU)
+ * ------------------------------------------------------------------------------------- */
+
+/* Per-power statistics after the all-reduce: */
+typedef struct {
+    uint64_t fingerprint; /* SUM over shards of the canonical linear hash                */
+    int64_t diag_min;     /* MIN over shards of min_i X_ii (MP_INF if no diagonal entry)  */
+    int64_t x00;          /* X_00 (only the shard owning column 0 contributes; 0xFFFF=inf) */
+    int64_t inf_count;    /* SUM over shards of the number of +inf entries               */
+} mp_power_stats;
+
+/* S(N) = sum_{t < N*N} splitmix64(t) mod 2^64 (the fingerprint of the all-ones matrix). */
+uint64_t mp_fingerprint_unit(int64_t N);
+
+/* Candidate test of the forward first-repeat search: returns 1 if A^k may equal
+ * c (x) A^j for c = x00_k - x00_j, i.e. both powers are inf-free and
+ * H_k - H_j == c * S(N) (mod 2^64), or both contain +inf with equal counts (exact
+ * comparison required); 0 if they certainly differ.  *c_out receives c. */
+int mp_repeat_candidate(const mp_power_stats *sk, const mp_power_stats *sj, uint64_t S,
+                        int32_t *c_out);
+
+/* ----------------------------------------------------------------------------------------
+ * Diagnostics
+ * ------------------------------------------------------------------------------------- */
+
+const char *mp_last_error(void); /* thread-local message for the last non-OK status     */
+void mp_shutdown(void);          /* frees cached device state and the gamma_2 cache       */
+const char *mp_version(void);    /* build string (kernel variant, arch)                   */
+
+/* Number of device kernels launched by this process so far (all entry points). */
+int64_t mp_kernel_launches(void);
+
+/* Profiling counters of the last minplus_power_until_periodic call: total milliseconds
+ * spent in the product kernel (CUDA events on the library stream), number of product
+ * launches, dense-equivalent inner steps (rows*inner*cols summed over launches) and the
+ * inner steps actually issued after skipping all-inf A tiles. */
+typedef struct {
+    double product_ms;
+    int64_t product_launches;
+    double dense_steps;
+    double issued_steps;
+    double total_ms;
+} mp_profile;
+mp_status mp_last_profile(mp_profile *out);
+
+/* Tuning knobs (process-wide; defaults in DESIGN.md).  block_sparse: skip all-inf
+ * A tiles (exact; NEXT-1).  device_budget_bytes: cap for the power store (0 = 90% of the
+ * free device memory at call time). */
+mp_status mp_set_options(int block_sparse, int64_t device_budget_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MINPLUS_H */
