@@ -121,6 +121,22 @@ typedef struct {
 mp_status minplus_power_until_periodic(const uint16_t *A, int64_t N, int max_k,
                                        mp_periodic_result *out);
 
+/* Same run with A already resident on the current device: dA is N x N with pitch lda
+ * (elements), boundary encoding, device memory owned by the caller and only read.  Work is
+ * enqueued on the library stream (see mp_set_stream); the call returns when the result is
+ * known.  Errors as minplus_power_until_periodic (MP_ERR_DOMAIN also for lda < N). */
+mp_status minplus_power_until_periodic_device(const uint16_t *dA, int64_t lda, int64_t N, int max_k,
+                                              mp_periodic_result *out);
+
+/* Parity hook: rows `rows[0..nrows)` of every power A^1..A^kmax, computed by the same
+ * device path (staging, product kernel, power store) without the periodicity search.
+ * out (caller-owned host buffer) receives kmax*nrows*N entries: out[((k-1)*nrows + r)*N + j]
+ * = (A^k)_{rows[r], j}, boundary encoding.  Single device (the distributed context is
+ * ignored).  Errors: MP_ERR_DOMAIN (N <= 0, kmax outside [1, MP_MAX_K], nrows <= 0, a row
+ * outside [0, N), NULL), MP_ERR_RANGE, MP_ERR_RESOURCE, MP_ERR_CUDA. */
+mp_status minplus_power_rows(const uint16_t *A, int64_t N, int kmax, const int64_t *rows, int nrows,
+                             uint16_t *out);
+
 /* ----------------------------------------------------------------------------------------
  * a6  gamma_2(P_n x C_m) (Theorem 2; Theorem 3; solving procedure P:219-222)
  * ------------------------------------------------------------------------------------- */
@@ -163,21 +179,24 @@ mp_status mp_shard_range(int64_t N, int world, int rank, int64_t *c0, int64_t *c
  * testable without a GPU)
  * ------------------------------------------------------------------------------------- */
 
-/* Per-power statistics after the all-reduce: */
+/* Per-power statistics after the all-reduce.  Every field is
+ * an int64 so that one SUM and one MIN all-reduce carry them: */
 typedef struct {
-    uint64_t fingerprint; /* SUM over shards of the canonical linear hash                */
-    int64_t diag_min;     /* MIN over shards of min_i X_ii (MP_INF if no diagonal entry)  */
-    int64_t x00;          /* X_00 (only the shard owning column 0 contributes; 0xFFFF=inf) */
-    int64_t inf_count;    /* SUM over shards of the number of +inf entries               */
+    int64_t fingerprint; /* SUM: canonical linear hash H (the uint64 bits, wrapping)          */
+    int64_t inf_count;   /* SUM: number of +inf entries                                      */
+    int64_t diag_min;    /* MIN: min_i X_ii (0xFFFF if every diagonal entry is +inf)          */
+    int64_t ref;         /* MIN: (t << 16) | x_t of the first finite entry in canonical order
+                            t = i*N + j; INT64_MAX if the matrix is all +inf                 */
 } mp_power_stats;
 
 /* S(N) = sum_{t < N*N} splitmix64(t) mod 2^64 (the fingerprint of the all-ones matrix). */
 uint64_t mp_fingerprint_unit(int64_t N);
 
 /* Candidate test of the forward first-repeat search: returns 1 if A^k may equal
- * c (x) A^j for c = x00_k - x00_j, i.e. both powers are inf-free and
- * H_k - H_j == c * S(N) (mod 2^64), or both contain +inf with equal counts (exact
- * comparison required); 0 if they certainly differ.  *c_out receives c. */
+ * c (x) A^j, with c = x_k - x_j taken at the first finite entry (whose position must agree):
+ * both powers inf-free and H_k - H_j == c * S(N) (mod 2^64), or both containing +inf with
+ * equal counts and equal first-finite positions (the exact comparison decides); both all
+ * +inf gives c = 0.  Returns 0 if they certainly differ.  *c_out receives c. */
 int mp_repeat_candidate(const mp_power_stats *sk, const mp_power_stats *sj, uint64_t S,
                         int32_t *c_out);
 
@@ -197,13 +216,20 @@ int64_t mp_kernel_launches(void);
  * launches, dense-equivalent inner steps (rows*inner*cols summed over launches) and the
  * inner steps actually issued after skipping all-inf A tiles. */
 typedef struct {
-    double product_ms;
-    int64_t product_launches;
-    double dense_steps;
-    double issued_steps;
-    double total_ms;
+    double product_ms;        /* sum of product-kernel durations (CUDA events)              */
+    int64_t product_launches; /* number of product launches                                 */
+    double dense_steps;       /* sum of N * N * w over the launches (dense-equivalent steps) */
+    double issued_steps;      /* steps the kernel executed after skipping all-inf A tiles   */
+    double total_ms;          /* whole run, first to last operation on the library stream  */
+    int64_t h2d_bytes;        /* host -> device bytes copied by the run                    */
+    int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
+
+/* Stream for the power runs on the current device (a cudaStream_t, e.g. torch's current
+ * stream, so that caller-side CUDA events bracket a run); NULL restores the library's own
+ * non-blocking stream.  Errors: MP_ERR_CUDA if no device. */
+mp_status mp_set_stream(void *stream);
 
 /* Tuning knobs (process-wide; defaults in DESIGN.md).  block_sparse: skip all-inf
  * A tiles (exact; NEXT-1).  device_budget_bytes: cap for the power store (0 = 90% of the

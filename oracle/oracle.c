@@ -338,29 +338,35 @@ int oracle_power_until_periodic(const uint16_t *A, int64_t N, int max_k, oracle_
 /* Row r of every power A^1..A^kmax, by repeated (min,+) vector-matrix products
  * e_r^T A^k = (e_r^T A^{k-1}) x A (associativity).  rows_out holds kmax*N entries; row k-1
  * is row r of A^k.  Used to check sampled outputs at sizes where full powers are too big
- * for the oracle (n = 11, 12).                                                           */
+ * for the oracle (n = 11, 12).  cur_j = min_l s(prev_l + A_lj): the l loop runs inside
+ * column chunks (the minimum over l does not depend on the visiting order); an inf term is
+ * carried as a sum >= 0xFFFF and mapped to inf by the final clamp, which is s() of G6.   */
 void oracle_power_rows(const uint16_t *A, int64_t N, int64_t r, int kmax, uint16_t *rows_out)
 {
     int k;
-    int64_t j;
     memcpy(rows_out, A + r * N, (size_t)N * sizeof(uint16_t));
     for (k = 2; k <= kmax; k++) {
         const uint16_t *prev = rows_out + (int64_t)(k - 2) * N;
         uint16_t *cur = rows_out + (int64_t)(k - 1) * N;
-        uint32_t *acc = (uint32_t *)malloc((size_t)N * sizeof(uint32_t));
-        int64_t l;
-        for (j = 0; j < N; j++) acc[j] = OR_INF;
-        for (l = 0; l < N; l++) {       /* cur_j = min_l s(prev_l + A_lj) */
-            uint32_t a = prev[l];
-            const uint16_t *Arow = A + l * N;
-            if (a == OR_INF) continue;
-            for (j = 0; j < N; j++) {
-                uint32_t s = (Arow[j] == OR_INF) ? OR_INF : a + Arow[j];
-                if (s < acc[j]) acc[j] = s;
+        int64_t jc;
+#pragma omp parallel for schedule(dynamic, 1)
+        for (jc = 0; jc < N; jc += 2048) {
+            const int64_t je = (jc + 2048 < N) ? jc + 2048 : N;
+            uint32_t acc[2048];
+            int64_t j, l;
+            for (j = jc; j < je; j++) acc[j - jc] = OR_INF;
+            for (l = 0; l < N; l++) {
+                const uint32_t a = prev[l];
+                const uint16_t *Arow = A + l * N;
+                if (a == OR_INF) continue;
+                for (j = jc; j < je; j++) {
+                    const uint32_t s = a + Arow[j]; /* >= 0xFFFF when A_lj is inf */
+                    if (s < acc[j - jc]) acc[j - jc] = s;
+                }
             }
+            for (j = jc; j < je; j++)
+                cur[j] = (uint16_t)(acc[j - jc] <= OR_FINITE_MAX ? acc[j - jc] : OR_INF);
         }
-        for (j = 0; j < N; j++) cur[j] = (uint16_t)(acc[j] <= OR_FINITE_MAX ? acc[j] : OR_INF);
-        free(acc);
     }
 }
 

@@ -1,0 +1,319 @@
+"""Thin ctypes binding of libminplus.so (include/minplus.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA kernels.
+There is no CPU fallback -- if the shared library is missing this module raises at import,
+and every computing call raises MinplusError(MP_ERR_CUDA) when no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _build
+
+MP_INF = 0xFFFF
+MP_FINITE_MAX = 0x7FFE
+MP_MAX_K = 256
+MP_MAX_N = 12
+
+STATUS = {0: "MP_OK", 1: "MP_ERR_DOMAIN", 2: "MP_ERR_RANGE", 3: "MP_ERR_RESOURCE",
+          4: "MP_ERR_NOT_PERIODIC", 5: "MP_ERR_CUDA", 6: "MP_ERR_COMM"}
+
+# Every symbol include/minplus.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "mp_count_words", "build_transition_matrix", "build_transition_matrix_into", "mp_free",
+    "minplus_mul", "minplus_mul_device", "minplus_power_until_periodic",
+    "minplus_power_until_periodic_device", "minplus_power_rows", "mp_set_stream",
+    "gamma2_cylinder",
+    "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
+    "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
+    "mp_last_profile", "mp_set_options",
+]
+
+
+class MinplusError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {message}")
+
+
+class _PeriodicResult(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_int32), ("lambda_", ctypes.c_int32), ("offset", ctypes.c_int32),
+                ("k_last", ctypes.c_int32), ("dense_from", ctypes.c_int32),
+                ("diag_min", ctypes.c_uint16 * (MP_MAX_K + 1)),
+                ("fingerprint", ctypes.c_uint64 * (MP_MAX_K + 1))]
+
+
+class PowerStats(ctypes.Structure):
+    _fields_ = [("fingerprint", ctypes.c_int64), ("inf_count", ctypes.c_int64),
+                ("diag_min", ctypes.c_int64), ("ref", ctypes.c_int64)]
+
+
+class _Profile(ctypes.Structure):
+    _fields_ = [("product_ms", ctypes.c_double), ("product_launches", ctypes.c_int64),
+                ("dense_steps", ctypes.c_double), ("issued_steps", ctypes.c_double),
+                ("total_ms", ctypes.c_double), ("h2d_bytes", ctypes.c_int64),
+                ("d2h_bytes", ctypes.c_int64)]
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.c_int64, ctypes.c_void_p)
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(_build.SO):
+        raise ImportError(f"{_build.SO} is missing: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(_build.SO)
+    P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    sig = {
+        "mp_count_words": ([i32, P], i32),
+        "build_transition_matrix": ([i32, P, P], i32),
+        "build_transition_matrix_into": ([i32, P, i64], i32),
+        "mp_free": ([P], None),
+        "minplus_mul": ([P, P, P, i64, i64, i64], i32),
+        "minplus_mul_device": ([P, i64, P, i64, P, i64, i64, i64, i64, P], i32),
+        "minplus_power_until_periodic": ([P, i64, i32, P], i32),
+        "minplus_power_rows": ([P, i64, i32, P, i32, P], i32),
+        "minplus_power_until_periodic_device": ([P, i64, i64, i32, P], i32),
+        "mp_set_stream": ([P], i32),
+        "gamma2_cylinder": ([i32, i64, P], i32),
+        "mp_gamma2_readoff": ([P, i64, P], i32),
+        "mp_dist_set": ([i32, i32, ALLREDUCE_FN, P], i32),
+        "mp_shard_range": ([i64, i32, i32, P, P], i32),
+        "mp_fingerprint_unit": ([i64], ctypes.c_uint64),
+        "mp_repeat_candidate": ([P, P, ctypes.c_uint64, P], i32),
+        "mp_last_error": ([], ctypes.c_char_p),
+        "mp_shutdown": ([], None),
+        "mp_version": ([], ctypes.c_char_p),
+        "mp_kernel_launches": ([], i64),
+        "mp_last_profile": ([P], i32),
+        "mp_set_options": ([i32, i64], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise MinplusError(status, lib.mp_last_error().decode(errors="replace"))
+
+
+def _host_u16(a) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a), dtype=np.uint16)
+    return a
+
+
+# --------------------------------------------------------------------------------- a1
+def count_words(n: int) -> int:
+    N = ctypes.c_int64(0)
+    _check(lib.mp_count_words(n, ctypes.byref(N)))
+    return N.value
+
+
+def build_transition_matrix(n: int) -> np.ndarray:
+    """A(D_n), N x N uint16 with 0xFFFF = +inf (Algorithm 1)."""
+    N = count_words(n)
+    A = np.empty((N, N), dtype=np.uint16)
+    _check(lib.build_transition_matrix_into(n, A.ctypes.data, N))
+    return A
+
+
+# --------------------------------------------------------------------------------- a3
+def minplus_mul(A, B) -> np.ndarray:
+    """C = A (x) B for host matrices, computed by the sm_100a kernel."""
+    A, B = _host_u16(A), _host_u16(B)
+    if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
+        raise MinplusError(1, f"shape mismatch {A.shape} x {B.shape}")
+    M, K = A.shape
+    N = B.shape[1]
+    C = np.empty((M, N), dtype=np.uint16)
+    _check(lib.minplus_mul(A.ctypes.data, B.ctypes.data, C.ctypes.data, M, K, N))
+    return C
+
+
+def minplus_mul_device(A, B, C=None, stream=None):
+    """C = A (x) B for torch CUDA tensors (uint16 or int16 storage, boundary encoding)."""
+    import torch
+    for t in (A, B):
+        if not t.is_cuda or t.element_size() != 2 or t.dim() != 2 or t.stride(1) != 1:
+            raise MinplusError(1, "expected 2-D row-major 16-bit CUDA tensors")
+    M, K = A.shape
+    K2, N = B.shape
+    if K != K2:
+        raise MinplusError(1, f"shape mismatch {tuple(A.shape)} x {tuple(B.shape)}")
+    if C is None:
+        C = torch.empty((M, N), dtype=A.dtype, device=A.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    with torch.cuda.device(A.device):
+        _check(lib.minplus_mul_device(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                                      C.data_ptr(), C.stride(0), M, K, N, stream.cuda_stream))
+    return C
+
+
+# ----------------------------------------------------------------------------- a3-a5
+@dataclass
+class PeriodicResult:
+    mu: int
+    lam: int
+    offset: int
+    k_last: int
+    dense_from: int
+    diag_min: list = field(default_factory=list)
+    fingerprint: list = field(default_factory=list)
+    _raw: object = None
+
+    def gamma2(self, m: int) -> int:
+        g = ctypes.c_int64(0)
+        _check(lib.mp_gamma2_readoff(ctypes.byref(self._raw), m, ctypes.byref(g)))
+        return g.value
+
+
+def _result(r: _PeriodicResult) -> PeriodicResult:
+    return PeriodicResult(r.mu, r.lambda_, r.offset, r.k_last, r.dense_from,
+                          [int(r.diag_min[k]) for k in range(r.k_last + 1)],
+                          [int(r.fingerprint[k]) for k in range(r.k_last + 1)], r)
+
+
+def minplus_power_until_periodic(A, max_k: int = 64) -> PeriodicResult:
+    """Powers A^k = A (x) A^{k-1} on the device until A^{mu+lambda} = b (x) A^mu."""
+    A = _host_u16(A)
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise MinplusError(1, f"A must be square, got {A.shape}")
+    r = _PeriodicResult()
+    _check(lib.minplus_power_until_periodic(A.ctypes.data, A.shape[0], max_k, ctypes.byref(r)))
+    return _result(r)
+
+
+def minplus_power_until_periodic_device(dA, max_k: int = 64) -> PeriodicResult:
+    """Same run with A resident on the device (a 2-D 16-bit torch CUDA tensor)."""
+    if not dA.is_cuda or dA.element_size() != 2 or dA.dim() != 2 or dA.stride(1) != 1 \
+            or dA.shape[0] != dA.shape[1]:
+        raise MinplusError(1, "expected a square row-major 16-bit CUDA tensor")
+    import torch
+    r = _PeriodicResult()
+    with torch.cuda.device(dA.device):
+        _check(lib.minplus_power_until_periodic_device(dA.data_ptr(), dA.stride(0), dA.shape[0],
+                                                       max_k, ctypes.byref(r)))
+    return _result(r)
+
+
+def set_stream(stream) -> None:
+    """Run power sequences on `stream` (torch.cuda.Stream or None for the library's own)."""
+    _check(lib.mp_set_stream(None if stream is None else stream.cuda_stream))
+
+
+def minplus_power_rows(A, rows, kmax: int) -> np.ndarray:
+    """Rows of A^1..A^kmax from the device path: array [kmax, len(rows), N]."""
+    A = _host_u16(A)
+    N = A.shape[0]
+    r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    out = np.empty((kmax, len(r), N), dtype=np.uint16)
+    _check(lib.minplus_power_rows(A.ctypes.data, N, kmax, r.ctypes.data, len(r), out.ctypes.data))
+    return out
+
+
+def gamma2_cylinder(n: int, m: int) -> int:
+    """gamma_2(P_n x C_m) (Theorems 2 and 3)."""
+    g = ctypes.c_int64(0)
+    _check(lib.gamma2_cylinder(n, m, ctypes.byref(g)))
+    return g.value
+
+
+# -------------------------------------------------------------------------- multi-GPU
+_keep_alive = []
+
+
+def dist_set(rank: int, world: int, allreduce) -> None:
+    """Registers allreduce(op, dev_ptr, count) -> None (op 0 = SUM, 1 = MIN) for the
+    column-sharded power run; allreduce=None clears the context."""
+    if allreduce is None:
+        _check(lib.mp_dist_set(0, 1, ALLREDUCE_FN(), None))
+        _keep_alive.clear()
+        return
+
+    def cb(ctx, op, dev_ptr, count, stream):
+        try:
+            allreduce(int(op), int(dev_ptr), int(count))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to C as MP_ERR_COMM
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    fn = ALLREDUCE_FN(cb)
+    _keep_alive[:] = [fn]
+    _check(lib.mp_dist_set(rank, world, fn, None))
+
+
+def dist_set_torch(group=None) -> None:
+    """Column sharding over torch.distributed (backend nccl: NVLink/NVSwitch)."""
+    import torch
+    import torch.distributed as dist
+
+    class _Dev:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                             "version": 3, "strides": None, "stream": None}
+
+    def allreduce(op, ptr, count):
+        t = torch.as_tensor(_Dev(ptr, count), device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MIN, group=group)
+        torch.cuda.synchronize()
+
+    dist_set(dist.get_rank(group), dist.get_world_size(group), allreduce)
+
+
+def shard_range(N: int, world: int, rank: int):
+    c0, c1 = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.mp_shard_range(N, world, rank, ctypes.byref(c0), ctypes.byref(c1)))
+    return c0.value, c1.value
+
+
+def fingerprint_unit(N: int) -> int:
+    return int(lib.mp_fingerprint_unit(N))
+
+
+def repeat_candidate(sk: PowerStats, sj: PowerStats, S: int):
+    c = ctypes.c_int32(0)
+    ok = lib.mp_repeat_candidate(ctypes.byref(sk), ctypes.byref(sj), S, ctypes.byref(c))
+    return (c.value if ok else None)
+
+
+# ------------------------------------------------------------------------ diagnostics
+def last_error() -> str:
+    return lib.mp_last_error().decode(errors="replace")
+
+
+def kernel_launches() -> int:
+    return int(lib.mp_kernel_launches())
+
+
+def last_profile() -> dict:
+    p = _Profile()
+    _check(lib.mp_last_profile(ctypes.byref(p)))
+    return {"product_ms": p.product_ms, "product_launches": p.product_launches,
+            "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
+            "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes}
+
+
+def set_options(block_sparse: bool = True, device_budget_bytes: int = 0) -> None:
+    _check(lib.mp_set_options(1 if block_sparse else 0, device_budget_bytes))
+
+
+def version() -> str:
+    return lib.mp_version().decode()
+
+
+def shutdown() -> None:
+    lib.mp_shutdown()

@@ -1,0 +1,760 @@
+// C ABI of the (min,+) power path: argument checking, device memory, the power /
+// periodicity driver and the gamma_2 read-off.  See include/minplus.h for the contract
+// and DESIGN.md for the design.  Product code only: shares nothing with oracle/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "minplus.h"
+#include "mp_internal.h"
+#include "mp_kernels.h"
+
+using namespace mp;
+
+namespace {
+
+std::recursive_mutex g_mu;
+thread_local std::string t_err;
+std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_h2d{0}, g_d2h{0};
+
+struct Dist {
+    int rank = 0, world = 1;
+    mp_allreduce_fn fn = nullptr;
+    void *ctx = nullptr;
+} g_dist;
+
+struct Opts {
+    int block_sparse = 1;
+    int64_t budget = 0;
+} g_opts;
+
+mp_profile g_prof{};
+std::map<std::tuple<int, int, int>, mp_periodic_result> g_cache; // (n, world, rank)
+
+mp_status fail(mp_status s, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(x)                                                                            \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) {                                                               \
+            cudaGetLastError();                                                                \
+            return fail(MP_ERR_CUDA, "%s failed: %s", #x, cudaGetErrorString(e_));            \
+        }                                                                                      \
+    } while (0)
+
+#define LAUNCH(x)                                                                              \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        g_launches.fetch_add(1);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            cudaGetLastError();                                                                \
+            return fail(MP_ERR_CUDA, "kernel %s failed: %s", #x, cudaGetErrorString(e_));     \
+        }                                                                                      \
+    } while (0)
+
+// cudaMemcpyAsync that also counts the bytes crossing the host/device boundary.
+#define COPY(dst, src, bytes, kind, stream)                                                    \
+    do {                                                                                       \
+        CUDA_TRY(cudaMemcpyAsync((dst), (src), (bytes), (kind), (stream)));                    \
+        if ((kind) == cudaMemcpyHostToDevice) g_h2d.fetch_add((int64_t)(bytes));               \
+        if ((kind) == cudaMemcpyDeviceToHost) g_d2h.fetch_add((int64_t)(bytes));               \
+    } while (0)
+
+#define TRY(x)                                                                                 \
+    do {                                                                                       \
+        mp_status s_ = (x);                                                                    \
+        if (s_ != MP_OK) return s_;                                                            \
+    } while (0)
+
+// Owning device buffer.
+struct DBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    ~DBuf() { release(); }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    mp_status alloc(size_t b, const char *what)
+    {
+        release();
+        if (b == 0) b = 16;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return fail(MP_ERR_RESOURCE, "device allocation of %zu bytes for %s failed (%s)", b, what,
+                        cudaGetErrorString(e));
+        }
+        bytes = b;
+        return MP_OK;
+    }
+    mp_status ensure(size_t b, const char *what) { return (bytes >= b && p) ? MP_OK : alloc(b, what); }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// Per-device state: a library stream and scratch for minplus_mul(_device).
+struct DevState {
+    cudaStream_t stream = nullptr;      // the library's own non-blocking stream
+    cudaStream_t user_stream = nullptr; // mp_set_stream override for power runs
+    DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c;
+};
+std::map<int, DevState> g_dev;
+
+mp_status current_device(int *dev_out, DevState **st)
+{
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(MP_ERR_CUDA, "no CUDA device available (%s); this library has no CPU fallback",
+                    e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+    }
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    auto it = g_dev.find(dev);
+    if (it == g_dev.end()) {
+        cudaDeviceProp prop;
+        CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major != 10)
+            return fail(MP_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100; this build targets sm_100a", dev,
+                        prop.name, prop.major, prop.minor);
+        DevState ds;
+        CUDA_TRY(cudaStreamCreateWithFlags(&ds.stream, cudaStreamNonBlocking));
+        it = g_dev.emplace(dev, std::move(ds)).first;
+    }
+    *dev_out = dev;
+    *st = &it->second;
+    return MP_OK;
+}
+
+bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes)
+{
+    const char *x = (const char *)a, *y = (const char *)b;
+    return x < y + bbytes && y < x + abytes;
+}
+
+size_t span_bytes(int64_t rows, int64_t cols, int64_t ld) { return (size_t)((rows - 1) * ld + cols) * 2; }
+
+int host_threads()
+{
+    unsigned h = std::thread::hardware_concurrency();
+    return h ? (int)std::min(h, 64u) : 4;
+}
+
+// ---------------------------------------------------------------------------------------
+// Product on device buffers (boundary encoding in and out).
+// ---------------------------------------------------------------------------------------
+mp_status mul_device_impl(DevState &st, const uint16_t *dA, int64_t lda, const uint16_t *dB, int64_t ldb,
+                          uint16_t *dC, int64_t ldc, int64_t M, int64_t K, int64_t N, cudaStream_t s)
+{
+    const int64_t Mp = pad_rows(M), Kp = pad_rows(K), Np = pad_cols(N);
+    TRY(st.at2.ensure((size_t)Kp * Mp * 4, "A (transposed, duplicated)"));
+    TRY(st.xb.ensure((size_t)Kp * Np * 2, "B (padded)"));
+    TRY(st.cb.ensure((size_t)Mp * Np * 2, "C (padded)"));
+    TRY(st.flag.ensure(16, "range flag"));
+    CUDA_TRY(cudaMemsetAsync(st.flag.p, 0, sizeof(int), s));
+    LAUNCH(launch_make_at2(dA, lda, M, K, st.at2.as<uint32_t>(), Mp, Kp, st.flag.as<int>(), s));
+    LAUNCH(launch_encode(dB, ldb, K, N, st.xb.as<uint16_t>(), Np, Kp, st.flag.as<int>(), s));
+    int flag = 0;
+    COPY(&flag, st.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (flag) return fail(MP_ERR_RANGE, "an input entry lies in (0x7FFE, 0xFFFF)");
+    LAUNCH(launch_minplus(st.at2.as<uint32_t>(), Mp, st.xb.as<uint16_t>(), Np, st.cb.as<uint16_t>(), Np, Mp, Np,
+                          Kp, nullptr, nullptr, s));
+    LAUNCH(launch_decode(st.cb.as<uint16_t>(), Np, M, N, dC, ldc, s));
+    return MP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Power / periodicity driver (a3-a5)
+// ---------------------------------------------------------------------------------------
+struct PowerRun {
+    int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
+    DBuf at2, x1, tmp0, tmp1, ktp, kti, stats, flag;
+    std::vector<DBuf> ring;
+    std::vector<int> slot_power;
+    bool sparse = false;
+    double issued_per_product = 0.0;
+    size_t slot_bytes() const { return (size_t)Np * ld * 2; }
+};
+
+mp_status allreduce(int op, int64_t *dev, int64_t count, cudaStream_t s)
+{
+    if (g_dist.world <= 1 || !g_dist.fn) return MP_OK;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (g_dist.fn(g_dist.ctx, op, dev, count, (void *)s) != 0)
+        return fail(MP_ERR_COMM, "all-reduce callback failed (op %d, %lld values)", op, (long long)count);
+    return MP_OK;
+}
+
+// Block-sparse l-tile lists of A (exact skipping of all-inf tiles).
+mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
+{
+    const int64_t Mt = R.Np / kBM, Kt = R.Np / kBK;
+    DBuf occ;
+    TRY(occ.alloc((size_t)(Mt * Kt), "tile occupancy"));
+    LAUNCH(launch_tile_occupancy(R.at2.as<uint32_t>(), R.Np, R.Np, occ.as<uint8_t>(), s));
+    std::vector<uint8_t> h((size_t)(Mt * Kt));
+    COPY(h.data(), occ.p, h.size(), cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int32_t> ptr((size_t)Mt + 1, 0), idx;
+    idx.reserve(h.size() / 4);
+    for (int64_t b = 0; b < Mt; ++b) {
+        for (int64_t k = 0; k < Kt; ++k)
+            if (h[(size_t)(b * Kt + k)]) idx.push_back((int32_t)k);
+        ptr[(size_t)b + 1] = (int32_t)idx.size();
+    }
+    if (idx.empty()) idx.push_back(0);
+    TRY(R.ktp.alloc(ptr.size() * 4, "tile list pointers"));
+    TRY(R.kti.alloc(idx.size() * 4, "tile list"));
+    COPY(R.ktp.p, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice, s);
+    COPY(R.kti.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    R.issued_per_product = (double)ptr[(size_t)Mt] * kBK * kBM * (double)R.ld;
+    return MP_OK;
+}
+
+mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
+{
+    LAUNCH(launch_minplus(R.at2.as<uint32_t>(), R.Np, X, R.ld, C, R.ld, R.Np, R.ld, R.Np,
+                          R.sparse ? R.ktp.as<int32_t>() : nullptr, R.sparse ? R.kti.as<int32_t>() : nullptr, s));
+    return MP_OK;
+}
+
+// Returns the device buffer holding power j, recomputing it into tmp buffers if it has been
+// evicted from the ring.
+mp_status power_buffer(PowerRun &R, int j, const uint16_t **out, cudaStream_t s)
+{
+    if (j == 1) {
+        *out = R.x1.as<uint16_t>();
+        return MP_OK;
+    }
+    for (size_t q = 0; q < R.ring.size(); ++q)
+        if (R.slot_power[q] == j) {
+            *out = R.ring[q].as<uint16_t>();
+            return MP_OK;
+        }
+    TRY(R.tmp0.ensure(R.slot_bytes(), "recompute buffer"));
+    TRY(R.tmp1.ensure(R.slot_bytes(), "recompute buffer"));
+    const uint16_t *cur = R.x1.as<uint16_t>();
+    for (int k = 2; k <= j; ++k) {
+        uint16_t *dst = (k & 1) ? R.tmp1.as<uint16_t>() : R.tmp0.as<uint16_t>();
+        TRY(product(R, cur, dst, s));
+        cur = dst;
+    }
+    *out = cur;
+    return MP_OK;
+}
+
+// Source of A: either a host matrix or the word masks of path order n.
+struct ASource {
+    const uint16_t *host = nullptr; // host matrix, pitch N
+    const uint16_t *dev = nullptr;  // device matrix, pitch lda
+    int64_t lda = 0;
+    int n = 0;                      // else: build A(D_n) from the word masks on the device
+};
+
+// Optional row capture (minplus_power_rows): no periodicity search, stop at kmax.
+struct Capture {
+    const int64_t *rows = nullptr;
+    int nrows = 0;
+    uint16_t *out = nullptr; // host
+};
+
+mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_result *out,
+                     const Capture *cap = nullptr)
+{
+    int dev = 0;
+    DevState *st = nullptr;
+    TRY(current_device(&dev, &st));
+    cudaStream_t s = st->user_stream ? st->user_stream : st->stream;
+    const int64_t h2d0 = g_h2d.load(), d2h0 = g_d2h.load();
+    cudaEvent_t ev_all0, ev_all1;
+    CUDA_TRY(cudaEventCreate(&ev_all0));
+    CUDA_TRY(cudaEventCreate(&ev_all1));
+    CUDA_TRY(cudaEventRecord(ev_all0, s));
+
+    PowerRun R;
+    R.N = N;
+    R.Np = pad_rows(N);
+    {
+        int64_t c0, c1;
+        mp_shard_range(N, g_dist.world, g_dist.rank, &c0, &c1);
+        R.c0 = c0;
+        R.w = c1 - c0;
+    }
+    if (cap) { // single device, whole matrix
+        R.c0 = 0;
+        R.w = N;
+    }
+    R.ld = pad_cols(R.w);
+
+    // a2: stage A as AT2 (transposed, duplicated, device encoding) and X1 = A[:, shard].
+    TRY(R.at2.alloc((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
+    TRY(R.x1.alloc(R.slot_bytes(), "power A^1"));
+    if (src.dev) {
+        DBuf flag;
+        TRY(flag.alloc(16, "range flag"));
+        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+        LAUNCH(launch_make_at2(src.dev, src.lda, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, flag.as<int>(), s));
+        int hflag = 0;
+        COPY(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
+    } else if (src.host) {
+        DBuf raw, flag;
+        TRY(raw.alloc((size_t)N * N * 2, "A staging"));
+        TRY(flag.alloc(16, "range flag"));
+        COPY(raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+        LAUNCH(launch_make_at2(raw.as<uint16_t>(), N, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, flag.as<int>(), s));
+        int hflag = 0;
+        COPY(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
+    } else {
+        std::vector<WordMask> words = enumerate_words(src.n);
+        DBuf dw;
+        TRY(dw.alloc(words.size() * sizeof(WordMask), "word masks"));
+        COPY(dw.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
+        LAUNCH(launch_build_from_words(dw.as<WordMask>(), N, src.n, R.at2.as<uint32_t>(), R.Np, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    LAUNCH(launch_x1_from_at2(R.at2.as<uint32_t>(), R.Np, R.c0, R.w, R.x1.as<uint16_t>(), R.ld, s));
+
+    R.sparse = g_opts.block_sparse != 0;
+    if (R.sparse) TRY(build_tile_lists(R, s));
+    else R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
+
+    // power store: a ring of device slots sized to the budget
+    {
+        size_t freeb = 0, totalb = 0;
+        CUDA_TRY(cudaMemGetInfo(&freeb, &totalb));
+        int64_t budget = g_opts.budget > 0 ? g_opts.budget : (int64_t)(0.90 * (double)freeb);
+        int64_t slots = budget / (int64_t)R.slot_bytes() - 2; // keep room for 2 recompute buffers
+        slots = std::min<int64_t>(slots, std::max(max_k, 2));
+        if (slots < 2)
+            return fail(MP_ERR_RESOURCE, "power store needs at least 2 slots of %zu bytes (budget %lld bytes)",
+                        R.slot_bytes(), (long long)budget);
+        R.ring.resize((size_t)slots);
+        R.slot_power.assign((size_t)slots, 0);
+        for (auto &b : R.ring) TRY(b.alloc(R.slot_bytes(), "power store slot"));
+    }
+    TRY(R.stats.alloc((size_t)(max_k + 1) * 4 * 8, "per-power statistics"));
+    TRY(R.flag.alloc(16, "compare flag"));
+
+    std::vector<mp_power_stats> hs((size_t)max_k + 1);
+    uint64_t S = 0;
+    {
+        unsigned long long *dS = reinterpret_cast<unsigned long long *>(R.flag.p);
+        CUDA_TRY(cudaMemsetAsync(dS, 0, 8, s));
+        LAUNCH(launch_unit_sum(N, dS, s));
+        COPY(&S, dS, 8, cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    double prod_ms = 0.0;
+    int64_t launches = 0;
+    const int64_t init[4] = {0, 0, 0xFFFF, INT64_MAX};
+
+    mp_periodic_result res;
+    std::memset(&res, 0, sizeof(res));
+    const uint16_t *prev = R.x1.as<uint16_t>();
+    bool found = false;
+    int k = 1;
+    for (k = 1; k <= max_k && !found; ++k) {
+        const uint16_t *cur = R.x1.as<uint16_t>();
+        if (k >= 2) {
+            const size_t q = (size_t)(k % (int)R.ring.size());
+            uint16_t *dst = R.ring[q].as<uint16_t>();
+            R.slot_power[q] = k;
+            CUDA_TRY(cudaEventRecord(e0, s));
+            TRY(product(R, prev, dst, s)); // A^k = A (x) A^{k-1}
+            CUDA_TRY(cudaEventRecord(e1, s));
+            ++launches;
+            cur = dst;
+        }
+        int64_t *sk = R.stats.as<int64_t>() + 4 * k;
+        COPY(sk, init, sizeof(init), cudaMemcpyHostToDevice, s);
+        LAUNCH(launch_stats(cur, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(sk), s));
+        TRY(allreduce(0, sk, 2, s));     // SUM: fingerprint, inf count
+        TRY(allreduce(1, sk + 2, 2, s)); // MIN: diagonal minimum, first finite entry
+        COPY(&hs[(size_t)k], sk, sizeof(mp_power_stats), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (k >= 2) {
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+            prod_ms += ms;
+        }
+        const mp_power_stats &cs = hs[(size_t)k];
+        res.diag_min[k] = (uint16_t)std::min<int64_t>(cs.diag_min, 0xFFFF);
+        res.fingerprint[k] = (uint64_t)cs.fingerprint;
+        if (!res.dense_from && cs.inf_count == 0) res.dense_from = k;
+
+        if (cap) {
+            DBuf rowbuf;
+            TRY(rowbuf.alloc((size_t)N * 2, "captured row"));
+            for (int r = 0; r < cap->nrows; ++r) {
+                LAUNCH(launch_decode(cur + cap->rows[r] * R.ld, R.ld, 1, N, rowbuf.as<uint16_t>(), N, s));
+                CUDA_TRY(cudaMemcpyAsync(cap->out + ((size_t)(k - 1) * cap->nrows + r) * N, rowbuf.p, (size_t)N * 2,
+                                         cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+            }
+            prev = cur;
+            if (k == max_k) found = true;
+            continue;
+        }
+
+        // a5: forward first-repeat search, j = k-1 down to 1
+        for (int j = k - 1; j >= 1 && !found; --j) {
+            int32_t c = 0;
+            if (!mp_repeat_candidate(&cs, &hs[(size_t)j], S, &c)) continue;
+            const uint16_t *Z = nullptr;
+            TRY(power_buffer(R, j, &Z, s));
+            int64_t *fl = R.flag.as<int64_t>();
+            CUDA_TRY(cudaMemsetAsync(fl, 0, 8, s));
+            LAUNCH(launch_compare(cur, Z, R.ld, N, R.w, c, reinterpret_cast<unsigned long long *>(fl), s));
+            TRY(allreduce(0, fl, 1, s));
+            int64_t bad = -1;
+            COPY(&bad, fl, 8, cudaMemcpyDeviceToHost, s);
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (bad == 0) {
+                found = true;
+                res.mu = j;
+                res.lambda = k - j;
+                res.offset = c;
+                res.k_last = k;
+            }
+        }
+        prev = cur;
+    }
+    CUDA_TRY(cudaEventRecord(ev_all1, s));
+    CUDA_TRY(cudaEventSynchronize(ev_all1));
+    float all_ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&all_ms, ev_all0, ev_all1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(ev_all0);
+    cudaEventDestroy(ev_all1);
+
+    g_prof.product_ms = prod_ms;
+    g_prof.product_launches = launches;
+    g_prof.dense_steps = (double)launches * (double)N * (double)N * (double)R.w;
+    g_prof.issued_steps = (double)launches * R.issued_per_product;
+    g_prof.total_ms = all_ms;
+    g_prof.h2d_bytes = g_h2d.load() - h2d0;
+    g_prof.d2h_bytes = g_d2h.load() - d2h0;
+
+    if (!found) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
+    *out = res;
+    return MP_OK;
+}
+
+} // namespace
+
+// =======================================================================================
+// Public ABI
+// =======================================================================================
+extern "C" {
+
+mp_status mp_count_words(int n, int64_t *N_out)
+{
+    if (!N_out || n < 2 || n > 13) return fail(MP_ERR_DOMAIN, "mp_count_words: n = %d outside [2, 13]", n);
+    *N_out = count_words(n);
+    return MP_OK;
+}
+
+mp_status build_transition_matrix_into(int n, uint16_t *A, int64_t N)
+{
+    if (!A || n < 2 || n > MP_MAX_N)
+        return fail(MP_ERR_DOMAIN, "build_transition_matrix: n = %d outside [2, %d] or NULL buffer", n, MP_MAX_N);
+    const std::vector<WordMask> words = enumerate_words(n);
+    if ((int64_t)words.size() != N)
+        return fail(MP_ERR_DOMAIN, "build_transition_matrix: N = %lld but |C_%d| = %zu", (long long)N, n,
+                    words.size());
+    fill_transition_matrix(words, n, A, host_threads());
+    return MP_OK;
+}
+
+mp_status build_transition_matrix(int n, uint16_t **A_out, int64_t *N_out)
+{
+    if (!A_out || !N_out || n < 2 || n > MP_MAX_N)
+        return fail(MP_ERR_DOMAIN, "build_transition_matrix: n = %d outside [2, %d] or NULL output", n, MP_MAX_N);
+    const int64_t N = count_words(n);
+    const size_t bytes = (size_t)N * (size_t)N * 2;
+    uint16_t *A = (uint16_t *)std::malloc(bytes);
+    if (!A) return fail(MP_ERR_RESOURCE, "host allocation of %zu bytes for A(D_%d) failed", bytes, n);
+    mp_status s = build_transition_matrix_into(n, A, N);
+    if (s != MP_OK) {
+        std::free(A);
+        return s;
+    }
+    *A_out = A;
+    *N_out = N;
+    return MP_OK;
+}
+
+void mp_free(void *p) { std::free(p); }
+
+mp_status minplus_mul(const uint16_t *A, const uint16_t *B, uint16_t *C, int64_t M, int64_t K, int64_t N)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!A || !B || !C || M <= 0 || K <= 0 || N <= 0)
+        return fail(MP_ERR_DOMAIN, "minplus_mul: NULL pointer or non-positive dimension (M=%lld K=%lld N=%lld)",
+                    (long long)M, (long long)K, (long long)N);
+    if (overlaps(C, (size_t)M * N * 2, A, (size_t)M * K * 2) || overlaps(C, (size_t)M * N * 2, B, (size_t)K * N * 2))
+        return fail(MP_ERR_DOMAIN, "minplus_mul: C overlaps A or B");
+    int dev = 0;
+    DevState *st = nullptr;
+    TRY(current_device(&dev, &st));
+    cudaStream_t s = st->stream;
+    TRY(st->stage_a.ensure((size_t)M * K * 2, "A staging"));
+    TRY(st->stage_b.ensure((size_t)K * N * 2, "B staging"));
+    TRY(st->stage_c.ensure((size_t)M * N * 2, "C staging"));
+    COPY(st->stage_a.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice, s);
+    COPY(st->stage_b.p, B, (size_t)K * N * 2, cudaMemcpyHostToDevice, s);
+    TRY(mul_device_impl(*st, st->stage_a.as<uint16_t>(), K, st->stage_b.as<uint16_t>(), N,
+                        st->stage_c.as<uint16_t>(), N, M, K, N, s));
+    COPY(C, st->stage_c.p, (size_t)M * N * 2, cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return MP_OK;
+}
+
+mp_status minplus_mul_device(const uint16_t *dA, int64_t lda, const uint16_t *dB, int64_t ldb, uint16_t *dC,
+                             int64_t ldc, int64_t M, int64_t K, int64_t N, void *stream)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!dA || !dB || !dC || M <= 0 || K <= 0 || N <= 0 || lda < K || ldb < N || ldc < N)
+        return fail(MP_ERR_DOMAIN, "minplus_mul_device: NULL pointer, non-positive dimension or ld < cols");
+    if (overlaps(dC, span_bytes(M, N, ldc), dA, span_bytes(M, K, lda)) ||
+        overlaps(dC, span_bytes(M, N, ldc), dB, span_bytes(K, N, ldb)))
+        return fail(MP_ERR_DOMAIN, "minplus_mul_device: C overlaps A or B");
+    int dev = 0;
+    DevState *st = nullptr;
+    TRY(current_device(&dev, &st));
+    return mul_device_impl(*st, dA, lda, dB, ldb, dC, ldc, M, K, N, (cudaStream_t)stream);
+}
+
+mp_status minplus_power_until_periodic(const uint16_t *A, int64_t N, int max_k, mp_periodic_result *out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!A || !out || N <= 0 || max_k < 2 || max_k > MP_MAX_K)
+        return fail(MP_ERR_DOMAIN, "minplus_power_until_periodic: NULL pointer, N <= 0 or max_k outside [2, %d]",
+                    MP_MAX_K);
+    ASource src;
+    src.host = A;
+    return run_powers(src, N, max_k, out);
+}
+
+mp_status minplus_power_until_periodic_device(const uint16_t *dA, int64_t lda, int64_t N, int max_k,
+                                              mp_periodic_result *out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!dA || !out || N <= 0 || lda < N || max_k < 2 || max_k > MP_MAX_K)
+        return fail(MP_ERR_DOMAIN,
+                    "minplus_power_until_periodic_device: NULL pointer, N <= 0, lda < N or max_k outside [2, %d]",
+                    MP_MAX_K);
+    ASource src;
+    src.dev = dA;
+    src.lda = lda;
+    return run_powers(src, N, max_k, out);
+}
+
+mp_status minplus_power_rows(const uint16_t *A, int64_t N, int kmax, const int64_t *rows, int nrows, uint16_t *out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!A || !rows || !out || N <= 0 || kmax < 1 || kmax > MP_MAX_K || nrows <= 0)
+        return fail(MP_ERR_DOMAIN, "minplus_power_rows: invalid arguments");
+    for (int r = 0; r < nrows; ++r)
+        if (rows[r] < 0 || rows[r] >= N) return fail(MP_ERR_DOMAIN, "minplus_power_rows: row %lld outside [0, N)",
+                                                     (long long)rows[r]);
+    ASource src;
+    src.host = A;
+    Capture cap;
+    cap.rows = rows;
+    cap.nrows = nrows;
+    cap.out = out;
+    mp_periodic_result res;
+    const Dist saved = g_dist;
+    g_dist = Dist();
+    mp_status st = run_powers(src, N, kmax, &res, &cap);
+    g_dist = saved;
+    return st;
+}
+
+mp_status mp_gamma2_readoff(const mp_periodic_result *r, int64_t m, int64_t *g)
+{
+    if (!r || !g || m < 3 || r->lambda <= 0 || r->k_last <= 0)
+        return fail(MP_ERR_DOMAIN, "mp_gamma2_readoff: m = %lld < 3 or invalid result", (long long)m);
+    if (m <= r->k_last) {
+        *g = r->diag_min[m];
+        return MP_OK;
+    }
+    // Theorem 3: gamma(m) = gamma(m - t*lambda) + t*b, m - t*lambda in (mu, k_last]
+    const int64_t t = (m - r->k_last + r->lambda - 1) / r->lambda;
+    *g = (int64_t)r->diag_min[m - t * r->lambda] + t * (int64_t)r->offset;
+    return MP_OK;
+}
+
+mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!gamma2_out || n < 2 || n > MP_MAX_N || m < 3)
+        return fail(MP_ERR_DOMAIN, "gamma2_cylinder: n = %d outside [2, %d] or m = %lld < 3", n, MP_MAX_N,
+                    (long long)m);
+    const auto key = std::make_tuple(n, g_dist.world, g_dist.rank);
+    auto it = g_cache.find(key);
+    if (it == g_cache.end()) {
+        mp_periodic_result r;
+        ASource src;
+        src.n = n;
+        TRY(run_powers(src, count_words(n), 64, &r));
+        it = g_cache.emplace(key, r).first;
+    }
+    return mp_gamma2_readoff(&it->second, m, gamma2_out);
+}
+
+mp_status mp_dist_set(int rank, int world, mp_allreduce_fn fn, void *ctx)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (fn == nullptr) {
+        g_dist = Dist();
+        return MP_OK;
+    }
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(MP_ERR_DOMAIN, "mp_dist_set: rank %d / world %d invalid", rank, world);
+    g_dist.rank = rank;
+    g_dist.world = world;
+    g_dist.fn = fn;
+    g_dist.ctx = ctx;
+    return MP_OK;
+}
+
+mp_status mp_shard_range(int64_t N, int world, int rank, int64_t *c0, int64_t *c1)
+{
+    if (!c0 || !c1 || N <= 0 || world < 1 || rank < 0 || rank >= world)
+        return fail(MP_ERR_DOMAIN, "mp_shard_range: invalid arguments");
+    const int64_t w = round_up((N + world - 1) / world, 8);
+    *c0 = std::min<int64_t>(N, (int64_t)rank * w);
+    *c1 = std::min<int64_t>(N, *c0 + w);
+    return MP_OK;
+}
+
+uint64_t mp_fingerprint_unit(int64_t N)
+{
+    const uint64_t T = (uint64_t)(N > 0 ? N : 0) * (uint64_t)(N > 0 ? N : 0);
+    const int nt = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)host_threads(), T / 65536 + 1));
+    std::vector<uint64_t> part((size_t)nt, 0);
+    std::vector<std::thread> pool;
+    for (int id = 0; id < nt; ++id)
+        pool.emplace_back([&, id] {
+            uint64_t acc = 0;
+            for (uint64_t t = (uint64_t)id; t < T; t += (uint64_t)nt) acc += mix64(t);
+            part[(size_t)id] = acc;
+        });
+    for (auto &th : pool) th.join();
+    uint64_t S = 0;
+    for (uint64_t v : part) S += v;
+    return S;
+}
+
+int mp_repeat_candidate(const mp_power_stats *sk, const mp_power_stats *sj, uint64_t S, int32_t *c_out)
+{
+    if (!sk || !sj) return 0;
+    if (sk->inf_count != sj->inf_count) return 0;
+    const bool allinf_k = sk->ref == INT64_MAX, allinf_j = sj->ref == INT64_MAX;
+    if (allinf_k || allinf_j) {
+        if (allinf_k != allinf_j) return 0;
+        if (c_out) *c_out = 0;
+        return 1;
+    }
+    if ((sk->ref >> 16) != (sj->ref >> 16)) return 0; // first finite entries at different places
+    const int32_t c = (int32_t)(sk->ref & 0xFFFF) - (int32_t)(sj->ref & 0xFFFF);
+    if (c_out) *c_out = c;
+    if (sk->inf_count > 0) return 1; // +inf present: the linear hash is not shift-equivariant
+    const uint64_t lhs = (uint64_t)sk->fingerprint - (uint64_t)sj->fingerprint;
+    const uint64_t rhs = (uint64_t)(int64_t)c * S;
+    return lhs == rhs ? 1 : 0;
+}
+
+const char *mp_last_error(void) { return t_err.c_str(); }
+
+void mp_shutdown(void)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_cache.clear();
+    for (auto &kv : g_dev) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first);
+        if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
+        kv.second.stream = nullptr;
+        cudaSetDevice(cur);
+    }
+    g_dev.clear();
+}
+
+const char *mp_version(void)
+{
+    return "minplus-b200 0.1 sm_100a: DPX VIADDMNMX.U16x2 128x256x32 tile, 4-stage cp.async, block-sparse A";
+}
+
+int64_t mp_kernel_launches(void) { return g_launches.load(); }
+
+mp_status mp_last_profile(mp_profile *out)
+{
+    if (!out) return fail(MP_ERR_DOMAIN, "mp_last_profile: NULL");
+    *out = g_prof;
+    return MP_OK;
+}
+
+mp_status mp_set_stream(void *stream)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    int dev = 0;
+    DevState *st = nullptr;
+    TRY(current_device(&dev, &st));
+    st->user_stream = (cudaStream_t)stream;
+    return MP_OK;
+}
+
+mp_status mp_set_options(int block_sparse, int64_t device_budget_bytes)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (device_budget_bytes < 0) return fail(MP_ERR_DOMAIN, "mp_set_options: negative budget");
+    g_opts.block_sparse = block_sparse;
+    g_opts.budget = device_budget_bytes;
+    return MP_OK;
+}
+
+} // extern "C"

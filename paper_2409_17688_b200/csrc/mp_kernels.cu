@@ -1,0 +1,504 @@
+// Device kernels of the (min,+) power path (sm_100a).  DESIGN.md "Kernels" describes each
+// with its roofline; the citations name the paper passage each one implements.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <algorithm>
+
+#include "mp_internal.h"
+#include "mp_kernels.h"
+
+namespace mp {
+
+// ---------------------------------------------------------------------------------------
+// small PTX helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------------------------------
+// a3: C = A (x) X on one column tile set.  P:53 "(A x B)_ij = min_k(a_ik + b_kj)";
+// Algorithm 2 line 2 "A^i = A x A^{i-1}".
+//
+// Operands:
+//   AT2 [Kp][lda] u32: AT2[l][i] = {a_il, a_il} (A transposed, each entry duplicated into
+//        both 16-bit halves so one DPX instruction adds it to two adjacent X columns);
+//   X   [Kp][ldx] u16 (device encoding, +inf = 0x7FFF); C [Mp][ldc] u16.
+// CTA tile kBM x kBN (128 x 256), stage depth kBK (32) along l, STAGES-deep cp.async ring.
+// Thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..64+4tr+3} and columns
+// {8tc..8tc+7, 128+8tc..128+8tc+7}: 64 packed accumulators = 128 outputs.  Per l it reads
+// 2+2 LDS.128 (A broadcast within each 8-lane phase, X contiguous per phase: conflict
+// free) and issues 64 VIADDMNMX.U16x2 (min(a+x, acc) on two lanes).
+// Block sparsity (exact; NEXT-1): if kt_ptr != nullptr the row tile blockIdx.y visits only
+// the l-tiles kt_idx[kt_ptr[by] .. kt_ptr[by+1]) in which A has a finite entry; an all-inf
+// A tile can only contribute +inf terms, which never lower a minimum.
+// ---------------------------------------------------------------------------------------
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_minplus(const uint32_t *__restrict__ AT2, int64_t lda, const uint16_t *__restrict__ X,
+              int64_t ldx, uint16_t *__restrict__ C, int64_t ldc, const int32_t *__restrict__ kt_ptr,
+              const int32_t *__restrict__ kt_idx, int num_kt)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int A_STAGE = kBK * kBM * 4; // 16 KB
+    constexpr int B_STAGE = kBK * kBN * 2; // 16 KB
+    const int by = blockIdx.y, bx = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tr = (warp >> 1) * 4 + (lane >> 3); // 0..15
+    const int tc = (warp & 1) * 8 + (lane & 7);   // 0..15
+
+    int kb = 0, ke = num_kt;
+    if (kt_ptr) {
+        kb = kt_ptr[by];
+        ke = kt_ptr[by + 1];
+    }
+    const int T = ke - kb;
+    const uint32_t *Ag = AT2 + (int64_t)by * kBM;
+    const uint16_t *Xg = X + (int64_t)bx * kBN;
+    const uint32_t sbase = smem_addr(smem);
+
+    auto load_stage = [&](int stage, int t) {
+        const int kt = kt_ptr ? __ldg(kt_idx + kb + t) : t;
+        const int64_t l0 = (int64_t)kt * kBK;
+        const uint32_t sA = sbase + stage * A_STAGE;
+        const uint32_t sB = sbase + STAGES * A_STAGE + stage * B_STAGE;
+#pragma unroll
+        for (int c = tid; c < kBK * 32; c += kThreads) { // 32 rows x 32 chunks of 16 B
+            const int r = c >> 5, cc = c & 31;
+            cp_async16(sA + r * 512 + cc * 16, Ag + (l0 + r) * lda + cc * 4);
+        }
+#pragma unroll
+        for (int c = tid; c < kBK * 32; c += kThreads) {
+            const int r = c >> 5, cc = c & 31;
+            cp_async16(sB + r * 512 + cc * 16, Xg + (l0 + r) * ldx + cc * 8);
+        }
+    };
+
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc[r][p] = 0xFFFFFFFFu;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < T) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    for (int t = 0; t < T; ++t) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int tn = t + STAGES - 1;
+            if (tn < T) load_stage(tn % STAGES, tn);
+            cp_async_commit();
+        }
+        const int stage = t % STAGES;
+        const uint32_t *As = reinterpret_cast<const uint32_t *>(smem + stage * A_STAGE);
+        const uint32_t *Bs = reinterpret_cast<const uint32_t *>(smem + STAGES * A_STAGE + stage * B_STAGE);
+#pragma unroll 8
+        for (int kk = 0; kk < kBK; ++kk) {
+            const uint4 a0 = *reinterpret_cast<const uint4 *>(As + kk * 128 + tr * 4);
+            const uint4 a1 = *reinterpret_cast<const uint4 *>(As + kk * 128 + 64 + tr * 4);
+            const uint4 b0 = *reinterpret_cast<const uint4 *>(Bs + kk * 128 + tc * 4);
+            const uint4 b1 = *reinterpret_cast<const uint4 *>(Bs + kk * 128 + 64 + tc * 4);
+            const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int p = 0; p < 8; ++p) acc[r][p] = __viaddmin_u16x2(a[r], b[p], acc[r][p]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // Epilogue: any lane sum >= 0x7FFF is +inf (G6) -> clamp to the device +inf.
+    const int64_t row0 = (int64_t)by * kBM;
+    const int64_t col0 = (int64_t)bx * kBN;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int64_t i = row0 + (r < 4 ? tr * 4 + r : 64 + tr * 4 + (r - 4));
+        uint4 v0, v1;
+        v0.x = __vminu2(acc[r][0], 0x7FFF7FFFu);
+        v0.y = __vminu2(acc[r][1], 0x7FFF7FFFu);
+        v0.z = __vminu2(acc[r][2], 0x7FFF7FFFu);
+        v0.w = __vminu2(acc[r][3], 0x7FFF7FFFu);
+        v1.x = __vminu2(acc[r][4], 0x7FFF7FFFu);
+        v1.y = __vminu2(acc[r][5], 0x7FFF7FFFu);
+        v1.z = __vminu2(acc[r][6], 0x7FFF7FFFu);
+        v1.w = __vminu2(acc[r][7], 0x7FFF7FFFu);
+        uint16_t *crow = C + i * ldc + col0;
+        *reinterpret_cast<uint4 *>(crow + tc * 8) = v0;
+        *reinterpret_cast<uint4 *>(crow + 128 + tc * 8) = v1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// a4: per-power statistics of a column shard X (rows 0..N-1, columns c0..c0+w-1 of the
+// global power, stored [Np][ld]); layout of out[] = mp_power_stats:
+//   out[0] += H = sum h(i*N + c0 + j) * x (mod 2^64), +inf counted as 0xFFFF;
+//   out[1] += number of +inf entries;
+//   out[2]  = min(out[2], min over i == c0 + j of x)  (Algorithm 5);
+//   out[3]  = min(out[3], (t << 16) | x) over finite entries, t = i*N + c0 + j.
+// The caller initialises out = {0, 0, 0xFFFF, INT64_MAX}.  HBM-bound: reads 2*N*w bytes.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_stats(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t c0, int64_t w,
+            unsigned long long *__restrict__ out)
+{
+    const int64_t chunks_per_row = (w + 7) / 8;
+    const int64_t total = N * chunks_per_row;
+    unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
+    unsigned dmin = 0xFFFFu;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = c / chunks_per_row;
+        const int64_t j0 = (c - i * chunks_per_row) * 8;
+        const uint4 v = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
+        const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int64_t j = j0 + e;
+            if (j >= w) break;
+            uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+            const int64_t gj = c0 + j;
+            const uint64_t t = (uint64_t)(i * N + gj);
+            if (x == kDevInf) {
+                x = kBndInf;
+                ++infc;
+            } else {
+                const unsigned long long key = (t << 16) | x;
+                if (key < ref) ref = key;
+            }
+            h += (unsigned long long)mix64(t) * x;
+            if (gj == i && x < dmin) dmin = x;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+        infc += __shfl_xor_sync(0xFFFFFFFFu, infc, o);
+        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
+        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, o));
+    }
+    __shared__ unsigned long long sh[8], si[8], sr[8];
+    __shared__ unsigned sd[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sh[warp] = h;
+        si[warp] = infc;
+        sd[warp] = dmin;
+        sr[warp] = ref;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long H = 0, I = 0, R = 0x7FFFFFFFFFFFFFFFull;
+        unsigned D = 0xFFFFu;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            H += sh[k];
+            I += si[k];
+            D = min(D, sd[k]);
+            R = min(R, sr[k]);
+        }
+        atomicAdd(out + 0, H);
+        atomicAdd(out + 1, I);
+        atomicMin(out + 2, (unsigned long long)D);
+        atomicMin(out + 3, R);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// a5: exact comparison Y == c (x) Z on a shard ("A^{n0+a} - A^{n0} being a constant
+// matrix"; reading G9: identical +inf pattern and constant difference on finite entries).
+// Adds the number of mismatching entries to *out.  HBM-bound: reads 4*N*w bytes.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_compare(const uint16_t *__restrict__ Y, const uint16_t *__restrict__ Z, int64_t ld, int64_t N,
+              int64_t w, int32_t c, unsigned long long *__restrict__ out)
+{
+    const int64_t chunks_per_row = (w + 7) / 8;
+    const int64_t total = N * chunks_per_row;
+    unsigned long long bad = 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / chunks_per_row;
+        const int64_t j0 = (q - i * chunks_per_row) * 8;
+        const uint4 vy = *reinterpret_cast<const uint4 *>(Y + i * ld + j0);
+        const uint4 vz = *reinterpret_cast<const uint4 *>(Z + i * ld + j0);
+        const uint32_t wy[4] = {vy.x, vy.y, vy.z, vy.w};
+        const uint32_t wz[4] = {vz.x, vz.y, vz.z, vz.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (j0 + e >= w) break;
+            const int32_t y = (wy[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
+            const int32_t z = (wz[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
+            const bool yi = (y == kDevInf), zi = (z == kDevInf);
+            if (yi != zi || (!yi && y - z != c)) ++bad;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
+}
+
+// ---------------------------------------------------------------------------------------
+// Staging kernels (boundary encoding -> device layout and back).
+// ---------------------------------------------------------------------------------------
+
+// dst [rows_p][ldd] u16 = enc(src[i][j]) for i < rows, j < cols, +inf padding elsewhere.
+// Any src entry in (0x7FFE, 0xFFFF) sets *range_flag.
+__global__ void k_encode(const uint16_t *__restrict__ src, int64_t lds, int64_t rows, int64_t cols,
+                         uint16_t *__restrict__ dst, int64_t ldd, int64_t rows_p,
+                         int *__restrict__ range_flag)
+{
+    const int64_t total = rows_p * ldd;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ldd, j = t - i * ldd;
+        uint16_t v = kDevInf;
+        if (i < rows && j < cols) {
+            const uint16_t s = src[i * lds + j];
+            if (s == kBndInf) v = kDevInf;
+            else if (s > kFiniteMax) { v = kDevInf; *range_flag = 1; }
+            else v = s;
+        }
+        dst[t] = v;
+    }
+}
+
+// AT2 [Kp][Mp] u32: AT2[l][i] = {enc(a_il), enc(a_il)}; +inf padding.  32x32 tiles through
+// shared memory so both the read of A (row-major) and the write of AT2 are coalesced.
+__global__ void k_make_at2(const uint16_t *__restrict__ A, int64_t lda, int64_t M, int64_t K,
+                           uint32_t *__restrict__ AT2, int64_t Mp, int64_t Kp, int *__restrict__ range_flag)
+{
+    __shared__ uint16_t tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.y * 32, l0 = (int64_t)blockIdx.x * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, l = l0 + threadIdx.x;
+        uint16_t v = kDevInf;
+        if (i < M && l < K) {
+            const uint16_t s = A[i * lda + l];
+            if (s == kBndInf) v = kDevInf;
+            else if (s > kFiniteMax) { v = kDevInf; *range_flag = 1; }
+            else v = s;
+        }
+        tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t l = l0 + r, i = i0 + threadIdx.x;
+        if (l < Kp && i < Mp) {
+            const uint32_t v = tile[threadIdx.x][r];
+            AT2[l * Mp + i] = v | (v << 16);
+        }
+    }
+}
+
+// Builds AT2 directly from the word masks (a1 on the device: A_qp = zeros(p) if p can
+// follow q).  One thread per AT2 entry (l, i) = (column word p, row word q);
+// consecutive threads write consecutive i (coalesced).
+__global__ void k_build_from_words(const WordMask *__restrict__ words, int64_t N, unsigned full,
+                                   uint32_t *__restrict__ AT2, int64_t Np)
+{
+    const int64_t total = Np * Np;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = t / Np, i = t - l * Np;
+        uint32_t v = kDevInf;
+        if (l < N && i < N) {
+            const WordMask q = words[i], p = words[l];
+            if (can_follow_mask(q, p, full)) v = p.zeros;
+        }
+        AT2[t] = v | (v << 16);
+    }
+}
+
+// X1[i][j] = A[i][c0 + j] = low half of AT2[c0 + j][i] for i < Np, j < w; +inf for
+// w <= j < ldx.  32x32 tiles through shared memory (coalesced read and write).
+__global__ void k_x1_from_at2(const uint32_t *__restrict__ AT2, int64_t Np, int64_t c0, int64_t w,
+                              uint16_t *__restrict__ X1, int64_t ldx)
+{
+    __shared__ uint16_t tile[32][33];
+    const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, i = i0 + threadIdx.x;
+        uint16_t v = kDevInf;
+        if (j < w && i < Np) v = (uint16_t)(AT2[(c0 + j) * Np + i] & 0xFFFFu);
+        tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, j = j0 + threadIdx.x;
+        if (i < Np && j < ldx) X1[i * ldx + j] = tile[threadIdx.x][r];
+    }
+}
+
+// dst (rows x cols, ldd, boundary encoding) = dec(src[i][j]) for the valid region.
+__global__ void k_decode(const uint16_t *__restrict__ src, int64_t lds, int64_t rows, int64_t cols,
+                         uint16_t *__restrict__ dst, int64_t ldd)
+{
+    const int64_t total = rows * cols;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / cols, j = t - i * cols;
+        const uint16_t v = src[i * lds + j];
+        dst[i * ldd + j] = (v == kDevInf) ? kBndInf : v;
+    }
+}
+
+// occ[bm * Ktiles + kt] = 1 if the kBM x kBK tile of A (read through AT2) has a finite entry.
+__global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, int64_t Kp,
+                                 uint8_t *__restrict__ occ)
+{
+    const int64_t Mt = Mp / kBM, Kt = Kp / kBK;
+    const int64_t total = Mt * Kt;
+    // one warp per tile
+    const int lane = threadIdx.x & 31;
+    for (int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < total;
+         tile += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t bm = tile / Kt, kt = tile - bm * Kt;
+        bool any = false;
+        for (int r = 0; r < kBK && !any; ++r) {
+            const uint32_t *row = AT2 + (kt * kBK + r) * Mp + bm * kBM;
+#pragma unroll
+            for (int e = 0; e < kBM / 32; ++e) any |= (row[lane + 32 * e] != 0x7FFF7FFFu);
+            any = __any_sync(0xFFFFFFFFu, any);
+        }
+        if (lane == 0) occ[tile] = any ? 1 : 0;
+    }
+}
+
+// S(N) = sum_{t < N*N} h(t) mod 2^64 (fingerprint of the all-ones matrix), accumulated
+// into *out (zeroed by the caller).  Pure ALU work, no memory traffic.
+__global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long *__restrict__ out)
+{
+    unsigned long long acc = 0;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x)
+        acc += mix64(t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+static int g_num_sms = 0;
+static int num_sms()
+{
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+static int grid_for(int64_t work, int per_block)
+{
+    int64_t g = (work + per_block - 1) / per_block;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+constexpr int kStages = 4;
+
+cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, int64_t ldx, uint16_t *C,
+                           int64_t ldc, int64_t Mp, int64_t ncols_p, int64_t Kp, const int32_t *kt_ptr,
+                           const int32_t *kt_idx, cudaStream_t s)
+{
+    static bool attr_set = false;
+    const int smem = kStages * (kBK * kBM * 4 + kBK * kBN * 2);
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_minplus<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kBM));
+    k_minplus<kStages><<<grid, kThreads, smem, s>>>(AT2, lda, X, ldx, C, ldc, kt_ptr, kt_idx,
+                                                    (int)(Kp / kBK));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, int64_t w,
+                         unsigned long long *out, cudaStream_t s)
+{
+    const int g = grid_for(N * ((w + 7) / 8), 256);
+    k_stats<<<g, 256, 0, s>>>(X, ld, N, c0, w, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int64_t N, int64_t w, int32_t c,
+                           unsigned long long *out, cudaStream_t s)
+{
+    const int g = grid_for(N * ((w + 7) / 8), 256);
+    k_compare<<<g, 256, 0, s>>>(Y, Z, ld, N, w, c, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
+                          int64_t ldd, int64_t rows_p, int *range_flag, cudaStream_t s)
+{
+    k_encode<<<grid_for(rows_p * ldd, 256), 256, 0, s>>>(src, lds, rows, cols, dst, ldd, rows_p, range_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_make_at2(const uint16_t *A, int64_t lda, int64_t M, int64_t K, uint32_t *AT2, int64_t Mp,
+                            int64_t Kp, int *range_flag, cudaStream_t s)
+{
+    dim3 grid((unsigned)((Kp + 31) / 32), (unsigned)((Mp + 31) / 32));
+    k_make_at2<<<grid, dim3(32, 8), 0, s>>>(A, lda, M, K, AT2, Mp, Kp, range_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_from_words(const WordMask *words, int64_t N, int n, uint32_t *AT2, int64_t Np,
+                                    cudaStream_t s)
+{
+    k_build_from_words<<<grid_for(Np * Np, 256), 256, 0, s>>>(words, N, (1u << n) - 1u, AT2, Np);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int64_t w, uint16_t *X1,
+                               int64_t ldx, cudaStream_t s)
+{
+    dim3 grid((unsigned)((ldx + 31) / 32), (unsigned)((Np + 31) / 32));
+    k_x1_from_at2<<<grid, dim3(32, 8), 0, s>>>(AT2, Np, c0, w, X1, ldx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
+                          int64_t ldd, cudaStream_t s)
+{
+    k_decode<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, lds, rows, cols, dst, ldd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s)
+{
+    const uint64_t T = (uint64_t)N * (uint64_t)N;
+    k_unit_sum<<<grid_for((int64_t)std::min<uint64_t>(T, 1ull << 40), 256), 256, 0, s>>>(T, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_occupancy(const uint32_t *AT2, int64_t Mp, int64_t Kp, uint8_t *occ, cudaStream_t s)
+{
+    const int64_t tiles = (Mp / kBM) * (Kp / kBK);
+    k_tile_occupancy<<<grid_for(tiles * 32, 256), 256, 0, s>>>(AT2, Mp, Kp, occ);
+    return cudaGetLastError();
+}
+
+} // namespace mp

@@ -1,0 +1,157 @@
+"""C-ABI checks that need no GPU: the library loads, exports every declared symbol, the
+host-side steps (a1 words / transition matrix, shard ranges, periodicity bookkeeping, read-off)
+match the oracle, and argument errors are reported before any device work."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2409_17688_b200 as mp
+from paper_2409_17688_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "minplus.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^(?!\s*typedef)\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\**\s*"
+                       r"([A-Za-z_][A-Za-z0-9_]*)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_exports_every_declared_symbol():
+    decl = declared_functions()
+    assert len(decl) >= 20
+    L = ctypes.CDLL(_native._build.SO)
+    for name in decl:
+        assert hasattr(L, name), name
+    assert sorted(_native.EXPORTS) == decl
+
+
+def test_no_cpu_fallback_symbols():
+    """The product library must not contain the oracle (no shared code, no CPU path)."""
+    L = ctypes.CDLL(_native._build.SO)
+    for sym in ("oracle_minplus_ijk", "oracle_minplus_ikj", "oracle_power_until_periodic"):
+        assert not hasattr(L, sym)
+
+
+def test_count_words_table1(oracle_mod):
+    for n in range(2, 14):
+        assert mp.count_words(n) == oracle_mod.count_words(n)
+    with pytest.raises(mp.MinplusError) as e:
+        mp.count_words(1)
+    assert e.value.status == 1
+
+
+@pytest.mark.parametrize("n", range(2, 11))
+def test_transition_matrix_equals_oracle(oracle_mod, n):
+    """a1 parity: the bitmask/DFS construction equals the letter-by-letter oracle bit for bit."""
+    assert np.array_equal(mp.build_transition_matrix(n), oracle_mod.transition_matrix(n))
+
+
+def test_transition_matrix_domain_errors():
+    for n in (0, 1, 13):
+        with pytest.raises(mp.MinplusError) as e:
+            mp.build_transition_matrix(n)
+        assert e.value.status == 1
+    A = np.empty(4, dtype=np.uint16)
+    assert _native.lib.build_transition_matrix_into(2, A.ctypes.data, 5) == 1
+
+
+def test_transition_matrix_n12_structure():
+    """n = 12 (the largest case): N = 52929 (Table 1), nnz = 21567085 (re-derived
+    by counting), labels <= 12, and no row is all +inf."""
+    A = mp.build_transition_matrix(12)
+    assert A.shape == (52929, 52929)
+    fin = A != 0xFFFF
+    assert int(fin.sum()) == 21567085
+    assert int(A[fin].max()) <= 12
+    assert fin.any(axis=1).all()
+
+
+def test_shard_ranges_cover():
+    for N in (1, 6, 15, 225, 3447, 52929):
+        for world in (1, 2, 3, 4, 8):
+            spans = [mp.shard_range(N, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == N
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0 and a0 <= a1
+            w = spans[0][1] - spans[0][0]
+            assert w % 8 == 0 or w == N
+    with pytest.raises(mp.MinplusError):
+        mp.shard_range(10, 2, 2)
+
+
+def test_fingerprint_unit_matches_oracle(oracle_mod):
+    for N in (1, 5, 37, 200):
+        assert mp.fingerprint_unit(N) == oracle_mod.fingerprint(np.ones((N, N), dtype=np.uint16))
+
+
+def _stats(oracle_mod, X):
+    N = X.shape[0]
+    fin = np.flatnonzero(X.ravel() != 0xFFFF)
+    ref = (int(fin[0]) << 16) | int(X.ravel()[fin[0]]) if len(fin) else 2**63 - 1
+    fp = oracle_mod.fingerprint(X)
+    return mp.PowerStats(fp - 2**64 if fp >= 2**63 else fp, int((X == 0xFFFF).sum()),
+                         int(np.diag(X).min()), ref)
+
+
+def test_repeat_candidate_logic(oracle_mod):
+    """The prefilter passes every true repeat (linearity of H) and rejects differing powers."""
+    A = oracle_mod.transition_matrix(4)
+    r = oracle_mod.power_until_periodic(A)
+    P = {1: A}
+    for k in range(2, r.k_last + 1):
+        P[k] = oracle_mod.minplus(A, P[k - 1])
+    S = mp.fingerprint_unit(A.shape[0])
+    st = {k: _stats(oracle_mod, P[k]) for k in P}
+    assert mp.repeat_candidate(st[r.k_last], st[r.mu], S) == r.offset
+    hits = [(k, j) for k in P for j in range(1, k) if mp.repeat_candidate(st[k], st[j], S) is not None
+            and oracle_mod.constant_difference(P[k], P[j]) is not None]
+    assert hits == [(r.k_last, r.mu)]
+    # all-inf pair: candidate with offset 0
+    Z = np.full((3, 3), 0xFFFF, dtype=np.uint16)
+    assert mp.repeat_candidate(_stats(oracle_mod, Z), _stats(oracle_mod, Z), 1) == 0
+
+
+def test_readoff_matches_oracle(oracle_mod):
+    """a6 on a result built from oracle values equals the oracle's read-off for m to 500."""
+    for n in (3, 5, 7):
+        o = oracle_mod.power_until_periodic(oracle_mod.transition_matrix(n))
+        r = _native._PeriodicResult()
+        r.mu, r.lambda_, r.offset, r.k_last, r.dense_from = o.mu, o.lam, o.offset, o.k_last, o.dense_from
+        for k, v in enumerate(o.diag_min):
+            r.diag_min[k] = v
+        res = _native._result(r)
+        for m in range(3, 500):
+            assert res.gamma2(m) == o.gamma2(m)
+        with pytest.raises(mp.MinplusError):
+            res.gamma2(2)
+
+
+def test_argument_errors_before_device():
+    with pytest.raises(mp.MinplusError) as e:
+        mp.minplus_mul(np.zeros((2, 3)), np.zeros((2, 3)))
+    assert e.value.status == 1
+    assert _native.lib.minplus_mul(None, None, None, 1, 1, 1) == 1
+    a = np.zeros((4, 4), dtype=np.uint16)
+    assert _native.lib.minplus_mul(a.ctypes.data, a.ctypes.data, a.ctypes.data, 4, 4, 4) == 1  # aliasing
+    g = ctypes.c_int64()
+    assert _native.lib.gamma2_cylinder(5, 2, ctypes.byref(g)) == 1
+    assert _native.lib.gamma2_cylinder(13, 5, ctypes.byref(g)) == 1
+    r = _native._PeriodicResult()
+    assert _native.lib.minplus_power_until_periodic(a.ctypes.data, 4, 1, ctypes.byref(r)) == 1
+    assert _native.lib.minplus_power_until_periodic(a.ctypes.data, 4, 257, ctypes.byref(r)) == 1
+
+
+def test_no_gpu_reports_cuda_error():
+    """Without an sm_100 device the computing calls fail loudly (no CPU fallback)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(mp.MinplusError) as e:
+        mp.minplus_mul(np.zeros((2, 2)), np.zeros((2, 2)))
+    assert e.value.status == 5
