@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -25,6 +26,7 @@ using namespace mp;
 namespace {
 
 std::recursive_mutex g_mu;
+constexpr double kDefaultRingBytes = 48.0 * 1024 * 1024 * 1024; // power-store cap unless set
 thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
 std::atomic<int64_t> g_h2d{0}, g_d2h{0};
@@ -120,12 +122,27 @@ struct DBuf {
     template <class T> T *as() const { return reinterpret_cast<T *>(p); }
 };
 
-// Per-device state: a library stream and scratch for minplus_mul(_device).
+// Workspace of the power driver, kept across calls (like a BLAS workspace) so repeated runs
+// do not pay cudaMalloc/cudaFree; released by mp_shutdown().
+struct PowerRun {
+    int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
+    DBuf at2, x1, tmp0, tmp1, ktp, kti, stats, flag;
+    std::vector<DBuf> ring;
+    std::vector<int> slot_power;
+    size_t cached_slot = 0; // slot size the cached buffers were allocated for
+    bool sparse = false;
+    double issued_per_product = 0.0;
+    size_t slot_bytes() const { return (size_t)Np * ld * 2; }
+};
+
+// Per-device state: a library stream, scratch for minplus_mul(_device), the power workspace.
 struct DevState {
     cudaStream_t stream = nullptr;      // the library's own non-blocking stream
     cudaStream_t user_stream = nullptr; // mp_set_stream override for power runs
     DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c;
+    std::unique_ptr<PowerRun> pr;
 };
+std::map<int64_t, uint64_t> g_unit_cache; // S(N)
 std::map<int, DevState> g_dev;
 
 mp_status current_device(int *dev_out, DevState **st)
@@ -196,19 +213,10 @@ mp_status mul_device_impl(DevState &st, const uint16_t *dA, int64_t lda, const u
 // ---------------------------------------------------------------------------------------
 // Power / periodicity driver (a3-a5)
 // ---------------------------------------------------------------------------------------
-struct PowerRun {
-    int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
-    DBuf at2, x1, tmp0, tmp1, ktp, kti, stats, flag;
-    std::vector<DBuf> ring;
-    std::vector<int> slot_power;
-    bool sparse = false;
-    double issued_per_product = 0.0;
-    size_t slot_bytes() const { return (size_t)Np * ld * 2; }
-};
 
 mp_status allreduce(int op, int64_t *dev, int64_t count, cudaStream_t s)
 {
-    if (g_dist.world <= 1 || !g_dist.fn) return MP_OK;
+    if (!g_dist.fn) return MP_OK; // a registered callback runs even for world == 1
     CUDA_TRY(cudaStreamSynchronize(s));
     if (g_dist.fn(g_dist.ctx, op, dev, count, (void *)s) != 0)
         return fail(MP_ERR_COMM, "all-reduce callback failed (op %d, %lld values)", op, (long long)count);
@@ -302,7 +310,8 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     CUDA_TRY(cudaEventCreate(&ev_all1));
     CUDA_TRY(cudaEventRecord(ev_all0, s));
 
-    PowerRun R;
+    if (!st->pr) st->pr.reset(new PowerRun());
+    PowerRun &R = *st->pr;
     R.N = N;
     R.Np = pad_rows(N);
     {
@@ -316,10 +325,17 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.w = N;
     }
     R.ld = pad_cols(R.w);
+    if (R.slot_bytes() != R.cached_slot) {
+        R.ring.clear();
+        R.tmp0.release();
+        R.tmp1.release();
+        R.x1.release();
+        R.cached_slot = R.slot_bytes();
+    }
 
     // a2: stage A as AT2 (transposed, duplicated, device encoding) and X1 = A[:, shard].
-    TRY(R.at2.alloc((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
-    TRY(R.x1.alloc(R.slot_bytes(), "power A^1"));
+    TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
+    TRY(R.x1.ensure(R.slot_bytes(), "power A^1"));
     if (src.dev) {
         DBuf flag;
         TRY(flag.alloc(16, "range flag"));
@@ -354,38 +370,54 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     if (R.sparse) TRY(build_tile_lists(R, s));
     else R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
 
-    // power store: a ring of device slots sized to the budget
+    // power store: a ring of device slots (allocated on first use, kept across calls)
     {
         size_t freeb = 0, totalb = 0;
         CUDA_TRY(cudaMemGetInfo(&freeb, &totalb));
-        int64_t budget = g_opts.budget > 0 ? g_opts.budget : (int64_t)(0.90 * (double)freeb);
-        int64_t slots = budget / (int64_t)R.slot_bytes() - 2; // keep room for 2 recompute buffers
+        size_t cached = 0;
+        for (auto &b : R.ring) cached += b.bytes;
+        const double avail = 0.90 * (double)(freeb + cached) - 2.0 * (double)R.slot_bytes(); // 2 recompute buffers
+        int64_t budget = g_opts.budget > 0 ? g_opts.budget
+                                           : (int64_t)std::min(avail, (double)kDefaultRingBytes);
+        int64_t slots = budget / (int64_t)R.slot_bytes();
         slots = std::min<int64_t>(slots, std::max(max_k, 2));
+        if (g_opts.budget > 0) slots -= 2;
         if (slots < 2)
             return fail(MP_ERR_RESOURCE, "power store needs at least 2 slots of %zu bytes (budget %lld bytes)",
                         R.slot_bytes(), (long long)budget);
         R.ring.resize((size_t)slots);
         R.slot_power.assign((size_t)slots, 0);
-        for (auto &b : R.ring) TRY(b.alloc(R.slot_bytes(), "power store slot"));
     }
-    TRY(R.stats.alloc((size_t)(max_k + 1) * 4 * 8, "per-power statistics"));
-    TRY(R.flag.alloc(16, "compare flag"));
+    TRY(R.stats.ensure((size_t)(max_k + 1) * 4 * 8, "per-power statistics"));
+    TRY(R.flag.ensure(16, "compare flag"));
+    {
+        std::vector<int64_t> init((size_t)(max_k + 1) * 4);
+        for (size_t q = 0; q < init.size(); q += 4) {
+            init[q] = 0;
+            init[q + 1] = 0;
+            init[q + 2] = 0xFFFF;
+            init[q + 3] = INT64_MAX;
+        }
+        COPY(R.stats.p, init.data(), init.size() * 8, cudaMemcpyHostToDevice, s);
+    }
 
     std::vector<mp_power_stats> hs((size_t)max_k + 1);
     uint64_t S = 0;
-    {
+    if (g_unit_cache.count(N)) {
+        S = g_unit_cache[N];
+    } else {
         unsigned long long *dS = reinterpret_cast<unsigned long long *>(R.flag.p);
         CUDA_TRY(cudaMemsetAsync(dS, 0, 8, s));
         LAUNCH(launch_unit_sum(N, dS, s));
         COPY(&S, dS, 8, cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));
+        g_unit_cache[N] = S;
     }
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     double prod_ms = 0.0;
     int64_t launches = 0;
-    const int64_t init[4] = {0, 0, 0xFFFF, INT64_MAX};
 
     mp_periodic_result res;
     std::memset(&res, 0, sizeof(res));
@@ -396,6 +428,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         const uint16_t *cur = R.x1.as<uint16_t>();
         if (k >= 2) {
             const size_t q = (size_t)(k % (int)R.ring.size());
+            TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
             uint16_t *dst = R.ring[q].as<uint16_t>();
             R.slot_power[q] = k;
             CUDA_TRY(cudaEventRecord(e0, s));
@@ -405,7 +438,6 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             cur = dst;
         }
         int64_t *sk = R.stats.as<int64_t>() + 4 * k;
-        COPY(sk, init, sizeof(init), cudaMemcpyHostToDevice, s);
         LAUNCH(launch_stats(cur, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(sk), s));
         TRY(allreduce(0, sk, 2, s));     // SUM: fingerprint, inf count
         TRY(allreduce(1, sk + 2, 2, s)); // MIN: diagonal minimum, first finite entry
@@ -717,6 +749,7 @@ void mp_shutdown(void)
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(kv.first);
+        kv.second.pr.reset();
         if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
         kv.second.stream = nullptr;
         cudaSetDevice(cur);
