@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--n", type=int, default=12, help="path order (12 = the paper's largest case)")
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--dense", action="store_true", help="disable block-sparse skipping of all-inf A tiles")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "dense", "tiles", "spmm"],
+                    help="product kernel (all exact): dense tiles, block-sparse tiles, grouped SpMM")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -172,7 +173,7 @@ def run_mine(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         mp.dist_set_torch()
-    mp.set_options(block_sparse=not args.dense)
+    mp.set_options(args.kernel)
     stream = torch.cuda.current_stream()
     mp.set_stream(stream)
 
@@ -264,7 +265,7 @@ def run_mine(args):
         "data": "synthetic: deterministic transfer matrix A(D_n) built on the host (no randomness, no datasets)",
         "config": {"workload": f"P_{args.n} x C_m: power-until-periodic run of A(D_{args.n}), N={N}, gamma_2 read-off",
                    "n": args.n, "N": N, "products_per_step": products, "mu_lambda_b": [res.mu, res.lam, res.offset],
-                   "gamma2_m1000": res.gamma2(1000), "block_sparse": not args.dense,
+                   "gamma2_m1000": res.gamma2(1000), "kernel": args.kernel,
                    "parallelism": f"column shards x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (each power 2*N^2 = %.2f GB > 126 MB)" % (2 * N * N / 1e9),
                    "ops": "dense-equivalent N^3 per product (one op = add+min on one u16 lane)"},

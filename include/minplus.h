@@ -231,10 +231,13 @@ mp_status mp_last_profile(mp_profile *out);
  * non-blocking stream.  Errors: MP_ERR_CUDA if no device. */
 mp_status mp_set_stream(void *stream);
 
-/* Tuning knobs (process-wide; defaults in DESIGN.md).  block_sparse: skip all-inf
- * A tiles (exact; NEXT-1).  device_budget_bytes: cap for the power store (0 = 90% of the
- * free device memory at call time). */
-mp_status mp_set_options(int block_sparse, int64_t device_budget_bytes);
+/* Tuning knobs (process-wide; defaults in DESIGN.md).  sparsity selects the product kernel
+ * of the power runs: 0 = dense 128x256x32 tiles over all of A; 1 = the same kernel skipping
+ * the all-inf tiles of A; 2 = the grouped (8-row) SpMM kernel over A's finite entries;
+ * -1 = automatic (the default: SpMM when it issues fewer than 60 % of the tile kernel's
+ * steps).  All are exact (an all-inf term never lowers a minimum).  device_budget_bytes caps
+ * the power store (0 = min(48 GiB, 90 % of free device memory)).  Errors: MP_ERR_DOMAIN. */
+mp_status mp_set_options(int sparsity, int64_t device_budget_bytes);
 
 #ifdef __cplusplus
 }

@@ -307,8 +307,12 @@ def last_profile() -> dict:
             "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes}
 
 
-def set_options(block_sparse: bool = True, device_budget_bytes: int = 0) -> None:
-    _check(lib.mp_set_options(1 if block_sparse else 0, device_budget_bytes))
+SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}
+
+
+def set_options(sparsity: str = "auto", device_budget_bytes: int = 0) -> None:
+    """Product kernel of the power runs: "auto" | "dense" | "tiles" | "spmm" (all exact)."""
+    _check(lib.mp_set_options(SPARSITY[sparsity], device_budget_bytes))
 
 
 def version() -> str:

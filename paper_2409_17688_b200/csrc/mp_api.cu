@@ -26,6 +26,7 @@ using namespace mp;
 namespace {
 
 std::recursive_mutex g_mu;
+constexpr double kSpmmAdvantage = 0.6; // auto: SpMM if it issues < 60% of the tile kernel's steps
 constexpr double kDefaultRingBytes = 48.0 * 1024 * 1024 * 1024; // power-store cap unless set
 thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
@@ -38,7 +39,7 @@ struct Dist {
 } g_dist;
 
 struct Opts {
-    int block_sparse = 1;
+    int sparsity = -1; // -1 auto, 0 dense tiles, 1 block-sparse tiles, 2 grouped SpMM
     int64_t budget = 0;
 } g_opts;
 
@@ -130,8 +131,12 @@ struct PowerRun {
     std::vector<DBuf> ring;
     std::vector<int> slot_power;
     size_t cached_slot = 0; // slot size the cached buffers were allocated for
-    bool sparse = false;
+    bool sparse = false;  // tile kernel with l-tile lists
+    bool spmm = false;    // grouped SpMM kernel
     double issued_per_product = 0.0;
+    double issued_tiles = 0.0, issued_spmm = 0.0;
+    // grouped sparse form of A (k_spmm8)
+    DBuf sp_m8, sp_tcnt, sp_tptr, sp_L, sp_posmap, sp_gcnt, sp_eptr, sp_epos, sp_ea;
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
 
@@ -246,12 +251,53 @@ mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
     COPY(R.ktp.p, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice, s);
     COPY(R.kti.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s);
     CUDA_TRY(cudaStreamSynchronize(s));
-    R.issued_per_product = (double)ptr[(size_t)Mt] * kBK * kBM * (double)R.ld;
+    R.issued_tiles = (double)ptr[(size_t)Mt] * kBK * kBM * (double)R.ld;
+    return MP_OK;
+}
+
+// Grouped sparse form of A (k_spmm8): group masks, per-tile union lists, group entries.
+mp_status build_sparse(PowerRun &R, cudaStream_t s)
+{
+    const int64_t Np = R.Np, G = Np / 8, Mt = Np / 128;
+    TRY(R.sp_m8.ensure((size_t)(G * Np), "group masks"));
+    TRY(R.sp_tcnt.ensure((size_t)Mt * 4, "tile counts"));
+    TRY(R.sp_tptr.ensure((size_t)(Mt + 1) * 8, "tile offsets"));
+    TRY(R.sp_posmap.ensure((size_t)(Mt * Np) * 4, "union positions"));
+    TRY(R.sp_gcnt.ensure((size_t)G * 4, "group counts"));
+    TRY(R.sp_eptr.ensure((size_t)(G + 1) * 8, "group offsets"));
+    LAUNCH(sparse_masks(R.at2.as<uint32_t>(), Np, R.sp_m8.as<uint8_t>(), s));
+    LAUNCH(sparse_tile_union(R.sp_m8.as<uint8_t>(), Np, nullptr, R.sp_tcnt.as<int32_t>(), nullptr, nullptr, s));
+    LAUNCH(scan_counts(R.sp_tcnt.as<int32_t>(), Mt, R.sp_tptr.as<int64_t>(), s));
+    LAUNCH(sparse_group_entries(R.sp_m8.as<uint8_t>(), nullptr, Np, nullptr, nullptr, R.sp_gcnt.as<int32_t>(),
+                                nullptr, nullptr, s));
+    LAUNCH(scan_counts(R.sp_gcnt.as<int32_t>(), G, R.sp_eptr.as<int64_t>(), s));
+    int64_t totals[2] = {0, 0};
+    COPY(&totals[0], R.sp_tptr.as<int64_t>() + Mt, 8, cudaMemcpyDeviceToHost, s);
+    COPY(&totals[1], R.sp_eptr.as<int64_t>() + G, 8, cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    TRY(R.sp_L.ensure((size_t)std::max<int64_t>(totals[0], 1) * 4, "union lists"));
+    TRY(R.sp_epos.ensure((size_t)std::max<int64_t>(totals[1], 1) * 4, "entry positions"));
+    TRY(R.sp_ea.ensure((size_t)std::max<int64_t>(totals[1], 1) * 32, "entry values"));
+    LAUNCH(sparse_tile_union(R.sp_m8.as<uint8_t>(), Np, R.sp_tptr.as<int64_t>(), nullptr, R.sp_L.as<int32_t>(),
+                             R.sp_posmap.as<int32_t>(), s));
+    LAUNCH(sparse_group_entries(R.sp_m8.as<uint8_t>(), R.at2.as<uint32_t>(), Np, R.sp_eptr.as<int64_t>(),
+                                R.sp_posmap.as<int32_t>(), nullptr, R.sp_epos.as<int32_t>(), R.sp_ea.as<uint4>(), s));
+    R.issued_spmm = (double)totals[1] * 8.0 * (double)R.ld;
     return MP_OK;
 }
 
 mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
 {
+    if (R.spmm) {
+        SparseA sa;
+        sa.L = R.sp_L.as<int32_t>();
+        sa.tptr = R.sp_tptr.as<int64_t>();
+        sa.epos = R.sp_epos.as<int32_t>();
+        sa.ea = R.sp_ea.as<uint4>();
+        sa.eptr = R.sp_eptr.as<int64_t>();
+        LAUNCH(launch_spmm(sa, X, R.ld, C, R.ld, R.Np, R.ld, s));
+        return MP_OK;
+    }
     LAUNCH(launch_minplus(R.at2.as<uint32_t>(), R.Np, X, R.ld, C, R.ld, R.Np, R.ld, R.Np,
                           R.sparse ? R.ktp.as<int32_t>() : nullptr, R.sparse ? R.kti.as<int32_t>() : nullptr, s));
     return MP_OK;
@@ -366,9 +412,22 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     }
     LAUNCH(launch_x1_from_at2(R.at2.as<uint32_t>(), R.Np, R.c0, R.w, R.x1.as<uint16_t>(), R.ld, s));
 
-    R.sparse = g_opts.block_sparse != 0;
-    if (R.sparse) TRY(build_tile_lists(R, s));
-    else R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
+    // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
+    R.sparse = R.spmm = false;
+    if (g_opts.sparsity != 0) TRY(build_tile_lists(R, s));
+    if (g_opts.sparsity == 2 || g_opts.sparsity < 0) TRY(build_sparse(R, s));
+    if (g_opts.sparsity == 0) {
+        R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
+    } else if (g_opts.sparsity == 1) {
+        R.sparse = true;
+        R.issued_per_product = R.issued_tiles;
+    } else if (g_opts.sparsity == 2 || R.issued_spmm < kSpmmAdvantage * R.issued_tiles) {
+        R.spmm = true;
+        R.issued_per_product = R.issued_spmm;
+    } else {
+        R.sparse = true;
+        R.issued_per_product = R.issued_tiles;
+    }
 
     // power store: a ring of device slots (allocated on first use, kept across calls)
     {
@@ -759,7 +818,8 @@ void mp_shutdown(void)
 
 const char *mp_version(void)
 {
-    return "minplus-b200 0.1 sm_100a: DPX VIADDMNMX.U16x2 128x256x32 tile, 4-stage cp.async, block-sparse A";
+    return "minplus-b200 0.2 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse) and "
+           "grouped (8-row) SpMM kernel, 4-stage cp.async";
 }
 
 int64_t mp_kernel_launches(void) { return g_launches.load(); }
@@ -781,11 +841,12 @@ mp_status mp_set_stream(void *stream)
     return MP_OK;
 }
 
-mp_status mp_set_options(int block_sparse, int64_t device_budget_bytes)
+mp_status mp_set_options(int sparsity, int64_t device_budget_bytes)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (device_budget_bytes < 0) return fail(MP_ERR_DOMAIN, "mp_set_options: negative budget");
-    g_opts.block_sparse = block_sparse;
+    if (sparsity < -1 || sparsity > 2) return fail(MP_ERR_DOMAIN, "mp_set_options: sparsity %d outside [-1, 2]", sparsity);
+    g_opts.sparsity = sparsity;
     g_opts.budget = device_budget_bytes;
     return MP_OK;
 }

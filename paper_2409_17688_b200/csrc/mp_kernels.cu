@@ -392,6 +392,243 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 }
 
 // ---------------------------------------------------------------------------------------
+// a3, sparse form (NEXT-1 ii, exact): grouped (min,+) SpMM.  Rows of A are taken in groups
+// of kG = 8; a group "entry" is an inner index l at which at least one of the 8 rows has a
+// finite A_il, carrying the 8 values {a, a} (+inf for the rows without an arc).  A CTA owns
+// kSpRows = 128 rows (16 groups) x kBN = 256 columns; the union of its groups' l indices,
+// in increasing order, is streamed through shared memory kSpChunk = 32 rows of X at a time
+// (cp.async ring), and each warp applies its two groups' entries that fall in the chunk:
+// per entry one LDS.128 (8 columns of X per lane) and 32 VIADDMNMX.U16x2 (8 rows x 4
+// column pairs).  Issued steps = 8 * entries * ld instead of 128 * 32 * ld per non-empty
+// tile; every skipped term is an all-+inf one, so the result is the same product.
+// ---------------------------------------------------------------------------------------
+constexpr int kG = 8;
+constexpr int kSpRows = 128;
+constexpr int kSpChunk = 32;
+
+// m8[g * Np + l] = bit r set iff A_(8g+r, l) is finite (read through AT2[l][8g+r]).
+__global__ void k_group_masks(const uint32_t *__restrict__ AT2, int64_t Np, uint8_t *__restrict__ m8)
+{
+    const int64_t G = Np / kG;
+    const int64_t total = G * Np;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = t / Np, l = t - g * Np;
+        const uint4 *p = reinterpret_cast<const uint4 *>(AT2 + l * Np + g * kG);
+        const uint4 v0 = p[0], v1 = p[1];
+        const uint32_t v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        unsigned m = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) m |= (v[r] != 0x7FFF7FFFu) ? (1u << r) : 0u;
+        m8[t] = (uint8_t)m;
+    }
+}
+
+// Block-ordered compaction helper: for flags f over [0, n) in increasing index order, calls
+// emit(index, rank) for each set flag; returns the count.  One block, blockDim.x % 32 == 0.
+template <class FlagF, class EmitF>
+__device__ int64_t block_compact(int64_t n, FlagF flag, EmitF emit)
+{
+    __shared__ int warp_tot[32];
+    __shared__ int64_t base_sh;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) base_sh = 0;
+    __syncthreads();
+    for (int64_t start = 0; start < n; start += blockDim.x) {
+        const int64_t i = start + threadIdx.x;
+        const bool f = (i < n) && flag(i);
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, f);
+        if (lane == 0) warp_tot[warp] = __popc(b);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) before += warp_tot[w];
+            total += warp_tot[w];
+        }
+        const int64_t base = base_sh;
+        if (f) emit(i, base + before + __popc(b & ((1u << lane) - 1u)));
+        __syncthreads();
+        if (threadIdx.x == 0) base_sh = base + total;
+        __syncthreads();
+    }
+    return base_sh;
+}
+
+// Per 128-row tile t: the union U_t of its 16 groups' l (count pass when out == nullptr).
+__global__ void k_tile_union(const uint8_t *__restrict__ m8, int64_t Np, const int64_t *__restrict__ tptr,
+                             int32_t *__restrict__ tcnt, int32_t *__restrict__ L, int32_t *__restrict__ posmap)
+{
+    const int64_t t = blockIdx.x;
+    const uint8_t *m = m8 + t * (kSpRows / kG) * Np;
+    auto flag = [&](int64_t l) {
+        unsigned any = 0;
+#pragma unroll
+        for (int j = 0; j < kSpRows / kG; ++j) any |= m[j * Np + l];
+        return any != 0;
+    };
+    if (!L) {
+        const int64_t c = block_compact(Np, flag, [](int64_t, int64_t) {});
+        if (threadIdx.x == 0) tcnt[t] = (int32_t)c;
+        return;
+    }
+    int32_t *Lt = L + tptr[t];
+    int32_t *pm = posmap + t * Np;
+    block_compact(Np, flag, [&](int64_t l, int64_t rank) {
+        Lt[rank] = (int32_t)l;
+        pm[l] = (int32_t)rank;
+    });
+}
+
+// Per group g: its entries in increasing l (count pass when epos == nullptr).
+__global__ void k_group_entries(const uint8_t *__restrict__ m8, const uint32_t *__restrict__ AT2, int64_t Np,
+                                const int64_t *__restrict__ eptr, const int32_t *__restrict__ posmap,
+                                int32_t *__restrict__ gcnt, int32_t *__restrict__ epos, uint4 *__restrict__ ea)
+{
+    const int64_t g = blockIdx.x;
+    const uint8_t *m = m8 + g * Np;
+    auto flag = [&](int64_t l) { return m[l] != 0; };
+    if (!epos) {
+        const int64_t c = block_compact(Np, flag, [](int64_t, int64_t) {});
+        if (threadIdx.x == 0) gcnt[g] = (int32_t)c;
+        return;
+    }
+    const int64_t e0 = eptr[g];
+    const int32_t *pm = posmap + (g / (kSpRows / kG)) * Np;
+    block_compact(Np, flag, [&](int64_t l, int64_t rank) {
+        const int64_t e = e0 + rank;
+        epos[e] = pm[l];
+        const uint4 *p = reinterpret_cast<const uint4 *>(AT2 + l * Np + g * kG);
+        ea[2 * e] = p[0];
+        ea[2 * e + 1] = p[1];
+    });
+}
+
+// Exclusive scan of n int32 counts into int64 offsets (out[n] = total); one block.
+__global__ void k_scan_counts(const int32_t *__restrict__ cnt, int64_t n, int64_t *__restrict__ out)
+{
+    __shared__ int64_t carry;
+    __shared__ int64_t wsum[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t start = 0; start < n; start += blockDim.x) {
+        const int64_t i = start + threadIdx.x;
+        int64_t v = (i < n) ? cnt[i] : 0, x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        int64_t before = 0, total = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) before += wsum[w];
+            total += wsum[w];
+        }
+        const int64_t c = carry;
+        if (i < n) out[i] = c + before + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_spmm8(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int32_t *__restrict__ epos,
+            const uint4 *__restrict__ ea, const int64_t *__restrict__ eptr, const uint16_t *__restrict__ X,
+            int64_t ldx, uint16_t *__restrict__ C, int64_t ldc)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int STAGE = kSpChunk * kBN * 2; // 16 KB
+    const int by = blockIdx.y, bx = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int32_t *Lt = L + tptr[by];
+    const int U = (int)(tptr[by + 1] - tptr[by]);
+    const int nch = (U + kSpChunk - 1) / kSpChunk;
+    const int64_t col0 = (int64_t)bx * kBN;
+    const uint32_t sbase = smem_addr(smem);
+
+    auto load_stage = [&](int stage, int c) {
+        const uint32_t sX = sbase + stage * STAGE;
+#pragma unroll
+        for (int q = tid; q < kSpChunk * 32; q += kThreads) {
+            const int r = q >> 5, cc = q & 31;
+            const int u = c * kSpChunk + r;
+            if (u < U) {
+                const int64_t l = __ldg(Lt + u);
+                cp_async16(sX + r * 512 + cc * 16, X + l * ldx + col0 + cc * 8);
+            }
+        }
+    };
+
+    const int g0 = by * (kSpRows / kG) + 2 * warp;
+    int64_t e[2] = {eptr[g0], eptr[g0 + 1]};
+    const int64_t eend[2] = {eptr[g0 + 1], eptr[g0 + 2]};
+
+    uint32_t acc[2][8][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) acc[q][r][p] = 0xFFFFFFFFu;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nch) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int cn = c + STAGES - 1;
+            if (cn < nch) load_stage(cn % STAGES, cn);
+            cp_async_commit();
+        }
+        const uint32_t *Xs = reinterpret_cast<const uint32_t *>(smem + (c % STAGES) * STAGE);
+        const int lim = (c + 1) * kSpChunk;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            int64_t ei = e[q];
+            const int64_t ee = eend[q];
+            while (ei < ee) {
+                const int p = __ldg(epos + ei);
+                if (p >= lim) break;
+                const uint4 x = *reinterpret_cast<const uint4 *>(Xs + (p - c * kSpChunk) * 128 + lane * 4);
+                const uint4 a0 = __ldg(ea + 2 * ei), a1 = __ldg(ea + 2 * ei + 1);
+                const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    acc[q][r][0] = __viaddmin_u16x2(a[r], x.x, acc[q][r][0]);
+                    acc[q][r][1] = __viaddmin_u16x2(a[r], x.y, acc[q][r][1]);
+                    acc[q][r][2] = __viaddmin_u16x2(a[r], x.z, acc[q][r][2]);
+                    acc[q][r][3] = __viaddmin_u16x2(a[r], x.w, acc[q][r][3]);
+                }
+                ++ei;
+            }
+            e[q] = ei;
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t i = (int64_t)by * kSpRows + 16 * warp + 8 * q + r;
+            uint4 v;
+            v.x = __vminu2(acc[q][r][0], 0x7FFF7FFFu);
+            v.y = __vminu2(acc[q][r][1], 0x7FFF7FFFu);
+            v.z = __vminu2(acc[q][r][2], 0x7FFF7FFFu);
+            v.w = __vminu2(acc[q][r][3], 0x7FFF7FFFu);
+            *reinterpret_cast<uint4 *>(C + i * ldc + col0 + lane * 8) = v;
+        }
+}
+
+// ---------------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------------
 static int g_num_sms = 0;
@@ -491,6 +728,49 @@ cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s)
 {
     const uint64_t T = (uint64_t)N * (uint64_t)N;
     k_unit_sum<<<grid_for((int64_t)std::min<uint64_t>(T, 1ull << 40), 256), 256, 0, s>>>(T, out);
+    return cudaGetLastError();
+}
+
+constexpr int kSpStages = 4;
+
+cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
+                        int64_t ncols_p, cudaStream_t s)
+{
+    static bool attr_set = false;
+    const int smem = kSpStages * kSpChunk * kBN * 2;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_spmm8<kSpStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kSpRows));
+    k_spmm8<kSpStages><<<grid, kThreads, smem, s>>>(sa.L, sa.tptr, sa.epos, sa.ea, sa.eptr, X, ldx, C, ldc);
+    return cudaGetLastError();
+}
+
+cudaError_t sparse_masks(const uint32_t *AT2, int64_t Np, uint8_t *m8, cudaStream_t s)
+{
+    k_group_masks<<<grid_for((Np / kG) * Np, 256), 256, 0, s>>>(AT2, Np, m8);
+    return cudaGetLastError();
+}
+
+cudaError_t sparse_tile_union(const uint8_t *m8, int64_t Np, const int64_t *tptr, int32_t *tcnt, int32_t *L,
+                              int32_t *posmap, cudaStream_t s)
+{
+    k_tile_union<<<(unsigned)(Np / kSpRows), 1024, 0, s>>>(m8, Np, tptr, tcnt, L, posmap);
+    return cudaGetLastError();
+}
+
+cudaError_t sparse_group_entries(const uint8_t *m8, const uint32_t *AT2, int64_t Np, const int64_t *eptr,
+                                 const int32_t *posmap, int32_t *gcnt, int32_t *epos, uint4 *ea, cudaStream_t s)
+{
+    k_group_entries<<<(unsigned)(Np / kG), 256, 0, s>>>(m8, AT2, Np, eptr, posmap, gcnt, epos, ea);
+    return cudaGetLastError();
+}
+
+cudaError_t scan_counts(const int32_t *cnt, int64_t n, int64_t *out, cudaStream_t s)
+{
+    k_scan_counts<<<1, 1024, 0, s>>>(cnt, n, out);
     return cudaGetLastError();
 }
 

@@ -23,7 +23,7 @@ def mp():
         pytest.skip("needs a GPU")
     torch.cuda.set_device(0)
     import paper_2409_17688_b200 as m
-    m.set_options(block_sparse=True, device_budget_bytes=0)
+    m.set_options("auto", device_budget_bytes=0)
     return m
 
 
@@ -92,12 +92,17 @@ def test_minplus_mul_device_strided(mp, oracle_mod):
 
 
 # ------------------------------------------------------------------- power sequences
+@pytest.mark.parametrize("kernel", ["tiles", "spmm"])
 @pytest.mark.parametrize("n", range(2, 10))
-def test_power_until_periodic_transfer(mp, oracle_mod, n):
+def test_power_until_periodic_transfer(mp, oracle_mod, n, kernel):
     """Every summary of the run equals the oracle's: (mu, lambda, b), k_last, dense_from,
     diag_min[k] and the fingerprint of every power A^k (a whole-matrix check), and Table 5."""
     A = mp.build_transition_matrix(n)
-    g = mp.minplus_power_until_periodic(A)
+    mp.set_options(kernel)
+    try:
+        g = mp.minplus_power_until_periodic(A)
+    finally:
+        mp.set_options("auto")
     o = oracle_mod.power_until_periodic(A)
     assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
     assert g.diag_min == o.diag_min
@@ -106,10 +111,10 @@ def test_power_until_periodic_transfer(mp, oracle_mod, n):
     assert (g.mu, g.lam, g.offset) == row
 
 
-@pytest.mark.parametrize("sparse", [True, False])
+@pytest.mark.parametrize("sparse", ["dense", "tiles", "spmm"])
 def test_power_rows_full_matrices(mp, oracle_mod, sparse):
     """Every entry of every power A^1..A^12 for n = 7 (N = 558, 5 x 3 tiles, ragged)."""
-    mp.set_options(block_sparse=sparse)
+    mp.set_options(sparse)
     try:
         A = mp.build_transition_matrix(7)
         rows = np.arange(A.shape[0])
@@ -120,16 +125,21 @@ def test_power_rows_full_matrices(mp, oracle_mod, sparse):
                 X = oracle_mod.minplus(A, X)
             assert np.array_equal(got[k - 1], X), k
     finally:
-        mp.set_options(block_sparse=True)
+        mp.set_options("auto")
 
 
+@pytest.mark.parametrize("kernel", ["dense", "tiles", "spmm", "auto"])
 @pytest.mark.parametrize("seed", range(4))
-def test_power_until_periodic_random(mp, oracle_mod, seed):
+def test_power_until_periodic_random(mp, oracle_mod, seed, kernel):
     """Random sparse matrices (the +inf pattern persists for several powers, exercising the
-    exact-compare path with +inf entries) and the degenerate cases."""
+    exact-compare path with +inf entries), with each product kernel."""
     N = [37, 130, 257, 300][seed]
     A = synth.transfer_like(N, N, [0.9, 0.95, 0.97, 0.5][seed], salt=100 + seed)
-    g = mp.minplus_power_until_periodic(A, max_k=64)
+    mp.set_options(kernel)
+    try:
+        g = mp.minplus_power_until_periodic(A, max_k=64)
+    finally:
+        mp.set_options("auto")
     o = oracle_mod.power_until_periodic(A, max_k=64)
     assert o.rc == 0
     assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
@@ -156,11 +166,11 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     lambda = 18, so the partner of the first repeat is long gone from the ring)."""
     A = mp.build_transition_matrix(7)
     slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 255) // 256) * 256) * 2
-    mp.set_options(block_sparse=True, device_budget_bytes=5 * slot)
+    mp.set_options("auto", device_budget_bytes=5 * slot)
     try:
         g = mp.minplus_power_until_periodic(A)
     finally:
-        mp.set_options(block_sparse=True, device_budget_bytes=0)
+        mp.set_options("auto", device_budget_bytes=0)
     assert (g.mu, g.lam, g.offset) == (23, 18, 53)
 
 
