@@ -151,6 +151,20 @@ mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out);
 /* Read-off only (host, no device): applies the a6 rule to a result. */
 mp_status mp_gamma2_readoff(const mp_periodic_result *r, int64_t m, int64_t *gamma2_out);
 
+/* The closed formula of P:496-502 (NEXT-2): gamma_2(P_n x C_m) = ceil(b*m/a) + alpha[m mod a]
+ * for m >= n0 (a = lambda, b = offset, n0 = mu; Theorem 3 solved with the boundary values
+ * diag_min[n0 .. n0+a-1], Algorithm 5), plus the cycle lengths 3 <= m < n0 where the formula
+ * does not hold ("exceptions", Table 7's starred rows).  Host only.
+ * Errors: MP_ERR_DOMAIN (NULL, invalid result, a > MP_MAX_K). */
+typedef struct {
+    int32_t a, b, n0;
+    int32_t alpha[MP_MAX_K];        /* alpha[k], 0 <= k < a                                   */
+    int32_t n_exceptions;
+    int64_t exception_m[MP_MAX_K];  /* cycle lengths with gamma_2 != the formula, ascending   */
+    int64_t exception_gamma2[MP_MAX_K];
+} mp_formula;
+mp_status mp_gamma2_formula(const mp_periodic_result *r, mp_formula *out);
+
 /* ----------------------------------------------------------------------------------------
  * Multi-GPU: one process per GPU (torchrun), column shards, a tiny all-reduce per power
  * ------------------------------------------------------------------------------------- */

@@ -30,7 +30,7 @@ EXPORTS = [
     "gamma2_cylinder",
     "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
-    "mp_last_profile", "mp_set_options",
+    "mp_last_profile", "mp_set_options", "mp_gamma2_formula",
 ]
 
 
@@ -51,6 +51,12 @@ class _PeriodicResult(ctypes.Structure):
 class PowerStats(ctypes.Structure):
     _fields_ = [("fingerprint", ctypes.c_int64), ("inf_count", ctypes.c_int64),
                 ("diag_min", ctypes.c_int64), ("ref", ctypes.c_int64)]
+
+
+class _Formula(ctypes.Structure):
+    _fields_ = [("a", ctypes.c_int32), ("b", ctypes.c_int32), ("n0", ctypes.c_int32),
+                ("alpha", ctypes.c_int32 * MP_MAX_K), ("n_exceptions", ctypes.c_int32),
+                ("exception_m", ctypes.c_int64 * MP_MAX_K), ("exception_gamma2", ctypes.c_int64 * MP_MAX_K)]
 
 
 class _Profile(ctypes.Structure):
@@ -92,6 +98,7 @@ def _load() -> ctypes.CDLL:
         "mp_kernel_launches": ([], i64),
         "mp_last_profile": ([P], i32),
         "mp_set_options": ([i32, i64], i32),
+        "mp_gamma2_formula": ([P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -177,6 +184,14 @@ class PeriodicResult:
         g = ctypes.c_int64(0)
         _check(lib.mp_gamma2_readoff(ctypes.byref(self._raw), m, ctypes.byref(g)))
         return g.value
+
+    def formula(self) -> dict:
+        """Closed formula gamma_2 = ceil(b m / a) + alpha[m mod a] for m >= n0, with the
+        exceptions below n0 (Table 7)."""
+        f = _Formula()
+        _check(lib.mp_gamma2_formula(ctypes.byref(self._raw), ctypes.byref(f)))
+        return {"a": f.a, "b": f.b, "n0": f.n0, "alpha": [f.alpha[k] for k in range(f.a)],
+                "exceptions": {int(f.exception_m[i]): int(f.exception_gamma2[i]) for i in range(f.n_exceptions)}}
 
 
 def _result(r: _PeriodicResult) -> PeriodicResult:

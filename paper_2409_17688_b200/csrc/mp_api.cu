@@ -717,6 +717,37 @@ mp_status mp_gamma2_readoff(const mp_periodic_result *r, int64_t m, int64_t *g)
     return MP_OK;
 }
 
+mp_status mp_gamma2_formula(const mp_periodic_result *r, mp_formula *out)
+{
+    if (!r || !out || r->lambda <= 0 || r->lambda > MP_MAX_K || r->mu < 1 || r->k_last != r->mu + r->lambda)
+        return fail(MP_ERR_DOMAIN, "mp_gamma2_formula: NULL or invalid periodic result");
+    mp_formula f;
+    std::memset(&f, 0, sizeof(f));
+    f.a = r->lambda;
+    f.b = r->offset;
+    f.n0 = r->mu;
+    auto ceil_div = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+    // boundary values gamma_2(m), n0 <= m < n0 + a (Algorithm 5) fix alpha per residue
+    for (int64_t m = r->mu; m < r->mu + r->lambda; ++m) {
+        if (m < 3) continue; // gamma_2 undefined below 3 (G17): use m + a instead
+        f.alpha[m % f.a] = (int32_t)(r->diag_min[m] - ceil_div((int64_t)f.b * m, f.a));
+    }
+    for (int64_t m = r->mu; m < 3; ++m) { // n0 < 3: take the residue from m + a (Lemma 1)
+        const int64_t mm = m + f.a;
+        f.alpha[m % f.a] = (int32_t)(r->diag_min[mm] - ceil_div((int64_t)f.b * mm, f.a));
+    }
+    for (int64_t m = 3; m < r->mu && f.n_exceptions < MP_MAX_K; ++m) {
+        const int64_t formula = ceil_div((int64_t)f.b * m, f.a) + f.alpha[m % f.a];
+        if ((int64_t)r->diag_min[m] != formula) {
+            f.exception_m[f.n_exceptions] = m;
+            f.exception_gamma2[f.n_exceptions] = r->diag_min[m];
+            ++f.n_exceptions;
+        }
+    }
+    *out = f;
+    return MP_OK;
+}
+
 mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);

@@ -155,3 +155,32 @@ def test_no_gpu_reports_cuda_error():
     with pytest.raises(mp.MinplusError) as e:
         mp.minplus_mul(np.zeros((2, 2)), np.zeros((2, 2)))
     assert e.value.status == 5
+
+
+def test_gamma2_formula_reproduces_table7(oracle_mod):
+    """NEXT-2: the closed formula built from the run (alpha from the boundary values,
+    exceptions below n0) reproduces Table 7 and its exception rows (G14, G15)."""
+    from conftest import golden
+    rows = golden("table7_alpha.txt")
+    exc = {(int(x[1]), int(x[2])): int(x[3]) for x in rows if x[0] == "exc"}
+    for x in rows:
+        if x[0] == "exc":
+            continue
+        n, a = int(x[0]), int(x[1])
+        if n > 9:
+            continue
+        ks = set() if x[2] == "-" else set(map(int, x[2].split(",")))
+        mmin = int(x[3])
+        o = oracle_mod.power_until_periodic(oracle_mod.transition_matrix(n))
+        r = _native._PeriodicResult()
+        r.mu, r.lambda_, r.offset, r.k_last, r.dense_from = o.mu, o.lam, o.offset, o.k_last, o.dense_from
+        for k, v in enumerate(o.diag_min):
+            r.diag_min[k] = v
+        f = _native._result(r).formula()
+        assert f["a"] == a
+        assert {k for k in range(a) if f["alpha"][k] == 1} == ks, n
+        assert all(v in (0, 1) for v in f["alpha"])
+        expect_exc = {m: g for (nn, m), g in exc.items() if nn == n}
+        if mmin:  # n = 7: alpha = 1 only from m = 19 on (G14) -> residues 1,2,4,5 below are exceptions
+            expect_exc.update({m: -(-o.offset * m // a) for m in range(3, mmin) if m % a in ks})
+        assert f["exceptions"] == expect_exc, (n, f["exceptions"], expect_exc)

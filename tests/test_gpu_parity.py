@@ -215,3 +215,6 @@ def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
         expect = exc.get((n, m), -(-b * m // a) + (1 if (m % a in ks and m >= mmin) else 0))
         assert g.gamma2(m) == expect, (n, m)
     assert mp.gamma2_cylinder(n, 1000) == {10: 4001, 11: 4334, 12: 4668}[n]
+    f = g.formula()  # NEXT-2: Table 7 row and the exception (G15) from the run itself
+    assert f["a"] == a and {k for k in range(a) if f["alpha"][k] == 1} == ks
+    assert f["exceptions"] == {m: v for (nn, m), v in exc.items() if nn == n}
