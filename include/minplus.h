@@ -32,7 +32,8 @@ extern "C" {
 #define MP_INF 0xFFFFu        /* +inf at the boundary                  */
 #define MP_FINITE_MAX 0x7FFEu /* largest finite input; a finite sum above it is +inf (G6) */
 #define MP_MAX_K 256          /* largest power index a periodic result can describe        */
-#define MP_MAX_N 12           /* largest path order n (n=13 exceeded 32 GB)         */
+#define MP_MAX_N 13           /* largest path order n: 13 is the paper's future work (P:250,
+                                 P:551: 34.6 GB per matrix exceeded its 32 GB GPU)           */
 
 typedef enum {
     MP_OK = 0,
@@ -51,7 +52,7 @@ typedef enum {
  * ------------------------------------------------------------------------------------- */
 
 /* |C_n|, the number of correct n-words (Table 1).  No allocation.
- * Errors: MP_ERR_DOMAIN if n < 2 or n > 13 (n = 13 is countable, not buildable here). */
+ * Errors: MP_ERR_DOMAIN if n < 2 or n > MP_MAX_N. */
 mp_status mp_count_words(int n, int64_t *N_out);
 
 /* A(D_n) by Algorithm 1: rows are the words q, columns the words p, both in

@@ -17,7 +17,7 @@ from . import _build
 MP_INF = 0xFFFF
 MP_FINITE_MAX = 0x7FFE
 MP_MAX_K = 256
-MP_MAX_N = 12
+MP_MAX_N = 13
 
 STATUS = {0: "MP_OK", 1: "MP_ERR_DOMAIN", 2: "MP_ERR_RANGE", 3: "MP_ERR_RESOURCE",
           4: "MP_ERR_NOT_PERIODIC", 5: "MP_ERR_CUDA", 6: "MP_ERR_COMM"}

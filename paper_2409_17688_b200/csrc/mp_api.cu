@@ -127,7 +127,9 @@ struct DBuf {
 // do not pay cudaMalloc/cudaFree; released by mp_shutdown().
 struct PowerRun {
     int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
-    DBuf at2, x1, tmp0, tmp1, ktp, kti, stats, flag;
+    DBuf at2, words, tmp0, tmp1, ktp, kti, stats, flag;
+    bool has_at2 = false; // matrix sources and the tile kernels stage AT2; SpMM on words does not
+    int n_words = 0;      // path order when A comes from the word masks
     std::vector<DBuf> ring;
     std::vector<int> slot_power;
     size_t cached_slot = 0; // slot size the cached buffers were allocated for
@@ -135,8 +137,10 @@ struct PowerRun {
     bool spmm = false;    // grouped SpMM kernel
     double issued_per_product = 0.0;
     double issued_tiles = 0.0, issued_spmm = 0.0;
-    // grouped sparse form of A (k_spmm8)
-    DBuf sp_m8, sp_tcnt, sp_tptr, sp_L, sp_posmap, sp_gcnt, sp_eptr, sp_epos, sp_ea;
+    // grouped sparse form of A (k_spmm): buffers handed out in order by sp_alloc
+    std::vector<DBuf> sp_bufs;
+    size_t sp_next = 0;
+    SparseWork sp;
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
 
@@ -255,34 +259,34 @@ mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
     return MP_OK;
 }
 
-// Grouped sparse form of A (k_spmm8): group masks, per-tile union lists, group entries.
+// Grouped sparse form of A (k_spmm): built on the device from AT2.
+cudaError_t sp_alloc(void **p, size_t bytes, void *ctx)
+{
+    PowerRun *R = static_cast<PowerRun *>(ctx);
+    if (R->sp_next >= R->sp_bufs.size()) R->sp_bufs.resize(R->sp_next + 1);
+    DBuf &b = R->sp_bufs[R->sp_next++];
+    if (b.ensure(bytes, "sparse form of A") != MP_OK) return cudaErrorMemoryAllocation;
+    *p = b.p;
+    return cudaSuccess;
+}
+
 mp_status build_sparse(PowerRun &R, cudaStream_t s)
 {
-    const int64_t Np = R.Np, G = Np / 8, Mt = Np / 128;
-    TRY(R.sp_m8.ensure((size_t)(G * Np), "group masks"));
-    TRY(R.sp_tcnt.ensure((size_t)Mt * 4, "tile counts"));
-    TRY(R.sp_tptr.ensure((size_t)(Mt + 1) * 8, "tile offsets"));
-    TRY(R.sp_posmap.ensure((size_t)(Mt * Np) * 4, "union positions"));
-    TRY(R.sp_gcnt.ensure((size_t)G * 4, "group counts"));
-    TRY(R.sp_eptr.ensure((size_t)(G + 1) * 8, "group offsets"));
-    LAUNCH(sparse_masks(R.at2.as<uint32_t>(), Np, R.sp_m8.as<uint8_t>(), s));
-    LAUNCH(sparse_tile_union(R.sp_m8.as<uint8_t>(), Np, nullptr, R.sp_tcnt.as<int32_t>(), nullptr, nullptr, s));
-    LAUNCH(scan_counts(R.sp_tcnt.as<int32_t>(), Mt, R.sp_tptr.as<int64_t>(), s));
-    LAUNCH(sparse_group_entries(R.sp_m8.as<uint8_t>(), nullptr, Np, nullptr, nullptr, R.sp_gcnt.as<int32_t>(),
-                                nullptr, nullptr, s));
-    LAUNCH(scan_counts(R.sp_gcnt.as<int32_t>(), G, R.sp_eptr.as<int64_t>(), s));
-    int64_t totals[2] = {0, 0};
-    COPY(&totals[0], R.sp_tptr.as<int64_t>() + Mt, 8, cudaMemcpyDeviceToHost, s);
-    COPY(&totals[1], R.sp_eptr.as<int64_t>() + G, 8, cudaMemcpyDeviceToHost, s);
-    CUDA_TRY(cudaStreamSynchronize(s));
-    TRY(R.sp_L.ensure((size_t)std::max<int64_t>(totals[0], 1) * 4, "union lists"));
-    TRY(R.sp_epos.ensure((size_t)std::max<int64_t>(totals[1], 1) * 4, "entry positions"));
-    TRY(R.sp_ea.ensure((size_t)std::max<int64_t>(totals[1], 1) * 32, "entry values"));
-    LAUNCH(sparse_tile_union(R.sp_m8.as<uint8_t>(), Np, R.sp_tptr.as<int64_t>(), nullptr, R.sp_L.as<int32_t>(),
-                             R.sp_posmap.as<int32_t>(), s));
-    LAUNCH(sparse_group_entries(R.sp_m8.as<uint8_t>(), R.at2.as<uint32_t>(), Np, R.sp_eptr.as<int64_t>(),
-                                R.sp_posmap.as<int32_t>(), nullptr, R.sp_epos.as<int32_t>(), R.sp_ea.as<uint4>(), s));
-    R.issued_spmm = (double)totals[1] * 8.0 * (double)R.ld;
+    R.sp_next = 0;
+    R.sp = SparseWork();
+    int64_t launches = 0;
+    const cudaError_t e =
+        R.has_at2 ? build_sparse_form(R.at2.as<uint32_t>(), R.Np, R.sp, s, sp_alloc, &R, &launches)
+                  : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, R.sp, s, sp_alloc, &R,
+                                            &launches);
+    g_launches.fetch_add(launches);
+    g_d2h.fetch_add(24);
+    if (e == cudaErrorMemoryAllocation) return MP_ERR_RESOURCE; // message set by DBuf::alloc
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MP_ERR_CUDA, "building the sparse form of A failed: %s", cudaGetErrorString(e));
+    }
+    R.issued_spmm = (double)R.sp.entries * 8.0 * (double)R.ld;
     return MP_OK;
 }
 
@@ -290,11 +294,11 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
 {
     if (R.spmm) {
         SparseA sa;
-        sa.L = R.sp_L.as<int32_t>();
-        sa.tptr = R.sp_tptr.as<int64_t>();
-        sa.epos = R.sp_epos.as<int32_t>();
-        sa.ea = R.sp_ea.as<uint4>();
-        sa.eptr = R.sp_eptr.as<int64_t>();
+        sa.L = R.sp.L;
+        sa.tptr = R.sp.tptr;
+        sa.tch = R.sp.tch;
+        sa.eoff = R.sp.eoff;
+        sa.E = R.sp.E;
         LAUNCH(launch_spmm(sa, X, R.ld, C, R.ld, R.Np, R.ld, s));
         return MP_OK;
     }
@@ -303,14 +307,20 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
     return MP_OK;
 }
 
-// Returns the device buffer holding power j, recomputing it into tmp buffers if it has been
-// evicted from the ring.
+// X_1 = A[:, c0:c0+w) in the device layout, from AT2 or straight from the word masks.
+mp_status make_power1(PowerRun &R, uint16_t *dst, cudaStream_t s)
+{
+    if (R.has_at2)
+        LAUNCH(launch_x1_from_at2(R.at2.as<uint32_t>(), R.Np, R.c0, R.w, dst, R.ld, s));
+    else
+        LAUNCH(launch_x1_from_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, R.c0, R.w, dst, R.ld, s));
+    return MP_OK;
+}
+
+// Returns the device buffer holding power j, recomputing it into two scratch buffers if it
+// has been evicted from the ring.
 mp_status power_buffer(PowerRun &R, int j, const uint16_t **out, cudaStream_t s)
 {
-    if (j == 1) {
-        *out = R.x1.as<uint16_t>();
-        return MP_OK;
-    }
     for (size_t q = 0; q < R.ring.size(); ++q)
         if (R.slot_power[q] == j) {
             *out = R.ring[q].as<uint16_t>();
@@ -318,7 +328,8 @@ mp_status power_buffer(PowerRun &R, int j, const uint16_t **out, cudaStream_t s)
         }
     TRY(R.tmp0.ensure(R.slot_bytes(), "recompute buffer"));
     TRY(R.tmp1.ensure(R.slot_bytes(), "recompute buffer"));
-    const uint16_t *cur = R.x1.as<uint16_t>();
+    TRY(make_power1(R, R.tmp1.as<uint16_t>(), s));
+    const uint16_t *cur = R.tmp1.as<uint16_t>();
     for (int k = 2; k <= j; ++k) {
         uint16_t *dst = (k & 1) ? R.tmp1.as<uint16_t>() : R.tmp0.as<uint16_t>();
         TRY(product(R, cur, dst, s));
@@ -375,58 +386,67 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.ring.clear();
         R.tmp0.release();
         R.tmp1.release();
-        R.x1.release();
         R.cached_slot = R.slot_bytes();
     }
 
-    // a2: stage A as AT2 (transposed, duplicated, device encoding) and X1 = A[:, shard].
-    TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
-    TRY(R.x1.ensure(R.slot_bytes(), "power A^1"));
-    if (src.dev) {
-        DBuf flag;
-        TRY(flag.alloc(16, "range flag"));
-        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-        LAUNCH(launch_make_at2(src.dev, src.lda, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, flag.as<int>(), s));
-        int hflag = 0;
-        COPY(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
-        CUDA_TRY(cudaStreamSynchronize(s));
-        if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
-    } else if (src.host) {
-        DBuf raw, flag;
-        TRY(raw.alloc((size_t)N * N * 2, "A staging"));
-        TRY(flag.alloc(16, "range flag"));
-        COPY(raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
-        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-        LAUNCH(launch_make_at2(raw.as<uint16_t>(), N, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, flag.as<int>(), s));
-        int hflag = 0;
-        COPY(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
-        CUDA_TRY(cudaStreamSynchronize(s));
-        if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
-    } else {
+    // a2: stage A.  Matrix sources: AT2 (transposed, duplicated, device encoding).  The words
+    // source with the SpMM kernel needs no AT2 at all: the sparse form and every regeneration
+    // of A^1 come straight from the word masks (69 GB saved at n = 13).
+    const bool words_src = !src.dev && !src.host;
+    R.has_at2 = !words_src || g_opts.sparsity == 0 || g_opts.sparsity == 1;
+    R.n_words = words_src ? src.n : 0;
+    if (words_src) {
         std::vector<WordMask> words = enumerate_words(src.n);
-        DBuf dw;
-        TRY(dw.alloc(words.size() * sizeof(WordMask), "word masks"));
-        COPY(dw.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
-        LAUNCH(launch_build_from_words(dw.as<WordMask>(), N, src.n, R.at2.as<uint32_t>(), R.Np, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
+        TRY(R.words.ensure(words.size() * sizeof(WordMask), "word masks"));
+        COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
     }
-    LAUNCH(launch_x1_from_at2(R.at2.as<uint32_t>(), R.Np, R.c0, R.w, R.x1.as<uint16_t>(), R.ld, s));
+    if (R.has_at2) {
+        TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
+        if (src.dev || src.host) {
+            DBuf raw, flag;
+            const uint16_t *dA = src.dev;
+            int64_t lda = src.lda;
+            if (src.host) {
+                TRY(raw.alloc((size_t)N * N * 2, "A staging"));
+                COPY(raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+                dA = raw.as<uint16_t>();
+                lda = N;
+            }
+            TRY(flag.alloc(16, "range flag"));
+            CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+            LAUNCH(launch_make_at2(dA, lda, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, flag.as<int>(), s));
+            int hflag = 0;
+            COPY(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
+        } else {
+            LAUNCH(launch_build_from_words(R.words.as<WordMask>(), N, src.n, R.at2.as<uint32_t>(), R.Np, s));
+        }
+    } else {
+        R.at2.release();
+    }
 
     // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
     R.sparse = R.spmm = false;
-    if (g_opts.sparsity != 0) TRY(build_tile_lists(R, s));
-    if (g_opts.sparsity == 2 || g_opts.sparsity < 0) TRY(build_sparse(R, s));
-    if (g_opts.sparsity == 0) {
-        R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
-    } else if (g_opts.sparsity == 1) {
-        R.sparse = true;
-        R.issued_per_product = R.issued_tiles;
-    } else if (g_opts.sparsity == 2 || R.issued_spmm < kSpmmAdvantage * R.issued_tiles) {
+    if (!R.has_at2) {
+        TRY(build_sparse(R, s));
         R.spmm = true;
         R.issued_per_product = R.issued_spmm;
     } else {
-        R.sparse = true;
-        R.issued_per_product = R.issued_tiles;
+        if (g_opts.sparsity != 0) TRY(build_tile_lists(R, s));
+        if (g_opts.sparsity == 2 || g_opts.sparsity < 0) TRY(build_sparse(R, s));
+        if (g_opts.sparsity == 0) {
+            R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
+        } else if (g_opts.sparsity == 1) {
+            R.sparse = true;
+            R.issued_per_product = R.issued_tiles;
+        } else if (g_opts.sparsity == 2 || R.issued_spmm < kSpmmAdvantage * R.issued_tiles) {
+            R.spmm = true;
+            R.issued_per_product = R.issued_spmm;
+        } else {
+            R.sparse = true;
+            R.issued_per_product = R.issued_tiles;
+        }
     }
 
     // power store: a ring of device slots (allocated on first use, kept across calls)
@@ -435,9 +455,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         CUDA_TRY(cudaMemGetInfo(&freeb, &totalb));
         size_t cached = 0;
         for (auto &b : R.ring) cached += b.bytes;
-        const double avail = 0.90 * (double)(freeb + cached) - 2.0 * (double)R.slot_bytes(); // 2 recompute buffers
-        int64_t budget = g_opts.budget > 0 ? g_opts.budget
-                                           : (int64_t)std::min(avail, (double)kDefaultRingBytes);
+        const double avail = 0.90 * (double)(freeb + cached);
+        const double cap_bytes = std::max((double)kDefaultRingBytes, 4.0 * (double)R.slot_bytes());
+        int64_t budget = g_opts.budget > 0 ? g_opts.budget : (int64_t)std::min(avail, cap_bytes);
         int64_t slots = budget / (int64_t)R.slot_bytes();
         slots = std::min<int64_t>(slots, std::max(max_k, 2));
         if (g_opts.budget > 0) slots -= 2;
@@ -480,21 +500,22 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
 
     mp_periodic_result res;
     std::memset(&res, 0, sizeof(res));
-    const uint16_t *prev = R.x1.as<uint16_t>();
+    const uint16_t *prev = nullptr;
     bool found = false;
     int k = 1;
     for (k = 1; k <= max_k && !found; ++k) {
-        const uint16_t *cur = R.x1.as<uint16_t>();
-        if (k >= 2) {
-            const size_t q = (size_t)(k % (int)R.ring.size());
-            TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
-            uint16_t *dst = R.ring[q].as<uint16_t>();
-            R.slot_power[q] = k;
+        const size_t q = (size_t)(k % (int)R.ring.size());
+        TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
+        uint16_t *dst = R.ring[q].as<uint16_t>();
+        R.slot_power[q] = k;
+        const uint16_t *cur = dst;
+        if (k == 1) {
+            TRY(make_power1(R, dst, s)); // X_1 = A[:, shard]
+        } else {
             CUDA_TRY(cudaEventRecord(e0, s));
             TRY(product(R, prev, dst, s)); // A^k = A (x) A^{k-1}
             CUDA_TRY(cudaEventRecord(e1, s));
             ++launches;
-            cur = dst;
         }
         int64_t *sk = R.stats.as<int64_t>() + 4 * k;
         LAUNCH(launch_stats(cur, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(sk), s));
@@ -580,7 +601,8 @@ extern "C" {
 
 mp_status mp_count_words(int n, int64_t *N_out)
 {
-    if (!N_out || n < 2 || n > 13) return fail(MP_ERR_DOMAIN, "mp_count_words: n = %d outside [2, 13]", n);
+    if (!N_out || n < 2 || n > MP_MAX_N)
+        return fail(MP_ERR_DOMAIN, "mp_count_words: n = %d outside [2, %d]", n, MP_MAX_N);
     *N_out = count_words(n);
     return MP_OK;
 }

@@ -392,29 +392,68 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 }
 
 // ---------------------------------------------------------------------------------------
-// a3, sparse form (NEXT-1 ii, exact): grouped (min,+) SpMM.  Rows of A are taken in groups
-// of kG = 8; a group "entry" is an inner index l at which at least one of the 8 rows has a
-// finite A_il, carrying the 8 values {a, a} (+inf for the rows without an arc).  A CTA owns
-// kSpRows = 128 rows (16 groups) x kBN = 256 columns; the union of its groups' l indices,
-// in increasing order, is streamed through shared memory kSpChunk = 32 rows of X at a time
-// (cp.async ring), and each warp applies its two groups' entries that fall in the chunk:
-// per entry one LDS.128 (8 columns of X per lane) and 32 VIADDMNMX.U16x2 (8 rows x 4
-// column pairs).  Issued steps = 8 * entries * ld instead of 128 * 32 * ld per non-empty
-// tile; every skipped term is an all-+inf one, so the result is the same product.
+// a3, sparse form (NEXT-1 ii, exact): grouped (min,+) SpMM.
+//
+// Rows of A are taken in groups of kG = 8.  A group "entry" is an inner index l at which at
+// least one of its 8 rows has a finite A_il; it carries the 8 values {a, a} (+inf for rows
+// without an arc).  A CTA owns kSpRows = 64 rows (8 groups) x kBN = 256 columns.  The union
+// U_t of its groups' l indices, in increasing order, is cut into chunks of kSpChunk = 16;
+// per chunk the CTA stages the 16 rows X[l, cols] and the chunk's entries (grouped by group)
+// in shared memory with cp.async.  Each of the 2 warps owns 128 columns (2 packed pairs per
+// lane) of ALL 8 groups, so both warps do identical work (no imbalance): per entry one
+// LDS.64 of X, two broadcast LDS.128 of the values and 16 VIADDMNMX.U16x2 (8 rows x 2
+// pairs).  Issued steps = 8 * entries * ld; every skipped term is an all-+inf one, so the
+// result is the same product.
+// Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s, 0, 0, 0} with s = row within the chunk.
 // ---------------------------------------------------------------------------------------
 constexpr int kG = 8;
-constexpr int kSpRows = 128;
-constexpr int kSpChunk = 32;
+constexpr int kSpRows = 64;
+constexpr int kSpGroups = kSpRows / kG;
+constexpr int kSpChunk = 16;
+constexpr int kSpThreads = 64;
 
-// m8[g * Np + l] = bit r set iff A_(8g+r, l) is finite (read through AT2[l][8g+r]).
-__global__ void k_group_masks(const uint32_t *__restrict__ AT2, int64_t Np, uint8_t *__restrict__ m8)
+// How the sparse-form builders read A: the 8 duplicated values of rows 8g..8g+7 at column l.
+struct AccAT2 { // from the staged AT2 (matrix sources)
+    const uint32_t *AT2;
+    int64_t Np;
+    __device__ __forceinline__ void row8(int64_t g, int64_t l, uint4 &v0, uint4 &v1) const
+    {
+        const uint4 *p = reinterpret_cast<const uint4 *>(AT2 + l * Np + g * kG);
+        v0 = p[0];
+        v1 = p[1];
+    }
+};
+struct AccWords { // straight from the word masks (A(D_n) without materialising AT2)
+    const WordMask *w;
+    int64_t N;
+    unsigned full;
+    __device__ __forceinline__ void row8(int64_t g, int64_t l, uint4 &v0, uint4 &v1) const
+    {
+        uint32_t v[8];
+        const bool lok = l < N;
+        WordMask p = {0, 0, 0, 0};
+        if (lok) p = w[l];
+        const uint32_t lab = (uint32_t)p.zeros | ((uint32_t)p.zeros << 16);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t i = g * kG + r;
+            v[r] = (lok && i < N && can_follow_mask(w[i], p, full)) ? lab : 0x7FFF7FFFu;
+        }
+        v0 = make_uint4(v[0], v[1], v[2], v[3]);
+        v1 = make_uint4(v[4], v[5], v[6], v[7]);
+    }
+};
+
+// m8[g * Np + l] = bit r set iff A_(8g+r, l) is finite.
+template <class Acc>
+__global__ void k_group_masks(Acc acc, int64_t Np, uint8_t *__restrict__ m8)
 {
     const int64_t G = Np / kG;
     const int64_t total = G * Np;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = t / Np, l = t - g * Np;
-        const uint4 *p = reinterpret_cast<const uint4 *>(AT2 + l * Np + g * kG);
-        const uint4 v0 = p[0], v1 = p[1];
+        uint4 v0, v1;
+        acc.row8(g, l, v0, v1);
         const uint32_t v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
         unsigned m = 0;
 #pragma unroll
@@ -423,7 +462,7 @@ __global__ void k_group_masks(const uint32_t *__restrict__ AT2, int64_t Np, uint
     }
 }
 
-// Block-ordered compaction helper: for flags f over [0, n) in increasing index order, calls
+// Block-ordered compaction: for flags over [0, n) in increasing index order, calls
 // emit(index, rank) for each set flag; returns the count.  One block, blockDim.x % 32 == 0.
 template <class FlagF, class EmitF>
 __device__ int64_t block_compact(int64_t n, FlagF flag, EmitF emit)
@@ -453,16 +492,17 @@ __device__ int64_t block_compact(int64_t n, FlagF flag, EmitF emit)
     return base_sh;
 }
 
-// Per 128-row tile t: the union U_t of its 16 groups' l (count pass when out == nullptr).
+// Per 64-row tile t: the ordered union U_t of its 8 groups' l.  Count pass (L == nullptr)
+// writes tcnt[t]; fill pass writes L[tptr[t] + rank] = l.
 __global__ void k_tile_union(const uint8_t *__restrict__ m8, int64_t Np, const int64_t *__restrict__ tptr,
-                             int32_t *__restrict__ tcnt, int32_t *__restrict__ L, int32_t *__restrict__ posmap)
+                             int32_t *__restrict__ tcnt, int32_t *__restrict__ L)
 {
     const int64_t t = blockIdx.x;
-    const uint8_t *m = m8 + t * (kSpRows / kG) * Np;
+    const uint8_t *m = m8 + t * kSpGroups * Np;
     auto flag = [&](int64_t l) {
         unsigned any = 0;
 #pragma unroll
-        for (int j = 0; j < kSpRows / kG; ++j) any |= m[j * Np + l];
+        for (int j = 0; j < kSpGroups; ++j) any |= m[j * Np + l];
         return any != 0;
     };
     if (!L) {
@@ -471,35 +511,60 @@ __global__ void k_tile_union(const uint8_t *__restrict__ m8, int64_t Np, const i
         return;
     }
     int32_t *Lt = L + tptr[t];
-    int32_t *pm = posmap + t * Np;
-    block_compact(Np, flag, [&](int64_t l, int64_t rank) {
-        Lt[rank] = (int32_t)l;
-        pm[l] = (int32_t)rank;
-    });
+    block_compact(Np, flag, [&](int64_t l, int64_t rank) { Lt[rank] = (int32_t)l; });
 }
 
-// Per group g: its entries in increasing l (count pass when epos == nullptr).
-__global__ void k_group_entries(const uint8_t *__restrict__ m8, const uint32_t *__restrict__ AT2, int64_t Np,
-                                const int64_t *__restrict__ eptr, const int32_t *__restrict__ posmap,
-                                int32_t *__restrict__ gcnt, int32_t *__restrict__ epos, uint4 *__restrict__ ea)
+// nch[t] = ceil(tcnt[t] / kSpChunk)
+__global__ void k_chunk_counts(const int32_t *__restrict__ tcnt, int64_t Mt, int32_t *__restrict__ nch)
 {
-    const int64_t g = blockIdx.x;
-    const uint8_t *m = m8 + g * Np;
-    auto flag = [&](int64_t l) { return m[l] != 0; };
-    if (!epos) {
-        const int64_t c = block_compact(Np, flag, [](int64_t, int64_t) {});
-        if (threadIdx.x == 0) gcnt[g] = (int32_t)c;
-        return;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Mt; t += (int64_t)gridDim.x * blockDim.x)
+        nch[t] = (tcnt[t] + kSpChunk - 1) / kSpChunk;
+}
+
+// chunk_tile[c] = t for every chunk c of tile t
+__global__ void k_chunk_tiles(const int64_t *__restrict__ tch, int64_t Mt, int32_t *__restrict__ chunk_tile)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Mt; t += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t c = tch[t]; c < tch[t + 1]; ++c) chunk_tile[c] = (int32_t)t;
+}
+
+// One thread per (chunk gc, group j): counts (E == nullptr) or writes, in increasing l, the
+// entries of group 8t+j whose l lies in chunk gc of tile t.
+template <class Acc>
+__global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t Np,
+                                const int32_t *__restrict__ L, const int64_t *__restrict__ tptr,
+                                const int64_t *__restrict__ tch, const int32_t *__restrict__ chunk_tile, int64_t TC,
+                                int32_t *__restrict__ ecnt, const int64_t *__restrict__ eoff, uint4 *__restrict__ E)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < TC * kSpGroups;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gc = q / kSpGroups;
+        const int j = (int)(q - gc * kSpGroups);
+        const int64_t t = chunk_tile[gc];
+        const int64_t c = gc - tch[t];
+        const int64_t U = tptr[t + 1] - tptr[t];
+        const int32_t *Lt = L + tptr[t];
+        const int64_t g = t * kSpGroups + j;
+        const uint8_t *m = m8 + g * Np;
+        int64_t e = E ? eoff[q] : 0;
+        int cnt = 0;
+        for (int s = 0; s < kSpChunk; ++s) {
+            const int64_t r = c * kSpChunk + s;
+            if (r >= U) break;
+            const int64_t l = Lt[r];
+            if (!m[l]) continue;
+            if (E) {
+                uint4 v0, v1;
+                acc.row8(g, l, v0, v1);
+                E[3 * e] = v0;
+                E[3 * e + 1] = v1;
+                E[3 * e + 2] = make_uint4((unsigned)s, 0u, 0u, 0u);
+                ++e;
+            }
+            ++cnt;
+        }
+        if (!E) ecnt[q] = cnt;
     }
-    const int64_t e0 = eptr[g];
-    const int32_t *pm = posmap + (g / (kSpRows / kG)) * Np;
-    block_compact(Np, flag, [&](int64_t l, int64_t rank) {
-        const int64_t e = e0 + rank;
-        epos[e] = pm[l];
-        const uint4 *p = reinterpret_cast<const uint4 *>(AT2 + l * Np + g * kG);
-        ea[2 * e] = p[0];
-        ea[2 * e + 1] = p[1];
-    });
 }
 
 // Exclusive scan of n int32 counts into int64 offsets (out[n] = total); one block.
@@ -535,25 +600,29 @@ __global__ void k_scan_counts(const int32_t *__restrict__ cnt, int64_t n, int64_
 }
 
 template <int STAGES>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_spmm8(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int32_t *__restrict__ epos,
-            const uint4 *__restrict__ ea, const int64_t *__restrict__ eptr, const uint16_t *__restrict__ X,
-            int64_t ldx, uint16_t *__restrict__ C, int64_t ldc)
+__global__ void __launch_bounds__(kSpThreads, 5)
+    k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
+           const int64_t *__restrict__ eoff, const uint4 *__restrict__ E, const uint16_t *__restrict__ X, int64_t ldx,
+           uint16_t *__restrict__ C, int64_t ldc)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int STAGE = kSpChunk * kBN * 2; // 16 KB
-    const int by = blockIdx.y, bx = blockIdx.x;
+    constexpr int XB = kSpChunk * kBN * 2;        // 8 KB of X rows
+    constexpr int EB = kSpGroups * kSpChunk * 48; // up to 6 KB of entries
+    constexpr int STAGE = XB + EB;
+    const int t = blockIdx.y, bx = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int32_t *Lt = L + tptr[by];
-    const int U = (int)(tptr[by + 1] - tptr[by]);
-    const int nch = (U + kSpChunk - 1) / kSpChunk;
+    const int32_t *Lt = L + tptr[t];
+    const int U = (int)(tptr[t + 1] - tptr[t]);
+    const int64_t c0 = tch[t];
+    const int nch = (int)(tch[t + 1] - c0);
     const int64_t col0 = (int64_t)bx * kBN;
     const uint32_t sbase = smem_addr(smem);
 
     auto load_stage = [&](int stage, int c) {
         const uint32_t sX = sbase + stage * STAGE;
+        const uint32_t sE = sX + XB;
 #pragma unroll
-        for (int q = tid; q < kSpChunk * 32; q += kThreads) {
+        for (int q = tid; q < kSpChunk * 32; q += kSpThreads) {
             const int r = q >> 5, cc = q & 31;
             const int u = c * kSpChunk + r;
             if (u < U) {
@@ -561,25 +630,23 @@ __global__ void __launch_bounds__(kThreads, 2)
                 cp_async16(sX + r * 512 + cc * 16, X + l * ldx + col0 + cc * 8);
             }
         }
+        const int64_t e0 = __ldg(eoff + (c0 + c) * kSpGroups), e1 = __ldg(eoff + (c0 + c + 1) * kSpGroups);
+        const int nq = (int)(e1 - e0) * 3;
+        for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * e0 + q);
     };
 
-    const int g0 = by * (kSpRows / kG) + 2 * warp;
-    int64_t e[2] = {eptr[g0], eptr[g0 + 1]};
-    const int64_t eend[2] = {eptr[g0 + 1], eptr[g0 + 2]};
-
-    uint32_t acc[2][8][4];
+    uint32_t acc[kSpGroups][8][2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int j = 0; j < kSpGroups; ++j)
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) acc[q][r][p] = 0xFFFFFFFFu;
+        for (int r = 0; r < 8; ++r) acc[j][r][0] = acc[j][r][1] = 0xFFFFFFFFu;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nch) load_stage(s, s);
         cp_async_commit();
     }
+    const int xoff = warp * 64 + lane * 2; // this lane's two packed pairs within a 128-u32 row
     for (int c = 0; c < nch; ++c) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
@@ -589,42 +656,39 @@ __global__ void __launch_bounds__(kThreads, 2)
             cp_async_commit();
         }
         const uint32_t *Xs = reinterpret_cast<const uint32_t *>(smem + (c % STAGES) * STAGE);
-        const int lim = (c + 1) * kSpChunk;
+        const uint4 *Es = reinterpret_cast<const uint4 *>(smem + (c % STAGES) * STAGE + XB);
+        const int64_t *off = eoff + (c0 + c) * kSpGroups;
+        const int64_t eb = __ldg(off);
+        int bound[kSpGroups + 1];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            int64_t ei = e[q];
-            const int64_t ee = eend[q];
-            while (ei < ee) {
-                const int p = __ldg(epos + ei);
-                if (p >= lim) break;
-                const uint4 x = *reinterpret_cast<const uint4 *>(Xs + (p - c * kSpChunk) * 128 + lane * 4);
-                const uint4 a0 = __ldg(ea + 2 * ei), a1 = __ldg(ea + 2 * ei + 1);
+        for (int j = 0; j <= kSpGroups; ++j) bound[j] = (int)(__ldg(off + j) - eb);
+#pragma unroll
+        for (int j = 0; j < kSpGroups; ++j) {
+#pragma unroll 2
+            for (int e = bound[j]; e < bound[j + 1]; ++e) {
+                const uint4 a0 = Es[3 * e], a1 = Es[3 * e + 1];
+                const int s = (int)Es[3 * e + 2].x;
+                const uint2 x = *reinterpret_cast<const uint2 *>(Xs + s * 128 + xoff);
                 const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    acc[q][r][0] = __viaddmin_u16x2(a[r], x.x, acc[q][r][0]);
-                    acc[q][r][1] = __viaddmin_u16x2(a[r], x.y, acc[q][r][1]);
-                    acc[q][r][2] = __viaddmin_u16x2(a[r], x.z, acc[q][r][2]);
-                    acc[q][r][3] = __viaddmin_u16x2(a[r], x.w, acc[q][r][3]);
+                    acc[j][r][0] = __viaddmin_u16x2(a[r], x.x, acc[j][r][0]);
+                    acc[j][r][1] = __viaddmin_u16x2(a[r], x.y, acc[j][r][1]);
                 }
-                ++ei;
             }
-            e[q] = ei;
         }
     }
     cp_async_wait<0>();
 
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int j = 0; j < kSpGroups; ++j)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const int64_t i = (int64_t)by * kSpRows + 16 * warp + 8 * q + r;
-            uint4 v;
-            v.x = __vminu2(acc[q][r][0], 0x7FFF7FFFu);
-            v.y = __vminu2(acc[q][r][1], 0x7FFF7FFFu);
-            v.z = __vminu2(acc[q][r][2], 0x7FFF7FFFu);
-            v.w = __vminu2(acc[q][r][3], 0x7FFF7FFFu);
-            *reinterpret_cast<uint4 *>(C + i * ldc + col0 + lane * 8) = v;
+            const int64_t i = (int64_t)t * kSpRows + kG * j + r;
+            uint2 v;
+            v.x = __vminu2(acc[j][r][0], 0x7FFF7FFFu);
+            v.y = __vminu2(acc[j][r][1], 0x7FFF7FFFu);
+            *reinterpret_cast<uint2 *>(C + i * ldc + col0 + 2 * xoff) = v;
         }
 }
 
@@ -731,46 +795,111 @@ cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s)
     return cudaGetLastError();
 }
 
-constexpr int kSpStages = 4;
+constexpr int kSpStages = 3;
 
 cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
                         int64_t ncols_p, cudaStream_t s)
 {
     static bool attr_set = false;
-    const int smem = kSpStages * kSpChunk * kBN * 2;
+    const int smem = kSpStages * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48);
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_spmm8<kSpStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_spmm<kSpStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kSpRows));
-    k_spmm8<kSpStages><<<grid, kThreads, smem, s>>>(sa.L, sa.tptr, sa.epos, sa.ea, sa.eptr, X, ldx, C, ldc);
+    k_spmm<kSpStages><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc);
     return cudaGetLastError();
 }
 
-cudaError_t sparse_masks(const uint32_t *AT2, int64_t Np, uint8_t *m8, cudaStream_t s)
+// Builds the grouped sparse form (all device work; two host reads of totals).
+template <class Acc>
+cudaError_t build_sparse_form_t(Acc AT2, int64_t Np, SparseWork &w, cudaStream_t s,
+                                cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
 {
-    k_group_masks<<<grid_for((Np / kG) * Np, 256), 256, 0, s>>>(AT2, Np, m8);
-    return cudaGetLastError();
+    const int64_t G = Np / kG, Mt = Np / kSpRows;
+    cudaError_t e;
+#define SP_LAUNCH(x)                                                                                                    \
+    do {                                                                                                                \
+        x;                                                                                                              \
+        ++*launches;                                                                                                    \
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;                                                          \
+    } while (0)
+#define SP_ALLOC(ptr, bytes)                                                                                            \
+    do {                                                                                                                \
+        if ((e = alloc((void **)&(ptr), (bytes), actx)) != cudaSuccess) return e;                                       \
+    } while (0)
+    SP_ALLOC(w.m8, (size_t)(G * Np));
+    SP_ALLOC(w.tcnt, (size_t)Mt * 4);
+    SP_ALLOC(w.tptr, (size_t)(Mt + 1) * 8);
+    SP_ALLOC(w.nch, (size_t)Mt * 4);
+    SP_ALLOC(w.tch, (size_t)(Mt + 1) * 8);
+    SP_LAUNCH((k_group_masks<<<grid_for(G * Np, 256), 256, 0, s>>>(AT2, Np, w.m8)));
+    SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, nullptr, w.tcnt, nullptr)));
+    SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(w.tcnt, Mt, w.tptr)));
+    SP_LAUNCH((k_chunk_counts<<<grid_for(Mt, 256), 256, 0, s>>>(w.tcnt, Mt, w.nch)));
+    SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(w.nch, Mt, w.tch)));
+    int64_t tot[2] = {0, 0};
+    if ((e = cudaMemcpyAsync(&tot[0], w.tptr + Mt, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(&tot[1], w.tch + Mt, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    w.total_union = tot[0];
+    w.total_chunks = tot[1];
+    const int64_t TC = std::max<int64_t>(tot[1], 1);
+    SP_ALLOC(w.L, (size_t)std::max<int64_t>(tot[0], 1) * 4);
+    SP_ALLOC(w.chunk_tile, (size_t)TC * 4);
+    SP_ALLOC(w.ecnt, (size_t)TC * kSpGroups * 4);
+    SP_ALLOC(w.eoff, (size_t)(TC * kSpGroups + 1) * 8);
+    SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, w.tptr, nullptr, w.L)));
+    SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
+    SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
+        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], w.ecnt, nullptr, nullptr)));
+    SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(w.ecnt, tot[1] * kSpGroups, w.eoff)));
+    int64_t ne = 0;
+    if ((e = cudaMemcpyAsync(&ne, w.eoff + tot[1] * kSpGroups, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    w.entries = ne;
+    SP_ALLOC(w.E, (size_t)std::max<int64_t>(ne, 1) * 48);
+    SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
+        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E)));
+#undef SP_LAUNCH
+#undef SP_ALLOC
+    return cudaSuccess;
 }
 
-cudaError_t sparse_tile_union(const uint8_t *m8, int64_t Np, const int64_t *tptr, int32_t *tcnt, int32_t *L,
-                              int32_t *posmap, cudaStream_t s)
+cudaError_t build_sparse_form(const uint32_t *AT2, int64_t Np, SparseWork &w, cudaStream_t s,
+                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
 {
-    k_tile_union<<<(unsigned)(Np / kSpRows), 1024, 0, s>>>(m8, Np, tptr, tcnt, L, posmap);
-    return cudaGetLastError();
+    return build_sparse_form_t(AccAT2{AT2, Np}, Np, w, s, alloc, actx, launches);
 }
 
-cudaError_t sparse_group_entries(const uint8_t *m8, const uint32_t *AT2, int64_t Np, const int64_t *eptr,
-                                 const int32_t *posmap, int32_t *gcnt, int32_t *epos, uint4 *ea, cudaStream_t s)
+cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, SparseWork &w,
+                                    cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
+                                    int64_t *launches)
 {
-    k_group_entries<<<(unsigned)(Np / kG), 256, 0, s>>>(m8, AT2, Np, eptr, posmap, gcnt, epos, ea);
-    return cudaGetLastError();
+    return build_sparse_form_t(AccWords{words, N, (1u << n) - 1u}, Np, w, s, alloc, actx, launches);
 }
 
-cudaError_t scan_counts(const int32_t *cnt, int64_t n, int64_t *out, cudaStream_t s)
+// X1[i][j] = A_(i, c0+j) from the word masks, +inf padding (rows >= N, columns >= w).
+__global__ void k_x1_from_words(const WordMask *__restrict__ words, int64_t N, unsigned full, int64_t Np,
+                                int64_t c0, int64_t w, uint16_t *__restrict__ X1, int64_t ldx)
 {
-    k_scan_counts<<<1, 1024, 0, s>>>(cnt, n, out);
+    const int64_t total = Np * ldx;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ldx, j = t - i * ldx;
+        uint16_t v = kDevInf;
+        if (i < N && j < w) {
+            const WordMask p = words[c0 + j];
+            if (can_follow_mask(words[i], p, full)) v = p.zeros;
+        }
+        X1[t] = v;
+    }
+}
+
+cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, int64_t w,
+                                 uint16_t *X1, int64_t ldx, cudaStream_t s)
+{
+    k_x1_from_words<<<grid_for(Np * ldx, 256), 256, 0, s>>>(words, N, (1u << n) - 1u, Np, c0, w, X1, ldx);
     return cudaGetLastError();
 }
 

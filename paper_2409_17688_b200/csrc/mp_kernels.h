@@ -26,22 +26,31 @@ cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int6
                                int64_t ldx, cudaStream_t s);
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
                           int64_t ldd, cudaStream_t s);
-// Grouped sparse form of A for the SpMM product (see k_spmm8).
+// Grouped sparse form of A for the SpMM product (see k_spmm in mp_kernels.cu).
 struct SparseA {
-    const int32_t *L = nullptr;    // concatenated per-tile union lists of l
-    const int64_t *tptr = nullptr; // [Np/128 + 1] offsets into L
-    const int32_t *epos = nullptr; // per entry: position of its l in its tile's union list
-    const uint4 *ea = nullptr;     // per entry: 8 duplicated values (2 x uint4)
-    const int64_t *eptr = nullptr; // [Np/8 + 1] offsets of each group's entries
+    const int32_t *L = nullptr;    // concatenated per-tile (64-row) ordered union lists of l
+    const int64_t *tptr = nullptr; // [Mt + 1] offsets into L
+    const int64_t *tch = nullptr;  // [Mt + 1] first chunk of each tile
+    const int64_t *eoff = nullptr; // [chunks * 8 + 1] entry offsets per (chunk, group)
+    const uint4 *E = nullptr;      // entries, 3 x uint4 each
+};
+// Device buffers of the sparse form (owned by the caller; allocated through `alloc`).
+struct SparseWork {
+    uint8_t *m8 = nullptr;
+    int32_t *tcnt = nullptr, *nch = nullptr, *L = nullptr, *chunk_tile = nullptr, *ecnt = nullptr;
+    int64_t *tptr = nullptr, *tch = nullptr, *eoff = nullptr;
+    uint4 *E = nullptr;
+    int64_t total_union = 0, total_chunks = 0, entries = 0;
 };
 cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
                         int64_t ncols_p, cudaStream_t s);
-cudaError_t sparse_masks(const uint32_t *AT2, int64_t Np, uint8_t *m8, cudaStream_t s);
-cudaError_t sparse_tile_union(const uint8_t *m8, int64_t Np, const int64_t *tptr, int32_t *tcnt, int32_t *L,
-                              int32_t *posmap, cudaStream_t s);
-cudaError_t sparse_group_entries(const uint8_t *m8, const uint32_t *AT2, int64_t Np, const int64_t *eptr,
-                                 const int32_t *posmap, int32_t *gcnt, int32_t *epos, uint4 *ea, cudaStream_t s);
-cudaError_t scan_counts(const int32_t *cnt, int64_t n, int64_t *out, cudaStream_t s);
+cudaError_t build_sparse_form(const uint32_t *AT2, int64_t Np, SparseWork &w, cudaStream_t s,
+                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);
+cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, SparseWork &w,
+                                    cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
+                                    int64_t *launches);
+cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, int64_t w,
+                                 uint16_t *X1, int64_t ldx, cudaStream_t s);
 cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s);
 cudaError_t launch_tile_occupancy(const uint32_t *AT2, int64_t Mp, int64_t Kp, uint8_t *occ, cudaStream_t s);
 

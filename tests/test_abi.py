@@ -41,6 +41,8 @@ def test_no_cpu_fallback_symbols():
 def test_count_words_table1(oracle_mod):
     for n in range(2, 14):
         assert mp.count_words(n) == oracle_mod.count_words(n)
+    with pytest.raises(mp.MinplusError):
+        mp.count_words(14)
     with pytest.raises(mp.MinplusError) as e:
         mp.count_words(1)
     assert e.value.status == 1
@@ -53,7 +55,7 @@ def test_transition_matrix_equals_oracle(oracle_mod, n):
 
 
 def test_transition_matrix_domain_errors():
-    for n in (0, 1, 13):
+    for n in (0, 1, 14):
         with pytest.raises(mp.MinplusError) as e:
             mp.build_transition_matrix(n)
         assert e.value.status == 1
@@ -141,7 +143,7 @@ def test_argument_errors_before_device():
     assert _native.lib.minplus_mul(a.ctypes.data, a.ctypes.data, a.ctypes.data, 4, 4, 4) == 1  # aliasing
     g = ctypes.c_int64()
     assert _native.lib.gamma2_cylinder(5, 2, ctypes.byref(g)) == 1
-    assert _native.lib.gamma2_cylinder(13, 5, ctypes.byref(g)) == 1
+    assert _native.lib.gamma2_cylinder(14, 5, ctypes.byref(g)) == 1
     r = _native._PeriodicResult()
     assert _native.lib.minplus_power_until_periodic(a.ctypes.data, 4, 1, ctypes.byref(r)) == 1
     assert _native.lib.minplus_power_until_periodic(a.ctypes.data, 4, 257, ctypes.byref(r)) == 1
