@@ -29,6 +29,21 @@ sys.path.insert(0, ROOT)
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 DPX_STEPS_PER_CLK_PER_SM = 128  # 64 VIADDMNMX.U16x2 lanes / clk / SM x 2 steps
+KERNEL_NAMES = {"dense": "k_minplus (dense tiles, VIADDMNMX.U16x2)",
+                "tiles": "k_minplus (block-sparse tiles, VIADDMNMX.U16x2)",
+                "spmm": "k_spmm (grouped SpMM, VIADDMNMX.U16x2)"}
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def traffic_bytes(kernel: str, n: int, world: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed ncu --set full capture of the same configuration (profiles/ncu_traffic.json)."""
+    try:
+        table = json.load(open(TRAFFIC_PATH))
+    except (OSError, ValueError):
+        return None
+    rec = table.get(f"{kernel.split()[0]}:{kernel.split('(')[1].split(',')[0]}:n{n}:g{world}")
+    return rec["bytes_per_launch"] if rec else None
 
 
 def parse():
@@ -202,6 +217,7 @@ def run_mine(args):
         p = mp.last_profile()
         prod_ms += p["product_ms"]
         prod_launches += p["product_launches"]
+        kernel_used = p["kernel"]
         dense += p["dense_steps"]
         issued += p["issued_steps"]
     e1.record(stream)
@@ -271,8 +287,9 @@ def run_mine(args):
                    "ops": "dense-equivalent N^3 per product (one op = add+min on one u16 lane)"},
         "seconds_to_gamma2": ms / args.steps / 1e3,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
-        "roofline": {"bound": "alu", "kernel": "k_minplus (VIADDMNMX.U16x2)", "achieved": achieved, "peak": peak,
-                     "unit": "Gstep/s", "frac": achieved / peak, "traffic": None,
+        "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used], "achieved": achieved, "peak": peak,
+                     "unit": "Gstep/s", "frac": achieved / peak,
+                     "traffic": traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world),
                      "peak_source": f"148 SM x 128 steps/clk/SM x {sm_mhz:.0f} MHz observed (DESIGN.md)",
                      "avg_launch_ms": avg_launch_ms, "issued_steps_per_launch": issued_per_launch,
                      "kernel_share_of_step": prod_ms / max(ms, 1e-9)},

@@ -149,6 +149,13 @@ mp_status minplus_power_rows(const uint16_t *A, int64_t N, int kmax, const int64
  * [mu, k_last].  Errors: MP_ERR_DOMAIN, and those of minplus_power_until_periodic. */
 mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out);
 
+/* The (mu, lambda, b, diag_min, fingerprint) record gamma2_cylinder(n, .) reads from: runs
+ * the power sequence of A(D_n) built on the device from the word masks (once per n per
+ * process) and copies the cached record to the caller-owned *out.  n = 13 needs the SpMM
+ * kernel (default) and about 4 x 34.6 GB of device memory for the power store.
+ * Errors: as gamma2_cylinder. */
+mp_status mp_gamma2_record(int n, mp_periodic_result *out);
+
 /* Read-off only (host, no device): applies the a6 rule to a result. */
 mp_status mp_gamma2_readoff(const mp_periodic_result *r, int64_t m, int64_t *gamma2_out);
 
@@ -238,6 +245,8 @@ typedef struct {
     double total_ms;          /* whole run, first to last operation on the library stream  */
     int64_t h2d_bytes;        /* host -> device bytes copied by the run                    */
     int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
+    int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,
+                                 2 grouped SpMM                                              */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
 

@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
         L.oracle_gamma2_readoff.restype = i64
         L.oracle_gamma2_bruteforce.argtypes = [ctypes.c_int, ctypes.c_int]
         L.oracle_gamma2_column_dp.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.oracle_gamma2_path_dp.argtypes = [ctypes.c_int, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -206,6 +207,11 @@ def gamma2_bruteforce(n: int, m: int) -> int:
 
 def gamma2_column_dp(n: int, m: int) -> int:
     return int(lib().oracle_gamma2_column_dp(n, m))
+
+
+def gamma2_path_dp(n: int, m: int) -> int:
+    """gamma_2(P_n x C_m) by DP along the path over row subsets of C_m (any n, m <= 8)."""
+    return int(lib().oracle_gamma2_path_dp(n, m))
 
 
 def num_threads() -> int:

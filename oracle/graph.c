@@ -56,6 +56,67 @@ static int column_ok(int n, unsigned prev, unsigned cur, unsigned next)
     return 1;
 }
 
+/* Row i of the cylinder (the m vertices (i, 0..m-1) of one copy of C_m, as a bit mask cur)
+ * is 2-dominated given the rows above (prev) and below (next): every vertex not in S has at
+ * least two neighbours in S among its two cycle neighbours and the vertices above/below. */
+static int row_ok(int m, unsigned prev, unsigned cur, unsigned next)
+{
+    int j;
+    for (j = 0; j < m; j++) {
+        int cnt;
+        if ((cur >> j) & 1) continue;
+        cnt = ((prev >> j) & 1) + ((next >> j) & 1) + ((cur >> ((j + 1) % m)) & 1) +
+              ((cur >> ((j + m - 1) % m)) & 1);
+        if (cnt < 2) return 0;
+    }
+    return 1;
+}
+
+/* gamma_2(P_n x C_m) by dynamic programming ALONG THE PATH over consecutive row subsets
+ * (S_{i-1}, S_i) of the cycle, with empty virtual rows above row 0 and below row n-1: any
+ * path order n, small cycle length 3 <= m <= 8.  Independent of the transfer matrix; it pins
+ * the large-n results at small m.  Returns -1 on bad arguments. */
+int oracle_gamma2_path_dp(int n, int m)
+{
+    int C, i, x, y, z, best = 1 << 30;
+    int *f, *g;
+    unsigned char *ok;
+    if (n < 1 || m < 3 || m > 8) return -1;
+    C = 1 << m;
+    ok = (unsigned char *)malloc((size_t)C * C * C);
+    f = (int *)malloc(sizeof(int) * C * C);
+    g = (int *)malloc(sizeof(int) * C * C);
+    for (x = 0; x < C; x++)
+        for (y = 0; y < C; y++)
+            for (z = 0; z < C; z++) ok[((size_t)x * C + y) * C + z] = (unsigned char)row_ok(m, x, y, z);
+    /* state after placing rows 0..i: (S_{i-1}, S_i); row i-1 already checked */
+    for (x = 0; x < C * C; x++) f[x] = 1 << 30;
+    for (y = 0; y < C; y++) f[0 * C + y] = __builtin_popcount(y); /* S_{-1} = empty */
+    for (i = 1; i < n; i++) {
+        for (x = 0; x < C * C; x++) g[x] = 1 << 30;
+        for (x = 0; x < C; x++)
+            for (y = 0; y < C; y++) {
+                int fv = f[x * C + y];
+                if (fv >= (1 << 30)) continue;
+                for (z = 0; z < C; z++)
+                    if (ok[((size_t)x * C + y) * C + z]) {
+                        int nv = fv + __builtin_popcount(z);
+                        if (nv < g[y * C + z]) g[y * C + z] = nv;
+                    }
+            }
+        { int *t = f; f = g; g = t; }
+    }
+    for (x = 0; x < C; x++)
+        for (y = 0; y < C; y++) {
+            int fv = f[x * C + y];
+            if (fv < best && ok[((size_t)x * C + y) * C + 0]) best = fv; /* S_n = empty */
+        }
+    free(ok);
+    free(f);
+    free(g);
+    return best;
+}
+
 /* Returns gamma_2, or -1 on bad arguments. */
 int oracle_gamma2_column_dp(int n, int m)
 {

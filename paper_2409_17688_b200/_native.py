@@ -30,7 +30,7 @@ EXPORTS = [
     "gamma2_cylinder",
     "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
-    "mp_last_profile", "mp_set_options", "mp_gamma2_formula",
+    "mp_last_profile", "mp_set_options", "mp_gamma2_formula", "mp_gamma2_record",
 ]
 
 
@@ -63,7 +63,7 @@ class _Profile(ctypes.Structure):
     _fields_ = [("product_ms", ctypes.c_double), ("product_launches", ctypes.c_int64),
                 ("dense_steps", ctypes.c_double), ("issued_steps", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("h2d_bytes", ctypes.c_int64),
-                ("d2h_bytes", ctypes.c_int64)]
+                ("d2h_bytes", ctypes.c_int64), ("kernel", ctypes.c_int32)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
@@ -99,6 +99,7 @@ def _load() -> ctypes.CDLL:
         "mp_last_profile": ([P], i32),
         "mp_set_options": ([i32, i64], i32),
         "mp_gamma2_formula": ([P, P], i32),
+        "mp_gamma2_record": ([i32, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -245,6 +246,13 @@ def gamma2_cylinder(n: int, m: int) -> int:
     return g.value
 
 
+def gamma2_record(n: int) -> PeriodicResult:
+    """The cached power-sequence record gamma2_cylinder(n, .) reads from."""
+    r = _PeriodicResult()
+    _check(lib.mp_gamma2_record(n, ctypes.byref(r)))
+    return _result(r)
+
+
 # -------------------------------------------------------------------------- multi-GPU
 _keep_alive = []
 
@@ -319,7 +327,8 @@ def last_profile() -> dict:
     _check(lib.mp_last_profile(ctypes.byref(p)))
     return {"product_ms": p.product_ms, "product_launches": p.product_launches,
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
-            "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes}
+            "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
+            "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?")}
 
 
 SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}

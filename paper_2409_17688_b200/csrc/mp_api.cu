@@ -586,6 +586,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.total_ms = all_ms;
     g_prof.h2d_bytes = g_h2d.load() - h2d0;
     g_prof.d2h_bytes = g_d2h.load() - d2h0;
+    g_prof.kernel = R.spmm ? 2 : (R.sparse ? 1 : 0);
 
     if (!found) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
     *out = res;
@@ -770,12 +771,11 @@ mp_status mp_gamma2_formula(const mp_periodic_result *r, mp_formula *out)
     return MP_OK;
 }
 
-mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out)
+mp_status mp_gamma2_record(int n, mp_periodic_result *out)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
-    if (!gamma2_out || n < 2 || n > MP_MAX_N || m < 3)
-        return fail(MP_ERR_DOMAIN, "gamma2_cylinder: n = %d outside [2, %d] or m = %lld < 3", n, MP_MAX_N,
-                    (long long)m);
+    if (!out || n < 2 || n > MP_MAX_N)
+        return fail(MP_ERR_DOMAIN, "mp_gamma2_record: n = %d outside [2, %d] or NULL", n, MP_MAX_N);
     const auto key = std::make_tuple(n, g_dist.world, g_dist.rank);
     auto it = g_cache.find(key);
     if (it == g_cache.end()) {
@@ -785,7 +785,19 @@ mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out)
         TRY(run_powers(src, count_words(n), 64, &r));
         it = g_cache.emplace(key, r).first;
     }
-    return mp_gamma2_readoff(&it->second, m, gamma2_out);
+    *out = it->second;
+    return MP_OK;
+}
+
+mp_status gamma2_cylinder(int n, int64_t m, int64_t *gamma2_out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!gamma2_out || n < 2 || n > MP_MAX_N || m < 3)
+        return fail(MP_ERR_DOMAIN, "gamma2_cylinder: n = %d outside [2, %d] or m = %lld < 3", n, MP_MAX_N,
+                    (long long)m);
+    mp_periodic_result r;
+    TRY(mp_gamma2_record(n, &r));
+    return mp_gamma2_readoff(&r, m, gamma2_out);
 }
 
 mp_status mp_dist_set(int rank, int world, mp_allreduce_fn fn, void *ctx)

@@ -599,6 +599,11 @@ __global__ void k_scan_counts(const int32_t *__restrict__ cnt, int64_t n, int64_
     if (threadIdx.x == 0) out[n] = carry;
 }
 
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+}
+
 template <int STAGES>
 __global__ void __launch_bounds__(kSpThreads, 5)
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
@@ -608,7 +613,9 @@ __global__ void __launch_bounds__(kSpThreads, 5)
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int XB = kSpChunk * kBN * 2;        // 8 KB of X rows
     constexpr int EB = kSpGroups * kSpChunk * 48; // up to 6 KB of entries
-    constexpr int STAGE = XB + EB;
+    constexpr int BB = 80;                        // the chunk's 9 entry offsets (int64)
+    constexpr int STAGE = XB + EB + BB;
+    constexpr int RPT = kSpChunk * 32 / kSpThreads; // X rows (16-byte columns) copied per thread
     const int t = blockIdx.y, bx = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int32_t *Lt = L + tptr[t];
@@ -618,21 +625,31 @@ __global__ void __launch_bounds__(kSpThreads, 5)
     const int64_t col0 = (int64_t)bx * kBN;
     const uint32_t sbase = smem_addr(smem);
 
+    // Register prefetch of what load_stage needs for the next chunk (its X row indices and
+    // entry range), issued one chunk ahead so the global-load latency hides behind compute.
+    int32_t pl[RPT];
+    int64_t pe0 = 0, pe1 = 0;
+    auto prefetch = [&](int c) {
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int u = c * kSpChunk + warp + 2 * k;
+            pl[k] = (c < nch && u < U) ? __ldg(Lt + u) : -1;
+        }
+        if (c < nch) {
+            pe0 = __ldg(eoff + (c0 + c) * kSpGroups);
+            pe1 = __ldg(eoff + (c0 + c + 1) * kSpGroups);
+        }
+    };
     auto load_stage = [&](int stage, int c) {
         const uint32_t sX = sbase + stage * STAGE;
         const uint32_t sE = sX + XB;
 #pragma unroll
-        for (int q = tid; q < kSpChunk * 32; q += kSpThreads) {
-            const int r = q >> 5, cc = q & 31;
-            const int u = c * kSpChunk + r;
-            if (u < U) {
-                const int64_t l = __ldg(Lt + u);
-                cp_async16(sX + r * 512 + cc * 16, X + l * ldx + col0 + cc * 8);
-            }
-        }
-        const int64_t e0 = __ldg(eoff + (c0 + c) * kSpGroups), e1 = __ldg(eoff + (c0 + c + 1) * kSpGroups);
-        const int nq = (int)(e1 - e0) * 3;
-        for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * e0 + q);
+        for (int k = 0; k < RPT; ++k)
+            if (pl[k] >= 0)
+                cp_async16(sX + (warp + 2 * k) * 512 + lane * 16, X + (int64_t)pl[k] * ldx + col0 + lane * 8);
+        const int nq = (int)(pe1 - pe0) * 3;
+        for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * pe0 + q);
+        if (tid <= kSpGroups) cp_async8(sE + EB + tid * 8, eoff + (c0 + c) * kSpGroups + tid);
     };
 
     uint32_t acc[kSpGroups][8][2];
@@ -641,10 +658,12 @@ __global__ void __launch_bounds__(kSpThreads, 5)
 #pragma unroll
         for (int r = 0; r < 8; ++r) acc[j][r][0] = acc[j][r][1] = 0xFFFFFFFFu;
 
+    prefetch(0);
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nch) load_stage(s, s);
         cp_async_commit();
+        prefetch(s + 1);
     }
     const int xoff = warp * 64 + lane * 2; // this lane's two packed pairs within a 128-u32 row
     for (int c = 0; c < nch; ++c) {
@@ -654,14 +673,16 @@ __global__ void __launch_bounds__(kSpThreads, 5)
             const int cn = c + STAGES - 1;
             if (cn < nch) load_stage(cn % STAGES, cn);
             cp_async_commit();
+            prefetch(cn + 1);
         }
-        const uint32_t *Xs = reinterpret_cast<const uint32_t *>(smem + (c % STAGES) * STAGE);
-        const uint4 *Es = reinterpret_cast<const uint4 *>(smem + (c % STAGES) * STAGE + XB);
-        const int64_t *off = eoff + (c0 + c) * kSpGroups;
-        const int64_t eb = __ldg(off);
+        const uint8_t *stage_p = smem + (c % STAGES) * STAGE;
+        const uint32_t *Xs = reinterpret_cast<const uint32_t *>(stage_p);
+        const uint4 *Es = reinterpret_cast<const uint4 *>(stage_p + XB);
+        const int64_t *Bs = reinterpret_cast<const int64_t *>(stage_p + XB + EB);
+        const int64_t eb = Bs[0];
         int bound[kSpGroups + 1];
 #pragma unroll
-        for (int j = 0; j <= kSpGroups; ++j) bound[j] = (int)(__ldg(off + j) - eb);
+        for (int j = 0; j <= kSpGroups; ++j) bound[j] = (int)(Bs[j] - eb);
 #pragma unroll
         for (int j = 0; j < kSpGroups; ++j) {
 #pragma unroll 2
@@ -801,7 +822,7 @@ cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint1
                         int64_t ncols_p, cudaStream_t s)
 {
     static bool attr_set = false;
-    const int smem = kSpStages * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48);
+    const int smem = kSpStages * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48 + 80);
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_spmm<kSpStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;

@@ -218,3 +218,26 @@ def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
     f = g.formula()  # NEXT-2: Table 7 row and the exception (G15) from the run itself
     assert f["a"] == a and {k for k in range(a) if f["alpha"][k] == 1} == ks
     assert f["exceptions"] == {m: v for (nn, m), v in exc.items() if nn == n}
+
+
+def test_gamma2_small_cycles_all_paths(mp, oracle_mod):
+    """gamma_2(P_n x C_m) for every path order n <= 13 at cycle lengths m <= 8 against the
+    DP along the path (a graph oracle independent of the transfer matrix): pins the full-size
+    runs n = 10, 11, 12 and the new n = 13 (NEXT-3)."""
+    for n in range(2, 14):
+        for m in range(3, 9 if n <= 12 else 8):
+            assert mp.gamma2_cylinder(n, m) == oracle_mod.gamma2_path_dp(n, m), (n, m)
+
+
+def test_n13_record(mp):
+    """NEXT-3: n = 13 on one B200 (no dense A: 69 GB).  Dense from k = 3
+    (P:342); the C_5 formula of [Garzon2022] quoted at P:504 (2n+1 for odd n); the paper's
+    conjecture (n+2)m/3 for 3 | m; Lemma 1 via the read-off far beyond k_last."""
+    r = mp.gamma2_record(13)
+    assert r.dense_from == 3 and r.k_last == r.mu + r.lam
+    assert r.gamma2(5) == 27
+    for m in range(3, 3000, 3):
+        assert r.gamma2(m) == 5 * m
+    f = r.formula()
+    for m in range(r.mu, r.mu + 200):
+        assert r.gamma2(m) == -(-f["b"] * m // f["a"]) + f["alpha"][m % f["a"]]

@@ -343,6 +343,21 @@ def test_gamma2_column_dp(oracle_mod):
             assert r.gamma2(m) == oracle_mod.gamma2_column_dp(n, m), (n, m)
 
 
+def test_gamma2_path_dp(oracle_mod):
+    """A third graph oracle, DP along the path over row subsets of the cycle: equals brute
+    force (n*m <= 24), the column DP, and the transfer-matrix read-off for n <= 9, m <= 8."""
+    for n in range(1, 9):
+        for m in range(3, min(8, 24 // n) + 1):
+            assert oracle_mod.gamma2_path_dp(n, m) == oracle_mod.gamma2_bruteforce(n, m), (n, m)
+    for n in (2, 3, 4, 5):
+        for m in range(3, 9):
+            assert oracle_mod.gamma2_path_dp(n, m) == oracle_mod.gamma2_column_dp(n, m), (n, m)
+    for n in range(6, 10):
+        r = oracle_mod.power_until_periodic(oracle_mod.transition_matrix(n))
+        for m in range(3, 9):
+            assert oracle_mod.gamma2_path_dp(n, m) == r.gamma2(m), (n, m)
+
+
 def test_gamma2_closed_forms(oracle_mod):
     """P_2: gamma_2 = m; P_3: ceil(4m/3) (from Table 5 a=6, b=8 and Table 7 all alpha=0);
     C_5 formula of [Garzon2022] quoted at P:504; the n >= 8, 3 | m formula (n+2)m/3 proven
