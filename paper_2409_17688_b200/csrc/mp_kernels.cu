@@ -604,6 +604,33 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void *src)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
 
+// acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's two
+// packed column pairs.
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][2], const uint4 &a0, const uint4 &a1, const uint2 &x)
+{
+    const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        acc[r][0] = __viaddmin_u16x2(a[r], x.x, acc[r][0]);
+        acc[r][1] = __viaddmin_u16x2(a[r], x.y, acc[r][1]);
+    }
+}
+
+// Non-coherent global loads kept at their program position (asm volatile), so a prefetch
+// issued one chunk ahead is not sunk next to its use by the scheduler.
+__device__ __forceinline__ int32_t ldg_nc_s32(const int32_t *p)
+{
+    int32_t v;
+    asm volatile("ld.global.nc.s32 %0, [%1];\n" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int64_t ldg_nc_s64(const int64_t *p)
+{
+    int64_t v;
+    asm volatile("ld.global.nc.s64 %0, [%1];\n" : "=l"(v) : "l"(p));
+    return v;
+}
+
 template <int STAGES>
 __global__ void __launch_bounds__(kSpThreads, 5)
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
@@ -633,11 +660,11 @@ __global__ void __launch_bounds__(kSpThreads, 5)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const int u = c * kSpChunk + warp + 2 * k;
-            pl[k] = (c < nch && u < U) ? __ldg(Lt + u) : -1;
+            pl[k] = (c < nch && u < U) ? ldg_nc_s32(Lt + u) : -1;
         }
         if (c < nch) {
-            pe0 = __ldg(eoff + (c0 + c) * kSpGroups);
-            pe1 = __ldg(eoff + (c0 + c + 1) * kSpGroups);
+            pe0 = ldg_nc_s64(eoff + (c0 + c) * kSpGroups);
+            pe1 = ldg_nc_s64(eoff + (c0 + c + 1) * kSpGroups);
         }
     };
     auto load_stage = [&](int stage, int c) {
@@ -683,19 +710,29 @@ __global__ void __launch_bounds__(kSpThreads, 5)
         int bound[kSpGroups + 1];
 #pragma unroll
         for (int j = 0; j <= kSpGroups; ++j) bound[j] = (int)(Bs[j] - eb);
+        // Entries of group j, software-pipelined one entry ahead with ping-pong register sets:
+        // the next entry's loads are unconditional (an index past the chunk reads padding inside
+        // the shared allocation; the row index is masked into the chunk), so the scheduler can
+        // issue the LDS chain entry -> row -> X row ahead of the current entry's 16 DPX.
 #pragma unroll
         for (int j = 0; j < kSpGroups; ++j) {
-#pragma unroll 2
-            for (int e = bound[j]; e < bound[j + 1]; ++e) {
-                const uint4 a0 = Es[3 * e], a1 = Es[3 * e + 1];
-                const int s = (int)Es[3 * e + 2].x;
-                const uint2 x = *reinterpret_cast<const uint2 *>(Xs + s * 128 + xoff);
-                const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    acc[j][r][0] = __viaddmin_u16x2(a[r], x.x, acc[j][r][0]);
-                    acc[j][r][1] = __viaddmin_u16x2(a[r], x.y, acc[j][r][1]);
-                }
+            int e = bound[j];
+            const int ee = bound[j + 1];
+            if (e >= ee) continue;
+            uint4 pa0 = Es[3 * e], pa1 = Es[3 * e + 1];
+            uint2 xa = *reinterpret_cast<const uint2 *>(Xs + ((int)Es[3 * e + 2].x & (kSpChunk - 1)) * 128 + xoff);
+            while (true) {
+                const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
+                const uint2 xb =
+                    *reinterpret_cast<const uint2 *>(Xs + ((int)Es[3 * e + 5].x & (kSpChunk - 1)) * 128 + xoff);
+                dpx_group(acc[j], pa0, pa1, xa);
+                if (e + 1 >= ee) break;
+                pa0 = Es[3 * e + 6];
+                pa1 = Es[3 * e + 7];
+                xa = *reinterpret_cast<const uint2 *>(Xs + ((int)Es[3 * e + 8].x & (kSpChunk - 1)) * 128 + xoff);
+                dpx_group(acc[j], pb0, pb1, xb);
+                if (e + 2 >= ee) break;
+                e += 2;
             }
         }
     }
@@ -822,7 +859,8 @@ cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint1
                         int64_t ncols_p, cudaStream_t s)
 {
     static bool attr_set = false;
-    const int smem = kSpStages * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48 + 80);
+    // + 64 B: the pipelined entry loop may read up to three uint4 past the last stage
+    const int smem = kSpStages * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48 + 80) + 64;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_spmm<kSpStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
