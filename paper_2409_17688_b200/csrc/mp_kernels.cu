@@ -2,6 +2,7 @@
 // with its roofline; the citations name the paper passage each one implements.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <algorithm>
 
 #include "mp_internal.h"
@@ -157,32 +158,31 @@ __global__ void __launch_bounds__(256)
     k_stats(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t c0, int64_t w,
             unsigned long long *__restrict__ out)
 {
-    const int64_t chunks_per_row = (w + 7) / 8;
-    const int64_t total = N * chunks_per_row;
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = c / chunks_per_row;
-        const int64_t j0 = (c - i * chunks_per_row) * 8;
-        const uint4 v = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
-        const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+    // rows strided over the blocks, 8-column chunks strided over the threads of a block
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
+        const uint64_t tbase = (uint64_t)(i * N + c0);
+        const uint16_t *row = X + i * ld;
+        for (int64_t j0 = (int64_t)threadIdx.x * 8; j0 < w; j0 += (int64_t)blockDim.x * 8) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(row + j0);
+            const uint32_t words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int64_t j = j0 + e;
-            if (j >= w) break;
-            uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-            const int64_t gj = c0 + j;
-            const uint64_t t = (uint64_t)(i * N + gj);
-            if (x == kDevInf) {
-                x = kBndInf;
-                ++infc;
-            } else {
-                const unsigned long long key = (t << 16) | x;
-                if (key < ref) ref = key;
+            for (int e = 0; e < 8; ++e) {
+                const int64_t j = j0 + e;
+                if (j >= w) break;
+                uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                const uint64_t t = tbase + (uint64_t)j;
+                if (x == kDevInf) {
+                    x = kBndInf;
+                    ++infc;
+                } else {
+                    const unsigned long long key = (t << 16) | x;
+                    if (key < ref) ref = key;
+                }
+                h += (unsigned long long)mix64(t) * x;
+                if (c0 + j == i && x < dmin) dmin = x;
             }
-            h += (unsigned long long)mix64(t) * x;
-            if (gj == i && x < dmin) dmin = x;
         }
     }
 #pragma unroll
@@ -227,24 +227,21 @@ __global__ void __launch_bounds__(256)
     k_compare(const uint16_t *__restrict__ Y, const uint16_t *__restrict__ Z, int64_t ld, int64_t N,
               int64_t w, int32_t c, unsigned long long *__restrict__ out)
 {
-    const int64_t chunks_per_row = (w + 7) / 8;
-    const int64_t total = N * chunks_per_row;
     unsigned long long bad = 0;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = q / chunks_per_row;
-        const int64_t j0 = (q - i * chunks_per_row) * 8;
-        const uint4 vy = *reinterpret_cast<const uint4 *>(Y + i * ld + j0);
-        const uint4 vz = *reinterpret_cast<const uint4 *>(Z + i * ld + j0);
-        const uint32_t wy[4] = {vy.x, vy.y, vy.z, vy.w};
-        const uint32_t wz[4] = {vz.x, vz.y, vz.z, vz.w};
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
+        for (int64_t j0 = (int64_t)threadIdx.x * 8; j0 < w; j0 += (int64_t)blockDim.x * 8) {
+            const uint4 vy = *reinterpret_cast<const uint4 *>(Y + i * ld + j0);
+            const uint4 vz = *reinterpret_cast<const uint4 *>(Z + i * ld + j0);
+            const uint32_t wy[4] = {vy.x, vy.y, vy.z, vy.w};
+            const uint32_t wz[4] = {vz.x, vz.y, vz.z, vz.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            if (j0 + e >= w) break;
-            const int32_t y = (wy[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
-            const int32_t z = (wz[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
-            const bool yi = (y == kDevInf), zi = (z == kDevInf);
-            if (yi != zi || (!yi && y - z != c)) ++bad;
+            for (int e = 0; e < 8; ++e) {
+                if (j0 + e >= w) break;
+                const int32_t y = (wy[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
+                const int32_t z = (wz[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
+                const bool yi = (y == kDevInf), zi = (z == kDevInf);
+                if (yi != zi || (!yi && y - z != c)) ++bad;
+            }
         }
     }
 #pragma unroll
@@ -558,7 +555,7 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
                 acc.row8(g, l, v0, v1);
                 E[3 * e] = v0;
                 E[3 * e + 1] = v1;
-                E[3 * e + 2] = make_uint4((unsigned)s, 0u, 0u, 0u);
+                E[3 * e + 2] = make_uint4((unsigned)s * 128u, 0u, 0u, 0u); // u32 offset of the X row
                 ++e;
             }
             ++cnt;
@@ -621,18 +618,18 @@ __device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][2], const uint4 &a0
 __device__ __forceinline__ int32_t ldg_nc_s32(const int32_t *p)
 {
     int32_t v;
-    asm volatile("ld.global.nc.s32 %0, [%1];\n" : "=r"(v) : "l"(p));
+    asm volatile("ld.global.nc.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ int64_t ldg_nc_s64(const int64_t *p)
 {
     int64_t v;
-    asm volatile("ld.global.nc.s64 %0, [%1];\n" : "=l"(v) : "l"(p));
+    asm volatile("ld.global.nc.s64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
 template <int STAGES>
-__global__ void __launch_bounds__(kSpThreads, 5)
+__global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 6 : 5))
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
            const int64_t *__restrict__ eoff, const uint4 *__restrict__ E, const uint16_t *__restrict__ X, int64_t ldx,
            uint16_t *__restrict__ C, int64_t ldc)
@@ -719,17 +716,22 @@ __global__ void __launch_bounds__(kSpThreads, 5)
             int e = bound[j];
             const int ee = bound[j + 1];
             if (e >= ee) continue;
+            // row offsets run two entries ahead, values and X rows one entry ahead
+            const uint32_t *Xl = Xs + xoff;
+            auto row = [&](int q) { return (int)(Es[3 * q + 2].x & ((kSpChunk - 1) * 128)); };
+            int sa = row(e), sb = row(e + 1);
             uint4 pa0 = Es[3 * e], pa1 = Es[3 * e + 1];
-            uint2 xa = *reinterpret_cast<const uint2 *>(Xs + ((int)Es[3 * e + 2].x & (kSpChunk - 1)) * 128 + xoff);
+            uint2 xa = *reinterpret_cast<const uint2 *>(Xl + sa);
             while (true) {
                 const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
-                const uint2 xb =
-                    *reinterpret_cast<const uint2 *>(Xs + ((int)Es[3 * e + 5].x & (kSpChunk - 1)) * 128 + xoff);
+                const uint2 xb = *reinterpret_cast<const uint2 *>(Xl + sb);
+                sa = row(e + 2);
                 dpx_group(acc[j], pa0, pa1, xa);
                 if (e + 1 >= ee) break;
                 pa0 = Es[3 * e + 6];
                 pa1 = Es[3 * e + 7];
-                xa = *reinterpret_cast<const uint2 *>(Xs + ((int)Es[3 * e + 8].x & (kSpChunk - 1)) * 128 + xoff);
+                xa = *reinterpret_cast<const uint2 *>(Xl + sa);
+                sb = row(e + 3);
                 dpx_group(acc[j], pb0, pb1, xb);
                 if (e + 2 >= ee) break;
                 e += 2;
@@ -796,7 +798,7 @@ cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, 
 cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, int64_t w,
                          unsigned long long *out, cudaStream_t s)
 {
-    const int g = grid_for(N * ((w + 7) / 8), 256);
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8); // row-strided blocks
     k_stats<<<g, 256, 0, s>>>(X, ld, N, c0, w, out);
     return cudaGetLastError();
 }
@@ -804,7 +806,7 @@ cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, i
 cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int64_t N, int64_t w, int32_t c,
                            unsigned long long *out, cudaStream_t s)
 {
-    const int g = grid_for(N * ((w + 7) / 8), 256);
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8); // row-strided blocks
     k_compare<<<g, 256, 0, s>>>(Y, Z, ld, N, w, c, out);
     return cudaGetLastError();
 }
@@ -853,22 +855,40 @@ cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s)
     return cudaGetLastError();
 }
 
-constexpr int kSpStages = 3;
-
-cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
-                        int64_t ncols_p, cudaStream_t s)
+template <int STAGES>
+static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
+                                 int64_t Mp, int64_t ncols_p, cudaStream_t s)
 {
     static bool attr_set = false;
     // + 64 B: the pipelined entry loop may read up to three uint4 past the last stage
-    const int smem = kSpStages * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48 + 80) + 64;
+    const int smem = STAGES * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48 + 80) + 64;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_spmm<kSpStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_spmm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kSpRows));
-    k_spmm<kSpStages><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc);
+    k_spmm<STAGES><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc);
     return cudaGetLastError();
+}
+
+// Pipeline depth of k_spmm: 2 stages (6 CTAs = 12 warps per SM) by default; MP_SPMM_STAGES=3
+// selects the 3-stage ring (5 CTAs per SM) for comparison.
+static int spmm_stages()
+{
+    static int st = 0;
+    if (!st) {
+        const char *e = getenv("MP_SPMM_STAGES");
+        st = (e && atoi(e) == 3) ? 3 : 2;
+    }
+    return st;
+}
+
+cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
+                        int64_t ncols_p, cudaStream_t s)
+{
+    return spmm_stages() == 3 ? launch_spmm_t<3>(sa, X, ldx, C, ldc, Mp, ncols_p, s)
+                              : launch_spmm_t<2>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
 }
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
