@@ -27,6 +27,8 @@ namespace {
 
 std::recursive_mutex g_mu;
 constexpr double kSpmmAdvantage = 0.6; // auto: SpMM if it issues < 60% of the tile kernel's steps
+constexpr int kBatch = 16;             // powers per host round trip when N <= kBatchMaxN
+constexpr int64_t kBatchMaxN = 4096;
 constexpr double kDefaultRingBytes = 48.0 * 1024 * 1024 * 1024; // power-store cap unless set
 thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
@@ -141,6 +143,12 @@ struct PowerRun {
     std::vector<DBuf> sp_bufs;
     size_t sp_next = 0;
     SparseWork sp;
+    std::vector<cudaEvent_t> events; // per-power product start/stop
+    ~PowerRun()
+    {
+        for (auto ev : events)
+            if (ev) cudaEventDestroy(ev);
+    }
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
 
@@ -467,17 +475,30 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.ring.resize((size_t)slots);
         R.slot_power.assign((size_t)slots, 0);
     }
-    TRY(R.stats.ensure((size_t)(max_k + 1) * 4 * 8, "per-power statistics"));
+    // per-power statistics: SUM fields {H, inf count} for k = 0..max_k, then MIN fields
+    // {diag min, first finite entry}, so a batch of powers reduces with one call of each
+    const size_t nst = (size_t)(max_k + 1) * 2;
+    TRY(R.stats.ensure(nst * 2 * 8, "per-power statistics"));
     TRY(R.flag.ensure(16, "compare flag"));
+    int64_t *st_sum = R.stats.as<int64_t>(), *st_min = st_sum + nst;
     {
-        std::vector<int64_t> init((size_t)(max_k + 1) * 4);
-        for (size_t q = 0; q < init.size(); q += 4) {
-            init[q] = 0;
-            init[q + 1] = 0;
-            init[q + 2] = 0xFFFF;
-            init[q + 3] = INT64_MAX;
+        std::vector<int64_t> init(nst * 2, 0);
+        for (size_t q = nst; q < init.size(); q += 2) {
+            init[q] = 0xFFFF;
+            init[q + 1] = INT64_MAX;
         }
         COPY(R.stats.p, init.data(), init.size() * 8, cudaMemcpyHostToDevice, s);
+    }
+    // Batch of powers between host synchronisations: products of small matrices take
+    // microseconds, so up to kBatch of them are enqueued back to back and their statistics
+    // read with one copy; powers computed past the first repeat are discarded.  The batch
+    // depends only on N, so every rank of a sharded run makes the same collective calls.
+    int B = (N <= kBatchMaxN && !cap) ? kBatch : 1;
+    B = std::max(1, std::min<int>(B, (int)R.ring.size() - 1));
+    if ((int)R.events.size() < 2 * (max_k + 1)) {
+        for (auto ev : R.events) cudaEventDestroy(ev);
+        R.events.assign((size_t)2 * (max_k + 1), nullptr);
+        for (auto &ev : R.events) CUDA_TRY(cudaEventCreate(&ev));
     }
 
     std::vector<mp_power_stats> hs((size_t)max_k + 1);
@@ -492,96 +513,113 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         CUDA_TRY(cudaStreamSynchronize(s));
         g_unit_cache[N] = S;
     }
-    cudaEvent_t e0, e1;
-    CUDA_TRY(cudaEventCreate(&e0));
-    CUDA_TRY(cudaEventCreate(&e1));
     double prod_ms = 0.0;
     int64_t launches = 0;
 
     mp_periodic_result res;
     std::memset(&res, 0, sizeof(res));
     const uint16_t *prev = nullptr;
+    std::vector<const uint16_t *> buf((size_t)max_k + 1, nullptr);
+    std::vector<int64_t> hsum(nst), hmin(nst);
     bool found = false;
-    int k = 1;
-    for (k = 1; k <= max_k && !found; ++k) {
-        const size_t q = (size_t)(k % (int)R.ring.size());
-        TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
-        uint16_t *dst = R.ring[q].as<uint16_t>();
-        R.slot_power[q] = k;
-        const uint16_t *cur = dst;
-        if (k == 1) {
-            TRY(make_power1(R, dst, s)); // X_1 = A[:, shard]
-        } else {
-            CUDA_TRY(cudaEventRecord(e0, s));
-            TRY(product(R, prev, dst, s)); // A^k = A (x) A^{k-1}
-            CUDA_TRY(cudaEventRecord(e1, s));
-            ++launches;
+    for (int kb = 1; kb <= max_k && !found; kb += B) {
+        const int ke = std::min(max_k, kb + B - 1);
+        for (int k = kb; k <= ke; ++k) {
+            const size_t q = (size_t)(k % (int)R.ring.size());
+            TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
+            uint16_t *dst = R.ring[q].as<uint16_t>();
+            R.slot_power[q] = k;
+            buf[(size_t)k] = dst;
+            if (k == 1) {
+                TRY(make_power1(R, dst, s)); // X_1 = A[:, shard]
+            } else {
+                CUDA_TRY(cudaEventRecord(R.events[2 * k], s));
+                TRY(product(R, prev, dst, s)); // A^k = A (x) A^{k-1}
+                CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
+                ++launches;
+            }
+            LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
+                                reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
+            prev = dst;
         }
-        int64_t *sk = R.stats.as<int64_t>() + 4 * k;
-        LAUNCH(launch_stats(cur, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(sk), s));
-        TRY(allreduce(0, sk, 2, s));     // SUM: fingerprint, inf count
-        TRY(allreduce(1, sk + 2, 2, s)); // MIN: diagonal minimum, first finite entry
-        COPY(&hs[(size_t)k], sk, sizeof(mp_power_stats), cudaMemcpyDeviceToHost, s);
+        const int nb = ke - kb + 1;
+        TRY(allreduce(0, st_sum + 2 * kb, 2 * nb, s)); // SUM: fingerprint, inf count
+        TRY(allreduce(1, st_min + 2 * kb, 2 * nb, s)); // MIN: diagonal minimum, first finite entry
+        COPY(hsum.data() + 2 * kb, st_sum + 2 * kb, (size_t)nb * 16, cudaMemcpyDeviceToHost, s);
+        COPY(hmin.data() + 2 * kb, st_min + 2 * kb, (size_t)nb * 16, cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));
-        if (k >= 2) {
-            float ms = 0.f;
-            CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-            prod_ms += ms;
-        }
-        const mp_power_stats &cs = hs[(size_t)k];
-        res.diag_min[k] = (uint16_t)std::min<int64_t>(cs.diag_min, 0xFFFF);
-        res.fingerprint[k] = (uint64_t)cs.fingerprint;
-        if (!res.dense_from && cs.inf_count == 0) res.dense_from = k;
 
-        if (cap) {
-            DBuf rowbuf;
-            TRY(rowbuf.alloc((size_t)N * 2, "captured row"));
-            for (int r = 0; r < cap->nrows; ++r) {
-                LAUNCH(launch_decode(cur + cap->rows[r] * R.ld, R.ld, 1, N, rowbuf.as<uint16_t>(), N, s));
-                CUDA_TRY(cudaMemcpyAsync(cap->out + ((size_t)(k - 1) * cap->nrows + r) * N, rowbuf.p, (size_t)N * 2,
-                                         cudaMemcpyDeviceToHost, s));
+        for (int k = kb; k <= ke && !found; ++k) {
+            if (k >= 2) {
+                float ms = 0.f;
+                CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[2 * k + 1]));
+                prod_ms += ms;
+            }
+            mp_power_stats &cs = hs[(size_t)k];
+            cs.fingerprint = hsum[2 * k];
+            cs.inf_count = hsum[2 * k + 1];
+            cs.diag_min = hmin[2 * k];
+            cs.ref = hmin[2 * k + 1];
+            res.diag_min[k] = (uint16_t)std::min<int64_t>(cs.diag_min, 0xFFFF);
+            res.fingerprint[k] = (uint64_t)cs.fingerprint;
+            if (!res.dense_from && cs.inf_count == 0) res.dense_from = k;
+            const uint16_t *cur = buf[(size_t)k];
+
+            if (cap) {
+                DBuf rowbuf;
+                TRY(rowbuf.alloc((size_t)N * 2, "captured row"));
+                for (int r = 0; r < cap->nrows; ++r) {
+                    LAUNCH(launch_decode(cur + cap->rows[r] * R.ld, R.ld, 1, N, rowbuf.as<uint16_t>(), N, s));
+                    CUDA_TRY(cudaMemcpyAsync(cap->out + ((size_t)(k - 1) * cap->nrows + r) * N, rowbuf.p,
+                                             (size_t)N * 2, cudaMemcpyDeviceToHost, s));
+                    CUDA_TRY(cudaStreamSynchronize(s));
+                }
+                if (k == max_k) found = true;
+                continue;
+            }
+
+            // a5: forward first-repeat search, j = k-1 down to 1
+            for (int j = k - 1; j >= 1 && !found; --j) {
+                int32_t c = 0;
+                if (!mp_repeat_candidate(&cs, &hs[(size_t)j], S, &c)) continue;
+                const uint16_t *Z = nullptr;
+                TRY(power_buffer(R, j, &Z, s));
+                int64_t *fl = R.flag.as<int64_t>();
+                CUDA_TRY(cudaMemsetAsync(fl, 0, 8, s));
+                LAUNCH(launch_compare(cur, Z, R.ld, N, R.w, c, reinterpret_cast<unsigned long long *>(fl), s));
+                TRY(allreduce(0, fl, 1, s));
+                int64_t bad = -1;
+                COPY(&bad, fl, 8, cudaMemcpyDeviceToHost, s);
                 CUDA_TRY(cudaStreamSynchronize(s));
-            }
-            prev = cur;
-            if (k == max_k) found = true;
-            continue;
-        }
-
-        // a5: forward first-repeat search, j = k-1 down to 1
-        for (int j = k - 1; j >= 1 && !found; --j) {
-            int32_t c = 0;
-            if (!mp_repeat_candidate(&cs, &hs[(size_t)j], S, &c)) continue;
-            const uint16_t *Z = nullptr;
-            TRY(power_buffer(R, j, &Z, s));
-            int64_t *fl = R.flag.as<int64_t>();
-            CUDA_TRY(cudaMemsetAsync(fl, 0, 8, s));
-            LAUNCH(launch_compare(cur, Z, R.ld, N, R.w, c, reinterpret_cast<unsigned long long *>(fl), s));
-            TRY(allreduce(0, fl, 1, s));
-            int64_t bad = -1;
-            COPY(&bad, fl, 8, cudaMemcpyDeviceToHost, s);
-            CUDA_TRY(cudaStreamSynchronize(s));
-            if (bad == 0) {
-                found = true;
-                res.mu = j;
-                res.lambda = k - j;
-                res.offset = c;
-                res.k_last = k;
+                if (bad == 0) {
+                    found = true;
+                    res.mu = j;
+                    res.lambda = k - j;
+                    res.offset = c;
+                    res.k_last = k;
+                }
             }
         }
-        prev = cur;
+        for (int k = std::max(2, kb); k <= ke && found && !cap; ++k) // discarded powers still ran
+            if (k > res.k_last) {
+                float ms = 0.f;
+                CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[2 * k + 1]));
+                prod_ms += ms;
+            }
     }
     CUDA_TRY(cudaEventRecord(ev_all1, s));
     CUDA_TRY(cudaEventSynchronize(ev_all1));
     float all_ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&all_ms, ev_all0, ev_all1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     cudaEventDestroy(ev_all0);
     cudaEventDestroy(ev_all1);
 
+    // dense-equivalent steps count the products up to the first repeat (useful work); the
+    // launches and their time include any product of the batch computed past it
+    const int64_t useful = found && !cap ? (int64_t)res.k_last - 1 : launches;
     g_prof.product_ms = prod_ms;
     g_prof.product_launches = launches;
-    g_prof.dense_steps = (double)launches * (double)N * (double)N * (double)R.w;
+    g_prof.dense_steps = (double)useful * (double)N * (double)N * (double)R.w;
     g_prof.issued_steps = (double)launches * R.issued_per_product;
     g_prof.total_ms = all_ms;
     g_prof.h2d_bytes = g_h2d.load() - h2d0;

@@ -147,16 +147,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------------------------------
 // a4: per-power statistics of a column shard X (rows 0..N-1, columns c0..c0+w-1 of the
-// global power, stored [Np][ld]); layout of out[] = mp_power_stats:
-//   out[0] += H = sum h(i*N + c0 + j) * x (mod 2^64), +inf counted as 0xFFFF;
-//   out[1] += number of +inf entries;
-//   out[2]  = min(out[2], min over i == c0 + j of x)  (Algorithm 5);
-//   out[3]  = min(out[3], (t << 16) | x) over finite entries, t = i*N + c0 + j.
-// The caller initialises out = {0, 0, 0xFFFF, INT64_MAX}.  HBM-bound: reads 2*N*w bytes.
+// global power, stored [Np][ld]).  The SUM-reduced and the MIN-reduced fields live in two
+// arrays so that a batch of powers is all-reduced with one SUM and one MIN call:
+//   out_sum[0] += H = sum h(i*N + c0 + j) * x (mod 2^64), +inf counted as 0xFFFF;
+//   out_sum[1] += number of +inf entries;
+//   out_min[0]  = min(out_min[0], min over i == c0 + j of x)  (Algorithm 5);
+//   out_min[1]  = min(out_min[1], (t << 16) | x) over finite entries, t = i*N + c0 + j.
+// The caller initialises {0, 0} and {0xFFFF, INT64_MAX}.  Reads 2*N*w bytes.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
     k_stats(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t c0, int64_t w,
-            unsigned long long *__restrict__ out)
+            unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
 {
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
@@ -211,10 +212,10 @@ __global__ void __launch_bounds__(256)
             D = min(D, sd[k]);
             R = min(R, sr[k]);
         }
-        atomicAdd(out + 0, H);
-        atomicAdd(out + 1, I);
-        atomicMin(out + 2, (unsigned long long)D);
-        atomicMin(out + 3, R);
+        atomicAdd(out_sum + 0, H);
+        atomicAdd(out_sum + 1, I);
+        atomicMin(out_min + 0, (unsigned long long)D);
+        atomicMin(out_min + 1, R);
     }
 }
 
@@ -796,10 +797,10 @@ cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, 
 }
 
 cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, int64_t w,
-                         unsigned long long *out, cudaStream_t s)
+                         unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s)
 {
     const int g = (int)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8); // row-strided blocks
-    k_stats<<<g, 256, 0, s>>>(X, ld, N, c0, w, out);
+    k_stats<<<g, 256, 0, s>>>(X, ld, N, c0, w, out_sum, out_min);
     return cudaGetLastError();
 }
 

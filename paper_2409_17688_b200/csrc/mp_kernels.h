@@ -13,7 +13,7 @@ cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, 
                            int64_t ldc, int64_t Mp, int64_t ncols_p, int64_t Kp, const int32_t *kt_ptr,
                            const int32_t *kt_idx, cudaStream_t s);
 cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, int64_t w,
-                         unsigned long long *out, cudaStream_t s);
+                         unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s);
 cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int64_t N, int64_t w, int32_t c,
                            unsigned long long *out, cudaStream_t s);
 cudaError_t launch_encode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,

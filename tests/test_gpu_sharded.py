@@ -69,7 +69,7 @@ def test_sharded_run_emulated(oracle_mod, n, world):
                     expected.append((k, j, c))
                     if oracle_mod.constant_difference(P[k], P[j]) == c:
                         break
-        state = {"k": 0, "cmp": 0}
+        state = {"k": 0, "kb": 1, "cmp": 0}
 
         class _Dev:
             def __init__(self, ptr, cnt):
@@ -79,19 +79,23 @@ def test_sharded_run_emulated(oracle_mod, n, world):
         def allreduce(op, ptr, count):
             t = torch.as_tensor(_Dev(ptr, count), device="cuda")
             vals = [int(v) for v in t.cpu().tolist()]
-            if op == 0 and count == 2:          # SUM {fingerprint, inf count} of power k
-                state["k"] += 1
-                k = state["k"]
-                fp = vals[0] + sum(p[0] for p in part[k])
-                inf = vals[1] + sum(p[1] for p in part[k])
-                out = [_i64(fp), inf]
-            elif op == 1 and count == 2:        # MIN {diag min, first finite entry}
-                k = state["k"]
-                out = [min([vals[0]] + [p[2] for p in part[k]]), min([vals[1]] + [p[3] for p in part[k]])]
+            if op == 0 and count >= 2:          # SUM {fingerprint, inf count} of a batch of powers
+                out = []
+                for q in range(count // 2):
+                    k = state["k"] + 1 + q
+                    got = part.get(k, [])       # powers past k_last: any value (discarded)
+                    out += [_i64(vals[2 * q] + sum(p[0] for p in got)), vals[2 * q + 1] + sum(p[1] for p in got)]
+                state["kb"] = state["k"] + 1
+                state["k"] += count // 2
+            elif op == 1 and count >= 2:        # MIN {diag min, first finite entry} of the batch
+                out = []
+                for q in range(count // 2):
+                    got = part.get(state["kb"] + q, [])
+                    out += [min([vals[2 * q]] + [p[2] for p in got]), min([vals[2 * q + 1]] + [p[3] for p in got])]
             elif op == 0 and count == 1:        # SUM of exact-compare mismatches
                 k, j, c = expected[state["cmp"]]
                 state["cmp"] += 1
-                assert k == state["k"]
+                assert state["kb"] <= k <= state["k"]
                 bad = vals[0]
                 for a, b in others:
                     Y, Z = P[k][:, a:b].astype(np.int64), P[j][:, a:b].astype(np.int64)
