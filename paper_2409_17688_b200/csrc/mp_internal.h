@@ -32,7 +32,8 @@ constexpr int kThreads = 256; // 8 warps, 8x16 outputs per thread
 // Pitches: every device matrix is padded with +inf to these multiples.
 MP_HD int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 MP_HD int64_t pad_rows(int64_t n) { return round_up(n > 0 ? n : 1, kBM); } // multiple of kBM and kBK
-MP_HD int64_t pad_cols(int64_t n) { return round_up(n > 0 ? n : 1, kBN); }
+constexpr int kLdAlign = 512; // column pitch of every device power: a multiple of both CTA widths
+MP_HD int64_t pad_cols(int64_t n) { return round_up(n > 0 ? n : 1, kLdAlign); }
 
 // ---------------------------------------------------------------------------------------
 // Words as bit masks (a1).  Letter i of a word (i = 0 is the top row of the column and the

@@ -394,21 +394,25 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 //
 // Rows of A are taken in groups of kG = 8.  A group "entry" is an inner index l at which at
 // least one of its 8 rows has a finite A_il; it carries the 8 values {a, a} (+inf for rows
-// without an arc).  A CTA owns kSpRows = 64 rows (8 groups) x kBN = 256 columns.  The union
-// U_t of its groups' l indices, in increasing order, is cut into chunks of kSpChunk = 16;
-// per chunk the CTA stages the 16 rows X[l, cols] and the chunk's entries (grouped by group)
-// in shared memory with cp.async.  Each of the 2 warps owns 128 columns (2 packed pairs per
-// lane) of ALL 8 groups, so both warps do identical work (no imbalance): per entry one
-// LDS.64 of X, two broadcast LDS.128 of the values and 16 VIADDMNMX.U16x2 (8 rows x 2
-// pairs).  Issued steps = 8 * entries * ld; every skipped term is an all-+inf one, so the
-// result is the same product.
-// Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s, 0, 0, 0} with s = row within the chunk.
+// without an arc).  A CTA owns kSpRows = 32 rows (4 groups) x kSpCols = 512 columns.  The
+// union U_t of its groups' l indices, in increasing order, is cut into chunks of kSpChunk =
+// 16; per chunk the CTA stages the 16 rows X[l, cols] (16 KB) and the chunk's entries
+// (grouped by group) in shared memory with cp.async.  Each of the 2 warps owns 256 columns
+// (4 packed pairs per lane) of ALL 4 groups, so both warps do identical work (no
+// imbalance): per entry one LDS.128 of X, two broadcast LDS.128 of the values and 32
+// VIADDMNMX.U16x2 (8 rows x 4 pairs) -- enough DPX per entry to keep the issue slots of the
+// shared-memory and loop instructions below the ALU pipe's rate.  Issued steps =
+// 8 * entries * ld; every skipped term is an all-+inf one, so the result is the same product.
+// Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowU32, 0, 0, 0}, s = row in the chunk.
 // ---------------------------------------------------------------------------------------
 constexpr int kG = 8;
-constexpr int kSpRows = 64;
+constexpr int kSpRows = 32;
 constexpr int kSpGroups = kSpRows / kG;
 constexpr int kSpChunk = 16;
 constexpr int kSpThreads = 64;
+constexpr int kSpCols = 512;            // columns per CTA (2 warps x 32 lanes x 8)
+constexpr int kSpRowU32 = kSpCols / 2;  // one staged X row, in packed u32 pairs
+static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
 // How the sparse-form builders read A: the 8 duplicated values of rows 8g..8g+7 at column l.
 struct AccAT2 { // from the staged AT2 (matrix sources)
@@ -556,7 +560,7 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
                 acc.row8(g, l, v0, v1);
                 E[3 * e] = v0;
                 E[3 * e + 1] = v1;
-                E[3 * e + 2] = make_uint4((unsigned)s * 128u, 0u, 0u, 0u); // u32 offset of the X row
+                E[3 * e + 2] = make_uint4((unsigned)s * (unsigned)kSpRowU32, 0u, 0u, 0u); // X row offset (u32)
                 ++e;
             }
             ++cnt;
@@ -602,15 +606,17 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void *src)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
 
-// acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's two
+// acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's four
 // packed column pairs.
-__device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][2], const uint4 &a0, const uint4 &a1, const uint2 &x)
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][4], const uint4 &a0, const uint4 &a1, const uint4 &x)
 {
     const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         acc[r][0] = __viaddmin_u16x2(a[r], x.x, acc[r][0]);
         acc[r][1] = __viaddmin_u16x2(a[r], x.y, acc[r][1]);
+        acc[r][2] = __viaddmin_u16x2(a[r], x.z, acc[r][2]);
+        acc[r][3] = __viaddmin_u16x2(a[r], x.w, acc[r][3]);
     }
 }
 
@@ -630,24 +636,24 @@ __device__ __forceinline__ int64_t ldg_nc_s64(const int64_t *p)
 }
 
 template <int STAGES>
-__global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 6 : 5))
+__global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
            const int64_t *__restrict__ eoff, const uint4 *__restrict__ E, const uint16_t *__restrict__ X, int64_t ldx,
            uint16_t *__restrict__ C, int64_t ldc)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int XB = kSpChunk * kBN * 2;        // 8 KB of X rows
-    constexpr int EB = kSpGroups * kSpChunk * 48; // up to 6 KB of entries
-    constexpr int BB = 80;                        // the chunk's 9 entry offsets (int64)
+    constexpr int XB = kSpChunk * kSpCols * 2;    // 16 KB of X rows
+    constexpr int EB = kSpGroups * kSpChunk * 48; // up to 3 KB of entries
+    constexpr int BB = 48;                        // the chunk's 5 entry offsets (int64)
     constexpr int STAGE = XB + EB + BB;
-    constexpr int RPT = kSpChunk * 32 / kSpThreads; // X rows (16-byte columns) copied per thread
+    constexpr int RPT = kSpChunk / 2;             // X rows each warp stages per chunk
     const int t = blockIdx.y, bx = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int32_t *Lt = L + tptr[t];
     const int U = (int)(tptr[t + 1] - tptr[t]);
     const int64_t c0 = tch[t];
     const int nch = (int)(tch[t + 1] - c0);
-    const int64_t col0 = (int64_t)bx * kBN;
+    const int64_t col0 = (int64_t)bx * kSpCols;
     const uint32_t sbase = smem_addr(smem);
 
     // Register prefetch of what load_stage needs for the next chunk (its X row indices and
@@ -670,18 +676,24 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 6 : 5))
         const uint32_t sE = sX + XB;
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
-            if (pl[k] >= 0)
-                cp_async16(sX + (warp + 2 * k) * 512 + lane * 16, X + (int64_t)pl[k] * ldx + col0 + lane * 8);
+            if (pl[k] >= 0) { // each lane copies two 16-byte pieces of the 1 KB row
+                const uint16_t *src = X + (int64_t)pl[k] * ldx + col0;
+                const uint32_t dst = sX + (warp + 2 * k) * (kSpCols * 2);
+                cp_async16(dst + lane * 16, src + lane * 8);
+                cp_async16(dst + 512 + lane * 16, src + 256 + lane * 8);
+            }
         const int nq = (int)(pe1 - pe0) * 3;
         for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * pe0 + q);
         if (tid <= kSpGroups) cp_async8(sE + EB + tid * 8, eoff + (c0 + c) * kSpGroups + tid);
     };
 
-    uint32_t acc[kSpGroups][8][2];
+    uint32_t acc[kSpGroups][8][4];
 #pragma unroll
     for (int j = 0; j < kSpGroups; ++j)
 #pragma unroll
-        for (int r = 0; r < 8; ++r) acc[j][r][0] = acc[j][r][1] = 0xFFFFFFFFu;
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) acc[j][r][p] = 0xFFFFFFFFu;
 
     prefetch(0);
 #pragma unroll
@@ -690,7 +702,7 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 6 : 5))
         cp_async_commit();
         prefetch(s + 1);
     }
-    const int xoff = warp * 64 + lane * 2; // this lane's two packed pairs within a 128-u32 row
+    const int xoff = warp * 128 + lane * 4; // this lane's four packed pairs within a staged row
     for (int c = 0; c < nch; ++c) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
@@ -719,19 +731,19 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 6 : 5))
             if (e >= ee) continue;
             // row offsets run two entries ahead, values and X rows one entry ahead
             const uint32_t *Xl = Xs + xoff;
-            auto row = [&](int q) { return (int)(Es[3 * q + 2].x & ((kSpChunk - 1) * 128)); };
+            auto row = [&](int q) { return (int)(Es[3 * q + 2].x & ((kSpChunk - 1) * kSpRowU32)); };
             int sa = row(e), sb = row(e + 1);
             uint4 pa0 = Es[3 * e], pa1 = Es[3 * e + 1];
-            uint2 xa = *reinterpret_cast<const uint2 *>(Xl + sa);
+            uint4 xa = *reinterpret_cast<const uint4 *>(Xl + sa);
             while (true) {
                 const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
-                const uint2 xb = *reinterpret_cast<const uint2 *>(Xl + sb);
+                const uint4 xb = *reinterpret_cast<const uint4 *>(Xl + sb);
                 sa = row(e + 2);
                 dpx_group(acc[j], pa0, pa1, xa);
                 if (e + 1 >= ee) break;
                 pa0 = Es[3 * e + 6];
                 pa1 = Es[3 * e + 7];
-                xa = *reinterpret_cast<const uint2 *>(Xl + sa);
+                xa = *reinterpret_cast<const uint4 *>(Xl + sa);
                 sb = row(e + 3);
                 dpx_group(acc[j], pb0, pb1, xb);
                 if (e + 2 >= ee) break;
@@ -746,10 +758,12 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 6 : 5))
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const int64_t i = (int64_t)t * kSpRows + kG * j + r;
-            uint2 v;
+            uint4 v;
             v.x = __vminu2(acc[j][r][0], 0x7FFF7FFFu);
             v.y = __vminu2(acc[j][r][1], 0x7FFF7FFFu);
-            *reinterpret_cast<uint2 *>(C + i * ldc + col0 + 2 * xoff) = v;
+            v.z = __vminu2(acc[j][r][2], 0x7FFF7FFFu);
+            v.w = __vminu2(acc[j][r][3], 0x7FFF7FFFu);
+            *reinterpret_cast<uint4 *>(C + i * ldc + col0 + 2 * xoff) = v;
         }
 }
 
@@ -862,13 +876,13 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
 {
     static bool attr_set = false;
     // + 64 B: the pipelined entry loop may read up to three uint4 past the last stage
-    const int smem = STAGES * (kSpChunk * kBN * 2 + kSpGroups * kSpChunk * 48 + 80) + 64;
+    const int smem = STAGES * (kSpChunk * kSpCols * 2 + kSpGroups * kSpChunk * 48 + 48) + 64;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_spmm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kSpRows));
+    dim3 grid((unsigned)(ncols_p / kSpCols), (unsigned)(Mp / kSpRows));
     k_spmm<STAGES><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc);
     return cudaGetLastError();
 }

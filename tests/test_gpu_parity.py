@@ -165,7 +165,7 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     """A device budget of 3 power slots forces the recompute path for evicted A^j (n = 7 has
     lambda = 18, so the partner of the first repeat is long gone from the ring)."""
     A = mp.build_transition_matrix(7)
-    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 255) // 256) * 256) * 2
+    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 511) // 512) * 512) * 2  # Np x ld x 2 B
     mp.set_options("auto", device_budget_bytes=5 * slot)
     try:
         g = mp.minplus_power_until_periodic(A)
