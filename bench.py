@@ -220,6 +220,7 @@ def run_mine(args):
         kernel_used = p["kernel"]
         dense += p["dense_steps"]
         issued += p["issued_steps"]
+        setup_ms = p["setup_ms"]
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -241,6 +242,7 @@ def run_mine(args):
         p = mp.last_profile()
         h2d += p["h2d_bytes"]
         d2h += p["d2h_bytes"]
+        e2e_setup_ms = p["setup_ms"]
     f1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -296,7 +298,9 @@ def run_mine(args):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_dense / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
                 "h2d_bytes_per_step": int(h2d / max(1, e2e_steps)), "d2h_bytes_per_step": int(d2h / max(1, e2e_steps)),
-                "seconds_to_gamma2": e2e_ms / e2e_steps / 1e3},
+                "seconds_to_gamma2": e2e_ms / e2e_steps / 1e3,
+                "setup_ms_last_step": e2e_setup_ms},
+        "setup_ms": setup_ms,
         "gpu_launches": int(launches),
         "clocks": clk,
     }

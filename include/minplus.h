@@ -166,6 +166,9 @@ mp_status mp_gamma2_readoff(const mp_periodic_result *r, int64_t m, int64_t *gam
  * Errors: MP_ERR_DOMAIN (NULL, invalid result, a > MP_MAX_K). */
 typedef struct {
     int32_t a, b, n0;
+    int32_t r0_k50;                 /* the r0 Algorithm 3 reports with K = 50 (Table 4): the
+                                       scan from i = K finds j = K - a first (K >= n0 + a);
+                                       -1 if K = 50 < n0 + a                                 */
     int32_t alpha[MP_MAX_K];        /* alpha[k], 0 <= k < a                                   */
     int32_t n_exceptions;
     int64_t exception_m[MP_MAX_K];  /* cycle lengths with gamma_2 != the formula, ascending   */
@@ -243,6 +246,7 @@ typedef struct {
     double dense_steps;       /* sum of N * N * w over the launches (dense-equivalent steps) */
     double issued_steps;      /* steps the kernel executed after skipping all-inf A tiles   */
     double total_ms;          /* whole run, first to last operation on the library stream  */
+    double setup_ms;          /* of which staging A and building the sparse form (a1-a2)   */
     int64_t h2d_bytes;        /* host -> device bytes copied by the run                    */
     int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
     int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,

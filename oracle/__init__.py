@@ -196,6 +196,38 @@ def power_rows(A: np.ndarray, r: int, kmax: int) -> np.ndarray:
     return out
 
 
+def powers(A: np.ndarray, K: int) -> dict:
+    """Algorithm 2: {i: A^i} for i = 1..K, A^i = A x A^(i-1)."""
+    P = {1: np.ascontiguousarray(A, dtype=np.uint16)}
+    for i in range(2, K + 1):
+        P[i] = minplus(A, P[i - 1])
+    return P
+
+
+def algorithm3(P: dict, K: int):
+    """Algorithm 3 verbatim: for i = K down to 1, for j = i-1 down to 1, the
+    first pair with A^i - A^j constant gives a = i - j, b = the constant, r0 = j."""
+    for i in range(K, 0, -1):
+        for j in range(i - 1, 0, -1):
+            c = constant_difference(P[i], P[j])
+            if c is not None:
+                return j, i - j, c
+    return None
+
+
+def algorithm4(P: dict, r0: int, a: int, b: int):
+    """Algorithm 4 verbatim: for i = r0 + a down to 1 (while i - a >= 1, reading
+    G11), exit at the first i with A^i - A^(i-a) != b; otherwise n0 = i - a."""
+    n0 = None
+    for i in range(r0 + a, 0, -1):
+        if i - a < 1:
+            break
+        if constant_difference(P[i], P[i - a]) != b:
+            break
+        n0 = i - a
+    return n0
+
+
 def gamma2(n: int, m: int, max_k: int = 64) -> int:
     """gamma_2(P_n x C_m) from the transfer matrix (Theorems 2 and 3)."""
     return power_until_periodic(transition_matrix(n), max_k).gamma2(m)

@@ -55,6 +55,7 @@ class PowerStats(ctypes.Structure):
 
 class _Formula(ctypes.Structure):
     _fields_ = [("a", ctypes.c_int32), ("b", ctypes.c_int32), ("n0", ctypes.c_int32),
+                ("r0_k50", ctypes.c_int32),
                 ("alpha", ctypes.c_int32 * MP_MAX_K), ("n_exceptions", ctypes.c_int32),
                 ("exception_m", ctypes.c_int64 * MP_MAX_K), ("exception_gamma2", ctypes.c_int64 * MP_MAX_K)]
 
@@ -62,8 +63,9 @@ class _Formula(ctypes.Structure):
 class _Profile(ctypes.Structure):
     _fields_ = [("product_ms", ctypes.c_double), ("product_launches", ctypes.c_int64),
                 ("dense_steps", ctypes.c_double), ("issued_steps", ctypes.c_double),
-                ("total_ms", ctypes.c_double), ("h2d_bytes", ctypes.c_int64),
-                ("d2h_bytes", ctypes.c_int64), ("kernel", ctypes.c_int32)]
+                ("total_ms", ctypes.c_double), ("setup_ms", ctypes.c_double),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("kernel", ctypes.c_int32)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
@@ -191,7 +193,7 @@ class PeriodicResult:
         exceptions below n0 (Table 7)."""
         f = _Formula()
         _check(lib.mp_gamma2_formula(ctypes.byref(self._raw), ctypes.byref(f)))
-        return {"a": f.a, "b": f.b, "n0": f.n0, "alpha": [f.alpha[k] for k in range(f.a)],
+        return {"a": f.a, "b": f.b, "n0": f.n0, "r0_k50": f.r0_k50, "alpha": [f.alpha[k] for k in range(f.a)],
                 "exceptions": {int(f.exception_m[i]): int(f.exception_gamma2[i]) for i in range(f.n_exceptions)}}
 
 
@@ -327,7 +329,7 @@ def last_profile() -> dict:
     _check(lib.mp_last_profile(ctypes.byref(p)))
     return {"product_ms": p.product_ms, "product_launches": p.product_launches,
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
-            "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
+            "setup_ms": p.setup_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
             "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?")}
 
 

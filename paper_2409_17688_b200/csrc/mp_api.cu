@@ -298,6 +298,7 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
     return MP_OK;
 }
 
+// C = A (x) X with the selected kernel.
 mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
 {
     if (R.spmm) {
@@ -469,9 +470,12 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         int64_t slots = budget / (int64_t)R.slot_bytes();
         slots = std::min<int64_t>(slots, std::max(max_k, 2));
         if (g_opts.budget > 0) slots -= 2;
-        if (slots < 2)
-            return fail(MP_ERR_RESOURCE, "power store needs at least 2 slots of %zu bytes (budget %lld bytes)",
-                        R.slot_bytes(), (long long)budget);
+        // a batched run (small N) needs the whole batch resident; the batch size depends on N
+        // only, so every rank of a sharded run issues the same collective calls
+        const int64_t need = (N <= kBatchMaxN && !cap) ? std::min(kBatch, max_k) + 1 : 2;
+        if (slots < need)
+            return fail(MP_ERR_RESOURCE, "power store needs at least %lld slots of %zu bytes (budget %lld bytes)",
+                        (long long)need, R.slot_bytes(), (long long)budget);
         R.ring.resize((size_t)slots);
         R.slot_power.assign((size_t)slots, 0);
     }
@@ -493,8 +497,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // microseconds, so up to kBatch of them are enqueued back to back and their statistics
     // read with one copy; powers computed past the first repeat are discarded.  The batch
     // depends only on N, so every rank of a sharded run makes the same collective calls.
-    int B = (N <= kBatchMaxN && !cap) ? kBatch : 1;
-    B = std::max(1, std::min<int>(B, (int)R.ring.size() - 1));
+    const int B = (N <= kBatchMaxN && !cap) ? std::min(kBatch, max_k) : 1; // ring >= B + 1 (above)
     if ((int)R.events.size() < 2 * (max_k + 1)) {
         for (auto ev : R.events) cudaEventDestroy(ev);
         R.events.assign((size_t)2 * (max_k + 1), nullptr);
@@ -515,6 +518,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     }
     double prod_ms = 0.0;
     int64_t launches = 0;
+    cudaEvent_t ev_setup;
+    CUDA_TRY(cudaEventCreate(&ev_setup));
+    CUDA_TRY(cudaEventRecord(ev_setup, s));
 
     mp_periodic_result res;
     std::memset(&res, 0, sizeof(res));
@@ -611,7 +617,6 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     CUDA_TRY(cudaEventSynchronize(ev_all1));
     float all_ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&all_ms, ev_all0, ev_all1));
-    cudaEventDestroy(ev_all0);
     cudaEventDestroy(ev_all1);
 
     // dense-equivalent steps count the products up to the first repeat (useful work); the
@@ -622,6 +627,13 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.dense_steps = (double)useful * (double)N * (double)N * (double)R.w;
     g_prof.issued_steps = (double)launches * R.issued_per_product;
     g_prof.total_ms = all_ms;
+    {
+        float sms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&sms, ev_all0, ev_setup));
+        g_prof.setup_ms = sms;
+        cudaEventDestroy(ev_setup);
+        cudaEventDestroy(ev_all0);
+    }
     g_prof.h2d_bytes = g_h2d.load() - h2d0;
     g_prof.d2h_bytes = g_d2h.load() - d2h0;
     g_prof.kernel = R.spmm ? 2 : (R.sparse ? 1 : 0);
@@ -787,6 +799,7 @@ mp_status mp_gamma2_formula(const mp_periodic_result *r, mp_formula *out)
     f.a = r->lambda;
     f.b = r->offset;
     f.n0 = r->mu;
+    f.r0_k50 = (50 >= r->mu + r->lambda) ? 50 - r->lambda : -1;
     auto ceil_div = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
     // boundary values gamma_2(m), n0 <= m < n0 + a (Algorithm 5) fix alpha per residue
     for (int64_t m = r->mu; m < r->mu + r->lambda; ++m) {

@@ -180,6 +180,8 @@ def test_gamma2_formula_reproduces_table7(oracle_mod):
             r.diag_min[k] = v
         f = _native._result(r).formula()
         assert f["a"] == a
+        t4 = {int(x[0]): int(x[1]) for x in golden("table4_recurrence.txt")}
+        assert f["r0_k50"] == t4[n]  # Table 4's r0 (Algorithm 3 with K = 50)
         assert {k for k in range(a) if f["alpha"][k] == 1} == ks, n
         assert all(v in (0, 1) for v in f["alpha"])
         expect_exc = {m: g for (nn, m), g in exc.items() if nn == n}

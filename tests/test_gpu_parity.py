@@ -162,11 +162,12 @@ def test_power_until_periodic_degenerate(mp, oracle_mod):
 
 
 def test_ring_eviction_recompute(mp, oracle_mod):
-    """A device budget of 3 power slots forces the recompute path for evicted A^j (n = 7 has
-    lambda = 18, so the partner of the first repeat is long gone from the ring)."""
+    """A device budget of 17 power slots (the minimum for a 16-power batch) forces the
+    recompute path for evicted A^j: n = 7 has lambda = 18, so the partner of the first repeat
+    has left the ring."""
     A = mp.build_transition_matrix(7)
     slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 511) // 512) * 512) * 2  # Np x ld x 2 B
-    mp.set_options("auto", device_budget_bytes=5 * slot)
+    mp.set_options("auto", device_budget_bytes=19 * slot)  # 19 - 2 reserved = 17 ring slots
     try:
         g = mp.minplus_power_until_periodic(A)
     finally:
@@ -218,6 +219,8 @@ def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
     f = g.formula()  # NEXT-2: Table 7 row and the exception (G15) from the run itself
     assert f["a"] == a and {k for k in range(a) if f["alpha"][k] == 1} == ks
     assert f["exceptions"] == {m: v for (nn, m), v in exc.items() if nn == n}
+    t4 = {int(x[0]): int(x[1]) for x in golden("table4_recurrence.txt")}
+    assert f["r0_k50"] == t4[n]  # Table 4
 
 
 def test_gamma2_small_cycles_all_paths(mp, oracle_mod):

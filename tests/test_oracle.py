@@ -273,6 +273,21 @@ def test_table5_recurrence_n10(oracle_mod, n):
     test_table5_recurrence(oracle_mod, n)
 
 
+@pytest.mark.parametrize("n", range(2, 9))
+def test_algorithms_3_and_4_verbatim(oracle_mod, n):
+    """NEXT-2: the paper's own Algorithm 3 with K = 50 reproduces Table 4 (r0, a, b)
+     and Algorithm 4 from there reproduces Table 5's n0, which equals
+    the forward first-repeat mu ("Why first-repeat detection equals Algs 3/4")."""
+    t4 = {int(r[0]): tuple(map(int, r[1:])) for r in golden("table4_recurrence.txt")}[n]
+    t5 = {int(r[0]): tuple(map(int, r[1:])) for r in golden("table5_recurrence.txt")}[n]
+    P = oracle_mod.powers(oracle_mod.transition_matrix(n), 50)
+    r0, a, b = oracle_mod.algorithm3(P, 50)
+    assert (r0, a, b) == t4
+    assert oracle_mod.algorithm4(P, r0, a, b) == t5[0]
+    r = oracle_mod.power_until_periodic(P[1])
+    assert (r.mu, r.lam, r.offset) == (t5[0], a, b)
+
+
 def test_periodicity_invariants(oracle_mod):
     """Lemma 1 on the oracle's own powers: A^{k+lambda} = b (x) A^k for several
     k >= mu beyond the first repeat; A^{i+j} = A^i x A^j."""
