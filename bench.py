@@ -211,6 +211,7 @@ def run_mine(args):
     launches0 = mp.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prod_ms, prod_launches, dense, issued = 0.0, 0, 0.0, 0.0
+    stats_ms, total_lib_ms, setup_ms = 0.0, 0.0, 0.0
     e0.record(stream)
     for _ in range(args.steps):
         res = mp.minplus_power_until_periodic_device(dA)
@@ -221,6 +222,8 @@ def run_mine(args):
         dense += p["dense_steps"]
         issued += p["issued_steps"]
         setup_ms = p["setup_ms"]
+        stats_ms += p["stats_ms"]
+        total_lib_ms += p["total_ms"]
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -301,6 +304,9 @@ def run_mine(args):
                 "seconds_to_gamma2": e2e_ms / e2e_steps / 1e3,
                 "setup_ms_last_step": e2e_setup_ms},
         "setup_ms": setup_ms,
+        "breakdown_ms_per_step": {"products": prod_ms / args.steps, "stats": stats_ms / args.steps,
+                                  "setup": setup_ms, "library_total": total_lib_ms / args.steps,
+                                  "step": ms / args.steps},
         "gpu_launches": int(launches),
         "clocks": clk,
     }

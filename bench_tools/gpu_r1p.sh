@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sharded.py -q -x -k "not large_n and not n13" > gpurun_out/r1p_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r1p_pytest.log
+for n in 9 11 12; do timeout 300 python bench.py --n $n --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/r1p_bench_n$n.log 2>&1; done

@@ -247,6 +247,7 @@ typedef struct {
     double issued_steps;      /* steps the kernel executed after skipping all-inf A tiles   */
     double total_ms;          /* whole run, first to last operation on the library stream  */
     double setup_ms;          /* of which staging A and building the sparse form (a1-a2)   */
+    double stats_ms;          /* sum of the per-power statistics kernel durations (a4)     */
     int64_t h2d_bytes;        /* host -> device bytes copied by the run                    */
     int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
     int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,

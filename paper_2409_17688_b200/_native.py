@@ -63,7 +63,7 @@ class _Formula(ctypes.Structure):
 class _Profile(ctypes.Structure):
     _fields_ = [("product_ms", ctypes.c_double), ("product_launches", ctypes.c_int64),
                 ("dense_steps", ctypes.c_double), ("issued_steps", ctypes.c_double),
-                ("total_ms", ctypes.c_double), ("setup_ms", ctypes.c_double),
+                ("total_ms", ctypes.c_double), ("setup_ms", ctypes.c_double), ("stats_ms", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("kernel", ctypes.c_int32)]
 
@@ -329,7 +329,7 @@ def last_profile() -> dict:
     _check(lib.mp_last_profile(ctypes.byref(p)))
     return {"product_ms": p.product_ms, "product_launches": p.product_launches,
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
-            "setup_ms": p.setup_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
+            "setup_ms": p.setup_ms, "stats_ms": p.stats_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
             "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?")}
 
 

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -47,6 +48,35 @@ struct Opts {
 
 mp_profile g_prof{};
 std::map<std::tuple<int, int, int>, mp_periodic_result> g_cache; // (n, world, rank)
+
+// MP_TRACE=1: phase timings of each power run on stderr (the stream is synchronised at every
+// mark, so tracing perturbs the timings it reports; for diagnosis, not for benchmarks).
+bool trace_on()
+{
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("MP_TRACE");
+        on = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return on == 1;
+}
+
+struct Tracer {
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0, t;
+    explicit Tracer(cudaStream_t st) : s(st), t0(std::chrono::steady_clock::now()), t(t0) {}
+    void mark(const char *what, int k = -1)
+    {
+        if (!trace_on()) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+        const double tot = std::chrono::duration<double, std::milli>(now - t0).count();
+        if (k >= 0) fprintf(stderr, "mp-trace %-26s k=%-3d %10.3f ms  (%10.3f ms)\n", what, k, ms, tot);
+        else fprintf(stderr, "mp-trace %-32s %10.3f ms  (%10.3f ms)\n", what, ms, tot);
+        t = now;
+    }
+};
 
 mp_status fail(mp_status s, const char *fmt, ...)
 {
@@ -129,7 +159,7 @@ struct DBuf {
 // do not pay cudaMalloc/cudaFree; released by mp_shutdown().
 struct PowerRun {
     int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
-    DBuf at2, words, tmp0, tmp1, ktp, kti, stats, flag;
+    DBuf at2, words, tmp0, tmp1, ktp, kti, occ, stats, flag, stage_raw;
     bool has_at2 = false; // matrix sources and the tile kernels stage AT2; SpMM on words does not
     int n_words = 0;      // path order when A comes from the word masks
     std::vector<DBuf> ring;
@@ -244,11 +274,10 @@ mp_status allreduce(int op, int64_t *dev, int64_t count, cudaStream_t s)
 mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
 {
     const int64_t Mt = R.Np / kBM, Kt = R.Np / kBK;
-    DBuf occ;
-    TRY(occ.alloc((size_t)(Mt * Kt), "tile occupancy"));
-    LAUNCH(launch_tile_occupancy(R.at2.as<uint32_t>(), R.Np, R.Np, occ.as<uint8_t>(), s));
+    TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
+    LAUNCH(launch_tile_occupancy(R.at2.as<uint32_t>(), R.Np, R.Np, R.occ.as<uint8_t>(), s));
     std::vector<uint8_t> h((size_t)(Mt * Kt));
-    COPY(h.data(), occ.p, h.size(), cudaMemcpyDeviceToHost, s);
+    COPY(h.data(), R.occ.p, h.size(), cudaMemcpyDeviceToHost, s);
     CUDA_TRY(cudaStreamSynchronize(s));
     std::vector<int32_t> ptr((size_t)Mt + 1, 0), idx;
     idx.reserve(h.size() / 4);
@@ -258,8 +287,8 @@ mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
         ptr[(size_t)b + 1] = (int32_t)idx.size();
     }
     if (idx.empty()) idx.push_back(0);
-    TRY(R.ktp.alloc(ptr.size() * 4, "tile list pointers"));
-    TRY(R.kti.alloc(idx.size() * 4, "tile list"));
+    TRY(R.ktp.ensure(ptr.size() * 4, "tile list pointers"));
+    TRY(R.kti.ensure(idx.size() * 4, "tile list"));
     COPY(R.ktp.p, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice, s);
     COPY(R.kti.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s);
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -375,6 +404,8 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     CUDA_TRY(cudaEventCreate(&ev_all0));
     CUDA_TRY(cudaEventCreate(&ev_all1));
     CUDA_TRY(cudaEventRecord(ev_all0, s));
+    Tracer tr(s);
+    tr.mark("start");
 
     if (!st->pr) st->pr.reset(new PowerRun());
     PowerRun &R = *st->pr;
@@ -412,20 +443,19 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     if (R.has_at2) {
         TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
         if (src.dev || src.host) {
-            DBuf raw, flag;
             const uint16_t *dA = src.dev;
             int64_t lda = src.lda;
-            if (src.host) {
-                TRY(raw.alloc((size_t)N * N * 2, "A staging"));
-                COPY(raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
-                dA = raw.as<uint16_t>();
+            if (src.host) { // staging buffer kept with the workspace (no 2N^2-byte malloc per call)
+                TRY(R.stage_raw.ensure((size_t)N * N * 2, "A staging"));
+                COPY(R.stage_raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+                dA = R.stage_raw.as<uint16_t>();
                 lda = N;
             }
-            TRY(flag.alloc(16, "range flag"));
-            CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-            LAUNCH(launch_make_at2(dA, lda, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, flag.as<int>(), s));
+            TRY(R.flag.ensure(16, "range flag"));
+            CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, sizeof(int), s));
+            LAUNCH(launch_make_at2(dA, lda, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, R.flag.as<int>(), s));
             int hflag = 0;
-            COPY(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+            COPY(&hflag, R.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
             CUDA_TRY(cudaStreamSynchronize(s));
             if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
         } else {
@@ -435,6 +465,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.at2.release();
     }
 
+    tr.mark("a2 stage A");
     // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
     R.sparse = R.spmm = false;
     if (!R.has_at2) {
@@ -458,6 +489,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         }
     }
 
+    tr.mark(R.spmm ? "kernel choice: spmm" : "kernel choice: tiles");
     // power store: a ring of device slots (allocated on first use, kept across calls)
     {
         size_t freeb = 0, totalb = 0;
@@ -479,6 +511,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.ring.resize((size_t)slots);
         R.slot_power.assign((size_t)slots, 0);
     }
+    tr.mark("power store");
     // per-power statistics: SUM fields {H, inf count} for k = 0..max_k, then MIN fields
     // {diag min, first finite entry}, so a batch of powers reduces with one call of each
     const size_t nst = (size_t)(max_k + 1) * 2;
@@ -498,9 +531,10 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // read with one copy; powers computed past the first repeat are discarded.  The batch
     // depends only on N, so every rank of a sharded run makes the same collective calls.
     const int B = (N <= kBatchMaxN && !cap) ? std::min(kBatch, max_k) : 1; // ring >= B + 1 (above)
-    if ((int)R.events.size() < 2 * (max_k + 1)) {
+    // events: [0, 2(max_k+1)) product start/stop per power, then stats start, stats stop
+    if ((int)R.events.size() < 4 * (max_k + 1)) {
         for (auto ev : R.events) cudaEventDestroy(ev);
-        R.events.assign((size_t)2 * (max_k + 1), nullptr);
+        R.events.assign((size_t)4 * (max_k + 1), nullptr);
         for (auto &ev : R.events) CUDA_TRY(cudaEventCreate(&ev));
     }
 
@@ -516,11 +550,12 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         CUDA_TRY(cudaStreamSynchronize(s));
         g_unit_cache[N] = S;
     }
-    double prod_ms = 0.0;
+    double prod_ms = 0.0, stats_ms = 0.0;
     int64_t launches = 0;
     cudaEvent_t ev_setup;
     CUDA_TRY(cudaEventCreate(&ev_setup));
     CUDA_TRY(cudaEventRecord(ev_setup, s));
+    tr.mark("statistics init");
 
     mp_periodic_result res;
     std::memset(&res, 0, sizeof(res));
@@ -544,8 +579,10 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
                 ++launches;
             }
+            if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s)); // stats start
             LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
                                 reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
+            if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[3 * (max_k + 1) + k], s)); // stats end
             prev = dst;
         }
         const int nb = ke - kb + 1;
@@ -554,12 +591,15 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         COPY(hsum.data() + 2 * kb, st_sum + 2 * kb, (size_t)nb * 16, cudaMemcpyDeviceToHost, s);
         COPY(hmin.data() + 2 * kb, st_min + 2 * kb, (size_t)nb * 16, cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));
+        tr.mark("powers + statistics", ke);
 
         for (int k = kb; k <= ke && !found; ++k) {
             if (k >= 2) {
                 float ms = 0.f;
                 CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[2 * k + 1]));
                 prod_ms += ms;
+                CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * (max_k + 1) + k], R.events[3 * (max_k + 1) + k]));
+                stats_ms += ms;
             }
             mp_power_stats &cs = hs[(size_t)k];
             cs.fingerprint = hsum[2 * k];
@@ -623,6 +663,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // launches and their time include any product of the batch computed past it
     const int64_t useful = found && !cap ? (int64_t)res.k_last - 1 : launches;
     g_prof.product_ms = prod_ms;
+    g_prof.stats_ms = stats_ms;
     g_prof.product_launches = launches;
     g_prof.dense_steps = (double)useful * (double)N * (double)N * (double)R.w;
     g_prof.issued_steps = (double)launches * R.issued_per_product;

@@ -165,9 +165,29 @@ __global__ void __launch_bounds__(256)
     for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
         const uint64_t tbase = (uint64_t)(i * N + c0);
         const uint16_t *row = X + i * ld;
+        if (threadIdx.x == 0 && i >= c0 && i < c0 + w) { // the row's diagonal entry, if in the shard
+            const uint32_t x = row[i - c0];
+            dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
+        }
         for (int64_t j0 = (int64_t)threadIdx.x * 8; j0 < w; j0 += (int64_t)blockDim.x * 8) {
             const uint4 v = *reinterpret_cast<const uint4 *>(row + j0);
             const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+            // fast path: a full chunk without +inf (every power from k = 3 on) needs no
+            // +inf bookkeeping, and its smallest finite key is its first entry
+            const bool full = j0 + 8 <= w;
+            const uint32_t anyinf = __vcmpeq2(v.x, 0x7FFF7FFFu) | __vcmpeq2(v.y, 0x7FFF7FFFu) |
+                                    __vcmpeq2(v.z, 0x7FFF7FFFu) | __vcmpeq2(v.w, 0x7FFF7FFFu);
+            if (full && !anyinf) {
+                const uint64_t t0 = tbase + (uint64_t)j0;
+                const unsigned long long key = (t0 << 16) | (v.x & 0xFFFFu);
+                if (key < ref) ref = key;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                    h += (unsigned long long)mix64(t0 + (uint64_t)e) * x;
+                }
+                continue;
+            }
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int64_t j = j0 + e;
@@ -182,7 +202,6 @@ __global__ void __launch_bounds__(256)
                     if (key < ref) ref = key;
                 }
                 h += (unsigned long long)mix64(t) * x;
-                if (c0 + j == i && x < dmin) dmin = x;
             }
         }
     }
