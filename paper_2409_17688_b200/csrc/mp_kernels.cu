@@ -624,6 +624,10 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void *src)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
+}
 
 // acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's four
 // packed column pairs.
@@ -664,8 +668,10 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
     constexpr int XB = kSpChunk * kSpCols * 2;    // 16 KB of X rows
     constexpr int EB = kSpGroups * kSpChunk * 48; // up to 3 KB of entries
     constexpr int BB = 48;                        // the chunk's 5 entry offsets (int64)
-    constexpr int STAGE = XB + EB + BB;
+    constexpr int MB = 16 + kSpChunk * 4;         // NEXT chunk's entry range + X row indices
+    constexpr int STAGE = XB + EB + BB + MB;
     constexpr int RPT = kSpChunk / 2;             // X rows each warp stages per chunk
+    static_assert(STAGES == 2, "the next-chunk metadata is staged one chunk ahead (2-stage ring)");
     const int t = blockIdx.y, bx = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int32_t *Lt = L + tptr[t];
@@ -675,40 +681,33 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
     const int64_t col0 = (int64_t)bx * kSpCols;
     const uint32_t sbase = smem_addr(smem);
 
-    // Register prefetch of what load_stage needs for the next chunk (its X row indices and
-    // entry range), issued one chunk ahead so the global-load latency hides behind compute.
-    // The entry range is addressed through an opaque zero so the compiler treats it as
-    // per-thread data: kept in ordinary registers it is first waited on where load_stage uses
-    // it, instead of being converted to a uniform register (R2UR) right after the load.
-    int32_t pl[RPT];
-    int64_t pe0 = 0, pe1 = 0;
-    int opaque0;
-    asm("mov.u32 %0, 0;" : "=r"(opaque0));
-    auto prefetch = [&](int c) {
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-            const int u = c * kSpChunk + warp + 2 * k;
-            pl[k] = (c < nch && u < U) ? ldg_nc_s32(Lt + u) : -1;
-        }
-        if (c < nch) {
-            pe0 = ldg_nc_s64(eoff + (c0 + c) * kSpGroups + opaque0);
-            pe1 = ldg_nc_s64(eoff + (c0 + c + 1) * kSpGroups + opaque0);
-        }
-    };
-    auto load_stage = [&](int stage, int c) {
+    // What load_stage(c) needs before it can issue its copies -- chunk c's entry range and
+    // X row indices -- travels through shared memory: load_stage(c-1) stages it with chunk
+    // c-1 by cp.async, so it has landed when the ring wait for chunk c-1 returns, and no
+    // global-load latency is exposed at a chunk boundary.  Chunk 0 reads it from global memory.
+    auto load_stage = [&](int stage, int c, const int64_t *range, const int32_t *rows) {
         const uint32_t sX = sbase + stage * STAGE;
         const uint32_t sE = sX + XB;
+        const uint32_t sM = sE + EB + BB;
 #pragma unroll
-        for (int k = 0; k < RPT; ++k)
-            if (pl[k] >= 0) { // each lane copies two 16-byte pieces of the 1 KB row
-                const uint16_t *src = X + (int64_t)pl[k] * ldx + col0;
-                const uint32_t dst = sX + (warp + 2 * k) * (kSpCols * 2);
+        for (int k = 0; k < RPT; ++k) {
+            const int r = warp + 2 * k;
+            if (c * kSpChunk + r < U) { // each lane copies two 16-byte pieces of the 1 KB row
+                const uint16_t *src = X + (int64_t)rows[r] * ldx + col0;
+                const uint32_t dst = sX + r * (kSpCols * 2);
                 cp_async16(dst + lane * 16, src + lane * 8);
                 cp_async16(dst + 512 + lane * 16, src + 256 + lane * 8);
             }
-        const int nq = (int)(pe1 - pe0) * 3;
-        for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * pe0 + q);
+        }
+        const int64_t e0 = range[0];
+        const int nq = (int)(range[1] - e0) * 3;
+        for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * e0 + q);
         if (tid <= kSpGroups) cp_async8(sE + EB + tid * 8, eoff + (c0 + c) * kSpGroups + tid);
+        if (c + 1 < nch) { // metadata of chunk c+1
+            if (tid < 2) cp_async8(sM + tid * 8, eoff + (c0 + c + 1 + tid) * kSpGroups);
+            const int u = (c + 1) * kSpChunk + (tid - 2);
+            if (tid >= 2 && tid < 2 + kSpChunk && u < U) cp_async4(sM + 16 + (tid - 2) * 4, Lt + u);
+        }
     };
 
     uint32_t acc[kSpGroups][8][4];
@@ -719,24 +718,25 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
 #pragma unroll
             for (int p = 0; p < 4; ++p) acc[j][r][p] = 0xFFFFFFFFu;
 
-    prefetch(0);
+    if (nch > 0) { // chunk 0: metadata straight from global memory
+        int64_t range0[2] = {eoff[c0 * kSpGroups], eoff[(c0 + 1) * kSpGroups]};
+        int32_t rows0[kSpChunk];
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nch) load_stage(s, s);
-        cp_async_commit();
-        prefetch(s + 1);
+        for (int r = 0; r < kSpChunk; ++r) rows0[r] = (r < U) ? Lt[r] : 0;
+        load_stage(0, 0, range0, rows0);
     }
+    cp_async_commit();
     const int xoff = warp * 128 + lane * 4; // this lane's four packed pairs within a staged row
     for (int c = 0; c < nch; ++c) {
-        cp_async_wait<STAGES - 2>();
+        cp_async_wait<0>();
         __syncthreads();
-        {
-            const int cn = c + STAGES - 1;
-            if (cn < nch) load_stage(cn % STAGES, cn);
-            cp_async_commit();
-            prefetch(cn + 1);
+        if (c + 1 < nch) { // chunk c+1's metadata arrived with chunk c
+            const uint8_t *meta = smem + (c & 1) * STAGE + XB + EB + BB;
+            load_stage((c + 1) & 1, c + 1, reinterpret_cast<const int64_t *>(meta),
+                       reinterpret_cast<const int32_t *>(meta + 16));
         }
-        const uint8_t *stage_p = smem + (c % STAGES) * STAGE;
+        cp_async_commit();
+        const uint8_t *stage_p = smem + (c & 1) * STAGE;
         const uint32_t *Xs = reinterpret_cast<const uint32_t *>(stage_p);
         const uint4 *Es = reinterpret_cast<const uint4 *>(stage_p + XB);
         const int64_t *Bs = reinterpret_cast<const int64_t *>(stage_p + XB + EB);
@@ -744,33 +744,40 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
         int bound[kSpGroups + 1];
 #pragma unroll
         for (int j = 0; j <= kSpGroups; ++j) bound[j] = (int)(Bs[j] - eb);
-        // Entries of group j, software-pipelined one entry ahead with ping-pong register sets:
-        // the next entry's loads are unconditional (an index past the chunk reads padding inside
-        // the shared allocation; the row index is masked into the chunk), so the scheduler can
-        // issue the LDS chain entry -> row -> X row ahead of the current entry's 16 DPX.
+        // The chunk's entries (group 0's, then group 1's, ...) are walked as ONE stream,
+        // software-pipelined across group boundaries: row offsets two entries ahead, values and
+        // X rows one entry ahead (ping-pong register sets A/B), so the LDS chain
+        // entry -> row -> X row of the next entry -- even when it opens the next group -- runs
+        // under the current entry's 32 DPX.  The look-ahead loads are unconditional: an index
+        // past the chunk reads padding inside the shared allocation and its row offset is masked
+        // into the chunk.
+        const uint32_t *Xl = Xs + xoff;
+        auto row = [&](int q) { return (int)(Es[3 * q + 2].x & ((kSpChunk - 1) * kSpRowU32)); };
+        int e = 0;
+        int sa = row(0), sb = row(1);
+        uint4 pa0 = Es[0], pa1 = Es[1];
+        uint4 xa = *reinterpret_cast<const uint4 *>(Xl + sa);
 #pragma unroll
         for (int j = 0; j < kSpGroups; ++j) {
-            int e = bound[j];
             const int ee = bound[j + 1];
-            if (e >= ee) continue;
-            // row offsets run two entries ahead, values and X rows one entry ahead
-            const uint32_t *Xl = Xs + xoff;
-            auto row = [&](int q) { return (int)(Es[3 * q + 2].x & ((kSpChunk - 1) * kSpRowU32)); };
-            int sa = row(e), sb = row(e + 1);
-            uint4 pa0 = Es[3 * e], pa1 = Es[3 * e + 1];
-            uint4 xa = *reinterpret_cast<const uint4 *>(Xl + sa);
-            while (true) {
+            while (e < ee) { // entry e is in A
                 const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
                 const uint4 xb = *reinterpret_cast<const uint4 *>(Xl + sb);
                 sa = row(e + 2);
                 dpx_group(acc[j], pa0, pa1, xa);
-                if (e + 1 >= ee) break;
+                if (e + 1 >= ee) { // entry e+1 opens the next group: hand it over in A
+                    pa0 = pb0;
+                    pa1 = pb1;
+                    xa = xb;
+                    sb = sa;
+                    e += 1;
+                    break;
+                }
                 pa0 = Es[3 * e + 6];
                 pa1 = Es[3 * e + 7];
                 xa = *reinterpret_cast<const uint4 *>(Xl + sa);
                 sb = row(e + 3);
                 dpx_group(acc[j], pb0, pb1, xb);
-                if (e + 2 >= ee) break;
                 e += 2;
             }
         }
@@ -903,7 +910,7 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
 {
     static bool attr_set = false;
     // + 64 B: the pipelined entry loop may read up to three uint4 past the last stage
-    const int smem = STAGES * (kSpChunk * kSpCols * 2 + kSpGroups * kSpChunk * 48 + 48) + 64;
+    const int smem = STAGES * (kSpChunk * kSpCols * 2 + kSpGroups * kSpChunk * 48 + 48 + 16 + kSpChunk * 4) + 64;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_spmm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
@@ -914,23 +921,12 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
     return cudaGetLastError();
 }
 
-// Pipeline depth of k_spmm: 2 stages (5 CTAs = 10 warps per SM) by default; MP_SPMM_STAGES=3
-// selects the 3-stage ring (4 CTAs per SM) for comparison.
-static int spmm_stages()
-{
-    static int st = 0;
-    if (!st) {
-        const char *e = getenv("MP_SPMM_STAGES");
-        st = (e && atoi(e) == 3) ? 3 : 2;
-    }
-    return st;
-}
-
+// k_spmm runs a 2-stage ring (5 CTAs = 10 warps per SM); a 3-stage ring measured slower
+// (fewer CTAs per SM: 155.7 vs 138.6 ms per n = 12 product in the v3 kernel).
 cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
                         int64_t ncols_p, cudaStream_t s)
 {
-    return spmm_stages() == 3 ? launch_spmm_t<3>(sa, X, ldx, C, ldc, Mp, ncols_p, s)
-                              : launch_spmm_t<2>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
+    return launch_spmm_t<2>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
 }
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
