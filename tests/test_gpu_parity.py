@@ -223,6 +223,24 @@ def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
     assert f["r0_k50"] == t4[n]  # Table 4
 
 
+@pytest.mark.parametrize("kernel", ["spmm", "tiles"])
+def test_gamma2_record_words_source(mp, oracle_mod, kernel):
+    """The gamma2_cylinder path builds A(D_n) on the device from the word masks (with SpMM no
+    AT2 at all): its whole record -- every power's fingerprint included -- equals the oracle's
+    run on the oracle's own transition matrix."""
+    mp.shutdown()  # drop the cached records
+    mp.set_options(kernel)
+    try:
+        for n in range(2, 10):
+            g = mp.gamma2_record(n)
+            o = oracle_mod.power_until_periodic(oracle_mod.transition_matrix(n))
+            assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+            assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint, n
+    finally:
+        mp.set_options("auto")
+        mp.shutdown()
+
+
 def test_gamma2_small_cycles_all_paths(mp, oracle_mod):
     """gamma_2(P_n x C_m) for every path order n <= 13 at cycle lengths m <= 8 against the
     DP along the path (a graph oracle independent of the transfer matrix): pins the full-size
