@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 // VIADDMNMX.U16x2 (8 rows x 4 pairs) -- enough DPX per entry to keep the issue slots of the
 // shared-memory and loop instructions below the ALU pipe's rate.  Issued steps =
 // 8 * entries * ld; every skipped term is an all-+inf one, so the result is the same product.
-// Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowU32, 0, 0, 0}, s = row in the chunk.
+// Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowBytes, 0, 0, 0}, s = row in the chunk.
 // ---------------------------------------------------------------------------------------
 constexpr int kG = 8;
 constexpr int kSpRows = 32;
@@ -430,7 +430,7 @@ constexpr int kSpGroups = kSpRows / kG;
 constexpr int kSpChunk = 16;
 constexpr int kSpThreads = 64;
 constexpr int kSpCols = 512;            // columns per CTA (2 warps x 32 lanes x 8)
-constexpr int kSpRowU32 = kSpCols / 2;  // one staged X row, in packed u32 pairs
+constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
 static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
 // How the sparse-form builders read A: the 8 duplicated values of rows 8g..8g+7 at column l.
@@ -579,7 +579,7 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
                 acc.row8(g, l, v0, v1);
                 E[3 * e] = v0;
                 E[3 * e + 1] = v1;
-                E[3 * e + 2] = make_uint4((unsigned)s * (unsigned)kSpRowU32, 0u, 0u, 0u); // X row offset (u32)
+                E[3 * e + 2] = make_uint4((unsigned)s * (unsigned)kSpRowBytes, 0u, 0u, 0u); // X row offset (bytes)
                 ++e;
             }
             ++cnt;
@@ -643,6 +643,15 @@ __device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][4], const uint4 &a0
     }
 }
 
+// 16-byte shared load from a 32-bit shared-window address (lane base + uniform offset folds
+// into one LDS [R + UR]).
+__device__ __forceinline__ uint4 lds128(uint32_t addr)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
 // Non-coherent global loads kept at their program position (asm volatile), so a prefetch
 // issued one chunk ahead is not sunk next to its use by the scheduler.
 __device__ __forceinline__ int32_t ldg_nc_s32(const int32_t *p)
@@ -666,7 +675,9 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
 {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int XB = kSpChunk * kSpCols * 2;    // 16 KB of X rows
-    constexpr int EB = kSpGroups * kSpChunk * 48; // up to 3 KB of entries
+    // up to 64 entries (3 KB) + 3 entries the pipelined walk may look ahead into (kept zero or
+    // stale-but-valid, so a look-ahead row offset always lands inside the stage's X rows)
+    constexpr int EB = (kSpGroups * kSpChunk + 3) * 48;
     constexpr int BB = 48;                        // the chunk's 5 entry offsets (int64)
     constexpr int MB = 16 + kSpChunk * 4;         // NEXT chunk's entry range + X row indices
     constexpr int STAGE = XB + EB + BB + MB;
@@ -718,6 +729,11 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
 #pragma unroll
             for (int p = 0; p < 4; ++p) acc[j][r][p] = 0xFFFFFFFFu;
 
+    // Zero both stages' entry areas once: until cp.async overwrites them, look-ahead reads of
+    // entries past a chunk's end then see row offset 0.
+    for (int q = tid; q < STAGES * (EB / 16); q += kSpThreads)
+        reinterpret_cast<uint4 *>(smem + (q / (EB / 16)) * STAGE + XB)[q % (EB / 16)] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
     if (nch > 0) { // chunk 0: metadata straight from global memory
         int64_t range0[2] = {eoff[c0 * kSpGroups], eoff[(c0 + 1) * kSpGroups]};
         int32_t rows0[kSpChunk];
@@ -749,20 +765,20 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
         // X rows one entry ahead (ping-pong register sets A/B), so the LDS chain
         // entry -> row -> X row of the next entry -- even when it opens the next group -- runs
         // under the current entry's 32 DPX.  The look-ahead loads are unconditional: an index
-        // past the chunk reads padding inside the shared allocation and its row offset is masked
-        // into the chunk.
-        const uint32_t *Xl = Xs + xoff;
-        auto row = [&](int q) { return (int)(Es[3 * q + 2].x & ((kSpChunk - 1) * kSpRowU32)); };
+        // past the chunk reads a zero or stale record of the entry area, whose row offset is a
+        // valid one.  Row offsets are bytes, so an X load is one LDS [lane base + offset].
+        const uint32_t Xl = smem_addr(Xs + xoff);
+        auto row = [&](int q) { return (int)Es[3 * q + 2].x; };
         int e = 0;
         int sa = row(0), sb = row(1);
         uint4 pa0 = Es[0], pa1 = Es[1];
-        uint4 xa = *reinterpret_cast<const uint4 *>(Xl + sa);
+        uint4 xa = lds128(Xl + sa);
 #pragma unroll
         for (int j = 0; j < kSpGroups; ++j) {
             const int ee = bound[j + 1];
             while (e < ee) { // entry e is in A
                 const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
-                const uint4 xb = *reinterpret_cast<const uint4 *>(Xl + sb);
+                const uint4 xb = lds128(Xl + sb);
                 sa = row(e + 2);
                 dpx_group(acc[j], pa0, pa1, xa);
                 if (e + 1 >= ee) { // entry e+1 opens the next group: hand it over in A
@@ -775,7 +791,7 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
                 }
                 pa0 = Es[3 * e + 6];
                 pa1 = Es[3 * e + 7];
-                xa = *reinterpret_cast<const uint4 *>(Xl + sa);
+                xa = lds128(Xl + sa);
                 sb = row(e + 3);
                 dpx_group(acc[j], pb0, pb1, xb);
                 e += 2;
@@ -910,7 +926,7 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
 {
     static bool attr_set = false;
     // + 64 B: the pipelined entry loop may read up to three uint4 past the last stage
-    const int smem = STAGES * (kSpChunk * kSpCols * 2 + kSpGroups * kSpChunk * 48 + 48 + 16 + kSpChunk * 4) + 64;
+    const int smem = STAGES * (kSpChunk * kSpCols * 2 + (kSpGroups * kSpChunk + 3) * 48 + 48 + 16 + kSpChunk * 4) + 64;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_spmm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
