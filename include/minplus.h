@@ -268,6 +268,12 @@ mp_status mp_set_stream(void *stream);
  * the power store (0 = min(48 GiB, 90 % of free device memory)).  Errors: MP_ERR_DOMAIN. */
 mp_status mp_set_options(int sparsity, int64_t device_budget_bytes);
 
+/* Row grouping of the SpMM kernel (sparsity 2): 0 = groups of 8 consecutive rows; 1 = rows
+ * grouped greedily by support overlap in windows of 512 rows (fewer issued steps, same
+ * product); -1 = automatic (the default: greedy from N >= 8192).
+ * Process-wide.  Errors: MP_ERR_DOMAIN. */
+mp_status mp_set_grouping(int mode);
+
 #ifdef __cplusplus
 }
 #endif

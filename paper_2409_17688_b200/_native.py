@@ -30,7 +30,7 @@ EXPORTS = [
     "gamma2_cylinder",
     "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
-    "mp_last_profile", "mp_set_options", "mp_gamma2_formula", "mp_gamma2_record",
+    "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_gamma2_formula", "mp_gamma2_record",
 ]
 
 
@@ -100,6 +100,7 @@ def _load() -> ctypes.CDLL:
         "mp_kernel_launches": ([], i64),
         "mp_last_profile": ([P], i32),
         "mp_set_options": ([i32, i64], i32),
+        "mp_set_grouping": ([i32], i32),
         "mp_gamma2_formula": ([P, P], i32),
         "mp_gamma2_record": ([i32, P], i32),
     }
@@ -339,6 +340,14 @@ SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}
 def set_options(sparsity: str = "auto", device_budget_bytes: int = 0) -> None:
     """Product kernel of the power runs: "auto" | "dense" | "tiles" | "spmm" (all exact)."""
     _check(lib.mp_set_options(SPARSITY[sparsity], device_budget_bytes))
+
+
+GROUPING = {"auto": -1, "consecutive": 0, "greedy": 1}
+
+
+def set_grouping(mode: str = "auto") -> None:
+    """Row grouping of the SpMM kernel: "auto" | "consecutive" | "greedy" (same product)."""
+    _check(lib.mp_set_grouping(GROUPING[mode]))
 
 
 def version() -> str:

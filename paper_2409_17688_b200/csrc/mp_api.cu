@@ -44,7 +44,9 @@ struct Dist {
 struct Opts {
     int sparsity = -1; // -1 auto, 0 dense tiles, 1 block-sparse tiles, 2 grouped SpMM
     int64_t budget = 0;
+    int grouping = -1; // -1 auto (greedy from kGroupMinN rows), 0 consecutive rows, 1 greedy
 } g_opts;
+constexpr int64_t kGroupMinN = 8192; // below this the grouping pass costs more than it saves
 
 mp_profile g_prof{};
 std::map<std::tuple<int, int, int>, mp_periodic_result> g_cache; // (n, world, rank)
@@ -160,7 +162,9 @@ struct DBuf {
 struct PowerRun {
     int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
     DBuf at2, words, tmp0, tmp1, ktp, kti, occ, stats, flag, stage_raw;
-    bool has_at2 = false; // matrix sources and the tile kernels stage AT2; SpMM on words does not
+    bool has_at2 = false; // only the tile kernels stage AT2; SpMM reads A or the word masks
+    const uint16_t *a_src = nullptr; // matrix sources: A (boundary encoding; the caller's buffer or
+    int64_t a_ld = 0;                // stage_raw), valid for the duration of the run
     int n_words = 0;      // path order when A comes from the word masks
     std::vector<DBuf> ring;
     std::vector<int> slot_power;
@@ -271,11 +275,10 @@ mp_status allreduce(int op, int64_t *dev, int64_t count, cudaStream_t s)
 }
 
 // Block-sparse l-tile lists of A (exact skipping of all-inf tiles).
+// R.occ holds the 128 x 32 tile occupancy (launch_check_a or launch_tile_occupancy).
 mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
 {
     const int64_t Mt = R.Np / kBM, Kt = R.Np / kBK;
-    TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
-    LAUNCH(launch_tile_occupancy(R.at2.as<uint32_t>(), R.Np, R.Np, R.occ.as<uint8_t>(), s));
     std::vector<uint8_t> h((size_t)(Mt * Kt));
     COPY(h.data(), R.occ.p, h.size(), cudaMemcpyDeviceToHost, s);
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -312,10 +315,11 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
     R.sp_next = 0;
     R.sp = SparseWork();
     int64_t launches = 0;
+    const bool group = g_opts.grouping == 1 || (g_opts.grouping < 0 && R.N >= kGroupMinN);
     const cudaError_t e =
-        R.has_at2 ? build_sparse_form(R.at2.as<uint32_t>(), R.Np, R.sp, s, sp_alloc, &R, &launches)
-                  : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, R.sp, s, sp_alloc, &R,
-                                            &launches);
+        R.a_src ? build_sparse_form(R.a_src, R.a_ld, R.N, R.Np, group, R.sp, s, sp_alloc, &R, &launches)
+                : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, group, R.sp, s, sp_alloc,
+                                            &R, &launches);
     g_launches.fetch_add(launches);
     g_d2h.fetch_add(24);
     if (e == cudaErrorMemoryAllocation) return MP_ERR_RESOURCE; // message set by DBuf::alloc
@@ -337,6 +341,7 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
         sa.tch = R.sp.tch;
         sa.eoff = R.sp.eoff;
         sa.E = R.sp.E;
+        sa.rows = R.sp.rows;
         LAUNCH(launch_spmm(sa, X, R.ld, C, R.ld, R.Np, R.ld, s));
         return MP_OK;
     }
@@ -345,10 +350,12 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
     return MP_OK;
 }
 
-// X_1 = A[:, c0:c0+w) in the device layout, from AT2 or straight from the word masks.
+// X_1 = A[:, c0:c0+w) in the device layout, from A, AT2 or straight from the word masks.
 mp_status make_power1(PowerRun &R, uint16_t *dst, cudaStream_t s)
 {
-    if (R.has_at2)
+    if (R.a_src) // range-checked already: the flag is scratch
+        LAUNCH(launch_encode(R.a_src + R.c0, R.a_ld, R.N, R.w, dst, R.ld, R.Np, R.flag.as<int>(), s));
+    else if (R.has_at2)
         LAUNCH(launch_x1_from_at2(R.at2.as<uint32_t>(), R.Np, R.c0, R.w, dst, R.ld, s));
     else
         LAUNCH(launch_x1_from_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, R.c0, R.w, dst, R.ld, s));
@@ -429,65 +436,77 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.cached_slot = R.slot_bytes();
     }
 
-    // a2: stage A.  Matrix sources: AT2 (transposed, duplicated, device encoding).  The words
-    // source with the SpMM kernel needs no AT2 at all: the sparse form and every regeneration
-    // of A^1 come straight from the word masks (69 GB saved at n = 13).
+    // a2: stage A.  Matrix sources are range-checked in place (host ones copied to a staging
+    // buffer first) and read directly by the SpMM sparse-form builder and by X_1; only the tile
+    // kernels need AT2 (transposed, duplicated, device encoding), built once they are chosen.
+    // The words source with SpMM needs no matrix at all (69 GB saved at n = 13).
     const bool words_src = !src.dev && !src.host;
-    R.has_at2 = !words_src || g_opts.sparsity == 0 || g_opts.sparsity == 1;
     R.n_words = words_src ? src.n : 0;
+    R.a_src = nullptr;
+    R.a_ld = 0;
+    TRY(R.flag.ensure(16, "range flag"));
+    const int64_t Mt = R.Np / kBM, Kt = R.Np / kBK;
     if (words_src) {
         std::vector<WordMask> words = enumerate_words(src.n);
         TRY(R.words.ensure(words.size() * sizeof(WordMask), "word masks"));
         COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
-    }
-    if (R.has_at2) {
-        TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
-        if (src.dev || src.host) {
-            const uint16_t *dA = src.dev;
-            int64_t lda = src.lda;
-            if (src.host) { // staging buffer kept with the workspace (no 2N^2-byte malloc per call)
-                TRY(R.stage_raw.ensure((size_t)N * N * 2, "A staging"));
-                COPY(R.stage_raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
-                dA = R.stage_raw.as<uint16_t>();
-                lda = N;
-            }
-            TRY(R.flag.ensure(16, "range flag"));
-            CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, sizeof(int), s));
-            LAUNCH(launch_make_at2(dA, lda, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, R.flag.as<int>(), s));
-            int hflag = 0;
-            COPY(&hflag, R.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
-            CUDA_TRY(cudaStreamSynchronize(s));
-            if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
-        } else {
-            LAUNCH(launch_build_from_words(R.words.as<WordMask>(), N, src.n, R.at2.as<uint32_t>(), R.Np, s));
-        }
     } else {
-        R.at2.release();
+        R.a_src = src.dev;
+        R.a_ld = src.lda;
+        if (src.host) { // staging buffer kept with the workspace (no 2N^2-byte malloc per call)
+            TRY(R.stage_raw.ensure((size_t)N * N * 2, "A staging"));
+            COPY(R.stage_raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+            R.a_src = R.stage_raw.as<uint16_t>();
+            R.a_ld = N;
+        }
+        const bool need_occ = g_opts.sparsity != 0 && g_opts.sparsity != 2;
+        if (need_occ) {
+            TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
+            CUDA_TRY(cudaMemsetAsync(R.occ.p, 0, (size_t)(Mt * Kt), s));
+        }
+        CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, sizeof(int), s));
+        LAUNCH(launch_check_a(R.a_src, R.a_ld, N, R.Np, need_occ ? R.occ.as<uint8_t>() : nullptr, R.flag.as<int>(), s));
+        int hflag = 0;
+        COPY(&hflag, R.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
     }
-
     tr.mark("a2 stage A");
+
     // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
     R.sparse = R.spmm = false;
-    if (!R.has_at2) {
+    R.has_at2 = false;
+    if (g_opts.sparsity == 2 || (g_opts.sparsity < 0 && words_src)) {
         TRY(build_sparse(R, s));
         R.spmm = true;
         R.issued_per_product = R.issued_spmm;
     } else {
-        if (g_opts.sparsity != 0) TRY(build_tile_lists(R, s));
-        if (g_opts.sparsity == 2 || g_opts.sparsity < 0) TRY(build_sparse(R, s));
-        if (g_opts.sparsity == 0) {
-            R.issued_per_product = (double)R.Np * R.Np * (double)R.ld;
-        } else if (g_opts.sparsity == 1) {
-            R.sparse = true;
-            R.issued_per_product = R.issued_tiles;
-        } else if (g_opts.sparsity == 2 || R.issued_spmm < kSpmmAdvantage * R.issued_tiles) {
-            R.spmm = true;
-            R.issued_per_product = R.issued_spmm;
-        } else {
-            R.sparse = true;
-            R.issued_per_product = R.issued_tiles;
+        if (g_opts.sparsity != 0 && !words_src) TRY(build_tile_lists(R, s)); // occupancy from A
+        if (g_opts.sparsity < 0) { // matrix source, auto
+            TRY(build_sparse(R, s));
+            if (R.issued_spmm < kSpmmAdvantage * R.issued_tiles) {
+                R.spmm = true;
+                R.issued_per_product = R.issued_spmm;
+            }
+        }
+        if (!R.spmm) { // the tile kernels: stage AT2
+            TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
+            if (words_src) {
+                LAUNCH(launch_build_from_words(R.words.as<WordMask>(), N, src.n, R.at2.as<uint32_t>(), R.Np, s));
+                if (g_opts.sparsity != 0) {
+                    TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
+                    LAUNCH(launch_tile_occupancy(R.at2.as<uint32_t>(), R.Np, R.Np, R.occ.as<uint8_t>(), s));
+                    TRY(build_tile_lists(R, s));
+                }
+            } else {
+                LAUNCH(launch_make_at2(R.a_src, R.a_ld, N, N, R.at2.as<uint32_t>(), R.Np, R.Np, R.flag.as<int>(), s));
+            }
+            R.has_at2 = true;
+            R.sparse = g_opts.sparsity != 0;
+            R.issued_per_product = R.sparse ? R.issued_tiles : (double)R.Np * R.Np * (double)R.ld;
         }
     }
+    if (!R.has_at2) R.at2.release();
 
     tr.mark(R.spmm ? "kernel choice: spmm" : "kernel choice: tiles");
     // power store: a ring of device slots (allocated on first use, kept across calls)
@@ -1005,6 +1024,14 @@ mp_status mp_set_options(int sparsity, int64_t device_budget_bytes)
     if (sparsity < -1 || sparsity > 2) return fail(MP_ERR_DOMAIN, "mp_set_options: sparsity %d outside [-1, 2]", sparsity);
     g_opts.sparsity = sparsity;
     g_opts.budget = device_budget_bytes;
+    return MP_OK;
+}
+
+mp_status mp_set_grouping(int mode)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (mode < -1 || mode > 1) return fail(MP_ERR_DOMAIN, "mp_set_grouping: mode %d outside [-1, 1]", mode);
+    g_opts.grouping = mode;
     return MP_OK;
 }
 

@@ -275,23 +275,37 @@ __global__ void __launch_bounds__(256)
 
 // dst [rows_p][ldd] u16 = enc(src[i][j]) for i < rows, j < cols, +inf padding elsewhere.
 // Any src entry in (0x7FFE, 0xFFFF) sets *range_flag.
+__device__ __forceinline__ uint32_t enc_dev(uint16_t s, bool &bad)
+{
+    if (s == kBndInf) return kDevInf;
+    if (s > kFiniteMax) {
+        bad = true;
+        return kDevInf;
+    }
+    return s;
+}
+
+// dst (rows_p x ldd, ldd even) = enc(src[:rows, :cols]), +inf padding.  Blocks stride over
+// rows, threads over column pairs (one u32 store each).
 __global__ void k_encode(const uint16_t *__restrict__ src, int64_t lds, int64_t rows, int64_t cols,
                          uint16_t *__restrict__ dst, int64_t ldd, int64_t rows_p,
                          int *__restrict__ range_flag)
 {
-    const int64_t total = rows_p * ldd;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / ldd, j = t - i * ldd;
-        uint16_t v = kDevInf;
-        if (i < rows && j < cols) {
-            const uint16_t s = src[i * lds + j];
-            if (s == kBndInf) v = kDevInf;
-            else if (s > kFiniteMax) { v = kDevInf; *range_flag = 1; }
-            else v = s;
+    bool bad = false;
+    for (int64_t i = blockIdx.x; i < rows_p; i += gridDim.x) {
+        uint32_t *d = reinterpret_cast<uint32_t *>(dst + i * ldd);
+        const uint16_t *srow = src + i * lds;
+        for (int64_t j = threadIdx.x; j < ldd / 2; j += blockDim.x) {
+            const int64_t c = 2 * j;
+            uint32_t a = kDevInf, b = kDevInf;
+            if (i < rows) {
+                if (c < cols) a = enc_dev(srow[c], bad);
+                if (c + 1 < cols) b = enc_dev(srow[c + 1], bad);
+            }
+            d[j] = a | (b << 16);
         }
-        dst[t] = v;
     }
+    if (bad) *range_flag = 1;
 }
 
 // AT2 [Kp][Mp] u32: AT2[l][i] = {enc(a_il), enc(a_il)}; +inf padding.  32x32 tiles through
@@ -433,21 +447,34 @@ constexpr int kSpCols = 512;            // columns per CTA (2 warps x 32 lanes x
 constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
 static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
-// How the sparse-form builders read A: the 8 duplicated values of rows 8g..8g+7 at column l.
-struct AccAT2 { // from the staged AT2 (matrix sources)
-    const uint32_t *AT2;
-    int64_t Np;
+// How the sparse-form builders read A: the 8 duplicated values (device encoding) of the rows
+// in group slot 8g..8g+7 at column l; finite(i, l) for i, l < N.  `rows` (may be null = identity) maps a slot to its row of A: the
+// row grouping of k_group_greedy.
+struct AccA { // matrix sources: A itself (row-major, boundary encoding, range-checked)
+    const uint16_t *A;
+    int64_t lda, N;
+    const int32_t *rows;
+    __device__ __forceinline__ uint32_t enc2(int64_t i, int64_t l) const
+    {
+        uint32_t x = (i < N && l < N) ? A[i * lda + l] : kBndInf;
+        if (x > kFiniteMax) x = kDevInf;
+        return x | (x << 16);
+    }
     __device__ __forceinline__ void row8(int64_t g, int64_t l, uint4 &v0, uint4 &v1) const
     {
-        const uint4 *p = reinterpret_cast<const uint4 *>(AT2 + l * Np + g * kG);
-        v0 = p[0];
-        v1 = p[1];
+        uint32_t v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = enc2(rows ? (int64_t)rows[g * kG + r] : g * kG + r, l);
+        v0 = make_uint4(v[0], v[1], v[2], v[3]);
+        v1 = make_uint4(v[4], v[5], v[6], v[7]);
     }
+    __device__ __forceinline__ bool finite(int64_t i, int64_t l) const { return A[i * lda + l] != kBndInf; }
 };
 struct AccWords { // straight from the word masks (A(D_n) without materialising AT2)
     const WordMask *w;
     int64_t N;
     unsigned full;
+    const int32_t *rows;
     __device__ __forceinline__ void row8(int64_t g, int64_t l, uint4 &v0, uint4 &v1) const
     {
         uint32_t v[8];
@@ -457,13 +484,299 @@ struct AccWords { // straight from the word masks (A(D_n) without materialising 
         const uint32_t lab = (uint32_t)p.zeros | ((uint32_t)p.zeros << 16);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const int64_t i = g * kG + r;
+            const int64_t i = rows ? (int64_t)rows[g * kG + r] : g * kG + r;
             v[r] = (lok && i < N && can_follow_mask(w[i], p, full)) ? lab : 0x7FFF7FFFu;
         }
         v0 = make_uint4(v[0], v[1], v[2], v[3]);
         v1 = make_uint4(v[4], v[5], v[6], v[7]);
     }
+    __device__ __forceinline__ bool finite(int64_t i, int64_t l) const
+    {
+        return i < N && l < N && can_follow_mask(w[i], w[l], full);
+    }
 };
+
+// ---------------------------------------------------------------------------------------
+// Row grouping (which rows share a tile and a group).  A group entry costs 8 rows x ld steps
+// whether 1 or 8 of its rows have a finite A_il, and every l in a tile's union stages an X
+// row, so rows with overlapping supports should share groups and tiles.  Three passes:
+//  1. support bitsets bits[i * nw + k] (bit b = A_(i, 32k + b) finite) and their CSR lists;
+//  2. tiles, greedily per window of kGrpWin consecutive rows: seed = the remaining row with
+//     the smallest support, then 31 times the remaining row adding the fewest new l to the
+//     tile's union (ties: the earliest);
+//  3. per tile, the 4 groups of 8 by steepest-descent swaps between groups (start: the pick
+//     order) while a swap lowers the sum of the 4 group unions.
+// rows[0..N) is the resulting slot -> row map, rows[N, Np) the padding rows.  Any grouping
+// gives the same product; this one only lowers the issued steps and the staged X rows
+// (DESIGN.md "Row grouping").
+// ---------------------------------------------------------------------------------------
+constexpr int kGrpWin = 512;
+constexpr int kRefThreads = 128;
+
+// bits[i * nw + k] (bit b = A_(i, 32k + b) finite): blocks stride over rows, each warp over
+// the row's words, one ballot per word.
+template <class Acc>
+__global__ void k_support_bits(Acc acc, int64_t N, int64_t nw, uint32_t *__restrict__ bits)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
+        for (int64_t k = warp; k < nw; k += nwarps) {
+            const int64_t l = k * 32 + lane;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, l < N && acc.finite(i, l));
+            if (lane == 0) bits[i * nw + k] = m;
+        }
+    }
+}
+
+// cnt[i] = |support of row i| (warp per row)
+__global__ void k_row_popc(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, int32_t *__restrict__ cnt)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int c = 0;
+        for (int64_t k = lane; k < nw; k += 32) c += __popc(bits[i * nw + k]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        if (lane == 0) cnt[i] = c;
+    }
+}
+
+// idx[off[i] ..] = the support of row i in increasing l (warp per row)
+// If wst != null it also records, per row i and window w of kGrpWin columns, the offset
+// (relative to off[i]) of the first entry with l >= w * kGrpWin: wst[i * nwin + w].
+__global__ void k_bits_csr(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, const int64_t *__restrict__ off,
+                           int32_t *__restrict__ idx, int32_t *__restrict__ wst, int64_t nwin)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t pos = off[i];
+        for (int64_t k0 = 0; k0 < nw; k0 += 32) {
+            const int64_t k = k0 + lane;
+            uint32_t w = k < nw ? bits[i * nw + k] : 0u;
+            const int c = __popc(w);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int64_t q = pos + incl - c;
+            if (wst && k < nw && (k % (kGrpWin / 32)) == 0) wst[i * nwin + k / (kGrpWin / 32)] = (int32_t)(q - off[i]);
+            while (w) {
+                const int b = __ffs(w) - 1;
+                w &= w - 1;
+                idx[q++] = (int32_t)(k * 32 + b);
+            }
+            pos += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+    }
+}
+
+// bitsT = the transpose of the N x N bit matrix bits (one warp per 32 x 32 block).
+__global__ void k_bits_transpose(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, uint32_t *__restrict__ bitsT)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t total = nw * nw;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t bi = t / nw, bk = t - bi * nw; // rows 32bi.., word bk
+        const int64_t i = bi * 32 + lane;
+        const uint32_t w = i < N ? bits[i * nw + bk] : 0u; // lane r: row 32bi + r
+        uint32_t out = 0;                                   // lane b: column 32bk + b over rows
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, (w >> b) & 1u);
+            if (lane == b) out = m;
+        }
+        const int64_t l = bk * 32 + lane;
+        if (l < N) bitsT[l * nw + bi] = out;
+    }
+}
+
+// Pass 2: tiles of kSpRows rows per window of kGrpWin rows (one CTA per window).  The score
+// newc[q] = |S_q \ U| of every live window row is kept incrementally: when a pick adds the
+// columns D = S_r \ U to the tile's union U, every live row holding an l in D loses one --
+// found through the column lists (CSC, rows ascending) -- so a pick costs its new columns'
+// column segments instead of a rescan of every candidate's support.
+__global__ void __launch_bounds__(kGrpWin) k_tile_greedy(const int64_t *__restrict__ off, const int32_t *__restrict__ idx,
+                                                        const int64_t *__restrict__ coff,
+                                                        const int32_t *__restrict__ cidx, const int32_t *__restrict__ cwst,
+                                                        int64_t nwin, int64_t nw, int64_t N, int32_t *__restrict__ rows)
+{
+    extern __shared__ uint32_t U[]; // the open tile's union, nw words
+    __shared__ int32_t newc[kGrpWin];
+    __shared__ uint8_t alive[kGrpWin];
+    __shared__ unsigned long long best;
+    const int tid = threadIdx.x;
+    const int64_t b0 = (int64_t)blockIdx.x * kGrpWin;
+    const int cnt = (int)(N - b0 < kGrpWin ? N - b0 : kGrpWin);
+    const int32_t lo = (int32_t)b0;
+    alive[tid] = tid < cnt ? 1 : 0;
+    int nrem = cnt;
+    int64_t out = b0;
+    while (nrem > 0) {
+        for (int64_t k = tid; k < nw; k += blockDim.x) U[k] = 0u;
+        if (tid < cnt) newc[tid] = (int32_t)(off[b0 + tid + 1] - off[b0 + tid]); // |S_q \ {}|
+        __syncthreads();
+        for (int m = 0; m < kSpRows && nrem > 0; ++m) {
+            if (tid == 0) best = ~0ull;
+            __syncthreads();
+            if (alive[tid]) atomicMin(&best, ((unsigned long long)(uint32_t)newc[tid] << 32) | (uint32_t)tid);
+            __syncthreads();
+            const int pos = (int)(best & 0xFFFFFFFFu);
+            const int64_t r = b0 + pos;
+            if (tid == 0) {
+                alive[pos] = 0;
+                rows[out] = (int32_t)r;
+            }
+            ++out;
+            --nrem;
+            // add S_r to U; for each new l, every live row of the window holding l loses one
+            for (int64_t q = off[r] + tid; q < off[r + 1]; q += blockDim.x) {
+                const int32_t l = idx[q];
+                const uint32_t bit = 1u << (l & 31);
+                if (atomicOr(&U[l >> 5], bit) & bit) continue;
+                // this window's segment of column l: [wst[l][w], wst[l][w+1])
+                const int64_t c0 = coff[l];
+                const int32_t *cw = cwst + (int64_t)l * nwin + blockIdx.x;
+                const int64_t a = c0 + cw[0];
+                const int64_t z = blockIdx.x + 1 < nwin ? c0 + cw[1] : coff[l + 1];
+                for (int64_t e = a; e < z; e += 4) {
+                    int32_t iv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) iv[u] = e + u < z ? cidx[e + u] : -1;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (iv[u] >= 0) atomicSub(&newc[iv[u] - lo], 1);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Pass 3: the 4 groups of each full tile (one CTA per tile).  Shared memory: the tile's
+// union over global columns G[nw] and its prefix counts P[nw] (local column numbering), then
+// -- overlaid on them -- per row its local bitset R[32][uw] and the union of the OTHER 7
+// rows of its group Um[32][uw].  Tiles whose union exceeds uw_max words keep the pick order.
+__global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__restrict__ off,
+                                                            const int32_t *__restrict__ idx, int64_t nw, int64_t N,
+                                                            int uw_max, int32_t *__restrict__ rows)
+{
+    extern __shared__ uint32_t sm[];
+    __shared__ int32_t slot_row[kSpRows];
+    __shared__ int sh_u;
+    __shared__ unsigned long long best;
+    __shared__ int gcost[kSpGroups];
+    const int tid = threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * kSpRows;
+    if (t0 + kSpRows > N) return; // the ragged last tile keeps the pick order
+    if (tid < kSpRows) slot_row[tid] = rows[t0 + tid];
+    uint32_t *G = sm;
+    uint32_t *P = sm + nw;
+    for (int64_t k = tid; k < nw; k += blockDim.x) G[k] = 0u;
+    __syncthreads();
+    for (int r = 0; r < kSpRows; ++r) {
+        const int32_t row = slot_row[r];
+        for (int64_t q = off[row] + tid; q < off[row + 1]; q += blockDim.x) {
+            const int32_t l = idx[q];
+            atomicOr(&G[l >> 5], 1u << (l & 31));
+        }
+    }
+    __syncthreads();
+    if (tid == 0) { // exclusive prefix of the word popcounts (nw <= 4112: serial is fine here)
+        int acc = 0;
+        for (int64_t k = 0; k < nw; ++k) {
+            P[k] = (uint32_t)acc;
+            acc += __popc(G[k]);
+        }
+        sh_u = acc;
+    }
+    __syncthreads();
+    const int u = sh_u, uw = (u + 31) / 32;
+    if (uw > uw_max) return;
+    // local bitsets, staged after the G/P area, then moved to the front
+    uint32_t *R = sm + 2 * nw;
+    for (int q = tid; q < kSpRows * uw; q += blockDim.x) R[q] = 0u;
+    __syncthreads();
+    for (int r = 0; r < kSpRows; ++r) {
+        const int32_t row = slot_row[r];
+        for (int64_t q = off[row] + tid; q < off[row + 1]; q += blockDim.x) {
+            const int32_t l = idx[q];
+            const uint32_t w = G[l >> 5];
+            const int loc = (int)P[l >> 5] + __popc(w & ((1u << (l & 31)) - 1u));
+            atomicOr(&R[r * uw + (loc >> 5)], 1u << (loc & 31));
+        }
+    }
+    __syncthreads();
+    uint32_t *R0 = sm, *Um = sm + kSpRows * uw;
+    for (int q = 0; q < kSpRows * uw; q += blockDim.x) { // move R to the front (no overlap hazard:
+        const int x = q + tid;                             // each round reads before it writes)
+        const uint32_t v = x < kSpRows * uw ? R[x] : 0u;
+        __syncthreads();
+        if (x < kSpRows * uw) R0[x] = v;
+        __syncthreads();
+    }
+    __shared__ int8_t member[kSpRows]; // member[s] = R0 row currently in slot s
+    if (tid < kSpRows) member[tid] = (int8_t)tid;
+    __syncthreads();
+    for (int it = 0; it < 64; ++it) {
+        // Um[s] = OR of the other 7 rows of slot s's group; group costs
+        for (int q = tid; q < kSpRows * uw; q += blockDim.x) {
+            const int sl = q / uw, k = q - sl * uw, g0 = (sl / kG) * kG;
+            uint32_t v = 0u;
+#pragma unroll
+            for (int j = 0; j < kG; ++j)
+                if (g0 + j != sl) v |= R0[member[g0 + j] * uw + k];
+            Um[sl * uw + k] = v;
+        }
+        if (tid < kSpGroups) gcost[tid] = 0;
+        if (tid == 0) best = ~0ull;
+        __syncthreads();
+        for (int q = tid; q < kSpGroups * uw; q += blockDim.x) {
+            const int g = q / uw, k = q - g * uw;
+            const int sl = g * kG;
+            atomicAdd(&gcost[g], __popc(Um[sl * uw + k] | R0[member[sl] * uw + k]));
+        }
+        __syncthreads();
+        // all 384 swaps (slot a in group A < group B of slot b)
+        for (int q = tid; q < 6 * kG * kG; q += blockDim.x) {
+            const int pr = q / (kG * kG), ab = q - pr * (kG * kG);
+            const int A = pr < 3 ? 0 : pr < 5 ? 1 : 2;
+            const int B = pr < 3 ? pr + 1 : pr < 5 ? pr - 1 : 3;
+            const int sa = A * kG + ab / kG, sb = B * kG + ab % kG;
+            const uint32_t *ra = R0 + member[sa] * uw, *rb = R0 + member[sb] * uw;
+            const uint32_t *ua = Um + sa * uw, *ub = Um + sb * uw;
+            int c = 0;
+            for (int k = 0; k < uw; ++k) c += __popc(ua[k] | rb[k]) + __popc(ub[k] | ra[k]);
+            const int d = c - gcost[A] - gcost[B];
+            if (d < 0)
+                atomicMin(&best, ((unsigned long long)(uint32_t)(d + (1 << 30)) << 32) | (uint32_t)q);
+        }
+        __syncthreads();
+        const unsigned long long bb = best;
+        if (bb == ~0ull) break;
+        if (tid == 0) {
+            const int q = (int)(bb & 0xFFFFFFFFu);
+            const int pr = q / (kG * kG), ab = q - pr * (kG * kG);
+            const int A = pr < 3 ? 0 : pr < 5 ? 1 : 2;
+            const int B = pr < 3 ? pr + 1 : pr < 5 ? pr - 1 : 3;
+            const int sa = A * kG + ab / kG, sb = B * kG + ab % kG;
+            const int8_t x = member[sa];
+            member[sa] = member[sb];
+            member[sb] = x;
+        }
+        __syncthreads();
+    }
+    if (tid < kSpRows) rows[t0 + tid] = slot_row[member[tid]];
+}
+
+__global__ void k_iota_rows(int32_t *__restrict__ rows, int64_t from, int64_t to)
+{
+    for (int64_t i = from + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < to; i += (int64_t)gridDim.x * blockDim.x)
+        rows[i] = (int32_t)i;
+}
 
 // m8[g * Np + l] = bit r set iff A_(8g+r, l) is finite.
 template <class Acc>
@@ -513,7 +826,7 @@ __device__ int64_t block_compact(int64_t n, FlagF flag, EmitF emit)
     return base_sh;
 }
 
-// Per 64-row tile t: the ordered union U_t of its 8 groups' l.  Count pass (L == nullptr)
+// Per 32-row tile t: the ordered union U_t of its 4 groups' l.  Count pass (L == nullptr)
 // writes tcnt[t]; fill pass writes L[tptr[t] + rank] = l.
 __global__ void k_tile_union(const uint8_t *__restrict__ m8, int64_t Np, const int64_t *__restrict__ tptr,
                              int32_t *__restrict__ tcnt, int32_t *__restrict__ L)
@@ -671,7 +984,7 @@ template <int STAGES>
 __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
            const int64_t *__restrict__ eoff, const uint4 *__restrict__ E, const uint16_t *__restrict__ X, int64_t ldx,
-           uint16_t *__restrict__ C, int64_t ldc)
+           uint16_t *__restrict__ C, int64_t ldc, const int32_t *__restrict__ rowmap)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int XB = kSpChunk * kSpCols * 2;    // 16 KB of X rows
@@ -807,7 +1120,8 @@ __global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
     for (int j = 0; j < kSpGroups; ++j)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const int64_t i = (int64_t)t * kSpRows + kG * j + r;
+            const int64_t slot = (int64_t)t * kSpRows + kG * j + r;
+            const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
             uint4 v;
             v.x = __vminu2(acc[j][r][0], 0x7FFF7FFFu);
             v.y = __vminu2(acc[j][r][1], 0x7FFF7FFFu);
@@ -879,7 +1193,9 @@ cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int
 cudaError_t launch_encode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
                           int64_t ldd, int64_t rows_p, int *range_flag, cudaStream_t s)
 {
-    k_encode<<<grid_for(rows_p * ldd, 256), 256, 0, s>>>(src, lds, rows, cols, dst, ldd, rows_p, range_flag);
+    if (ldd % 2) return cudaErrorInvalidValue; // padded pitches are multiples of 512
+    k_encode<<<(unsigned)std::min<int64_t>(std::max<int64_t>(rows_p, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
+        src, lds, rows, cols, dst, ldd, rows_p, range_flag);
     return cudaGetLastError();
 }
 
@@ -933,7 +1249,7 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
         attr_set = true;
     }
     dim3 grid((unsigned)(ncols_p / kSpCols), (unsigned)(Mp / kSpRows));
-    k_spmm<STAGES><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc);
+    k_spmm<STAGES><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
     return cudaGetLastError();
 }
 
@@ -947,7 +1263,7 @@ cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint1
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
 template <class Acc>
-cudaError_t build_sparse_form_t(Acc AT2, int64_t Np, SparseWork &w, cudaStream_t s,
+cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, SparseWork &w, cudaStream_t s,
                                 cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
 {
     const int64_t G = Np / kG, Mt = Np / kSpRows;
@@ -962,6 +1278,57 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t Np, SparseWork &w, cudaStream_t
     do {                                                                                                                \
         if ((e = alloc((void **)&(ptr), (bytes), actx)) != cudaSuccess) return e;                                       \
     } while (0)
+    w.rows = nullptr;
+    if (group) { // row grouping first: every later builder reads A through it
+        const int64_t nw = (N + 31) / 32;
+        uint32_t *bits = nullptr;
+        int32_t *cnt = nullptr, *idx = nullptr;
+        int64_t *off = nullptr;
+        SP_ALLOC(w.rows, (size_t)Np * 4);
+        SP_ALLOC(bits, (size_t)N * nw * 4);
+        SP_ALLOC(cnt, (size_t)N * 4);
+        SP_ALLOC(off, (size_t)(N + 1) * 8);
+        SP_LAUNCH((k_support_bits<<<(unsigned)std::min<int64_t>(N, (int64_t)num_sms() * 8), 256, 0, s>>>(AT2, N, nw, bits)));
+        SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, cnt)));
+        SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(cnt, N, off)));
+        int64_t nnz = 0;
+        if ((e = cudaMemcpyAsync(&nnz, off + N, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+        SP_ALLOC(idx, (size_t)std::max<int64_t>(nnz, 1) * 4);
+        SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, off, idx, nullptr, 0)));
+        // column lists: the transposed bits through the same two kernels (bits is reused)
+        uint32_t *bitsT = nullptr;
+        int64_t *coff = nullptr;
+        int32_t *cidx = nullptr;
+        SP_ALLOC(bitsT, (size_t)N * nw * 4);
+        SP_ALLOC(coff, (size_t)(N + 1) * 8);
+        SP_ALLOC(cidx, (size_t)std::max<int64_t>(nnz, 1) * 4);
+        SP_LAUNCH((k_bits_transpose<<<grid_for(nw * nw * 32, 256), 256, 0, s>>>(bits, nw, N, bitsT)));
+        SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, cnt)));
+        SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(cnt, N, coff)));
+        const int64_t nwin = (N + kGrpWin - 1) / kGrpWin;
+        int32_t *cwst = nullptr;
+        SP_ALLOC(cwst, (size_t)N * nwin * 4);
+        SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, coff, cidx, cwst, nwin)));
+        const int smem_g = (int)(nw * 4);
+        if ((e = cudaFuncSetAttribute(k_tile_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g)) != cudaSuccess)
+            return e;
+        SP_LAUNCH((k_tile_greedy<<<(unsigned)((N + kGrpWin - 1) / kGrpWin), kGrpWin, smem_g, s>>>(
+            off, idx, coff, cidx, cwst, nwin, nw, N, w.rows)));
+        // pass 3: shared memory = max(G + P + R staging, R + Um); tile unions up to 12288 l
+        // (n = 12: consecutive tiles reach 9600 at most, greedy tiles fewer)
+        const int64_t uw_max = 384;
+        if (N >= kSpRows) {
+            const int smem_r = (int)(4 * std::max<int64_t>(2 * nw + kSpRows * uw_max, 2 * kSpRows * uw_max));
+            if ((e = cudaFuncSetAttribute(k_tile_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_r)) !=
+                cudaSuccess)
+                return e;
+            SP_LAUNCH((k_tile_refine<<<(unsigned)(N / kSpRows), kRefThreads, smem_r, s>>>(off, idx, nw, N, (int)uw_max,
+                                                                                         w.rows)));
+        }
+        if (Np > N) SP_LAUNCH((k_iota_rows<<<grid_for(Np - N, 256), 256, 0, s>>>(w.rows, N, Np)));
+        AT2.rows = w.rows;
+    }
     SP_ALLOC(w.m8, (size_t)(G * Np));
     SP_ALLOC(w.tcnt, (size_t)Mt * 4);
     SP_ALLOC(w.tptr, (size_t)(Mt + 1) * 8);
@@ -1000,17 +1367,19 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t Np, SparseWork &w, cudaStream_t
     return cudaSuccess;
 }
 
-cudaError_t build_sparse_form(const uint32_t *AT2, int64_t Np, SparseWork &w, cudaStream_t s,
-                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
+cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group, SparseWork &w,
+                              cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
+                              int64_t *launches)
 {
-    return build_sparse_form_t(AccAT2{AT2, Np}, Np, w, s, alloc, actx, launches);
+    return build_sparse_form_t(AccA{A, lda, N, nullptr}, N, Np, group, w, s, alloc, actx, launches);
 }
 
-cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, SparseWork &w,
+cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
                                     int64_t *launches)
 {
-    return build_sparse_form_t(AccWords{words, N, (1u << n) - 1u}, Np, w, s, alloc, actx, launches);
+    return build_sparse_form_t(AccWords{words, N, (1u << n) - 1u, nullptr}, N, Np, group, w, s, alloc, actx,
+                               launches);
 }
 
 // X1[i][j] = A_(i, c0+j) from the word masks, +inf padding (rows >= N, columns >= w).
@@ -1033,6 +1402,49 @@ cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_
                                  uint16_t *X1, int64_t ldx, cudaStream_t s)
 {
     k_x1_from_words<<<grid_for(Np * ldx, 256), 256, 0, s>>>(words, N, (1u << n) - 1u, Np, c0, w, X1, ldx);
+    return cudaGetLastError();
+}
+
+// Range check of A (row-major, boundary encoding) and, if occ != null, the occupancy of its
+// 128 x 32 tiles (occ zeroed by the caller): one warp per (row, 32-column tile).
+__global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N, int64_t Kt, uint8_t *__restrict__ occ,
+                          int *__restrict__ range_flag)
+{
+    const int lane = threadIdx.x & 31;
+    bool bad = false;
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
+        const uint16_t *row = A + i * lda;
+        for (int64_t j0 = 0; j0 < Kt * 16; j0 += blockDim.x) { // column pairs; a warp = 2 tiles
+            const int64_t j = j0 + threadIdx.x, c = 2 * j;
+            bool f = false;
+            if (c < N) {
+                const uint16_t x = row[c];
+                f = x != kBndInf;
+                bad |= f && x > kFiniteMax;
+            }
+            if (c + 1 < N) {
+                const uint16_t x = row[c + 1];
+                f |= x != kBndInf;
+                bad |= x != kBndInf && x > kFiniteMax;
+            }
+            const uint32_t b = __ballot_sync(0xFFFFFFFFu, f);
+            if (occ && lane == 0) {
+                const int64_t kt = (j - lane) / 16;
+                uint8_t *o = occ + (i / kBM) * Kt + kt;
+                if ((b & 0xFFFFu) && kt < Kt && !o[0]) o[0] = 1;
+                if ((b >> 16) && kt + 1 < Kt && !o[1]) o[1] = 1;
+            }
+        }
+    }
+    if (bad) *range_flag = 1;
+}
+
+cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
+                           cudaStream_t s)
+{
+    const int64_t Kt = Np / kBK;
+    k_check_a<<<(unsigned)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
+        A, lda, N, Kt, occ, range_flag);
     return cudaGetLastError();
 }
 

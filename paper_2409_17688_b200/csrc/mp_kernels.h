@@ -28,11 +28,12 @@ cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_
                           int64_t ldd, cudaStream_t s);
 // Grouped sparse form of A for the SpMM product (see k_spmm in mp_kernels.cu).
 struct SparseA {
-    const int32_t *L = nullptr;    // concatenated per-tile (64-row) ordered union lists of l
+    const int32_t *L = nullptr;    // concatenated per-tile (32-row) ordered union lists of l
     const int64_t *tptr = nullptr; // [Mt + 1] offsets into L
     const int64_t *tch = nullptr;  // [Mt + 1] first chunk of each tile
     const int64_t *eoff = nullptr; // [chunks * 8 + 1] entry offsets per (chunk, group)
     const uint4 *E = nullptr;      // entries, 3 x uint4 each
+    const int32_t *rows = nullptr; // group slot -> row of A (null: identity)
 };
 // Device buffers of the sparse form (owned by the caller; allocated through `alloc`).
 struct SparseWork {
@@ -40,18 +41,26 @@ struct SparseWork {
     int32_t *tcnt = nullptr, *nch = nullptr, *L = nullptr, *chunk_tile = nullptr, *ecnt = nullptr;
     int64_t *tptr = nullptr, *tch = nullptr, *eoff = nullptr;
     uint4 *E = nullptr;
+    int32_t *rows = nullptr; // row grouping (null: consecutive rows)
     int64_t total_union = 0, total_chunks = 0, entries = 0;
 };
 cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
                         int64_t ncols_p, cudaStream_t s);
-cudaError_t build_sparse_form(const uint32_t *AT2, int64_t Np, SparseWork &w, cudaStream_t s,
-                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);
-cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, SparseWork &w,
+// group: form the row groups with k_group_greedy (else groups are consecutive rows).
+// A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
+cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group, SparseWork &w,
+                              cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
+                              int64_t *launches);
+cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
                                     int64_t *launches);
 cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, int64_t w,
                                  uint16_t *X1, int64_t ldx, cudaStream_t s);
 cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s);
+// Range check of a row-major A (flag set if an entry lies in (0x7FFE, 0xFFFF)) and, if occ is
+// not null, the occupancy of its 128 x 32 tiles (occ zeroed by the caller).
+cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
+                           cudaStream_t s);
 cudaError_t launch_tile_occupancy(const uint32_t *AT2, int64_t Mp, int64_t Kp, uint8_t *occ, cudaStream_t s);
 
 } // namespace mp

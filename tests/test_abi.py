@@ -147,6 +147,8 @@ def test_argument_errors_before_device():
     r = _native._PeriodicResult()
     assert _native.lib.minplus_power_until_periodic(a.ctypes.data, 4, 1, ctypes.byref(r)) == 1
     assert _native.lib.minplus_power_until_periodic(a.ctypes.data, 4, 257, ctypes.byref(r)) == 1
+    assert _native.lib.mp_set_grouping(2) == 1 and _native.lib.mp_set_options(3, 0) == 1
+    assert _native.lib.mp_set_grouping(-1) == 0
 
 
 def test_no_gpu_reports_cuda_error():

@@ -27,6 +27,17 @@ def mp():
     return m
 
 
+def use_kernel(mp, kernel):
+    """kernel: a sparsity option, or "spmm-greedy" = SpMM with greedily grouped rows."""
+    mp.set_options("spmm" if kernel == "spmm-greedy" else kernel)
+    mp.set_grouping("greedy" if kernel == "spmm-greedy" else "consecutive" if kernel == "spmm" else "auto")
+
+
+def reset_kernel(mp):
+    mp.set_options("auto")
+    mp.set_grouping("auto")
+
+
 # ----------------------------------------------------------------------------- products
 SHAPES = [(1, 1, 1), (1, 300, 257), (300, 1, 5), (129, 33, 1), (127, 257, 1031), (128, 32, 256),
           (129, 97, 257), (300, 517, 301), (1031, 513, 600), (4097, 31, 70), (40, 4097, 300)]
@@ -92,17 +103,17 @@ def test_minplus_mul_device_strided(mp, oracle_mod):
 
 
 # ------------------------------------------------------------------- power sequences
-@pytest.mark.parametrize("kernel", ["tiles", "spmm"])
+@pytest.mark.parametrize("kernel", ["tiles", "spmm", "spmm-greedy"])
 @pytest.mark.parametrize("n", range(2, 10))
 def test_power_until_periodic_transfer(mp, oracle_mod, n, kernel):
     """Every summary of the run equals the oracle's: (mu, lambda, b), k_last, dense_from,
     diag_min[k] and the fingerprint of every power A^k (a whole-matrix check), and Table 5."""
     A = mp.build_transition_matrix(n)
-    mp.set_options(kernel)
+    use_kernel(mp, kernel)
     try:
         g = mp.minplus_power_until_periodic(A)
     finally:
-        mp.set_options("auto")
+        reset_kernel(mp)
     o = oracle_mod.power_until_periodic(A)
     assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
     assert g.diag_min == o.diag_min
@@ -111,10 +122,10 @@ def test_power_until_periodic_transfer(mp, oracle_mod, n, kernel):
     assert (g.mu, g.lam, g.offset) == row
 
 
-@pytest.mark.parametrize("sparse", ["dense", "tiles", "spmm"])
+@pytest.mark.parametrize("sparse", ["dense", "tiles", "spmm", "spmm-greedy"])
 def test_power_rows_full_matrices(mp, oracle_mod, sparse):
     """Every entry of every power A^1..A^12 for n = 7 (N = 558, 5 x 3 tiles, ragged)."""
-    mp.set_options(sparse)
+    use_kernel(mp, sparse)
     try:
         A = mp.build_transition_matrix(7)
         rows = np.arange(A.shape[0])
@@ -125,21 +136,22 @@ def test_power_rows_full_matrices(mp, oracle_mod, sparse):
                 X = oracle_mod.minplus(A, X)
             assert np.array_equal(got[k - 1], X), k
     finally:
-        mp.set_options("auto")
+        reset_kernel(mp)
 
 
-@pytest.mark.parametrize("kernel", ["dense", "tiles", "spmm", "auto"])
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("kernel", ["dense", "tiles", "spmm", "spmm-greedy", "auto"])
+@pytest.mark.parametrize("seed", range(5))
 def test_power_until_periodic_random(mp, oracle_mod, seed, kernel):
     """Random sparse matrices (the +inf pattern persists for several powers, exercising the
-    exact-compare path with +inf entries), with each product kernel."""
-    N = [37, 130, 257, 300][seed]
-    A = synth.transfer_like(N, N, [0.9, 0.95, 0.97, 0.5][seed], salt=100 + seed)
-    mp.set_options(kernel)
+    exact-compare path with +inf entries), with each product kernel; seed 4 spans three
+    grouping windows (1100 rows, ragged)."""
+    N = [37, 130, 257, 300, 1100][seed]
+    A = synth.transfer_like(N, N, [0.9, 0.95, 0.97, 0.5, 0.97][seed], salt=100 + seed)
+    use_kernel(mp, kernel)
     try:
         g = mp.minplus_power_until_periodic(A, max_k=64)
     finally:
-        mp.set_options("auto")
+        reset_kernel(mp)
     o = oracle_mod.power_until_periodic(A, max_k=64)
     assert o.rc == 0
     assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
@@ -159,6 +171,16 @@ def test_power_until_periodic_degenerate(mp, oracle_mod):
     with pytest.raises(mp.MinplusError) as e:
         mp.minplus_power_until_periodic(P, max_k=20)
     assert e.value.status == 4
+    for kernel in ("dense", "tiles", "spmm", "auto"):  # entries in (0x7FFE, 0xFFFF): MP_ERR_RANGE
+        use_kernel(mp, kernel)
+        try:
+            B = synth.transfer_like(100, 100, 0.5, salt=3)
+            B[7, 9] = 0x8000
+            with pytest.raises(mp.MinplusError) as e:
+                mp.minplus_power_until_periodic(B)
+            assert e.value.status == 2
+        finally:
+            reset_kernel(mp)
 
 
 def test_ring_eviction_recompute(mp, oracle_mod):
@@ -223,13 +245,13 @@ def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
     assert f["r0_k50"] == t4[n]  # Table 4
 
 
-@pytest.mark.parametrize("kernel", ["spmm", "tiles"])
+@pytest.mark.parametrize("kernel", ["spmm", "spmm-greedy", "tiles"])
 def test_gamma2_record_words_source(mp, oracle_mod, kernel):
     """The gamma2_cylinder path builds A(D_n) on the device from the word masks (with SpMM no
     AT2 at all): its whole record -- every power's fingerprint included -- equals the oracle's
     run on the oracle's own transition matrix."""
     mp.shutdown()  # drop the cached records
-    mp.set_options(kernel)
+    use_kernel(mp, kernel)
     try:
         for n in range(2, 10):
             g = mp.gamma2_record(n)
@@ -237,7 +259,7 @@ def test_gamma2_record_words_source(mp, oracle_mod, kernel):
             assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
             assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint, n
     finally:
-        mp.set_options("auto")
+        reset_kernel(mp)
         mp.shutdown()
 
 
