@@ -27,6 +27,38 @@ template <int N> __device__ __forceinline__ void cp_async_wait()
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// mbarrier + bulk-copy (TMA, non-tensor) helpers
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    asm volatile("{\n"
+                 ".reg .pred p;\n"
+                 "WAIT_%=:\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 "@!p bra WAIT_%=;\n"
+                 "}\n" ::"r"(bar),
+                 "r"(parity)
+                 : "memory");
+}
+// global -> shared bulk copy completing `bytes` on the mbarrier (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------------------
 // a3: C = A (x) X on one column tile set.  P:53 "(A x B)_ij = min_k(a_ik + b_kj)";
 // Algorithm 2 line 2 "A^i = A x A^{i-1}".
@@ -430,21 +462,29 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 // without an arc).  A CTA owns kSpRows = 32 rows (4 groups) x kSpCols = 512 columns.  The
 // union U_t of its groups' l indices, in increasing order, is cut into chunks of kSpChunk =
 // 16; per chunk the CTA stages the 16 rows X[l, cols] (16 KB) and the chunk's entries
-// (grouped by group) in shared memory with cp.async.  Each of the 2 warps owns 256 columns
-// (4 packed pairs per lane) of ALL 4 groups, so both warps do identical work (no
-// imbalance): per entry one LDS.128 of X, two broadcast LDS.128 of the values and 32
-// VIADDMNMX.U16x2 (8 rows x 4 pairs) -- enough DPX per entry to keep the issue slots of the
-// shared-memory and loop instructions below the ALU pipe's rate.  Issued steps =
-// 8 * entries * ld; every skipped term is an all-+inf one, so the result is the same product.
+// (grouped by group) in shared memory with cp.async.  Warp j owns group j over all 512
+// columns (8 packed pairs per lane): per entry two broadcast LDS.128 of the values, two
+// LDS.128 of X and 64 VIADDMNMX.U16x2 (8 rows x 8 pairs), so the shared-memory and loop
+// instructions per DPX are half those of a 4-pair layout.  The groups' entry counts per
+// chunk differ, so a warp may wait at the chunk barrier; 4 CTAs (16 warps) per SM cover it.
+// Issued steps = 8 * entries * ld; every skipped term is an all-+inf one, so the result is
+// the same product.
 // Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowBytes, 0, 0, 0}, s = row in the chunk.
 // ---------------------------------------------------------------------------------------
 constexpr int kG = 8;
 constexpr int kSpRows = 32;
 constexpr int kSpGroups = kSpRows / kG;
 constexpr int kSpChunk = 16;
-constexpr int kSpThreads = 64;
-constexpr int kSpCols = 512;            // columns per CTA (2 warps x 32 lanes x 8)
+constexpr int kSpCols = 512;            // columns per CTA (32 lanes x 16)
 constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
+constexpr int kSpConsumers = kSpGroups;  // warp j < 4 computes group j
+constexpr int kSpThreads = 32 * (kSpConsumers + 1); // + one producer warp
+constexpr int kSpStages = 3;
+// One ring stage: X rows | entries (+3 look-ahead records) | the chunk's 6 entry offsets.
+constexpr int kSpEntryBytes = (kSpGroups * kSpChunk + 3) * 48;
+constexpr int kSpStageBytes = kSpChunk * kSpRowBytes + kSpEntryBytes + 48;
+constexpr int kSpSmemBytes = kSpStages * kSpStageBytes + 2 * kSpStages * 8;
+constexpr int kSpCtasPerSm = 3; // 3 x 57.6 KB of shared memory
 static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
 // How the sparse-form builders read A: the 8 duplicated values (device encoding) of the rows
@@ -942,17 +982,22 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
 }
 
-// acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's four
+// acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's eight
 // packed column pairs.
-__device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][4], const uint4 &a0, const uint4 &a1, const uint4 &x)
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][8], const uint4 &a0, const uint4 &a1, const uint4 &x0,
+                                          const uint4 &x1)
 {
     const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-        acc[r][0] = __viaddmin_u16x2(a[r], x.x, acc[r][0]);
-        acc[r][1] = __viaddmin_u16x2(a[r], x.y, acc[r][1]);
-        acc[r][2] = __viaddmin_u16x2(a[r], x.z, acc[r][2]);
-        acc[r][3] = __viaddmin_u16x2(a[r], x.w, acc[r][3]);
+        acc[r][0] = __viaddmin_u16x2(a[r], x0.x, acc[r][0]);
+        acc[r][1] = __viaddmin_u16x2(a[r], x0.y, acc[r][1]);
+        acc[r][2] = __viaddmin_u16x2(a[r], x0.z, acc[r][2]);
+        acc[r][3] = __viaddmin_u16x2(a[r], x0.w, acc[r][3]);
+        acc[r][4] = __viaddmin_u16x2(a[r], x1.x, acc[r][4]);
+        acc[r][5] = __viaddmin_u16x2(a[r], x1.y, acc[r][5]);
+        acc[r][6] = __viaddmin_u16x2(a[r], x1.z, acc[r][6]);
+        acc[r][7] = __viaddmin_u16x2(a[r], x1.w, acc[r][7]);
     }
 }
 
@@ -980,155 +1025,133 @@ __device__ __forceinline__ int64_t ldg_nc_s64(const int64_t *p)
     return v;
 }
 
-template <int STAGES>
-__global__ void __launch_bounds__(kSpThreads, (STAGES <= 2 ? 5 : 4))
+// Warp-specialised ring (kSpStages deep): the producer warp fills a stage with bulk copies
+// (16 X rows of 1 KB, the chunk's entries, its entry offsets) that complete on the stage's
+// "full" mbarrier; consumer warp j waits on it, walks group j's entries, and arrives on the
+// stage's "empty" mbarrier.  No CTA-wide barrier in the loop, so a warp whose group has few
+// entries in one chunk runs ahead into the next (up to the ring depth) instead of idling.
+__global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
            const int64_t *__restrict__ eoff, const uint4 *__restrict__ E, const uint16_t *__restrict__ X, int64_t ldx,
            uint16_t *__restrict__ C, int64_t ldc, const int32_t *__restrict__ rowmap)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int XB = kSpChunk * kSpCols * 2;    // 16 KB of X rows
-    // up to 64 entries (3 KB) + 3 entries the pipelined walk may look ahead into (kept zero or
-    // stale-but-valid, so a look-ahead row offset always lands inside the stage's X rows)
-    constexpr int EB = (kSpGroups * kSpChunk + 3) * 48;
-    constexpr int BB = 48;                        // the chunk's 5 entry offsets (int64)
-    constexpr int MB = 16 + kSpChunk * 4;         // NEXT chunk's entry range + X row indices
-    constexpr int STAGE = XB + EB + BB + MB;
-    constexpr int RPT = kSpChunk / 2;             // X rows each warp stages per chunk
-    static_assert(STAGES == 2, "the next-chunk metadata is staged one chunk ahead (2-stage ring)");
+    constexpr int XB = kSpChunk * kSpRowBytes; // 16 KB of X rows
+    constexpr int EB = kSpEntryBytes;           // up to 64 entries + 3 look-ahead records
+    constexpr int STAGE = kSpStageBytes;
+    static_assert(STAGE % 16 == 0 && XB % 16 == 0 && EB % 16 == 0, "stage layout");
     const int t = blockIdx.y, bx = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int32_t *Lt = L + tptr[t];
-    const int U = (int)(tptr[t + 1] - tptr[t]);
+    const int64_t tp0 = tptr[t];
+    const int U = (int)(tptr[t + 1] - tp0);
     const int64_t c0 = tch[t];
     const int nch = (int)(tch[t + 1] - c0);
     const int64_t col0 = (int64_t)bx * kSpCols;
     const uint32_t sbase = smem_addr(smem);
+    const uint32_t bar_full = sbase + kSpStages * STAGE, bar_empty = bar_full + kSpStages * 8;
 
-    // What load_stage(c) needs before it can issue its copies -- chunk c's entry range and
-    // X row indices -- travels through shared memory: load_stage(c-1) stages it with chunk
-    // c-1 by cp.async, so it has landed when the ring wait for chunk c-1 returns, and no
-    // global-load latency is exposed at a chunk boundary.  Chunk 0 reads it from global memory.
-    auto load_stage = [&](int stage, int c, const int64_t *range, const int32_t *rows) {
-        const uint32_t sX = sbase + stage * STAGE;
-        const uint32_t sE = sX + XB;
-        const uint32_t sM = sE + EB + BB;
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-            const int r = warp + 2 * k;
-            if (c * kSpChunk + r < U) { // each lane copies two 16-byte pieces of the 1 KB row
-                const uint16_t *src = X + (int64_t)rows[r] * ldx + col0;
-                const uint32_t dst = sX + r * (kSpCols * 2);
-                cp_async16(dst + lane * 16, src + lane * 8);
-                cp_async16(dst + 512 + lane * 16, src + 256 + lane * 8);
-            }
-        }
-        const int64_t e0 = range[0];
-        const int nq = (int)(range[1] - e0) * 3;
-        for (int q = tid; q < nq; q += kSpThreads) cp_async16(sE + q * 16, E + 3 * e0 + q);
-        if (tid <= kSpGroups) cp_async8(sE + EB + tid * 8, eoff + (c0 + c) * kSpGroups + tid);
-        if (c + 1 < nch) { // metadata of chunk c+1
-            if (tid < 2) cp_async8(sM + tid * 8, eoff + (c0 + c + 1 + tid) * kSpGroups);
-            const int u = (c + 1) * kSpChunk + (tid - 2);
-            if (tid >= 2 && tid < 2 + kSpChunk && u < U) cp_async4(sM + 16 + (tid - 2) * 4, Lt + u);
-        }
-    };
-
-    uint32_t acc[kSpGroups][8][4];
-#pragma unroll
-    for (int j = 0; j < kSpGroups; ++j)
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) acc[j][r][p] = 0xFFFFFFFFu;
-
-    // Zero both stages' entry areas once: until cp.async overwrites them, look-ahead reads of
-    // entries past a chunk's end then see row offset 0.
-    for (int q = tid; q < STAGES * (EB / 16); q += kSpThreads)
+    // Zero the entry areas once (look-ahead reads past a chunk's entries then see a valid row
+    // offset, 0 or a stale one); init the barriers; order both before the async proxy.
+    for (int q = tid; q < kSpStages * (EB / 16); q += kSpThreads)
         reinterpret_cast<uint4 *>(smem + (q / (EB / 16)) * STAGE + XB)[q % (EB / 16)] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    if (nch > 0) { // chunk 0: metadata straight from global memory
-        int64_t range0[2] = {eoff[c0 * kSpGroups], eoff[(c0 + 1) * kSpGroups]};
-        int32_t rows0[kSpChunk];
-#pragma unroll
-        for (int r = 0; r < kSpChunk; ++r) rows0[r] = (r < U) ? Lt[r] : 0;
-        load_stage(0, 0, range0, rows0);
-    }
-    cp_async_commit();
-    const int xoff = warp * 128 + lane * 4; // this lane's four packed pairs within a staged row
-    for (int c = 0; c < nch; ++c) {
-        cp_async_wait<0>();
-        __syncthreads();
-        if (c + 1 < nch) { // chunk c+1's metadata arrived with chunk c
-            const uint8_t *meta = smem + (c & 1) * STAGE + XB + EB + BB;
-            load_stage((c + 1) & 1, c + 1, reinterpret_cast<const int64_t *>(meta),
-                       reinterpret_cast<const int32_t *>(meta + 16));
+    if (tid == 0) {
+        for (int st = 0; st < kSpStages; ++st) {
+            mbar_init(bar_full + st * 8, 1);
+            mbar_init(bar_empty + st * 8, kSpConsumers);
         }
-        cp_async_commit();
-        const uint8_t *stage_p = smem + (c & 1) * STAGE;
-        const uint32_t *Xs = reinterpret_cast<const uint32_t *>(stage_p);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+
+    if (warp == kSpConsumers) { // producer
+        const int32_t *Lt = L + tp0;
+        for (int c = 0; c < nch; ++c) {
+            const int st = c % kSpStages;
+            if (c >= kSpStages) mbar_wait(bar_empty + st * 8, ((c / kSpStages) - 1) & 1);
+            const int64_t gc = c0 + c;
+            const int64_t e0 = eoff[gc * kSpGroups], e1 = eoff[(gc + 1) * kSpGroups];
+            const int nrows = min(kSpChunk, U - c * kSpChunk);
+            const uint32_t ebytes = (uint32_t)(e1 - e0) * 48u;
+            const uint32_t sX = sbase + st * STAGE;
+            int32_t l = 0;
+            if (lane < nrows) l = Lt[c * kSpChunk + lane];
+            if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + 48u);
+            __syncwarp();
+            if (lane < nrows)
+                bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
+            if (lane == 16 && ebytes) bulk_g2s(sX + XB, E + 3 * e0, ebytes, bar_full + st * 8);
+            if (lane == 17) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, 48u, bar_full + st * 8);
+        }
+        return;
+    }
+
+    // consumer warp: group j = warp
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc[r][p] = 0xFFFFFFFFu;
+    for (int c = 0; c < nch; ++c) {
+        const int st = c % kSpStages;
+        mbar_wait(bar_full + st * 8, (c / kSpStages) & 1);
+        const uint8_t *stage_p = smem + st * STAGE;
         const uint4 *Es = reinterpret_cast<const uint4 *>(stage_p + XB);
         const int64_t *Bs = reinterpret_cast<const int64_t *>(stage_p + XB + EB);
         const int64_t eb = Bs[0];
-        int bound[kSpGroups + 1];
-#pragma unroll
-        for (int j = 0; j <= kSpGroups; ++j) bound[j] = (int)(Bs[j] - eb);
-        // The chunk's entries (group 0's, then group 1's, ...) are walked as ONE stream,
-        // software-pipelined across group boundaries: row offsets two entries ahead, values and
-        // X rows one entry ahead (ping-pong register sets A/B), so the LDS chain
-        // entry -> row -> X row of the next entry -- even when it opens the next group -- runs
-        // under the current entry's 32 DPX.  The look-ahead loads are unconditional: an index
-        // past the chunk reads a zero or stale record of the entry area, whose row offset is a
-        // valid one.  Row offsets are bytes, so an X load is one LDS [lane base + offset].
-        const uint32_t Xl = smem_addr(Xs + xoff);
-        auto row = [&](int q) { return (int)Es[3 * q + 2].x; };
-        int e = 0;
-        int sa = row(0), sb = row(1);
-        uint4 pa0 = Es[0], pa1 = Es[1];
-        uint4 xa = lds128(Xl + sa);
-#pragma unroll
-        for (int j = 0; j < kSpGroups; ++j) {
-            const int ee = bound[j + 1];
-            while (e < ee) { // entry e is in A
+        const int e0 = (int)(Bs[warp] - eb), e1 = (int)(Bs[warp + 1] - eb);
+        // Entries walked with values and X rows one entry ahead (ping-pong A/B) and row offsets
+        // two ahead.  Look-ahead reads past the group's end read the next group's records or a
+        // zero/stale record of the entry area, whose row offset is a valid one.  Row offsets
+        // are bytes, so an X load is one LDS [lane base + offset].
+        const uint32_t Xl = sbase + st * STAGE + lane * 16;
+        auto row = [&](int q) { return Es[3 * q + 2].x; };
+        if (e0 < e1) {
+            int e = e0;
+            uint4 pa0 = Es[3 * e], pa1 = Es[3 * e + 1];
+            uint32_t s = row(e);
+            uint4 xa0 = lds128(Xl + s), xa1 = lds128(Xl + s + 512);
+            s = row(e + 1);
+            for (;;) {
                 const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
-                const uint4 xb = lds128(Xl + sb);
-                sa = row(e + 2);
-                dpx_group(acc[j], pa0, pa1, xa);
-                if (e + 1 >= ee) { // entry e+1 opens the next group: hand it over in A
-                    pa0 = pb0;
-                    pa1 = pb1;
-                    xa = xb;
-                    sb = sa;
-                    e += 1;
-                    break;
-                }
+                const uint4 xb0 = lds128(Xl + s), xb1 = lds128(Xl + s + 512);
+                s = row(e + 2);
+                dpx_group(acc, pa0, pa1, xa0, xa1);
+                if (e + 1 >= e1) break;
                 pa0 = Es[3 * e + 6];
                 pa1 = Es[3 * e + 7];
-                xa = lds128(Xl + sa);
-                sb = row(e + 3);
-                dpx_group(acc[j], pb0, pb1, xb);
+                xa0 = lds128(Xl + s);
+                xa1 = lds128(Xl + s + 512);
+                s = row(e + 3);
+                dpx_group(acc, pb0, pb1, xb0, xb1);
                 e += 2;
+                if (e >= e1) break;
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty + st * 8);
     }
-    cp_async_wait<0>();
 
     // Epilogue: any lane sum >= 0x7FFF is +inf (G6) -> clamp to the device +inf, store.
     // (The a4 statistics stay in k_stats: fused here they cost more, 9 ms vs 5.7 ms per n = 12
-    // power, because only this CTA's 2 warps run the hashing while it holds its SM slot.)
+    // power, because only this CTA's warps run the hashing while it holds its SM slot.)
 #pragma unroll
-    for (int j = 0; j < kSpGroups; ++j)
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int64_t slot = (int64_t)t * kSpRows + kG * j + r;
-            const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
-            uint4 v;
-            v.x = __vminu2(acc[j][r][0], 0x7FFF7FFFu);
-            v.y = __vminu2(acc[j][r][1], 0x7FFF7FFFu);
-            v.z = __vminu2(acc[j][r][2], 0x7FFF7FFFu);
-            v.w = __vminu2(acc[j][r][3], 0x7FFF7FFFu);
-            *reinterpret_cast<uint4 *>(C + i * ldc + col0 + 2 * xoff) = v;
-        }
+    for (int r = 0; r < 8; ++r) {
+        const int64_t slot = (int64_t)t * kSpRows + kG * warp + r;
+        const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
+        uint16_t *crow = C + i * ldc + col0 + 8 * lane;
+        uint4 v;
+        v.x = __vminu2(acc[r][0], 0x7FFF7FFFu);
+        v.y = __vminu2(acc[r][1], 0x7FFF7FFFu);
+        v.z = __vminu2(acc[r][2], 0x7FFF7FFFu);
+        v.w = __vminu2(acc[r][3], 0x7FFF7FFFu);
+        *reinterpret_cast<uint4 *>(crow) = v;
+        v.x = __vminu2(acc[r][4], 0x7FFF7FFFu);
+        v.y = __vminu2(acc[r][5], 0x7FFF7FFFu);
+        v.z = __vminu2(acc[r][6], 0x7FFF7FFFu);
+        v.w = __vminu2(acc[r][7], 0x7FFF7FFFu);
+        *reinterpret_cast<uint4 *>(crow + 256) = v;
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1236,29 +1259,18 @@ cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s)
     return cudaGetLastError();
 }
 
-template <int STAGES>
-static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
-                                 int64_t Mp, int64_t ncols_p, cudaStream_t s)
+cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
+                        int64_t ncols_p, cudaStream_t s)
 {
     static bool attr_set = false;
-    // + 64 B: the pipelined entry loop may read up to three uint4 past the last stage
-    const int smem = STAGES * (kSpChunk * kSpCols * 2 + (kSpGroups * kSpChunk + 3) * 48 + 48 + 16 + kSpChunk * 4) + 64;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_spmm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_spmm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     dim3 grid((unsigned)(ncols_p / kSpCols), (unsigned)(Mp / kSpRows));
-    k_spmm<STAGES><<<grid, kSpThreads, smem, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
+    k_spmm<<<grid, kSpThreads, kSpSmemBytes, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
     return cudaGetLastError();
-}
-
-// k_spmm runs a 2-stage ring (5 CTAs = 10 warps per SM); a 3-stage ring measured slower
-// (fewer CTAs per SM: 155.7 vs 138.6 ms per n = 12 product in the v3 kernel).
-cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
-                        int64_t ncols_p, cudaStream_t s)
-{
-    return launch_spmm_t<2>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
 }
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
@@ -1349,7 +1361,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     SP_ALLOC(w.L, (size_t)std::max<int64_t>(tot[0], 1) * 4);
     SP_ALLOC(w.chunk_tile, (size_t)TC * 4);
     SP_ALLOC(w.ecnt, (size_t)TC * kSpGroups * 4);
-    SP_ALLOC(w.eoff, (size_t)(TC * kSpGroups + 1) * 8);
+    SP_ALLOC(w.eoff, (size_t)(TC * kSpGroups + 2) * 8); // + 1: k_spmm copies 6 offsets per chunk
     SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, w.tptr, nullptr, w.L)));
     SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
