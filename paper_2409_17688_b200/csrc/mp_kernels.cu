@@ -45,7 +45,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
     asm volatile("{\n"
                  ".reg .pred p;\n"
                  "WAIT_%=:\n"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 0x989680;\n"
                  "@!p bra WAIT_%=;\n"
                  "}\n" ::"r"(bar),
                  "r"(parity)
@@ -472,19 +472,33 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 // Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowBytes, 0, 0, 0}, s = row in the chunk.
 // ---------------------------------------------------------------------------------------
 constexpr int kG = 8;
-constexpr int kSpRows = 32;
+#ifndef MP_SP_ROWS
+#define MP_SP_ROWS 32
+#endif
+constexpr int kSpRows = MP_SP_ROWS; // one CTA tile: kSpRows / 8 groups, one consumer warp each
 constexpr int kSpGroups = kSpRows / kG;
-constexpr int kSpChunk = 16;
+#ifndef MP_SP_CHUNK
+#define MP_SP_CHUNK 16
+#endif
+#ifndef MP_SP_STAGES
+#define MP_SP_STAGES 3
+#endif
+#ifndef MP_SP_CTAS
+#define MP_SP_CTAS 3
+#endif
+constexpr int kSpChunk = MP_SP_CHUNK;
 constexpr int kSpCols = 512;            // columns per CTA (32 lanes x 16)
 constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
-constexpr int kSpConsumers = kSpGroups;  // warp j < 4 computes group j
+constexpr int kSpConsumers = kSpGroups;  // warp j < kSpGroups computes group j
 constexpr int kSpThreads = 32 * (kSpConsumers + 1); // + one producer warp
-constexpr int kSpStages = 3;
-// One ring stage: X rows | entries (+3 look-ahead records) | the chunk's 6 entry offsets.
+constexpr int kSpStages = MP_SP_STAGES;
+// One ring stage: X rows | entries (+3 look-ahead records) | the chunk's kSpGroups + 1 entry
+// offsets (copied as a 16-byte multiple).
 constexpr int kSpEntryBytes = (kSpGroups * kSpChunk + 3) * 48;
-constexpr int kSpStageBytes = kSpChunk * kSpRowBytes + kSpEntryBytes + 48;
+constexpr int kSpOffBytes = ((kSpGroups + 1) * 8 + 15) / 16 * 16;
+constexpr int kSpStageBytes = kSpChunk * kSpRowBytes + kSpEntryBytes + kSpOffBytes;
 constexpr int kSpSmemBytes = kSpStages * kSpStageBytes + 2 * kSpStages * 8;
-constexpr int kSpCtasPerSm = 3; // 3 x 57.6 KB of shared memory
+constexpr int kSpCtasPerSm = MP_SP_CTAS;
 static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
 // How the sparse-form builders read A: the 8 duplicated values (device encoding) of the rows
@@ -552,6 +566,8 @@ struct AccWords { // straight from the word masks (A(D_n) without materialising 
 // ---------------------------------------------------------------------------------------
 constexpr int kGrpWin = 512;
 constexpr int kRefThreads = 128;
+constexpr int kRefRows = 32;  // pass 3 refines 32-row halves of a tile into 4 groups each
+constexpr int kRefGroups = 4;
 
 // bits[i * nw + k] (bit b = A_(i, 32k + b) finite): blocks stride over rows, each warp over
 // the row's words, one ballot per word.
@@ -705,19 +721,19 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
                                                             int uw_max, int32_t *__restrict__ rows)
 {
     extern __shared__ uint32_t sm[];
-    __shared__ int32_t slot_row[kSpRows];
+    __shared__ int32_t slot_row[kRefRows];
     __shared__ int sh_u;
     __shared__ unsigned long long best;
-    __shared__ int gcost[kSpGroups];
+    __shared__ int gcost[kRefGroups];
     const int tid = threadIdx.x;
-    const int64_t t0 = (int64_t)blockIdx.x * kSpRows;
-    if (t0 + kSpRows > N) return; // the ragged last tile keeps the pick order
-    if (tid < kSpRows) slot_row[tid] = rows[t0 + tid];
+    const int64_t t0 = (int64_t)blockIdx.x * kRefRows;
+    if (t0 + kRefRows > N) return; // the ragged last tile keeps the pick order
+    if (tid < kRefRows) slot_row[tid] = rows[t0 + tid];
     uint32_t *G = sm;
     uint32_t *P = sm + nw;
     for (int64_t k = tid; k < nw; k += blockDim.x) G[k] = 0u;
     __syncthreads();
-    for (int r = 0; r < kSpRows; ++r) {
+    for (int r = 0; r < kRefRows; ++r) {
         const int32_t row = slot_row[r];
         for (int64_t q = off[row] + tid; q < off[row + 1]; q += blockDim.x) {
             const int32_t l = idx[q];
@@ -738,9 +754,9 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
     if (uw > uw_max) return;
     // local bitsets, staged after the G/P area, then moved to the front
     uint32_t *R = sm + 2 * nw;
-    for (int q = tid; q < kSpRows * uw; q += blockDim.x) R[q] = 0u;
+    for (int q = tid; q < kRefRows * uw; q += blockDim.x) R[q] = 0u;
     __syncthreads();
-    for (int r = 0; r < kSpRows; ++r) {
+    for (int r = 0; r < kRefRows; ++r) {
         const int32_t row = slot_row[r];
         for (int64_t q = off[row] + tid; q < off[row + 1]; q += blockDim.x) {
             const int32_t l = idx[q];
@@ -750,20 +766,20 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
         }
     }
     __syncthreads();
-    uint32_t *R0 = sm, *Um = sm + kSpRows * uw;
-    for (int q = 0; q < kSpRows * uw; q += blockDim.x) { // move R to the front (no overlap hazard:
+    uint32_t *R0 = sm, *Um = sm + kRefRows * uw;
+    for (int q = 0; q < kRefRows * uw; q += blockDim.x) { // move R to the front (no overlap hazard:
         const int x = q + tid;                             // each round reads before it writes)
-        const uint32_t v = x < kSpRows * uw ? R[x] : 0u;
+        const uint32_t v = x < kRefRows * uw ? R[x] : 0u;
         __syncthreads();
-        if (x < kSpRows * uw) R0[x] = v;
+        if (x < kRefRows * uw) R0[x] = v;
         __syncthreads();
     }
-    __shared__ int8_t member[kSpRows]; // member[s] = R0 row currently in slot s
-    if (tid < kSpRows) member[tid] = (int8_t)tid;
+    __shared__ int8_t member[kRefRows]; // member[s] = R0 row currently in slot s
+    if (tid < kRefRows) member[tid] = (int8_t)tid;
     __syncthreads();
     for (int it = 0; it < 64; ++it) {
         // Um[s] = OR of the other 7 rows of slot s's group; group costs
-        for (int q = tid; q < kSpRows * uw; q += blockDim.x) {
+        for (int q = tid; q < kRefRows * uw; q += blockDim.x) {
             const int sl = q / uw, k = q - sl * uw, g0 = (sl / kG) * kG;
             uint32_t v = 0u;
 #pragma unroll
@@ -771,10 +787,10 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
                 if (g0 + j != sl) v |= R0[member[g0 + j] * uw + k];
             Um[sl * uw + k] = v;
         }
-        if (tid < kSpGroups) gcost[tid] = 0;
+        if (tid < kRefGroups) gcost[tid] = 0;
         if (tid == 0) best = ~0ull;
         __syncthreads();
-        for (int q = tid; q < kSpGroups * uw; q += blockDim.x) {
+        for (int q = tid; q < kRefGroups * uw; q += blockDim.x) {
             const int g = q / uw, k = q - g * uw;
             const int sl = g * kG;
             atomicAdd(&gcost[g], __popc(Um[sl * uw + k] | R0[member[sl] * uw + k]));
@@ -809,7 +825,7 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
         }
         __syncthreads();
     }
-    if (tid < kSpRows) rows[t0 + tid] = slot_row[member[tid]];
+    if (tid < kRefRows) rows[t0 + tid] = slot_row[member[tid]];
 }
 
 __global__ void k_iota_rows(int32_t *__restrict__ rows, int64_t from, int64_t to)
@@ -1066,22 +1082,34 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
 
     if (warp == kSpConsumers) { // producer
         const int32_t *Lt = L + tp0;
+        // chunk c's metadata (entry range, X row indices) is loaded one chunk ahead, so after
+        // a stage frees up only the bulk copies themselves remain to be issued
+        auto meta = [&](int c, int64_t &e0, int64_t &e1, int32_t &l) {
+            if (c >= nch) return;
+            const int64_t gc = c0 + c;
+            e0 = eoff[gc * kSpGroups];
+            e1 = eoff[(gc + 1) * kSpGroups];
+            l = (c * kSpChunk + lane < U) ? Lt[c * kSpChunk + lane] : 0;
+        };
+        int64_t ne0 = 0, ne1 = 0;
+        int32_t nl = 0;
+        meta(0, ne0, ne1, nl);
         for (int c = 0; c < nch; ++c) {
             const int st = c % kSpStages;
+            const int64_t e0 = ne0, e1 = ne1;
+            const int32_t l = nl;
+            meta(c + 1, ne0, ne1, nl);
             if (c >= kSpStages) mbar_wait(bar_empty + st * 8, ((c / kSpStages) - 1) & 1);
             const int64_t gc = c0 + c;
-            const int64_t e0 = eoff[gc * kSpGroups], e1 = eoff[(gc + 1) * kSpGroups];
             const int nrows = min(kSpChunk, U - c * kSpChunk);
             const uint32_t ebytes = (uint32_t)(e1 - e0) * 48u;
             const uint32_t sX = sbase + st * STAGE;
-            int32_t l = 0;
-            if (lane < nrows) l = Lt[c * kSpChunk + lane];
-            if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + 48u);
+            if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + kSpOffBytes);
             __syncwarp();
             if (lane < nrows)
                 bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
-            if (lane == 16 && ebytes) bulk_g2s(sX + XB, E + 3 * e0, ebytes, bar_full + st * 8);
-            if (lane == 17) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, 48u, bar_full + st * 8);
+            if (lane == 0 && ebytes) bulk_g2s(sX + XB, E + 3 * e0, ebytes, bar_full + st * 8);
+            if (lane == 1) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, kSpOffBytes, bar_full + st * 8);
         }
         return;
     }
@@ -1330,12 +1358,12 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
         // pass 3: shared memory = max(G + P + R staging, R + Um); tile unions up to 12288 l
         // (n = 12: consecutive tiles reach 9600 at most, greedy tiles fewer)
         const int64_t uw_max = 384;
-        if (N >= kSpRows) {
-            const int smem_r = (int)(4 * std::max<int64_t>(2 * nw + kSpRows * uw_max, 2 * kSpRows * uw_max));
+        if (N >= kRefRows) {
+            const int smem_r = (int)(4 * std::max<int64_t>(2 * nw + kRefRows * uw_max, 2 * kRefRows * uw_max));
             if ((e = cudaFuncSetAttribute(k_tile_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_r)) !=
                 cudaSuccess)
                 return e;
-            SP_LAUNCH((k_tile_refine<<<(unsigned)(N / kSpRows), kRefThreads, smem_r, s>>>(off, idx, nw, N, (int)uw_max,
+            SP_LAUNCH((k_tile_refine<<<(unsigned)(N / kRefRows), kRefThreads, smem_r, s>>>(off, idx, nw, N, (int)uw_max,
                                                                                          w.rows)));
         }
         if (Np > N) SP_LAUNCH((k_iota_rows<<<grid_for(Np - N, 256), 256, 0, s>>>(w.rows, N, Np)));
@@ -1361,7 +1389,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     SP_ALLOC(w.L, (size_t)std::max<int64_t>(tot[0], 1) * 4);
     SP_ALLOC(w.chunk_tile, (size_t)TC * 4);
     SP_ALLOC(w.ecnt, (size_t)TC * kSpGroups * 4);
-    SP_ALLOC(w.eoff, (size_t)(TC * kSpGroups + 2) * 8); // + 1: k_spmm copies 6 offsets per chunk
+    SP_ALLOC(w.eoff, (size_t)(TC * kSpGroups + kSpOffBytes / 8) * 8); // k_spmm copies kSpOffBytes per chunk
     SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, w.tptr, nullptr, w.L)));
     SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
