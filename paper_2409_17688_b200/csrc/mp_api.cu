@@ -327,7 +327,7 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
         cudaGetLastError();
         return fail(MP_ERR_CUDA, "building the sparse form of A failed: %s", cudaGetErrorString(e));
     }
-    R.issued_spmm = (double)R.sp.entries * 8.0 * (double)R.ld;
+    R.issued_spmm = (double)R.sp.entries * (double)R.sp.group_rows * (double)R.ld;
     return MP_OK;
 }
 

@@ -471,7 +471,13 @@ __global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long
 // the same product.
 // Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowBytes, 0, 0, 0}, s = row in the chunk.
 // ---------------------------------------------------------------------------------------
-constexpr int kG = 8;
+#ifndef MP_SP_G
+#define MP_SP_G 4
+#endif
+constexpr int kG = MP_SP_G;             // rows per group (4 or 8)
+static_assert(kG == 4 || kG == 8, "group size");
+constexpr int kEntU4 = kG / 4 + 1;      // entry record: kG values {a, a}, then {row offset, 0, 0, 0}
+constexpr int kEntBytes = 16 * kEntU4;
 #ifndef MP_SP_ROWS
 #define MP_SP_ROWS 32
 #endif
@@ -494,16 +500,16 @@ constexpr int kSpThreads = 32 * (kSpConsumers + 1); // + one producer warp
 constexpr int kSpStages = MP_SP_STAGES;
 // One ring stage: X rows | entries (+3 look-ahead records) | the chunk's kSpGroups + 1 entry
 // offsets (copied as a 16-byte multiple).
-constexpr int kSpEntryBytes = (kSpGroups * kSpChunk + 3) * 48;
+constexpr int kSpEntryBytes = (kSpGroups * kSpChunk + 3) * kEntBytes;
 constexpr int kSpOffBytes = ((kSpGroups + 1) * 8 + 15) / 16 * 16;
 constexpr int kSpStageBytes = kSpChunk * kSpRowBytes + kSpEntryBytes + kSpOffBytes;
 constexpr int kSpSmemBytes = kSpStages * kSpStageBytes + 2 * kSpStages * 8;
 constexpr int kSpCtasPerSm = MP_SP_CTAS;
 static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
-// How the sparse-form builders read A: the 8 duplicated values (device encoding) of the rows
-// in group slot 8g..8g+7 at column l; finite(i, l) for i, l < N.  `rows` (may be null = identity) maps a slot to its row of A: the
-// row grouping of k_group_greedy.
+// How the sparse-form builders read A: the kG duplicated values (device encoding) of the rows
+// in group slots kG*g .. kG*g + kG-1 at column l; finite(i, l) for i, l < N.  `rows` (may be
+// null = identity) maps a slot to its row of A: the row grouping of pass 2/3 below.
 struct AccA { // matrix sources: A itself (row-major, boundary encoding, range-checked)
     const uint16_t *A;
     int64_t lda, N;
@@ -514,13 +520,10 @@ struct AccA { // matrix sources: A itself (row-major, boundary encoding, range-c
         if (x > kFiniteMax) x = kDevInf;
         return x | (x << 16);
     }
-    __device__ __forceinline__ void row8(int64_t g, int64_t l, uint4 &v0, uint4 &v1) const
+    __device__ __forceinline__ void rowv(int64_t g, int64_t l, uint32_t (&v)[kG]) const
     {
-        uint32_t v[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) v[r] = enc2(rows ? (int64_t)rows[g * kG + r] : g * kG + r, l);
-        v0 = make_uint4(v[0], v[1], v[2], v[3]);
-        v1 = make_uint4(v[4], v[5], v[6], v[7]);
+        for (int r = 0; r < kG; ++r) v[r] = enc2(rows ? (int64_t)rows[g * kG + r] : g * kG + r, l);
     }
     __device__ __forceinline__ bool finite(int64_t i, int64_t l) const { return A[i * lda + l] != kBndInf; }
 };
@@ -529,20 +532,17 @@ struct AccWords { // straight from the word masks (A(D_n) without materialising 
     int64_t N;
     unsigned full;
     const int32_t *rows;
-    __device__ __forceinline__ void row8(int64_t g, int64_t l, uint4 &v0, uint4 &v1) const
+    __device__ __forceinline__ void rowv(int64_t g, int64_t l, uint32_t (&v)[kG]) const
     {
-        uint32_t v[8];
         const bool lok = l < N;
         WordMask p = {0, 0, 0, 0};
         if (lok) p = w[l];
         const uint32_t lab = (uint32_t)p.zeros | ((uint32_t)p.zeros << 16);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < kG; ++r) {
             const int64_t i = rows ? (int64_t)rows[g * kG + r] : g * kG + r;
             v[r] = (lok && i < N && can_follow_mask(w[i], p, full)) ? lab : 0x7FFF7FFFu;
         }
-        v0 = make_uint4(v[0], v[1], v[2], v[3]);
-        v1 = make_uint4(v[4], v[5], v[6], v[7]);
     }
     __device__ __forceinline__ bool finite(int64_t i, int64_t l) const
     {
@@ -566,8 +566,19 @@ struct AccWords { // straight from the word masks (A(D_n) without materialising 
 // ---------------------------------------------------------------------------------------
 constexpr int kGrpWin = 512;
 constexpr int kRefThreads = 128;
-constexpr int kRefRows = 32;  // pass 3 refines 32-row halves of a tile into 4 groups each
-constexpr int kRefGroups = 4;
+constexpr int kRefRows = 32; // pass 3 refines 32-row blocks of a tile into groups of kG
+constexpr int kRefGroups = kRefRows / kG;
+constexpr int kRefPairs = kRefGroups * (kRefGroups - 1) / 2;
+// pr-th pair (A < B) of groups in lexicographic order
+__device__ __forceinline__ void ref_pair(int pr, int &A, int &B)
+{
+    A = 0;
+    while (pr >= kRefGroups - 1 - A) {
+        pr -= kRefGroups - 1 - A;
+        ++A;
+    }
+    B = A + 1 + pr;
+}
 
 // bits[i * nw + k] (bit b = A_(i, 32k + b) finite): blocks stride over rows, each warp over
 // the row's words, one ballot per word.
@@ -796,11 +807,11 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
             atomicAdd(&gcost[g], __popc(Um[sl * uw + k] | R0[member[sl] * uw + k]));
         }
         __syncthreads();
-        // all 384 swaps (slot a in group A < group B of slot b)
-        for (int q = tid; q < 6 * kG * kG; q += blockDim.x) {
+        // every swap (slot a in group A < group B of slot b)
+        for (int q = tid; q < kRefPairs * kG * kG; q += blockDim.x) {
             const int pr = q / (kG * kG), ab = q - pr * (kG * kG);
-            const int A = pr < 3 ? 0 : pr < 5 ? 1 : 2;
-            const int B = pr < 3 ? pr + 1 : pr < 5 ? pr - 1 : 3;
+            int A, B;
+            ref_pair(pr, A, B);
             const int sa = A * kG + ab / kG, sb = B * kG + ab % kG;
             const uint32_t *ra = R0 + member[sa] * uw, *rb = R0 + member[sb] * uw;
             const uint32_t *ua = Um + sa * uw, *ub = Um + sb * uw;
@@ -816,8 +827,8 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
         if (tid == 0) {
             const int q = (int)(bb & 0xFFFFFFFFu);
             const int pr = q / (kG * kG), ab = q - pr * (kG * kG);
-            const int A = pr < 3 ? 0 : pr < 5 ? 1 : 2;
-            const int B = pr < 3 ? pr + 1 : pr < 5 ? pr - 1 : 3;
+            int A, B;
+            ref_pair(pr, A, B);
             const int sa = A * kG + ab / kG, sb = B * kG + ab % kG;
             const int8_t x = member[sa];
             member[sa] = member[sb];
@@ -834,7 +845,7 @@ __global__ void k_iota_rows(int32_t *__restrict__ rows, int64_t from, int64_t to
         rows[i] = (int32_t)i;
 }
 
-// m8[g * Np + l] = bit r set iff A_(8g+r, l) is finite.
+// m8[g * Np + l] = bit r set iff A_(slot kG*g + r, l) is finite.
 template <class Acc>
 __global__ void k_group_masks(Acc acc, int64_t Np, uint8_t *__restrict__ m8)
 {
@@ -842,12 +853,11 @@ __global__ void k_group_masks(Acc acc, int64_t Np, uint8_t *__restrict__ m8)
     const int64_t total = G * Np;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = t / Np, l = t - g * Np;
-        uint4 v0, v1;
-        acc.row8(g, l, v0, v1);
-        const uint32_t v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        uint32_t v[kG];
+        acc.rowv(g, l, v);
         unsigned m = 0;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) m |= (v[r] != 0x7FFF7FFFu) ? (1u << r) : 0u;
+        for (int r = 0; r < kG; ++r) m |= (v[r] != 0x7FFF7FFFu) ? (1u << r) : 0u;
         m8[t] = (uint8_t)m;
     }
 }
@@ -944,11 +954,12 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
             const int64_t l = Lt[r];
             if (!m[l]) continue;
             if (E) {
-                uint4 v0, v1;
-                acc.row8(g, l, v0, v1);
-                E[3 * e] = v0;
-                E[3 * e + 1] = v1;
-                E[3 * e + 2] = make_uint4((unsigned)s * (unsigned)kSpRowBytes, 0u, 0u, 0u); // X row offset (bytes)
+                uint32_t v[kG];
+                acc.rowv(g, l, v);
+#pragma unroll
+                for (int u = 0; u < kG / 4; ++u)
+                    E[kEntU4 * e + u] = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                E[kEntU4 * e + kG / 4] = make_uint4((unsigned)s * (unsigned)kSpRowBytes, 0u, 0u, 0u); // X row (bytes)
                 ++e;
             }
             ++cnt;
@@ -998,22 +1009,23 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
 }
 
-// acc[r][p] = min(a_r + x_p, acc[r][p]) for the 8 rows of a group entry and this lane's eight
-// packed column pairs.
-__device__ __forceinline__ void dpx_group(uint32_t (&acc)[8][8], const uint4 &a0, const uint4 &a1, const uint4 &x0,
+// acc[r][p] = min(a_r + x_p, acc[r][p]) for the kG rows of a group entry and this lane's
+// eight packed column pairs.
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][8], const uint4 (&av)[kG / 4], const uint4 &x0,
                                           const uint4 &x1)
 {
-    const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        acc[r][0] = __viaddmin_u16x2(a[r], x0.x, acc[r][0]);
-        acc[r][1] = __viaddmin_u16x2(a[r], x0.y, acc[r][1]);
-        acc[r][2] = __viaddmin_u16x2(a[r], x0.z, acc[r][2]);
-        acc[r][3] = __viaddmin_u16x2(a[r], x0.w, acc[r][3]);
-        acc[r][4] = __viaddmin_u16x2(a[r], x1.x, acc[r][4]);
-        acc[r][5] = __viaddmin_u16x2(a[r], x1.y, acc[r][5]);
-        acc[r][6] = __viaddmin_u16x2(a[r], x1.z, acc[r][6]);
-        acc[r][7] = __viaddmin_u16x2(a[r], x1.w, acc[r][7]);
+    for (int r = 0; r < kG; ++r) {
+        const uint4 &q = av[r / 4];
+        const uint32_t a = (r % 4 == 0) ? q.x : (r % 4 == 1) ? q.y : (r % 4 == 2) ? q.z : q.w;
+        acc[r][0] = __viaddmin_u16x2(a, x0.x, acc[r][0]);
+        acc[r][1] = __viaddmin_u16x2(a, x0.y, acc[r][1]);
+        acc[r][2] = __viaddmin_u16x2(a, x0.z, acc[r][2]);
+        acc[r][3] = __viaddmin_u16x2(a, x0.w, acc[r][3]);
+        acc[r][4] = __viaddmin_u16x2(a, x1.x, acc[r][4]);
+        acc[r][5] = __viaddmin_u16x2(a, x1.y, acc[r][5]);
+        acc[r][6] = __viaddmin_u16x2(a, x1.z, acc[r][6]);
+        acc[r][7] = __viaddmin_u16x2(a, x1.w, acc[r][7]);
     }
 }
 
@@ -1102,22 +1114,22 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
             if (c >= kSpStages) mbar_wait(bar_empty + st * 8, ((c / kSpStages) - 1) & 1);
             const int64_t gc = c0 + c;
             const int nrows = min(kSpChunk, U - c * kSpChunk);
-            const uint32_t ebytes = (uint32_t)(e1 - e0) * 48u;
+            const uint32_t ebytes = (uint32_t)(e1 - e0) * kEntBytes;
             const uint32_t sX = sbase + st * STAGE;
             if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + kSpOffBytes);
             __syncwarp();
             if (lane < nrows)
                 bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
-            if (lane == 0 && ebytes) bulk_g2s(sX + XB, E + 3 * e0, ebytes, bar_full + st * 8);
+            if (lane == 0 && ebytes) bulk_g2s(sX + XB, E + kEntU4 * e0, ebytes, bar_full + st * 8);
             if (lane == 1) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, kSpOffBytes, bar_full + st * 8);
         }
         return;
     }
 
     // consumer warp: group j = warp
-    uint32_t acc[8][8];
+    uint32_t acc[kG][8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < kG; ++r)
 #pragma unroll
         for (int p = 0; p < 8; ++p) acc[r][p] = 0xFFFFFFFFu;
     for (int c = 0; c < nch; ++c) {
@@ -1133,25 +1145,29 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
         // zero/stale record of the entry area, whose row offset is a valid one.  Row offsets
         // are bytes, so an X load is one LDS [lane base + offset].
         const uint32_t Xl = sbase + st * STAGE + lane * 16;
-        auto row = [&](int q) { return Es[3 * q + 2].x; };
+        auto row = [&](int q) { return Es[kEntU4 * q + kG / 4].x; };
+        auto vals = [&](int q, uint4(&v)[kG / 4]) {
+#pragma unroll
+            for (int u = 0; u < kG / 4; ++u) v[u] = Es[kEntU4 * q + u];
+        };
         if (e0 < e1) {
             int e = e0;
-            uint4 pa0 = Es[3 * e], pa1 = Es[3 * e + 1];
+            uint4 pa[kG / 4], pb[kG / 4];
+            vals(e, pa);
             uint32_t s = row(e);
             uint4 xa0 = lds128(Xl + s), xa1 = lds128(Xl + s + 512);
             s = row(e + 1);
             for (;;) {
-                const uint4 pb0 = Es[3 * e + 3], pb1 = Es[3 * e + 4];
+                vals(e + 1, pb);
                 const uint4 xb0 = lds128(Xl + s), xb1 = lds128(Xl + s + 512);
                 s = row(e + 2);
-                dpx_group(acc, pa0, pa1, xa0, xa1);
+                dpx_group(acc, pa, xa0, xa1);
                 if (e + 1 >= e1) break;
-                pa0 = Es[3 * e + 6];
-                pa1 = Es[3 * e + 7];
+                vals(e + 2, pa);
                 xa0 = lds128(Xl + s);
                 xa1 = lds128(Xl + s + 512);
                 s = row(e + 3);
-                dpx_group(acc, pb0, pb1, xb0, xb1);
+                dpx_group(acc, pb, xb0, xb1);
                 e += 2;
                 if (e >= e1) break;
             }
@@ -1164,7 +1180,7 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
     // (The a4 statistics stay in k_stats: fused here they cost more, 9 ms vs 5.7 ms per n = 12
     // power, because only this CTA's warps run the hashing while it holds its SM slot.)
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < kG; ++r) {
         const int64_t slot = (int64_t)t * kSpRows + kG * warp + r;
         const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
         uint16_t *crow = C + i * ldc + col0 + 8 * lane;
@@ -1399,7 +1415,8 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     if ((e = cudaMemcpyAsync(&ne, w.eoff + tot[1] * kSpGroups, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     w.entries = ne;
-    SP_ALLOC(w.E, (size_t)std::max<int64_t>(ne, 1) * 48);
+    SP_ALLOC(w.E, (size_t)std::max<int64_t>(ne, 1) * kEntBytes);
+    w.group_rows = kG;
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E)));
 #undef SP_LAUNCH

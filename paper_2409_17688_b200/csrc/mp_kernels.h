@@ -42,6 +42,7 @@ struct SparseWork {
     int64_t *tptr = nullptr, *tch = nullptr, *eoff = nullptr;
     uint4 *E = nullptr;
     int32_t *rows = nullptr; // row grouping (null: consecutive rows)
+    int group_rows = 0;      // rows per group: issued steps = entries * group_rows * ld
     int64_t total_union = 0, total_chunks = 0, entries = 0;
 };
 cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
