@@ -104,8 +104,8 @@ typedef struct {
     int32_t dense_from; /* first k with no +inf entry (0 if none up to k_last)     */
     uint16_t diag_min[MP_MAX_K + 1];    /* diag_min[k] = min_i (A^k)_ii, 1 <= k <= k_last
                                            (Algorithm 5); MP_INF if none     */
-    uint64_t fingerprint[MP_MAX_K + 1]; /* H(A^k) = sum_t splitmix64(t) * x_t mod 2^64,
-                                           t = i*N + j, +inf as 0xFFFF      */
+    uint64_t fingerprint[MP_MAX_K + 1]; /* H(A^k) = sum_ij s(2i) s(2j+1) x_ij mod 2^64,
+                                           s = splitmix64, +inf as 0xFFFF   */
 } mp_periodic_result;
 
 /* A^1 = A, A^k = A x A^{k-1} (Algorithm 2, left multiplication G8) for
@@ -214,7 +214,8 @@ typedef struct {
                             t = i*N + j; INT64_MAX if the matrix is all +inf                 */
 } mp_power_stats;
 
-/* S(N) = sum_{t < N*N} splitmix64(t) mod 2^64 (the fingerprint of the all-ones matrix). */
+/* S(N) = sum_{i,j < N} s(2i) s(2j+1) mod 2^64, s = splitmix64 (the fingerprint of the
+ * all-ones matrix). */
 uint64_t mp_fingerprint_unit(int64_t N);
 
 /* Candidate test of the forward first-repeat search: returns 1 if A^k may equal

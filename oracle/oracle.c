@@ -202,10 +202,12 @@ void oracle_minplus_ikj(const uint16_t *A, const uint16_t *B, uint16_t *C, int64
 
 /* ------------------------------------------------------------------------------------ */
 /* c4 fingerprint (SURVEY.md section 8(a) note a4):
- *   h(t) = splitmix64 finaliser of t + 0x9E3779B97F4A7C15;
- *   H(X) = sum over t = i*N + j of h(t) * x_t  (mod 2^64), inf encoded as 0xFFFF.
+ *   s(z)   = splitmix64 finaliser of z + 0x9E3779B97F4A7C15;
+ *   h(i,j) = s(2i) * s(2j + 1)  (row weight times column weight);
+ *   H(X)   = sum over i, j of h(i,j) * x_ij  (mod 2^64), inf encoded as 0xFFFF.
  * Not a paper quantity: a checksum both sides define independently so whole matrices can
- * be compared without moving them.  Pinned by the splitmix64 test vectors and linearity. */
+ * be compared without moving them.  Pinned by the splitmix64 test vectors, linearity,
+ * additivity and single entries. */
 /* ------------------------------------------------------------------------------------ */
 
 uint64_t oracle_splitmix64(uint64_t t)
@@ -219,13 +221,16 @@ uint64_t oracle_splitmix64(uint64_t t)
 uint64_t oracle_fingerprint(const uint16_t *X, int64_t R, int64_t Ncols)
 {
     uint64_t H = 0;
-    int64_t t;
-    for (t = 0; t < R * Ncols; t++) H += oracle_splitmix64((uint64_t)t) * (uint64_t)X[t];
+    int64_t i, j;
+    for (i = 0; i < R; i++)
+        for (j = 0; j < Ncols; j++)
+            H += oracle_splitmix64(2 * (uint64_t)i) * oracle_splitmix64(2 * (uint64_t)j + 1) *
+                 (uint64_t)X[i * Ncols + j];
     return H;
 }
 
-/* Fingerprint of the column block [c0, c1) of an R x Ncols matrix, with canonical global
- * indices t = i*Ncols + j (the additive shard contribution used by the multi-rank tests). */
+/* Fingerprint of the column block [c0, c1) of an R x Ncols matrix, with the global column
+ * index j (the additive shard contribution used by the multi-rank tests). */
 uint64_t oracle_fingerprint_cols(const uint16_t *X, int64_t R, int64_t Ncols, int64_t c0,
                                  int64_t c1)
 {
@@ -233,7 +238,8 @@ uint64_t oracle_fingerprint_cols(const uint16_t *X, int64_t R, int64_t Ncols, in
     int64_t i, j;
     for (i = 0; i < R; i++)
         for (j = c0; j < c1; j++)
-            H += oracle_splitmix64((uint64_t)(i * Ncols + j)) * (uint64_t)X[i * Ncols + j];
+            H += oracle_splitmix64(2 * (uint64_t)i) * oracle_splitmix64(2 * (uint64_t)j + 1) *
+                 (uint64_t)X[i * Ncols + j];
     return H;
 }
 

@@ -193,7 +193,6 @@ struct DevState {
     DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c;
     std::unique_ptr<PowerRun> pr;
 };
-std::map<int64_t, uint64_t> g_unit_cache; // S(N)
 std::map<int, DevState> g_dev;
 
 mp_status current_device(int *dev_out, DevState **st)
@@ -558,17 +557,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     }
 
     std::vector<mp_power_stats> hs((size_t)max_k + 1);
-    uint64_t S = 0;
-    if (g_unit_cache.count(N)) {
-        S = g_unit_cache[N];
-    } else {
-        unsigned long long *dS = reinterpret_cast<unsigned long long *>(R.flag.p);
-        CUDA_TRY(cudaMemsetAsync(dS, 0, 8, s));
-        LAUNCH(launch_unit_sum(N, dS, s));
-        COPY(&S, dS, 8, cudaMemcpyDeviceToHost, s);
-        CUDA_TRY(cudaStreamSynchronize(s));
-        g_unit_cache[N] = S;
-    }
+    const uint64_t S = mp_fingerprint_unit(N); // O(N) on the host
     double prod_ms = 0.0, stats_ms = 0.0;
     int64_t launches = 0;
     cudaEvent_t ev_setup;
@@ -939,20 +928,13 @@ mp_status mp_shard_range(int64_t N, int world, int rank, int64_t *c0, int64_t *c
 
 uint64_t mp_fingerprint_unit(int64_t N)
 {
-    const uint64_t T = (uint64_t)(N > 0 ? N : 0) * (uint64_t)(N > 0 ? N : 0);
-    const int nt = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)host_threads(), T / 65536 + 1));
-    std::vector<uint64_t> part((size_t)nt, 0);
-    std::vector<std::thread> pool;
-    for (int id = 0; id < nt; ++id)
-        pool.emplace_back([&, id] {
-            uint64_t acc = 0;
-            for (uint64_t t = (uint64_t)id; t < T; t += (uint64_t)nt) acc += mix64(t);
-            part[(size_t)id] = acc;
-        });
-    for (auto &th : pool) th.join();
-    uint64_t S = 0;
-    for (uint64_t v : part) S += v;
-    return S;
+    // S(N) = sum over i, j < N of s(2i) s(2j+1) = (sum_i s(2i)) (sum_j s(2j+1))  (mod 2^64)
+    uint64_t a = 0, b = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        a += mix64(2 * (uint64_t)i);
+        b += mix64(2 * (uint64_t)i + 1);
+    }
+    return a * b;
 }
 
 int mp_repeat_candidate(const mp_power_stats *sk, const mp_power_stats *sj, uint64_t S, int32_t *c_out)

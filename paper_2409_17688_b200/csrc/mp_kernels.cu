@@ -181,59 +181,62 @@ __global__ void __launch_bounds__(kThreads, 1)
 // a4: per-power statistics of a column shard X (rows 0..N-1, columns c0..c0+w-1 of the
 // global power, stored [Np][ld]).  The SUM-reduced and the MIN-reduced fields live in two
 // arrays so that a batch of powers is all-reduced with one SUM and one MIN call:
-//   out_sum[0] += H = sum h(i*N + c0 + j) * x (mod 2^64), +inf counted as 0xFFFF;
+//   out_sum[0] += H = sum s(2i) s(2(c0+j)+1) x_ij (mod 2^64), +inf counted as 0xFFFF
+//                 (row weight times column weight);
 //   out_sum[1] += number of +inf entries;
 //   out_min[0]  = min(out_min[0], min over i == c0 + j of x)  (Algorithm 5);
 //   out_min[1]  = min(out_min[1], (t << 16) | x) over finite entries, t = i*N + c0 + j.
-// The caller initialises {0, 0} and {0xFFFF, INT64_MAX}.  Reads 2*N*w bytes.
+// The caller initialises {0, 0} and {0xFFFF, INT64_MAX}.  Reads 2*N*w bytes.  Block (x, y)
+// covers kStCols columns x a range of rows; a thread keeps the 8 column weights of its
+// 16-byte column slice in registers, so an element costs a 64-bit multiply-add and a row one
+// row weight.
 // ---------------------------------------------------------------------------------------
+constexpr int kStCols = 256 * 8;
 __global__ void __launch_bounds__(256)
-    k_stats(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t c0, int64_t w,
+    k_stats(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t c0, int64_t w, int64_t rpb,
             unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
 {
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
-    // rows strided over the blocks, 8-column chunks strided over the threads of a block
-    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
-        const uint64_t tbase = (uint64_t)(i * N + c0);
-        const uint16_t *row = X + i * ld;
-        if (threadIdx.x == 0 && i >= c0 && i < c0 + w) { // the row's diagonal entry, if in the shard
-            const uint32_t x = row[i - c0];
-            dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
-        }
-        for (int64_t j0 = (int64_t)threadIdx.x * 8; j0 < w; j0 += (int64_t)blockDim.x * 8) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(row + j0);
+    const int64_t j0 = (int64_t)blockIdx.x * kStCols + (int64_t)threadIdx.x * 8;
+    const int64_t i0 = (int64_t)blockIdx.y * rpb, i1 = min(N, i0 + rpb);
+    if (j0 < w) {
+        const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
+        uint64_t b[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) b[e] = e < nc ? mix64(2 * (uint64_t)(c0 + j0 + e) + 1) : 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
             const uint32_t words[4] = {v.x, v.y, v.z, v.w};
-            // fast path: a full chunk without +inf (every power from k = 3 on) needs no
-            // +inf bookkeeping, and its smallest finite key is its first entry
-            const bool full = j0 + 8 <= w;
+            const uint64_t t0 = (uint64_t)(i * N + c0 + j0);
             const uint32_t anyinf = __vcmpeq2(v.x, 0x7FFF7FFFu) | __vcmpeq2(v.y, 0x7FFF7FFFu) |
                                     __vcmpeq2(v.z, 0x7FFF7FFFu) | __vcmpeq2(v.w, 0x7FFF7FFFu);
-            if (full && !anyinf) {
-                const uint64_t t0 = tbase + (uint64_t)j0;
+            uint64_t rs = 0;
+            if (nc == 8 && !anyinf) { // every power from k = 3 on: no +inf bookkeeping
                 const unsigned long long key = (t0 << 16) | (v.x & 0xFFFFu);
                 if (key < ref) ref = key;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                    h += (unsigned long long)mix64(t0 + (uint64_t)e) * x;
-                }
-                continue;
-            }
+                for (int e = 0; e < 8; ++e) rs += b[e] * ((words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+            } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int64_t j = j0 + e;
-                if (j >= w) break;
-                uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                const uint64_t t = tbase + (uint64_t)j;
-                if (x == kDevInf) {
-                    x = kBndInf;
-                    ++infc;
-                } else {
-                    const unsigned long long key = (t << 16) | x;
-                    if (key < ref) ref = key;
+                for (int e = 0; e < 8; ++e) {
+                    if (e >= nc) break;
+                    uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                    if (x == kDevInf) {
+                        x = kBndInf;
+                        ++infc;
+                    } else {
+                        const unsigned long long key = ((t0 + (uint64_t)e) << 16) | x;
+                        if (key < ref) ref = key;
+                    }
+                    rs += b[e] * x;
                 }
-                h += (unsigned long long)mix64(t) * x;
+            }
+            h += mix64(2 * (uint64_t)i) * rs;
+            const int64_t d = i - c0 - j0; // the row's diagonal entry, if in this slice
+            if (d >= 0 && d < nc) {
+                const uint32_t x = (words[d >> 1] >> ((d & 1) * 16)) & 0xFFFFu;
+                dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
             }
         }
     }
@@ -444,16 +447,6 @@ __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, i
 
 // S(N) = sum_{t < N*N} h(t) mod 2^64 (fingerprint of the all-ones matrix), accumulated
 // into *out (zeroed by the caller).  Pure ALU work, no memory traffic.
-__global__ void __launch_bounds__(256) k_unit_sum(uint64_t T, unsigned long long *__restrict__ out)
-{
-    unsigned long long acc = 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x)
-        acc += mix64(t);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
-}
-
 // ---------------------------------------------------------------------------------------
 // a3, sparse form (NEXT-1 ii, exact): grouped (min,+) SpMM.
 //
@@ -1244,8 +1237,10 @@ cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, 
 cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, int64_t w,
                          unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s)
 {
-    const int g = (int)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8); // row-strided blocks
-    k_stats<<<g, 256, 0, s>>>(X, ld, N, c0, w, out_sum, out_min);
+    const int64_t gx = std::max<int64_t>(1, (w + kStCols - 1) / kStCols);
+    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t)num_sms() * 8 / gx));
+    const int64_t rpb = (N + gy - 1) / gy;
+    k_stats<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(X, ld, N, c0, w, rpb, out_sum, out_min);
     return cudaGetLastError();
 }
 
@@ -1293,13 +1288,6 @@ cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_
                           int64_t ldd, cudaStream_t s)
 {
     k_decode<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, lds, rows, cols, dst, ldd);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s)
-{
-    const uint64_t T = (uint64_t)N * (uint64_t)N;
-    k_unit_sum<<<grid_for((int64_t)std::min<uint64_t>(T, 1ull << 40), 256), 256, 0, s>>>(T, out);
     return cudaGetLastError();
 }
 

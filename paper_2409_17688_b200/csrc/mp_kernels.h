@@ -57,7 +57,6 @@ cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int
                                     int64_t *launches);
 cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, int64_t w,
                                  uint16_t *X1, int64_t ldx, cudaStream_t s);
-cudaError_t launch_unit_sum(int64_t N, unsigned long long *out, cudaStream_t s);
 // Range check of a row-major A (flag set if an entry lies in (0x7FFE, 0xFFFF)) and, if occ is
 // not null, the occupancy of its 128 x 32 tiles (occ zeroed by the caller).
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,

@@ -241,7 +241,7 @@ def test_splitmix64_vectors(oracle_mod):
 
 def test_fingerprint_linear_and_additive(oracle_mod):
     """H(c (x) X) = H(X) + c*S for inf-free X (S = H(all-ones)); H is additive over column
-    blocks; a single entry gives h(t)*x."""
+    blocks; a single entry (i, j) gives s(2i)*s(2j+1)*x."""
     X = synth.power_like(23, 29, salt=50)
     S = oracle_mod.fingerprint(np.ones_like(X))
     for c in (1, 3, 14):
@@ -251,7 +251,10 @@ def test_fingerprint_linear_and_additive(oracle_mod):
     assert sum(parts) % 2**64 == oracle_mod.fingerprint(X)
     Z = np.zeros_like(X)
     Z[4, 5] = 9
-    assert oracle_mod.fingerprint(Z) == (9 * oracle_mod.splitmix64(4 * 29 + 5)) % 2**64
+    assert oracle_mod.fingerprint(Z) == (9 * oracle_mod.splitmix64(2 * 4) * oracle_mod.splitmix64(2 * 5 + 1)) % 2**64
+    Z[4, 5] = 0
+    Z[0, 0] = 1  # h(0, 0) = s(0) * s(1)
+    assert oracle_mod.fingerprint(Z) == (0xE220A8397B1DCDAF * oracle_mod.splitmix64(1)) % 2**64
 
 
 # -------------------------------------------------------------------- c5/c6 periodicity
