@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -168,6 +169,7 @@ struct PowerRun {
     int n_words = 0;      // path order when A comes from the word masks
     std::vector<DBuf> ring;
     std::vector<int> slot_power;
+    std::tuple<size_t, int64_t, int, bool> ring_key{0, 0, 0, false}; // what the slot count was decided for
     size_t cached_slot = 0; // slot size the cached buffers were allocated for
     bool sparse = false;  // tile kernel with l-tile lists
     bool spmm = false;    // grouped SpMM kernel
@@ -508,8 +510,11 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     if (!R.has_at2) R.at2.release();
 
     tr.mark(R.spmm ? "kernel choice: spmm" : "kernel choice: tiles");
-    // power store: a ring of device slots (allocated on first use, kept across calls)
-    {
+    // power store: a ring of device slots (allocated on first use, kept across calls).  The
+    // slot count is decided once per (slot size, budget, max_k): cudaMemGetInfo can take
+    // milliseconds when the driver has deferred work, so it is not called on every run.
+    const std::tuple<size_t, int64_t, int, bool> ring_key{R.slot_bytes(), g_opts.budget, max_k, cap != nullptr};
+    if (R.ring.empty() || ring_key != R.ring_key) {
         size_t freeb = 0, totalb = 0;
         CUDA_TRY(cudaMemGetInfo(&freeb, &totalb));
         size_t cached = 0;
@@ -527,8 +532,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             return fail(MP_ERR_RESOURCE, "power store needs at least %lld slots of %zu bytes (budget %lld bytes)",
                         (long long)need, R.slot_bytes(), (long long)budget);
         R.ring.resize((size_t)slots);
-        R.slot_power.assign((size_t)slots, 0);
+        R.ring_key = ring_key;
     }
+    R.slot_power.assign(R.ring.size(), 0);
     tr.mark("power store");
     // per-power statistics: SUM fields {H, inf count} for k = 0..max_k, then MIN fields
     // {diag min, first finite entry}, so a batch of powers reduces with one call of each

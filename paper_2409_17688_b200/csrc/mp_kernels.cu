@@ -498,6 +498,16 @@ constexpr int kSpOffBytes = ((kSpGroups + 1) * 8 + 15) / 16 * 16;
 constexpr int kSpStageBytes = kSpChunk * kSpRowBytes + kSpEntryBytes + kSpOffBytes;
 constexpr int kSpSmemBytes = kSpStages * kSpStageBytes + 2 * kSpStages * 8;
 constexpr int kSpCtasPerSm = MP_SP_CTAS;
+#ifndef MP_SP_LDGSTS
+#define MP_SP_LDGSTS 0
+#endif
+#ifndef MP_SP_BALANCE
+#define MP_SP_BALANCE 0
+#endif
+#ifndef MP_SP_BAND
+#define MP_SP_BAND 1000000
+#endif
+constexpr int kSpBand = MP_SP_BAND; // column blocks per band of the CTA order
 static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
 // How the sparse-form builders read A: the kG duplicated values (device encoding) of the rows
@@ -562,6 +572,10 @@ constexpr int kRefThreads = 128;
 constexpr int kRefRows = 32; // pass 3 refines 32-row blocks of a tile into groups of kG
 constexpr int kRefGroups = kRefRows / kG;
 constexpr int kRefPairs = kRefGroups * (kRefGroups - 1) / 2;
+#ifndef MP_REF_BALANCE
+#define MP_REF_BALANCE 0
+#endif
+constexpr int kRefBalance = MP_REF_BALANCE; // weight of the largest group in the swap objective
 // pr-th pair (A < B) of groups in lexicographic order
 __device__ __forceinline__ void ref_pair(int pr, int &A, int &B)
 {
@@ -781,7 +795,7 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
     __shared__ int8_t member[kRefRows]; // member[s] = R0 row currently in slot s
     if (tid < kRefRows) member[tid] = (int8_t)tid;
     __syncthreads();
-    for (int it = 0; it < 64; ++it) {
+    for (int it = 0; it < 160; ++it) {
         // Um[s] = OR of the other 7 rows of slot s's group; group costs
         for (int q = tid; q < kRefRows * uw; q += blockDim.x) {
             const int sl = q / uw, k = q - sl * uw, g0 = (sl / kG) * kG;
@@ -800,6 +814,8 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
             atomicAdd(&gcost[g], __popc(Um[sl * uw + k] | R0[member[sl] * uw + k]));
         }
         __syncthreads();
+        int gmax = 0;
+        for (int g = 0; g < kRefGroups; ++g) gmax = max(gmax, gcost[g]);
         // every swap (slot a in group A < group B of slot b)
         for (int q = tid; q < kRefPairs * kG * kG; q += blockDim.x) {
             const int pr = q / (kG * kG), ab = q - pr * (kG * kG);
@@ -808,9 +824,18 @@ __global__ void __launch_bounds__(kRefThreads) k_tile_refine(const int64_t *__re
             const int sa = A * kG + ab / kG, sb = B * kG + ab % kG;
             const uint32_t *ra = R0 + member[sa] * uw, *rb = R0 + member[sb] * uw;
             const uint32_t *ua = Um + sa * uw, *ub = Um + sb * uw;
-            int c = 0;
-            for (int k = 0; k < uw; ++k) c += __popc(ua[k] | rb[k]) + __popc(ub[k] | ra[k]);
-            const int d = c - gcost[A] - gcost[B];
+            int na = 0, nb = 0;
+            for (int k = 0; k < uw; ++k) {
+                na += __popc(ua[k] | rb[k]);
+                nb += __popc(ub[k] | ra[k]);
+            }
+            // objective: sum of the group unions + kRefBalance * groups * their maximum (the
+            // consumer warp of the largest group bounds the tile's time in k_spmm)
+            int mo = 0; // max over the other groups
+            for (int g = 0; g < kRefGroups; ++g)
+                if (g != A && g != B) mo = max(mo, gcost[g]);
+            const int d = (na + nb - gcost[A] - gcost[B]) +
+                          kRefBalance * kRefGroups * (max(mo, max(na, nb)) - gmax);
             if (d < 0)
                 atomicMin(&best, ((unsigned long long)(uint32_t)(d + (1 << 30)) << 32) | (uint32_t)q);
         }
@@ -905,6 +930,78 @@ __global__ void k_tile_union(const uint8_t *__restrict__ m8, int64_t Np, const i
     }
     int32_t *Lt = L + tptr[t];
     block_compact(Np, flag, [&](int64_t l, int64_t rank) { Lt[rank] = (int32_t)l; });
+}
+
+// Reorders each tile's union list L_t so that every chunk of kSpChunk l's carries about the
+// same number of entries for each of the tile's groups (any order of U_t gives the same
+// product; the SpMM's consumer warps then wait less on each other within the ring).  Per l
+// the mask of the groups with an entry at l; greedily, the next l comes from the mask class
+// that does not raise the chunk's largest per-group count (a class avoiding every group at
+// the maximum), with the most groups, ties to the higher class; l ascending within a class.
+// One thread per tile.
+__global__ void k_tile_balance(const uint8_t *__restrict__ m8, int64_t Np, const int64_t *__restrict__ tptr,
+                               int64_t Mt, int32_t *__restrict__ L, int32_t *__restrict__ tmp)
+{
+    constexpr int NC = 1 << kSpGroups;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= Mt) return;
+    int32_t *Lt = L + tptr[t], *Tt = tmp + tptr[t];
+    const int u = (int)(tptr[t + 1] - tptr[t]);
+    const uint8_t *m = m8 + t * kSpGroups * Np;
+    auto mask = [&](int32_t l) {
+        unsigned k = 0;
+#pragma unroll
+        for (int j = 0; j < kSpGroups; ++j) k |= (m[j * Np + l] != 0) ? (1u << j) : 0u;
+        return k;
+    };
+    int head[NC], end[NC];
+    for (int c = 0; c < NC; ++c) head[c] = 0;
+    for (int i = 0; i < u; ++i) ++head[mask(Lt[i])];
+    int acc = 0;
+    for (int c = 0; c < NC; ++c) {
+        const int n = head[c];
+        head[c] = acc;
+        acc += n;
+        end[c] = acc;
+    }
+    for (int i = 0; i < u; ++i) {
+        const int32_t l = Lt[i];
+        const unsigned c = mask(l);
+        Tt[--end[c] + 0] = l; // filled from the back: restored below
+    }
+    // Tt[head[c] .. ) now holds class c in descending l; reverse each class to ascending
+    for (int c = 0; c < NC; ++c) {
+        int a = head[c], z = (c + 1 < NC ? head[c + 1] : u) - 1;
+        end[c] = z + 1;
+        while (a < z) {
+            const int32_t x = Tt[a];
+            Tt[a++] = Tt[z];
+            Tt[z--] = x;
+        }
+    }
+    int g[kSpGroups];
+    for (int j = 0; j < kSpGroups; ++j) g[j] = 0;
+    for (int i = 0, k = 0; i < u; ++i, ++k) {
+        if (k == kSpChunk) {
+            k = 0;
+            for (int j = 0; j < kSpGroups; ++j) g[j] = 0;
+        }
+        int gm = 0;
+        for (int j = 0; j < kSpGroups; ++j) gm = max(gm, g[j]);
+        unsigned am = 0;
+        for (int j = 0; j < kSpGroups; ++j) am |= (g[j] == gm) ? (1u << j) : 0u;
+        int best = -1, bkey = -1;
+        for (int c = NC - 1; c >= 1; --c) {
+            if (head[c] >= end[c]) continue;
+            const int key = ((c & am) == 0 ? 64 : 0) + __popc(c);
+            if (key > bkey) {
+                bkey = key;
+                best = c;
+            }
+        }
+        Lt[i] = Tt[head[best]++];
+        for (int j = 0; j < kSpGroups; ++j) g[j] += (best >> j) & 1;
+    }
 }
 
 // nch[t] = ceil(tcnt[t] / kSpChunk)
@@ -1061,7 +1158,18 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
     constexpr int EB = kSpEntryBytes;           // up to 64 entries + 3 look-ahead records
     constexpr int STAGE = kSpStageBytes;
     static_assert(STAGE % 16 == 0 && XB % 16 == 0 && EB % 16 == 0, "stage layout");
-    const int t = blockIdx.y, bx = blockIdx.x;
+    // CTA order: bands of kSpBand column blocks, row tiles fastest within a band, so the CTAs
+    // resident at once read X rows of few column blocks (L2 reuse of the staged X rows).
+    int t, bx;
+    {
+        const int nbx = (int)gridDim.y, Mt = (int)gridDim.x;
+        const int64_t L = (int64_t)blockIdx.y * Mt + blockIdx.x;
+        const int band = (int)(L / ((int64_t)Mt * kSpBand));
+        const int64_t r = L - (int64_t)band * Mt * kSpBand;
+        const int bw = min(kSpBand, nbx - band * kSpBand);
+        t = (int)(r / bw);
+        bx = band * kSpBand + (int)(r % bw);
+    }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t tp0 = tptr[t];
     const int U = (int)(tptr[t + 1] - tp0);
@@ -1077,7 +1185,7 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
         reinterpret_cast<uint4 *>(smem + (q / (EB / 16)) * STAGE + XB)[q % (EB / 16)] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         for (int st = 0; st < kSpStages; ++st) {
-            mbar_init(bar_full + st * 8, 1);
+            mbar_init(bar_full + st * 8, MP_SP_LDGSTS ? 32 : 1);
             mbar_init(bar_empty + st * 8, kSpConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1109,12 +1217,26 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
             const int nrows = min(kSpChunk, U - c * kSpChunk);
             const uint32_t ebytes = (uint32_t)(e1 - e0) * kEntBytes;
             const uint32_t sX = sbase + st * STAGE;
+#if MP_SP_LDGSTS
+            // 16-byte cp.async by all 32 lanes; each lane's completion arrives on "full"
+            // (initialised with 32 arrivals) through cp.async.mbarrier.arrive.noinc
+            for (int r = 0; r < nrows; ++r) {
+                const int32_t lr = __shfl_sync(0xFFFFFFFFu, l, r);
+                const uint16_t *src = X + (int64_t)lr * ldx + col0;
+                cp_async16(sX + r * kSpRowBytes + lane * 16, src + lane * 8);
+                cp_async16(sX + r * kSpRowBytes + 512 + lane * 16, src + 256 + lane * 8);
+            }
+            for (uint32_t q = lane; q < ebytes / 16; q += 32) cp_async16(sX + XB + q * 16, E + kEntU4 * e0 + q);
+            if (lane < kSpOffBytes / 16) cp_async16(sX + XB + EB + lane * 16, eoff + gc * kSpGroups + 2 * lane);
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_full + st * 8) : "memory");
+#else
             if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + kSpOffBytes);
             __syncwarp();
             if (lane < nrows)
                 bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
             if (lane == 0 && ebytes) bulk_g2s(sX + XB, E + kEntU4 * e0, ebytes, bar_full + st * 8);
             if (lane == 1) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, kSpOffBytes, bar_full + st * 8);
+#endif
         }
         return;
     }
@@ -1300,7 +1422,7 @@ cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint1
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)(ncols_p / kSpCols), (unsigned)(Mp / kSpRows));
+    dim3 grid((unsigned)(Mp / kSpRows), (unsigned)(ncols_p / kSpCols)); // x: tiles, y: column blocks (remapped)
     k_spmm<<<grid, kSpThreads, kSpSmemBytes, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
     return cudaGetLastError();
 }
@@ -1395,6 +1517,13 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     SP_ALLOC(w.ecnt, (size_t)TC * kSpGroups * 4);
     SP_ALLOC(w.eoff, (size_t)(TC * kSpGroups + kSpOffBytes / 8) * 8); // k_spmm copies kSpOffBytes per chunk
     SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, w.tptr, nullptr, w.L)));
+#if MP_SP_BALANCE
+    {
+        int32_t *tmpL = nullptr;
+        SP_ALLOC(tmpL, (size_t)std::max<int64_t>(tot[0], 1) * 4);
+        SP_LAUNCH((k_tile_balance<<<(unsigned)((Mt + 63) / 64), 64, 0, s>>>(w.m8, Np, w.tptr, Mt, w.L, tmpL)));
+    }
+#endif
     SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], w.ecnt, nullptr, nullptr)));
