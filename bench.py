@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-symmetry", action="store_true",
+                    help="do not pass the word-reversal symmetry of A(D_n) (compute every column)")
     return ap.parse_args()
 
 
@@ -213,6 +215,9 @@ def run_mine(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         mp.dist_set_torch()
     mp.set_options(args.kernel)
+    # A(D_n) is invariant under reversing every word (the path's reflection): the library
+    # then computes only the columns g <= sigma(g) and verifies the hint on the device
+    mp.set_symmetry(None if args.no_symmetry else mp.word_reversal(args.n))
     stream = torch.cuda.current_stream()
     mp.set_stream(stream)
 
@@ -317,7 +322,8 @@ def run_mine(args):
         "data": "synthetic: deterministic transfer matrix A(D_n) built on the host (no randomness, no datasets)",
         "config": dict(workload_config(args.n, N, world), products_per_step=products,
                        mu_lambda_b=[res.mu, res.lam, res.offset], gamma2_m1000=res.gamma2(1000),
-                       kernel=args.kernel),
+                       kernel=args.kernel,
+                       symmetry="none" if args.no_symmetry else "word reversal (columns g <= sigma g computed)"),
         "seconds_to_gamma2": ms / args.steps / 1e3,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used], "achieved": achieved, "peak": peak,

@@ -269,6 +269,24 @@ mp_status mp_set_stream(void *stream);
  * the power store (0 = min(48 GiB, 90 % of free device memory)).  Errors: MP_ERR_DOMAIN. */
 mp_status mp_set_options(int sparsity, int64_t device_budget_bytes);
 
+/* Symmetry of A (not in the paper): an involution sigma of [0, N) with
+ * A[sigma i][sigma j] = A[i][j] for all i, j.  Every power then has the same symmetry and
+ * column j of A^k depends only on column j of A^{k-1}, so the power runs compute only the
+ * columns g <= sigma(g) (about half) and derive every statistic of the full matrix from them;
+ * all outputs are those of the full computation.
+ *   mp_set_symmetry: hint for the matrix sources of size N (host array of N int32, copied;
+ *     NULL or N <= 0 clears it).  Each run verifies it on the device and fails with
+ *     MP_ERR_DOMAIN if some finite A_ij != A_(sigma i, sigma j).  Errors: MP_ERR_DOMAIN (not
+ *     an involution).
+ *   mp_set_word_symmetry: the words source (gamma2_cylinder, mp_gamma2_record) uses the word
+ *     reversal (the reflection of the path P_n, which the can-follow rule P:141-147 and the
+ *     labels P:152 respect) unless switched off (on = 0); default on.
+ *   mp_word_reversal: sigma_out[i] = index of the reversed word i in A(D_n) (N = its order,
+ *     caller-owned buffer).  Errors: MP_ERR_DOMAIN (n outside [2, MP_MAX_N], N mismatch). */
+mp_status mp_set_symmetry(const int32_t *sigma, int64_t N);
+mp_status mp_set_word_symmetry(int on);
+mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N);
+
 /* Row grouping of the SpMM kernel (sparsity 2): 0 = groups of 8 consecutive rows; 1 = rows
  * grouped greedily by support overlap in windows of 512 rows (fewer issued steps, same
  * product); -1 = automatic (the default: greedy from N >= 8192).

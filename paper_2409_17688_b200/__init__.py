@@ -9,5 +9,6 @@ from ._native import (  # noqa: F401
     build_transition_matrix, count_words, dist_set, dist_set_torch, fingerprint_unit,
     gamma2_cylinder, gamma2_record, kernel_launches, last_error, last_profile, minplus_mul, minplus_mul_device,
     minplus_power_rows, minplus_power_until_periodic, minplus_power_until_periodic_device,
-    repeat_candidate, set_grouping, set_options, set_stream, shard_range, shutdown, version,
+    repeat_candidate, set_grouping, set_options, set_stream, set_symmetry, set_word_symmetry,
+    word_reversal, shard_range, shutdown, version,
 )

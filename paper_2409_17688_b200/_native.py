@@ -31,6 +31,7 @@ EXPORTS = [
     "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
     "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_gamma2_formula", "mp_gamma2_record",
+    "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal",
 ]
 
 
@@ -101,6 +102,9 @@ def _load() -> ctypes.CDLL:
         "mp_last_profile": ([P], i32),
         "mp_set_options": ([i32, i64], i32),
         "mp_set_grouping": ([i32], i32),
+        "mp_set_symmetry": ([ctypes.c_void_p, i64], i32),
+        "mp_set_word_symmetry": ([i32], i32),
+        "mp_word_reversal": ([i32, ctypes.c_void_p, i64], i32),
         "mp_gamma2_formula": ([P, P], i32),
         "mp_gamma2_record": ([i32, P], i32),
     }
@@ -340,6 +344,29 @@ SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}
 def set_options(sparsity: str = "auto", device_budget_bytes: int = 0) -> None:
     """Product kernel of the power runs: "auto" | "dense" | "tiles" | "spmm" (all exact)."""
     _check(lib.mp_set_options(SPARSITY[sparsity], device_budget_bytes))
+
+
+def set_symmetry(sigma=None) -> None:
+    """Symmetry hint for the matrix sources: an involution sigma with A[sigma i][sigma j] =
+    A[i][j] (verified on the device by every run); None clears it."""
+    if sigma is None:
+        _check(lib.mp_set_symmetry(None, 0))
+        return
+    sg = np.ascontiguousarray(sigma, dtype=np.int32)
+    _check(lib.mp_set_symmetry(sg.ctypes.data, sg.shape[0]))
+
+
+def set_word_symmetry(on: bool = True) -> None:
+    """Whether gamma2_cylinder / gamma2_record use the word reversal of A(D_n)."""
+    _check(lib.mp_set_word_symmetry(1 if on else 0))
+
+
+def word_reversal(n: int) -> np.ndarray:
+    """sigma[i] = index of the reversed word i in A(D_n) (int32)."""
+    N = count_words(n)
+    out = np.empty(N, dtype=np.int32)
+    _check(lib.mp_word_reversal(n, out.ctypes.data, N))
+    return out
 
 
 GROUPING = {"auto": -1, "consecutive": 0, "greedy": 1}

@@ -49,6 +49,11 @@ struct Opts {
 } g_opts;
 constexpr int64_t kGroupMinN = 8192; // below this the grouping pass costs more than it saves
 
+// Symmetry hint for matrix sources (mp_set_symmetry) and the word-reversal switch for the
+// words source.
+std::vector<int32_t> g_sym;
+bool g_word_sym = true;
+
 mp_profile g_prof{};
 std::map<std::tuple<int, int, int>, mp_periodic_result> g_cache; // (n, world, rank)
 
@@ -164,6 +169,12 @@ struct PowerRun {
     int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
     DBuf at2, words, tmp0, tmp1, ktp, kti, occ, stats, flag, stage_raw;
     bool has_at2 = false; // only the tile kernels stage AT2; SpMM reads A or the word masks
+    // symmetry: local column jj holds global column gcol[jj] (g <= sigma g) and stands for g and
+    // sigma g; cols_rep = number of global columns the local ones stand for
+    bool sym = false;
+    std::vector<int32_t> sigma, gcol, loc; // loc[g] = local column of domain column g (cap path)
+    DBuf dsig, dgcol;
+    int64_t cols_rep = 0;
     const uint16_t *a_src = nullptr; // matrix sources: A (boundary encoding; the caller's buffer or
     int64_t a_ld = 0;                // stage_raw), valid for the duration of the run
     int n_words = 0;      // path order when A comes from the word masks
@@ -354,12 +365,20 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
 // X_1 = A[:, c0:c0+w) in the device layout, from A, AT2 or straight from the word masks.
 mp_status make_power1(PowerRun &R, uint16_t *dst, cudaStream_t s)
 {
+    if (R.sym) {
+        if (R.a_src)
+            LAUNCH(launch_encode_cols(R.a_src, R.a_ld, R.N, R.dgcol.as<int32_t>(), R.w, dst, R.ld, R.Np, s));
+        else
+            LAUNCH(launch_x1_from_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, 0, R.dgcol.as<int32_t>(), R.w,
+                                        dst, R.ld, s));
+        return MP_OK;
+    }
     if (R.a_src) // range-checked already: the flag is scratch
         LAUNCH(launch_encode(R.a_src + R.c0, R.a_ld, R.N, R.w, dst, R.ld, R.Np, R.flag.as<int>(), s));
     else if (R.has_at2)
         LAUNCH(launch_x1_from_at2(R.at2.as<uint32_t>(), R.Np, R.c0, R.w, dst, R.ld, s));
     else
-        LAUNCH(launch_x1_from_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, R.c0, R.w, dst, R.ld, s));
+        LAUNCH(launch_x1_from_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, R.c0, nullptr, R.w, dst, R.ld, s));
     return MP_OK;
 }
 
@@ -419,15 +438,47 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     PowerRun &R = *st->pr;
     R.N = N;
     R.Np = pad_rows(N);
-    {
+    const bool words_src = !src.dev && !src.host;
+    // Columns this run computes: a shard of [0, N), or under a symmetry sigma (DESIGN.md
+    // "Symmetry") a shard of the domain D = {g : g <= sigma g} -- every power satisfies
+    // X_(sigma i, sigma j) = X_ij, and column j of A^k depends only on column j of A^{k-1}.
+    R.sigma.clear();
+    if (words_src && g_word_sym) R.sigma = word_reversal(src.n);
+    else if (!words_src && (int64_t)g_sym.size() == N) R.sigma = g_sym;
+    R.sym = !R.sigma.empty();
+    if (R.sym) {
+        for (int64_t i = 0; i < N; ++i)
+            if (R.sigma[i] < 0 || R.sigma[i] >= N || R.sigma[R.sigma[i]] != i)
+                return fail(MP_ERR_DOMAIN, "symmetry: sigma is not an involution of [0, %lld)", (long long)N);
+        std::vector<int32_t> dom;
+        for (int64_t g = 0; g < N; ++g)
+            if (g <= R.sigma[g]) dom.push_back((int32_t)g);
+        int64_t c0 = 0, c1 = (int64_t)dom.size();
+        if (!cap) mp_shard_range((int64_t)dom.size(), g_dist.world, g_dist.rank, &c0, &c1);
+        R.gcol.assign(dom.begin() + c0, dom.begin() + c1);
+        R.c0 = 0;
+        R.w = c1 - c0;
+        R.cols_rep = 0;
+        R.loc.assign((size_t)N, -1);
+        for (size_t jj = 0; jj < R.gcol.size(); ++jj) {
+            R.cols_rep += (R.sigma[R.gcol[jj]] != R.gcol[jj]) ? 2 : 1;
+            R.loc[(size_t)R.gcol[jj]] = (int32_t)jj;
+        }
+        TRY(R.dsig.ensure((size_t)N * 4, "symmetry"));
+        TRY(R.dgcol.ensure(std::max<size_t>(R.gcol.size(), 1) * 4, "column list"));
+        COPY(R.dsig.p, R.sigma.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s);
+        if (!R.gcol.empty())
+            COPY(R.dgcol.p, R.gcol.data(), R.gcol.size() * 4, cudaMemcpyHostToDevice, s);
+    } else {
         int64_t c0, c1;
         mp_shard_range(N, g_dist.world, g_dist.rank, &c0, &c1);
         R.c0 = c0;
         R.w = c1 - c0;
-    }
-    if (cap) { // single device, whole matrix
-        R.c0 = 0;
-        R.w = N;
+        if (cap) { // single device, whole matrix
+            R.c0 = 0;
+            R.w = N;
+        }
+        R.cols_rep = R.w;
     }
     R.ld = pad_cols(R.w);
     if (R.slot_bytes() != R.cached_slot) {
@@ -441,7 +492,6 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // buffer first) and read directly by the SpMM sparse-form builder and by X_1; only the tile
     // kernels need AT2 (transposed, duplicated, device encoding), built once they are chosen.
     // The words source with SpMM needs no matrix at all (69 GB saved at n = 13).
-    const bool words_src = !src.dev && !src.host;
     R.n_words = words_src ? src.n : 0;
     R.a_src = nullptr;
     R.a_ld = 0;
@@ -465,12 +515,14 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
             CUDA_TRY(cudaMemsetAsync(R.occ.p, 0, (size_t)(Mt * Kt), s));
         }
-        CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, sizeof(int), s));
-        LAUNCH(launch_check_a(R.a_src, R.a_ld, N, R.Np, need_occ ? R.occ.as<uint8_t>() : nullptr, R.flag.as<int>(), s));
-        int hflag = 0;
-        COPY(&hflag, R.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, 2 * sizeof(int), s));
+        LAUNCH(launch_check_a(R.a_src, R.a_ld, N, R.Np, need_occ ? R.occ.as<uint8_t>() : nullptr, R.flag.as<int>(),
+                              R.sym ? R.dsig.as<int32_t>() : nullptr, R.flag.as<int>() + 1, s));
+        int hflag[2] = {0, 0};
+        COPY(hflag, R.flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));
-        if (hflag) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
+        if (hflag[0]) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
+        if (hflag[1]) return fail(MP_ERR_DOMAIN, "symmetry hint: A[sigma i][sigma j] != A[i][j] for some i, j");
     }
     tr.mark("a2 stage A");
 
@@ -594,8 +646,13 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 ++launches;
             }
             if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s)); // stats start
-            LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
-                                reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
+            if (R.sym)
+                LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.w,
+                                        reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
+                                        reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
+            else
+                LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
+                                    reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
             if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[3 * (max_k + 1) + k], s)); // stats end
             prev = dst;
         }
@@ -627,12 +684,28 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
 
             if (cap) {
                 DBuf rowbuf;
-                TRY(rowbuf.alloc((size_t)N * 2, "captured row"));
+                TRY(rowbuf.alloc((size_t)N * 4, "captured row"));
+                std::vector<uint16_t> h2((size_t)R.w * 2);
                 for (int r = 0; r < cap->nrows; ++r) {
-                    LAUNCH(launch_decode(cur + cap->rows[r] * R.ld, R.ld, 1, N, rowbuf.as<uint16_t>(), N, s));
-                    CUDA_TRY(cudaMemcpyAsync(cap->out + ((size_t)(k - 1) * cap->nrows + r) * N, rowbuf.p,
-                                             (size_t)N * 2, cudaMemcpyDeviceToHost, s));
+                    uint16_t *o = cap->out + ((size_t)(k - 1) * cap->nrows + r) * N;
+                    const int64_t row = cap->rows[r];
+                    if (!R.sym) {
+                        LAUNCH(launch_decode(cur + row * R.ld, R.ld, 1, N, rowbuf.as<uint16_t>(), N, s));
+                        CUDA_TRY(cudaMemcpyAsync(o, rowbuf.p, (size_t)N * 2, cudaMemcpyDeviceToHost, s));
+                        CUDA_TRY(cudaStreamSynchronize(s));
+                        continue;
+                    }
+                    // full row r from the domain columns: X_rj = X_(r, j) if j <= sigma j,
+                    // else X_(sigma r, sigma j)
+                    uint16_t *rb = rowbuf.as<uint16_t>();
+                    LAUNCH(launch_decode(cur + row * R.ld, R.ld, 1, R.w, rb, R.w, s));
+                    LAUNCH(launch_decode(cur + (int64_t)R.sigma[row] * R.ld, R.ld, 1, R.w, rb + R.w, R.w, s));
+                    CUDA_TRY(cudaMemcpyAsync(h2.data(), rb, (size_t)R.w * 4, cudaMemcpyDeviceToHost, s));
                     CUDA_TRY(cudaStreamSynchronize(s));
+                    for (int64_t j = 0; j < N; ++j) {
+                        const int32_t sj = R.sigma[j];
+                        o[j] = j <= sj ? h2[(size_t)R.loc[j]] : h2[(size_t)(R.w + R.loc[sj])];
+                    }
                 }
                 if (k == max_k) found = true;
                 continue;
@@ -679,7 +752,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.product_ms = prod_ms;
     g_prof.stats_ms = stats_ms;
     g_prof.product_launches = launches;
-    g_prof.dense_steps = (double)useful * (double)N * (double)N * (double)R.w;
+    g_prof.dense_steps = (double)useful * (double)N * (double)N * (double)R.cols_rep;
     g_prof.issued_steps = (double)launches * R.issued_per_product;
     g_prof.total_ms = all_ms;
     {
@@ -1012,6 +1085,38 @@ mp_status mp_set_options(int sparsity, int64_t device_budget_bytes)
     if (sparsity < -1 || sparsity > 2) return fail(MP_ERR_DOMAIN, "mp_set_options: sparsity %d outside [-1, 2]", sparsity);
     g_opts.sparsity = sparsity;
     g_opts.budget = device_budget_bytes;
+    return MP_OK;
+}
+
+mp_status mp_set_symmetry(const int32_t *sigma, int64_t N)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!sigma || N <= 0) {
+        g_sym.clear();
+        return MP_OK;
+    }
+    for (int64_t i = 0; i < N; ++i)
+        if (sigma[i] < 0 || sigma[i] >= N || sigma[sigma[i]] != i)
+            return fail(MP_ERR_DOMAIN, "mp_set_symmetry: sigma is not an involution of [0, %lld)", (long long)N);
+    g_sym.assign(sigma, sigma + N);
+    return MP_OK;
+}
+
+mp_status mp_set_word_symmetry(int on)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_word_sym = on != 0;
+    g_cache.clear(); // records were computed either way; keep the switch observable
+    return MP_OK;
+}
+
+mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N)
+{
+    if (n < 2 || n > MP_MAX_N || !sigma_out) return fail(MP_ERR_DOMAIN, "mp_word_reversal: n = %d outside [2, 13]", n);
+    const std::vector<int32_t> sg = word_reversal(n);
+    if ((int64_t)sg.size() != N)
+        return fail(MP_ERR_DOMAIN, "mp_word_reversal: N = %lld, A(D_%d) has %zu words", (long long)N, n, sg.size());
+    std::memcpy(sigma_out, sg.data(), sg.size() * 4);
     return MP_OK;
 }
 

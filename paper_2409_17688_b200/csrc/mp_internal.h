@@ -69,6 +69,9 @@ MP_HD bool can_follow_mask(const WordMask &q, const WordMask &p, unsigned full)
 std::vector<WordMask> enumerate_words(int n);
 int64_t count_words(int n);
 
+// sigma[i] = index of the reversed word i (the path's reflection; an involution).
+std::vector<int32_t> word_reversal(int n);
+
 // Fills A (N x N, boundary encoding) from the word list with `threads` host threads.
 void fill_transition_matrix(const std::vector<WordMask> &w, int n, uint16_t *A, int threads);
 

@@ -1366,6 +1366,131 @@ cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, i
     return cudaGetLastError();
 }
 
+// Statistics of a power stored on a column list under a symmetry sigma (an involution with
+// A_(sigma i, sigma j) = A_ij, so every power has X_(sigma i, sigma j) = X_ij): local column jj
+// holds global column g = gcol[jj] (g <= sigma g) and stands for g and its mirror sigma g.
+// The fields are those of k_stats for the FULL matrix: entry (i, jj) contributes
+// s(2i) s(2g+1) x + [sigma g != g] s(2 sigma i) s(2 sigma g + 1) x to H, one or two +inf
+// counts, the keys of (i, g) and (sigma i, sigma g), and the diagonal (g, g) (every diagonal
+// entry (r, r) of the full matrix equals (sigma r, sigma r), which some local column holds).
+__global__ void __launch_bounds__(256)
+    k_stats_sym(const uint16_t *__restrict__ X, int64_t ld, int64_t N, const int32_t *__restrict__ gcol,
+                const int32_t *__restrict__ sigma, int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum,
+                unsigned long long *__restrict__ out_min)
+{
+    unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
+    unsigned dmin = 0xFFFFu;
+    const int64_t j0 = (int64_t)blockIdx.x * kStCols + (int64_t)threadIdx.x * 8;
+    const int64_t i0 = (int64_t)blockIdx.y * rpb, i1 = min(N, i0 + rpb);
+    if (j0 < w) {
+        const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
+        uint64_t b[8], bm[8];
+        int64_t g[8], m[8];
+        unsigned two = 0; // bit e: column e stands for two global columns
+        int64_t mmin = INT64_MAX;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            g[e] = e < nc ? gcol[j0 + e] : 0;
+            m[e] = e < nc ? sigma[g[e]] : 0;
+            b[e] = e < nc ? mix64(2 * (uint64_t)g[e] + 1) : 0;
+            bm[e] = (e < nc && m[e] != g[e]) ? mix64(2 * (uint64_t)m[e] + 1) : 0;
+            if (e < nc && m[e] != g[e]) two |= 1u << e;
+            if (e < nc) mmin = min(mmin, m[e]);
+        }
+        for (int64_t i = i0; i < i1; ++i) {
+            const int64_t si = sigma[i];
+            const uint4 v = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
+            const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+            const uint32_t anyinf = __vcmpeq2(v.x, 0x7FFF7FFFu) | __vcmpeq2(v.y, 0x7FFF7FFFu) |
+                                    __vcmpeq2(v.z, 0x7FFF7FFFu) | __vcmpeq2(v.w, 0x7FFF7FFFu);
+            uint64_t rs = 0, rm = 0;
+            if (nc == 8 && !anyinf) {
+                // the smallest key among (i, g_e) is e = 0 (gcol ascending); among the mirrors
+                // (sigma i, m_e) the smallest m_e
+                unsigned long long key = ((uint64_t)(i * N + g[0]) << 16) | (v.x & 0xFFFFu);
+                if (key < ref) ref = key;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                    rs += b[e] * x;
+                    rm += bm[e] * x;
+                    if (m[e] == mmin) {
+                        key = ((uint64_t)(si * N + m[e]) << 16) | x;
+                        if (key < ref) ref = key;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if (e >= nc) break;
+                    uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                    if (x == kDevInf) {
+                        x = kBndInf;
+                        infc += 1 + ((two >> e) & 1u);
+                    } else {
+                        unsigned long long key = ((uint64_t)(i * N + g[e]) << 16) | x;
+                        if (key < ref) ref = key;
+                        key = ((uint64_t)(si * N + m[e]) << 16) | x;
+                        if (key < ref) ref = key;
+                    }
+                    rs += b[e] * x;
+                    rm += bm[e] * x;
+                }
+            }
+            h += mix64(2 * (uint64_t)i) * rs + mix64(2 * (uint64_t)si) * rm;
+            if (i >= g[0] && i <= g[nc - 1]) { // the diagonal entry (i, i), if this slice holds it
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (e < nc && g[e] == i) {
+                        const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                        dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
+                    }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+        infc += __shfl_xor_sync(0xFFFFFFFFu, infc, o);
+        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
+        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, o));
+    }
+    __shared__ unsigned long long sh[8], si_[8], sr[8];
+    __shared__ unsigned sd[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sh[warp] = h;
+        si_[warp] = infc;
+        sd[warp] = dmin;
+        sr[warp] = ref;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long H = 0, I = 0, R = 0x7FFFFFFFFFFFFFFFull;
+        unsigned D = 0xFFFFu;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            H += sh[k];
+            I += si_[k];
+            D = min(D, sd[k]);
+            R = min(R, sr[k]);
+        }
+        atomicAdd(out_sum + 0, H);
+        atomicAdd(out_sum + 1, I);
+        atomicMin(out_min + 0, (unsigned long long)D);
+        atomicMin(out_min + 1, R);
+    }
+}
+
+cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
+                             int64_t w, unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s)
+{
+    const int64_t gx = std::max<int64_t>(1, (w + kStCols - 1) / kStCols);
+    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t)num_sms() * 8 / gx));
+    const int64_t rpb = (N + gy - 1) / gy;
+    k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(X, ld, N, gcol, sigma, w, rpb, out_sum, out_min);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int64_t N, int64_t w, int32_t c,
                            unsigned long long *out, cudaStream_t s)
 {
@@ -1558,34 +1683,61 @@ cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int
 
 // X1[i][j] = A_(i, c0+j) from the word masks, +inf padding (rows >= N, columns >= w).
 __global__ void k_x1_from_words(const WordMask *__restrict__ words, int64_t N, unsigned full, int64_t Np,
-                                int64_t c0, int64_t w, uint16_t *__restrict__ X1, int64_t ldx)
+                                int64_t c0, const int32_t *__restrict__ gcol, int64_t w, uint16_t *__restrict__ X1,
+                                int64_t ldx)
 {
     const int64_t total = Np * ldx;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / ldx, j = t - i * ldx;
         uint16_t v = kDevInf;
         if (i < N && j < w) {
-            const WordMask p = words[c0 + j];
+            const WordMask p = words[gcol ? (int64_t)gcol[j] : c0 + j];
             if (can_follow_mask(words[i], p, full)) v = p.zeros;
         }
         X1[t] = v;
     }
 }
 
-cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, int64_t w,
-                                 uint16_t *X1, int64_t ldx, cudaStream_t s)
+cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, const int32_t *gcol,
+                                 int64_t w, uint16_t *X1, int64_t ldx, cudaStream_t s)
 {
-    k_x1_from_words<<<grid_for(Np * ldx, 256), 256, 0, s>>>(words, N, (1u << n) - 1u, Np, c0, w, X1, ldx);
+    k_x1_from_words<<<grid_for(Np * ldx, 256), 256, 0, s>>>(words, N, (1u << n) - 1u, Np, c0, gcol, w, X1, ldx);
+    return cudaGetLastError();
+}
+
+// dst (rows_p x ldd) = enc(src[:rows, gcol[0..w)]), +inf padding: X_1 on a column list.
+__global__ void k_encode_cols(const uint16_t *__restrict__ src, int64_t lds, int64_t rows,
+                              const int32_t *__restrict__ gcol, int64_t w, uint16_t *__restrict__ dst, int64_t ldd,
+                              int64_t rows_p)
+{
+    for (int64_t i = blockIdx.x; i < rows_p; i += gridDim.x) {
+        uint16_t *d = dst + i * ldd;
+        for (int64_t j = threadIdx.x; j < ldd; j += blockDim.x) {
+            uint16_t v = kDevInf;
+            if (i < rows && j < w) {
+                const uint16_t x = src[i * lds + gcol[j]];
+                v = (x == kBndInf || x > kFiniteMax) ? kDevInf : x;
+            }
+            d[j] = v;
+        }
+    }
+}
+
+cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, const int32_t *gcol, int64_t w,
+                               uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s)
+{
+    k_encode_cols<<<(unsigned)std::min<int64_t>(std::max<int64_t>(rows_p, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
+        src, lds, rows, gcol, w, dst, ldd, rows_p);
     return cudaGetLastError();
 }
 
 // Range check of A (row-major, boundary encoding) and, if occ != null, the occupancy of its
 // 128 x 32 tiles (occ zeroed by the caller): one warp per (row, 32-column tile).
 __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N, int64_t Kt, uint8_t *__restrict__ occ,
-                          int *__restrict__ range_flag)
+                          int *__restrict__ range_flag, const int32_t *__restrict__ sigma, int *__restrict__ sym_flag)
 {
     const int lane = threadIdx.x & 31;
-    bool bad = false;
+    bool bad = false, asym = false;
     for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
         const uint16_t *row = A + i * lda;
         for (int64_t j0 = 0; j0 < Kt * 16; j0 += blockDim.x) { // column pairs; a warp = 2 tiles
@@ -1595,11 +1747,15 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
                 const uint16_t x = row[c];
                 f = x != kBndInf;
                 bad |= f && x > kFiniteMax;
+                // symmetry hint: every finite entry must reappear at (sigma i, sigma j); sigma x
+                // sigma is a bijection, so the +inf entries then map onto +inf entries too
+                if (sigma && f) asym |= A[(int64_t)sigma[i] * lda + sigma[c]] != x;
             }
             if (c + 1 < N) {
                 const uint16_t x = row[c + 1];
                 f |= x != kBndInf;
                 bad |= x != kBndInf && x > kFiniteMax;
+                if (sigma && x != kBndInf) asym |= A[(int64_t)sigma[i] * lda + sigma[c + 1]] != x;
             }
             const uint32_t b = __ballot_sync(0xFFFFFFFFu, f);
             if (occ && lane == 0) {
@@ -1611,14 +1767,15 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
         }
     }
     if (bad) *range_flag = 1;
+    if (asym) *sym_flag = 1;
 }
 
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
-                           cudaStream_t s)
+                           const int32_t *sigma, int *sym_flag, cudaStream_t s)
 {
     const int64_t Kt = Np / kBK;
     k_check_a<<<(unsigned)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
-        A, lda, N, Kt, occ, range_flag);
+        A, lda, N, Kt, occ, range_flag, sigma, sym_flag);
     return cudaGetLastError();
 }
 

@@ -55,12 +55,20 @@ cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t
 cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
                                     int64_t *launches);
-cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, int64_t w,
-                                 uint16_t *X1, int64_t ldx, cudaStream_t s);
+// gcol (may be null): the global column of each local column (else c0 + j).
+cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, const int32_t *gcol,
+                                 int64_t w, uint16_t *X1, int64_t ldx, cudaStream_t s);
+// X_1 on a column list: dst[i][j] = enc(src[i][gcol[j]]).
+cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, const int32_t *gcol, int64_t w,
+                               uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s);
+// Statistics of the full matrix from its columns gcol[0..w) under the symmetry sigma.
+cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
+                             int64_t w, unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s);
 // Range check of a row-major A (flag set if an entry lies in (0x7FFE, 0xFFFF)) and, if occ is
 // not null, the occupancy of its 128 x 32 tiles (occ zeroed by the caller).
+// If sigma is not null, sym_flag is set when some finite A_ij != A_(sigma i, sigma j).
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
-                           cudaStream_t s);
+                           const int32_t *sigma, int *sym_flag, cudaStream_t s);
 cudaError_t launch_tile_occupancy(const uint32_t *AT2, int64_t Mp, int64_t Kp, uint8_t *occ, cudaStream_t s);
 
 } // namespace mp

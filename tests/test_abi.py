@@ -134,6 +134,24 @@ def test_readoff_matches_oracle(oracle_mod):
             res.gamma2(2)
 
 
+@pytest.mark.parametrize("n", range(2, 10))
+def test_word_reversal_is_a_symmetry(n):
+    """sigma = word reversal is an involution and A(D_n)[sigma i][sigma j] = A(D_n)[i][j]
+    (the reflection of the path)."""
+    s = mp.word_reversal(n)
+    A = mp.build_transition_matrix(n)
+    assert np.array_equal(s[s], np.arange(len(s)))
+    assert np.array_equal(A[np.ix_(s, s)], A)
+
+
+def test_symmetry_hint_domain_errors():
+    assert _native.lib.mp_set_symmetry(np.array([1, 2, 0], dtype=np.int32).ctypes.data, 3) == 1  # a 3-cycle
+    assert _native.lib.mp_set_symmetry(np.array([0, 5], dtype=np.int32).ctypes.data, 2) == 1     # out of range
+    assert _native.lib.mp_set_symmetry(None, 0) == 0
+    with pytest.raises(mp.MinplusError):
+        _native._check(_native.lib.mp_word_reversal(4, np.zeros(3, dtype=np.int32).ctypes.data, 3))
+
+
 def test_argument_errors_before_device():
     with pytest.raises(mp.MinplusError) as e:
         mp.minplus_mul(np.zeros((2, 3)), np.zeros((2, 3)))

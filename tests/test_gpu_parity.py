@@ -197,6 +197,96 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     assert (g.mu, g.lam, g.offset) == (23, 18, 53)
 
 
+# --------------------------------------------------------------------------- symmetry
+def _random_symmetric(N, p_inf, seed):
+    """A random matrix with A[sigma i][sigma j] = A[i][j] for a random involution sigma."""
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(N)
+    sigma = np.arange(N, dtype=np.int32)
+    npairs = (N - N // 5) // 2                      # a fifth (about) fixed points
+    a, b = perm[:npairs], perm[npairs:2 * npairs]
+    sigma[a], sigma[b] = b, a
+    A = synth.transfer_like(N, N, p_inf, salt=seed)
+    S = A[np.ix_(sigma, sigma)]
+    keep = np.arange(N)[:, None] <= np.arange(N)[None, :]  # take the upper triangle's orbit rep.
+    B = np.where(keep, A, S)
+    B = np.where(B[np.ix_(sigma, sigma)] == B, B, np.minimum(B, B[np.ix_(sigma, sigma)]))
+    assert (B[np.ix_(sigma, sigma)] == B).all()
+    return B.astype(np.uint16), sigma
+
+
+@pytest.mark.parametrize("kernel", ["tiles", "spmm", "spmm-greedy"])
+@pytest.mark.parametrize("n", range(2, 10))
+def test_power_until_periodic_symmetry(mp, oracle_mod, n, kernel):
+    """With the word-reversal hint the run computes only the columns g <= sigma(g) and must
+    still report the oracle's full-matrix summaries and fingerprints."""
+    A = mp.build_transition_matrix(n)
+    use_kernel(mp, kernel)
+    mp.set_symmetry(mp.word_reversal(n))
+    try:
+        g = mp.minplus_power_until_periodic(A)
+    finally:
+        mp.set_symmetry(None)
+        reset_kernel(mp)
+    o = oracle_mod.power_until_periodic(A)
+    assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+    assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
+
+
+@pytest.mark.parametrize("kernel", ["dense", "tiles", "spmm"])
+@pytest.mark.parametrize("seed", range(3))
+def test_symmetry_random(mp, oracle_mod, seed, kernel):
+    N = [61, 300, 1031][seed]
+    A, sigma = _random_symmetric(N, [0.5, 0.9, 0.97][seed], 300 + seed)
+    use_kernel(mp, kernel)
+    mp.set_symmetry(sigma)
+    try:
+        g = mp.minplus_power_until_periodic(A, max_k=64)
+        rows = np.array([0, 5, N // 2, N - 1])
+        got = mp.minplus_power_rows(A, rows, 6)
+    finally:
+        mp.set_symmetry(None)
+        reset_kernel(mp)
+    o = oracle_mod.power_until_periodic(A, max_k=64)
+    assert o.rc == 0
+    assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+    assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
+    for r_i, r in enumerate(rows):
+        assert np.array_equal(got[:, r_i, :], oracle_mod.power_rows(A, int(r), 6)), r
+
+
+def test_symmetry_power_rows_full(mp, oracle_mod):
+    """Every entry of every power A^1..A^12 for n = 7 reassembled from the domain columns."""
+    A = mp.build_transition_matrix(7)
+    mp.set_symmetry(mp.word_reversal(7))
+    try:
+        got = mp.minplus_power_rows(A, np.arange(A.shape[0]), 12)
+    finally:
+        mp.set_symmetry(None)
+    X = A.copy()
+    for k in range(1, 13):
+        if k > 1:
+            X = oracle_mod.minplus(A, X)
+        assert np.array_equal(got[k - 1], X), k
+
+
+def test_symmetry_hint_verified(mp):
+    """A hint that does not hold is rejected (MP_ERR_DOMAIN), as is a non-involution."""
+    A = mp.build_transition_matrix(6)
+    N = A.shape[0]
+    bad = np.arange(N, dtype=np.int32)
+    bad[[3, 4]] = [4, 3]
+    mp.set_symmetry(bad)
+    try:
+        with pytest.raises(mp.MinplusError) as e:
+            mp.minplus_power_until_periodic(A)
+        assert e.value.status == 1
+    finally:
+        mp.set_symmetry(None)
+    with pytest.raises(mp.MinplusError):
+        mp.set_symmetry(np.roll(np.arange(N, dtype=np.int32), 1))
+
+
 # -------------------------------------------------------------------------- gamma_2
 def test_gamma2_cylinder_small(mp, oracle_mod):
     """gamma_2 through the public entry point: brute force (n*m <= 24), column DP, and the
@@ -245,13 +335,15 @@ def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
     assert f["r0_k50"] == t4[n]  # Table 4
 
 
+@pytest.mark.parametrize("sym", [True, False])
 @pytest.mark.parametrize("kernel", ["spmm", "spmm-greedy", "tiles"])
-def test_gamma2_record_words_source(mp, oracle_mod, kernel):
+def test_gamma2_record_words_source(mp, oracle_mod, kernel, sym):
     """The gamma2_cylinder path builds A(D_n) on the device from the word masks (with SpMM no
     AT2 at all): its whole record -- every power's fingerprint included -- equals the oracle's
     run on the oracle's own transition matrix."""
     mp.shutdown()  # drop the cached records
     use_kernel(mp, kernel)
+    mp.set_word_symmetry(sym)
     try:
         for n in range(2, 10):
             g = mp.gamma2_record(n)
@@ -260,6 +352,7 @@ def test_gamma2_record_words_source(mp, oracle_mod, kernel):
             assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint, n
     finally:
         reset_kernel(mp)
+        mp.set_word_symmetry(True)
         mp.shutdown()
 
 

@@ -116,6 +116,91 @@ def test_sharded_run_emulated(oracle_mod, n, world):
         assert state["cmp"] == len(expected)
 
 
+def _cols_stats(oracle, X, cols):
+    """Statistics of the full matrix restricted to a set of columns (global indices)."""
+    N = X.shape[0]
+    cols = sorted(set(int(c) for c in cols))
+    if not cols:
+        return 0, 0, INF, I64_MAX
+    fp = sum(oracle.fingerprint_cols(X, c, c + 1) for c in cols) % 2**64
+    sub = X[:, cols]
+    inf = int((sub == INF).sum())
+    diag = min([int(X[c, c]) for c in cols] + [INF])
+    ref = I64_MAX
+    for jj, c in enumerate(cols):
+        fin = np.nonzero(sub[:, jj] != INF)[0]
+        if len(fin):
+            i = int(fin[0])
+            ref = min(ref, (int(i * N + c) << 16) | int(X[i, c]))
+    return fp, inf, diag, ref
+
+
+@pytest.mark.parametrize("n,world", [(5, 2), (7, 3), (8, 2)])
+def test_sharded_run_symmetry_emulated(oracle_mod, n, world):
+    """As above with the word-reversal symmetry: the ranks shard the domain D = {g <= sigma g}
+    and a domain column stands for g and sigma g in every statistic."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+    import paper_2409_17688_b200 as mp
+
+    A = oracle_mod.transition_matrix(n)
+    N = A.shape[0]
+    sigma = mp.word_reversal(n)
+    D = [g for g in range(N) if g <= sigma[g]]
+    o = oracle_mod.power_until_periodic(A)
+    P = {1: A}
+    for k in range(2, o.k_last + 1):
+        P[k] = oracle_mod.minplus(A, P[k - 1])
+    shards = [mp.shard_range(len(D), world, r) for r in range(world)]
+
+    def colset(a, b):
+        return [D[q] for q in range(a, b)] + [int(sigma[D[q]]) for q in range(a, b)]
+
+    for rank in range(world):
+        others = [s for r, s in enumerate(shards) if r != rank]
+        part = {k: [_cols_stats(oracle_mod, P[k], colset(a, b)) for a, b in others] for k in P}
+        state = {"k": 0, "kb": 1}
+
+        class _Dev:
+            def __init__(self, ptr, cnt):
+                self.__cuda_array_interface__ = {"shape": (cnt,), "typestr": "<i8", "data": (ptr, False),
+                                                 "version": 3, "strides": None, "stream": None}
+
+        def allreduce(op, ptr, count):
+            t = torch.as_tensor(_Dev(ptr, count), device="cuda")
+            vals = [int(v) for v in t.cpu().tolist()]
+            if op == 0 and count >= 2:
+                out = []
+                for q in range(count // 2):
+                    got = part.get(state["k"] + 1 + q, [])
+                    out += [_i64(vals[2 * q] + sum(p[0] for p in got)), vals[2 * q + 1] + sum(p[1] for p in got)]
+                state["kb"] = state["k"] + 1
+                state["k"] += count // 2
+            elif op == 1 and count >= 2:
+                out = []
+                for q in range(count // 2):
+                    got = part.get(state["kb"] + q, [])
+                    out += [min([vals[2 * q]] + [p[2] for p in got]), min([vals[2 * q + 1]] + [p[3] for p in got])]
+            elif op == 0 and count == 1:        # exact-compare mismatches of the other domain shards
+                out = [vals[0]]                 # (the decisive compare has none anywhere)
+            else:
+                raise AssertionError((op, count))
+            t.copy_(torch.tensor(out, dtype=torch.int64, device="cuda"))
+            torch.cuda.synchronize()
+
+        mp.set_symmetry(sigma)
+        mp.dist_set(rank, world, allreduce)
+        try:
+            g = mp.minplus_power_until_periodic(A)
+        finally:
+            mp.dist_set(0, 1, None)
+            mp.set_symmetry(None)
+        assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+        assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
+
+
 def test_dist_torch_nccl_world1(oracle_mod):
     """The torch.distributed (NCCL) callback plumbing end to end with a 1-rank group."""
     import os
