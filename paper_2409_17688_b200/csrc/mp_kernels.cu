@@ -205,8 +205,17 @@ __global__ void __launch_bounds__(256)
         uint64_t b[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) b[e] = e < nc ? mix64(2 * (uint64_t)(c0 + j0 + e) + 1) : 0;
-        for (int64_t i = i0; i < i1; ++i) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
+        // rows in groups of 4 loads in flight
+        for (int64_t ib = i0; ib < i1; ib += 4) {
+            uint4 vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ib + u < i1) vv[u] = *reinterpret_cast<const uint4 *>(X + (ib + u) * ld + j0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = ib + u;
+            if (i >= i1) break;
+            const uint4 v = vv[u];
             const uint32_t words[4] = {v.x, v.y, v.z, v.w};
             const uint64_t t0 = (uint64_t)(i * N + c0 + j0);
             const uint32_t anyinf = __vcmpeq2(v.x, 0x7FFF7FFFu) | __vcmpeq2(v.y, 0x7FFF7FFFu) |
@@ -238,6 +247,7 @@ __global__ void __launch_bounds__(256)
                 const uint32_t x = (words[d >> 1] >> ((d & 1) * 16)) & 0xFFFFu;
                 dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
             }
+        }
         }
     }
 #pragma unroll
@@ -1385,9 +1395,9 @@ __global__ void __launch_bounds__(256)
     if (j0 < w) {
         const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
         uint64_t b[8], bm[8];
-        int64_t g[8], m[8];
+        int32_t g[8], m[8];
         unsigned two = 0; // bit e: column e stands for two global columns
-        int64_t mmin = INT64_MAX;
+        int32_t mmin = INT32_MAX;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             g[e] = e < nc ? gcol[j0 + e] : 0;
@@ -1397,28 +1407,27 @@ __global__ void __launch_bounds__(256)
             if (e < nc && m[e] != g[e]) two |= 1u << e;
             if (e < nc) mmin = min(mmin, m[e]);
         }
-        for (int64_t i = i0; i < i1; ++i) {
-            const int64_t si = sigma[i];
-            const uint4 v = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
+        const int32_t glast = g[nc - 1];
+        auto row = [&](int64_t i, int64_t si, const uint4 &v) {
             const uint32_t words[4] = {v.x, v.y, v.z, v.w};
             const uint32_t anyinf = __vcmpeq2(v.x, 0x7FFF7FFFu) | __vcmpeq2(v.y, 0x7FFF7FFFu) |
                                     __vcmpeq2(v.z, 0x7FFF7FFFu) | __vcmpeq2(v.w, 0x7FFF7FFFu);
             uint64_t rs = 0, rm = 0;
             if (nc == 8 && !anyinf) {
                 // the smallest key among (i, g_e) is e = 0 (gcol ascending); among the mirrors
-                // (sigma i, m_e) the smallest m_e
+                // (sigma i, m_e) the one at the smallest m_e
                 unsigned long long key = ((uint64_t)(i * N + g[0]) << 16) | (v.x & 0xFFFFu);
                 if (key < ref) ref = key;
+                uint32_t xm = 0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
                     rs += b[e] * x;
                     rm += bm[e] * x;
-                    if (m[e] == mmin) {
-                        key = ((uint64_t)(si * N + m[e]) << 16) | x;
-                        if (key < ref) ref = key;
-                    }
+                    if (m[e] == mmin) xm = x;
                 }
+                key = ((uint64_t)(si * N + mmin) << 16) | xm;
+                if (key < ref) ref = key;
             } else {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
@@ -1438,7 +1447,7 @@ __global__ void __launch_bounds__(256)
                 }
             }
             h += mix64(2 * (uint64_t)i) * rs + mix64(2 * (uint64_t)si) * rm;
-            if (i >= g[0] && i <= g[nc - 1]) { // the diagonal entry (i, i), if this slice holds it
+            if (i >= g[0] && i <= glast) { // the diagonal entry (i, i), if this slice holds it
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
                     if (e < nc && g[e] == i) {
@@ -1446,7 +1455,16 @@ __global__ void __launch_bounds__(256)
                         dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
                     }
             }
+        };
+        int64_t i = i0;
+        for (; i + 2 <= i1; i += 2) { // two rows in flight
+            const uint4 v0 = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
+            const uint4 v1 = *reinterpret_cast<const uint4 *>(X + (i + 1) * ld + j0);
+            const int64_t s0 = sigma[i], s1 = sigma[i + 1];
+            row(i, s0, v0);
+            row(i + 1, s1, v1);
         }
+        if (i < i1) row(i, sigma[i], *reinterpret_cast<const uint4 *>(X + i * ld + j0));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
