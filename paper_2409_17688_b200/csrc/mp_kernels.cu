@@ -511,6 +511,9 @@ constexpr int kSpCtasPerSm = MP_SP_CTAS;
 #ifndef MP_SP_LDGSTS
 #define MP_SP_LDGSTS 0
 #endif
+#ifndef MP_SP_NOCOMPUTE
+#define MP_SP_NOCOMPUTE 0
+#endif
 #ifndef MP_SP_BALANCE
 #define MP_SP_BALANCE 0
 #endif
@@ -1286,13 +1289,21 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
                 vals(e + 1, pb);
                 const uint4 xb0 = lds128(Xl + s), xb1 = lds128(Xl + s + 512);
                 s = row(e + 2);
+#if !MP_SP_NOCOMPUTE
                 dpx_group(acc, pa, xa0, xa1);
+#else // diagnostic build: the data path alone (results are not meaningful)
+                acc[0][0] ^= pa[0].x ^ xa0.x ^ xa1.y;
+#endif
                 if (e + 1 >= e1) break;
                 vals(e + 2, pa);
                 xa0 = lds128(Xl + s);
                 xa1 = lds128(Xl + s + 512);
                 s = row(e + 3);
+#if !MP_SP_NOCOMPUTE
                 dpx_group(acc, pb, xb0, xb1);
+#else
+                acc[0][1] ^= pb[0].x ^ xb0.x ^ xb1.y;
+#endif
                 e += 2;
                 if (e >= e1) break;
             }
