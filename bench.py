@@ -35,14 +35,14 @@ KERNEL_NAMES = {"dense": "k_minplus (dense tiles, VIADDMNMX.U16x2)",
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
-def traffic_bytes(kernel: str, n: int, world: int):
+def traffic_bytes(kernel: str, n: int, world: int, sym: bool = False):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
     committed ncu --set full capture of the same configuration (profiles/ncu_traffic.json)."""
     try:
         table = json.load(open(TRAFFIC_PATH))
     except (OSError, ValueError):
         return None
-    rec = table.get(f"{kernel.split()[0]}:{kernel.split('(')[1].split(',')[0]}:n{n}:g{world}")
+    rec = table.get(f"{kernel.split()[0]}:{kernel.split('(')[1].split(',')[0]}:n{n}:g{world}" + (":sym" if sym else ""))
     return rec["bytes_per_launch"] if rec else None
 
 
@@ -328,7 +328,7 @@ def run_mine(args):
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used], "achieved": achieved, "peak": peak,
                      "unit": "Gstep/s", "frac": achieved / peak,
-                     "traffic": traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world),
+                     "traffic": traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world, not args.no_symmetry),
                      "peak_source": f"148 SM x 128 steps/clk/SM x {sm_mhz:.0f} MHz observed (DESIGN.md)",
                      "avg_launch_ms": avg_launch_ms, "issued_steps_per_launch": issued_per_launch,
                      "kernel_share_of_step": prod_ms / max(ms, 1e-9)},
