@@ -1055,8 +1055,9 @@ void mp_shutdown(void)
 
 const char *mp_version(void)
 {
-    return "minplus-b200 0.2 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse) and "
-           "grouped (8-row) SpMM kernel, 4-stage cp.async";
+    return "minplus-b200 0.3 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse, 4-stage "
+           "cp.async) and warp-specialised grouped SpMM (4-row groups, greedy row grouping, bulk copies + mbarrier "
+           "ring); column symmetry";
 }
 
 int64_t mp_kernel_launches(void) { return g_launches.load(); }
