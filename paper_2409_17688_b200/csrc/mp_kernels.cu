@@ -192,6 +192,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // row weight.
 // ---------------------------------------------------------------------------------------
 constexpr int kStCols = 256 * 8;
+#ifndef MP_ST_ROWS
+#define MP_ST_ROWS 4
+#endif
+constexpr int kStRows = MP_ST_ROWS; // rows whose loads k_stats_sym keeps in flight
+__device__ __forceinline__ uint4 ldg_nc_v4(const void *p)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
 __global__ void __launch_bounds__(256)
     k_stats(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t c0, int64_t w, int64_t rpb,
             unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
@@ -1468,14 +1478,18 @@ __global__ void __launch_bounds__(256)
             }
         };
         int64_t i = i0;
-        for (; i + 2 <= i1; i += 2) { // two rows in flight
-            const uint4 v0 = *reinterpret_cast<const uint4 *>(X + i * ld + j0);
-            const uint4 v1 = *reinterpret_cast<const uint4 *>(X + (i + 1) * ld + j0);
-            const int64_t s0 = sigma[i], s1 = sigma[i + 1];
-            row(i, s0, v0);
-            row(i + 1, s1, v1);
+        for (; i + kStRows <= i1; i += kStRows) { // kStRows rows' loads in flight
+            uint4 vv[kStRows];
+            int32_t ss[kStRows];
+#pragma unroll
+            for (int u = 0; u < kStRows; ++u) {
+                vv[u] = ldg_nc_v4(X + (i + u) * ld + j0);
+                ss[u] = sigma[i + u];
+            }
+#pragma unroll
+            for (int u = 0; u < kStRows; ++u) row(i + u, ss[u], vv[u]);
         }
-        if (i < i1) row(i, sigma[i], *reinterpret_cast<const uint4 *>(X + i * ld + j0));
+        for (; i < i1; ++i) row(i, sigma[i], *reinterpret_cast<const uint4 *>(X + i * ld + j0));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
