@@ -288,6 +288,19 @@ def run_mine(args):
     e2e_ms = sum(a.elapsed_time(b) for a, b in fev)
     assert (r2.mu, r2.lam, r2.offset) == (res.mu, res.lam, res.offset)
 
+    # SURVEY.md section 8(d) "seconds to gamma_2": a cold gamma2_cylinder(n, 1000) call (no
+    # cached record, no workspace), wall clock: word masks on the host, A(D_n) built on the
+    # device, the whole power run, the read-off
+    mp.shutdown()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g2_1000 = mp.gamma2_cylinder(args.n, 1000)
+    torch.cuda.synchronize()
+    g2_seconds = time.perf_counter() - t0
+    assert g2_1000 == res.gamma2(1000)
+    barrier()
+
     vals = torch.tensor([ms, e2e_ms, dense, issued, prod_ms, float(prod_launches), float(launches),
                          float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -337,6 +350,8 @@ def run_mine(args):
                 "h2d_bytes_per_step": int(h2d / max(1, e2e_steps)), "d2h_bytes_per_step": int(d2h / max(1, e2e_steps)),
                 "seconds_to_gamma2": e2e_ms / e2e_steps / 1e3,
                 "setup_ms_last_step": e2e_setup_ms},
+        "gamma2_cylinder": {"n": args.n, "m": 1000, "gamma2": g2_1000, "seconds_cold_wall": g2_seconds,
+                            "note": "words source, word-reversal symmetry, includes allocation"},
         "setup_ms": setup_ms,
         "breakdown_ms_per_step": {"products": prod_ms / args.steps, "stats": stats_ms / args.steps,
                                   "setup": setup_ms, "library_total": total_lib_ms / args.steps,
