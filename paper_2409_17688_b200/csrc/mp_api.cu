@@ -172,8 +172,10 @@ struct PowerRun {
     // symmetry: local column jj holds global column gcol[jj] (g <= sigma g) and stands for g and
     // sigma g; cols_rep = number of global columns the local ones stand for
     bool sym = false;
+    DBuf bits;            // support bitsets written by k_check_a (matrix sources, grouped SpMM)
+    bool bits_ok = false;
     std::vector<int32_t> sigma, gcol, loc; // loc[g] = local column of domain column g (cap path)
-    DBuf dsig, dgcol;
+    DBuf dsig, dgcol, dloc; // dloc[g] = local column of global column g, or -1
     int64_t cols_rep = 0;
     const uint16_t *a_src = nullptr; // matrix sources: A (boundary encoding; the caller's buffer or
     int64_t a_ld = 0;                // stage_raw), valid for the duration of the run
@@ -329,7 +331,8 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
     int64_t launches = 0;
     const bool group = g_opts.grouping == 1 || (g_opts.grouping < 0 && R.N >= kGroupMinN);
     const cudaError_t e =
-        R.a_src ? build_sparse_form(R.a_src, R.a_ld, R.N, R.Np, group, R.sp, s, sp_alloc, &R, &launches)
+        R.a_src ? build_sparse_form(R.a_src, R.a_ld, R.N, R.Np, group, group && R.bits_ok ? R.bits.as<uint32_t>() : nullptr,
+                                    R.sp, s, sp_alloc, &R, &launches)
                 : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, group, R.sp, s, sp_alloc,
                                             &R, &launches);
     g_launches.fetch_add(launches);
@@ -365,6 +368,11 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
 // X_1 = A[:, c0:c0+w) in the device layout, from A, AT2 or straight from the word masks.
 mp_status make_power1(PowerRun &R, uint16_t *dst, cudaStream_t s)
 {
+    if (R.spmm && R.sp.off) { // row lists of A available (grouped path): fill + scatter
+        LAUNCH(launch_x1_csr(R.sp.off, R.sp.idx, R.N, R.a_src, R.a_ld, R.a_src ? nullptr : R.words.as<WordMask>(),
+                             R.dloc.as<int32_t>(), dst, R.ld, R.Np, s));
+        return MP_OK;
+    }
     if (R.sym) {
         if (R.a_src)
             LAUNCH(launch_encode_cols(R.a_src, R.a_ld, R.N, R.dgcol.as<int32_t>(), R.w, dst, R.ld, R.Np, s));
@@ -481,6 +489,15 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.cols_rep = R.w;
     }
     R.ld = pad_cols(R.w);
+    {
+        std::vector<int32_t> dl((size_t)N, -1);
+        if (R.sym)
+            for (size_t jj = 0; jj < R.gcol.size(); ++jj) dl[(size_t)R.gcol[jj]] = (int32_t)jj;
+        else
+            for (int64_t j = 0; j < R.w; ++j) dl[(size_t)(R.c0 + j)] = (int32_t)j;
+        TRY(R.dloc.ensure((size_t)N * 4, "column map"));
+        COPY(R.dloc.p, dl.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s);
+    }
     if (R.slot_bytes() != R.cached_slot) {
         R.ring.clear();
         R.tmp0.release();
@@ -493,6 +510,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // kernels need AT2 (transposed, duplicated, device encoding), built once they are chosen.
     // The words source with SpMM needs no matrix at all (69 GB saved at n = 13).
     R.n_words = words_src ? src.n : 0;
+    R.bits_ok = false;
     R.a_src = nullptr;
     R.a_ld = 0;
     TRY(R.flag.ensure(16, "range flag"));
@@ -515,9 +533,14 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
             CUDA_TRY(cudaMemsetAsync(R.occ.p, 0, (size_t)(Mt * Kt), s));
         }
+        // the grouped SpMM path needs A's support bitsets: the range check writes them
+        R.bits_ok = (g_opts.sparsity == 2 || g_opts.sparsity < 0) &&
+                    (g_opts.grouping == 1 || (g_opts.grouping < 0 && N >= kGroupMinN));
+        if (R.bits_ok) TRY(R.bits.ensure((size_t)N * ((N + 31) / 32) * 4, "support bitsets"));
         CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, 2 * sizeof(int), s));
         LAUNCH(launch_check_a(R.a_src, R.a_ld, N, R.Np, need_occ ? R.occ.as<uint8_t>() : nullptr, R.flag.as<int>(),
-                              R.sym ? R.dsig.as<int32_t>() : nullptr, R.flag.as<int>() + 1, s));
+                              R.sym ? R.dsig.as<int32_t>() : nullptr, R.flag.as<int>() + 1,
+                              R.bits_ok ? R.bits.as<uint32_t>() : nullptr, s));
         int hflag[2] = {0, 0};
         COPY(hflag, R.flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));

@@ -590,7 +590,7 @@ struct AccWords { // straight from the word masks (A(D_n) without materialising 
 // gives the same product; this one only lowers the issued steps and the staged X rows
 // (DESIGN.md "Row grouping").
 // ---------------------------------------------------------------------------------------
-constexpr int kGrpWin = 512;
+constexpr int kGrpWin = 256; // 512 gave 1 % fewer staged X rows at twice the pass-2 time
 constexpr int kRefThreads = 128;
 constexpr int kRefRows = 32; // pass 3 refines 32-row blocks of a tile into groups of kG
 constexpr int kRefGroups = kRefRows / kG;
@@ -903,6 +903,27 @@ __global__ void k_group_masks(Acc acc, int64_t Np, uint8_t *__restrict__ m8)
     }
 }
 
+// m8 from the support bits (the grouped path): bit r of m8[g * Np + l] = bit l of the row in
+// slot kG*g + r (rows >= N, l >= N: 0).  Consecutive threads share a bits word.
+__global__ void k_group_masks_bits(const uint32_t *__restrict__ bits, int64_t nw, int64_t N,
+                                   const int32_t *__restrict__ rows, int64_t Np, uint8_t *__restrict__ m8)
+{
+    const int64_t G = Np / kG;
+    const int64_t total = G * Np;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = t / Np, l = t - g * Np;
+        unsigned m = 0;
+        if (l < N) {
+#pragma unroll
+            for (int r = 0; r < kG; ++r) {
+                const int64_t i = rows[g * kG + r];
+                if (i < N) m |= ((bits[i * nw + (l >> 5)] >> (l & 31)) & 1u) << r;
+            }
+        }
+        m8[t] = (uint8_t)m;
+    }
+}
+
 // Block-ordered compaction: for flags over [0, n) in increasing index order, calls
 // emit(index, rank) for each set flag; returns the count.  One block, blockDim.x % 32 == 0.
 template <class FlagF, class EmitF>
@@ -1081,8 +1102,62 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
     }
 }
 
-// Exclusive scan of n int32 counts into int64 offsets (out[n] = total); one block.
-__global__ void k_scan_counts(const int32_t *__restrict__ cnt, int64_t n, int64_t *__restrict__ out)
+// Multi-block exclusive scan (reduce, scan the block sums, scan with offsets), for the long
+// count arrays (per (chunk, group) entry counts: 1.7 M at n = 12).
+constexpr int kScanSeg = 4096; // elements per block (1024 threads x 4)
+__global__ void __launch_bounds__(1024) k_scan_reduce(const int32_t *__restrict__ cnt, int64_t n,
+                                                      int64_t *__restrict__ bsum)
+{
+    __shared__ int64_t ws[32];
+    const int64_t b0 = (int64_t)blockIdx.x * kScanSeg;
+    int64_t v = 0;
+    for (int q = threadIdx.x; q < kScanSeg; q += blockDim.x)
+        if (b0 + q < n) v += cnt[b0 + q];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+__global__ void __launch_bounds__(1024) k_scan_apply(const int32_t *__restrict__ cnt, int64_t n,
+                                                     const int64_t *__restrict__ boff, int64_t *__restrict__ out)
+{
+    __shared__ int64_t ws[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int64_t b0 = (int64_t)blockIdx.x * kScanSeg + (int64_t)threadIdx.x * 4;
+    int64_t v[4], sum = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        v[u] = (b0 + u < n) ? cnt[b0 + u] : 0;
+        sum += v[u];
+    }
+    int64_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    int64_t before = boff[blockIdx.x];
+    for (int w = 0; w < warp; ++w) before += ws[w];
+    int64_t run = before + x - sum;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if (b0 + u < n) out[b0 + u] = run;
+        run += v[u];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[n] = run;
+    (void)nwarps;
+}
+
+// Exclusive scan of n counts into int64 offsets (out[n] = total); one block.
+template <class T>
+__global__ void k_scan_counts(const T *__restrict__ cnt, int64_t n, int64_t *__restrict__ out)
 {
     __shared__ int64_t carry;
     __shared__ int64_t wsum[32];
@@ -1597,8 +1672,9 @@ cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint1
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
 template <class Acc>
-cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, SparseWork &w, cudaStream_t s,
-                                cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
+cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, const uint32_t *pre_bits, SparseWork &w,
+                                cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
+                                int64_t *launches)
 {
     const int64_t G = Np / kG, Mt = Np / kSpRows;
     cudaError_t e;
@@ -1612,24 +1688,50 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     do {                                                                                                                \
         if ((e = alloc((void **)&(ptr), (bytes), actx)) != cudaSuccess) return e;                                       \
     } while (0)
+    // exclusive scan of n int32 counts into int64 offsets: one block for short arrays, else
+    // reduce / scan the block sums / apply
+#define SP_SCAN(cnt, n, out)                                                                                           \
+    do {                                                                                                                \
+        const int64_t n_ = (n);                                                                                         \
+        if (n_ <= 4 * kScanSeg) {                                                                                       \
+            SP_LAUNCH((k_scan_counts<int32_t><<<1, 1024, 0, s>>>((cnt), n_, (out))));                                   \
+        } else {                                                                                                        \
+            const int64_t nb_ = (n_ + kScanSeg - 1) / kScanSeg;                                                         \
+            int64_t *bs_ = nullptr, *bo_ = nullptr;                                                                     \
+            SP_ALLOC(bs_, (size_t)nb_ * 8);                                                                             \
+            SP_ALLOC(bo_, (size_t)(nb_ + 1) * 8);                                                                       \
+            SP_LAUNCH((k_scan_reduce<<<(unsigned)nb_, 1024, 0, s>>>((cnt), n_, bs_)));                                  \
+            SP_LAUNCH((k_scan_counts<int64_t><<<1, 1024, 0, s>>>(bs_, nb_, bo_)));                                      \
+            SP_LAUNCH((k_scan_apply<<<(unsigned)nb_, 1024, 0, s>>>((cnt), n_, bo_, (out))));                            \
+        }                                                                                                               \
+    } while (0)
     w.rows = nullptr;
+    w.bits = nullptr;
+    w.off = nullptr;
+    w.idx = nullptr;
     if (group) { // row grouping first: every later builder reads A through it
         const int64_t nw = (N + 31) / 32;
-        uint32_t *bits = nullptr;
+        uint32_t *bits = const_cast<uint32_t *>(pre_bits); // from k_check_a for matrix sources
         int32_t *cnt = nullptr, *idx = nullptr;
         int64_t *off = nullptr;
         SP_ALLOC(w.rows, (size_t)Np * 4);
-        SP_ALLOC(bits, (size_t)N * nw * 4);
         SP_ALLOC(cnt, (size_t)N * 4);
         SP_ALLOC(off, (size_t)(N + 1) * 8);
-        SP_LAUNCH((k_support_bits<<<(unsigned)std::min<int64_t>(N, (int64_t)num_sms() * 8), 256, 0, s>>>(AT2, N, nw, bits)));
+        if (!bits) {
+            SP_ALLOC(bits, (size_t)N * nw * 4);
+            SP_LAUNCH(
+                (k_support_bits<<<(unsigned)std::min<int64_t>(N, (int64_t)num_sms() * 8), 256, 0, s>>>(AT2, N, nw, bits)));
+        }
+        w.bits = bits;
         SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, cnt)));
-        SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(cnt, N, off)));
+        SP_SCAN(cnt, N, off);
         int64_t nnz = 0;
         if ((e = cudaMemcpyAsync(&nnz, off + N, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
         SP_ALLOC(idx, (size_t)std::max<int64_t>(nnz, 1) * 4);
         SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, off, idx, nullptr, 0)));
+        w.off = off;
+        w.idx = idx;
         // column lists: the transposed bits through the same two kernels (bits is reused)
         uint32_t *bitsT = nullptr;
         int64_t *coff = nullptr;
@@ -1639,7 +1741,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
         SP_ALLOC(cidx, (size_t)std::max<int64_t>(nnz, 1) * 4);
         SP_LAUNCH((k_bits_transpose<<<grid_for(nw * nw * 32, 256), 256, 0, s>>>(bits, nw, N, bitsT)));
         SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, cnt)));
-        SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(cnt, N, coff)));
+        SP_SCAN(cnt, N, coff);
         const int64_t nwin = (N + kGrpWin - 1) / kGrpWin;
         int32_t *cwst = nullptr;
         SP_ALLOC(cwst, (size_t)N * nwin * 4);
@@ -1668,11 +1770,14 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     SP_ALLOC(w.tptr, (size_t)(Mt + 1) * 8);
     SP_ALLOC(w.nch, (size_t)Mt * 4);
     SP_ALLOC(w.tch, (size_t)(Mt + 1) * 8);
-    SP_LAUNCH((k_group_masks<<<grid_for(G * Np, 256), 256, 0, s>>>(AT2, Np, w.m8)));
+    if (group)
+        SP_LAUNCH((k_group_masks_bits<<<grid_for(G * Np, 256), 256, 0, s>>>(w.bits, (N + 31) / 32, N, w.rows, Np, w.m8)));
+    else
+        SP_LAUNCH((k_group_masks<<<grid_for(G * Np, 256), 256, 0, s>>>(AT2, Np, w.m8)));
     SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, nullptr, w.tcnt, nullptr)));
-    SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(w.tcnt, Mt, w.tptr)));
+    SP_SCAN(w.tcnt, Mt, w.tptr);
     SP_LAUNCH((k_chunk_counts<<<grid_for(Mt, 256), 256, 0, s>>>(w.tcnt, Mt, w.nch)));
-    SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(w.nch, Mt, w.tch)));
+    SP_SCAN(w.nch, Mt, w.tch);
     int64_t tot[2] = {0, 0};
     if ((e = cudaMemcpyAsync(&tot[0], w.tptr + Mt, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(&tot[1], w.tch + Mt, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
@@ -1695,7 +1800,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], w.ecnt, nullptr, nullptr)));
-    SP_LAUNCH((k_scan_counts<<<1, 1024, 0, s>>>(w.ecnt, tot[1] * kSpGroups, w.eoff)));
+    SP_SCAN(w.ecnt, tot[1] * kSpGroups, w.eoff);
     int64_t ne = 0;
     if ((e = cudaMemcpyAsync(&ne, w.eoff + tot[1] * kSpGroups, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
@@ -1704,23 +1809,24 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, Spar
     w.group_rows = kG;
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E)));
+#undef SP_SCAN
 #undef SP_LAUNCH
 #undef SP_ALLOC
     return cudaSuccess;
 }
 
-cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group, SparseWork &w,
-                              cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
-                              int64_t *launches)
+cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group,
+                              const uint32_t *pre_bits, SparseWork &w, cudaStream_t s,
+                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
 {
-    return build_sparse_form_t(AccA{A, lda, N, nullptr}, N, Np, group, w, s, alloc, actx, launches);
+    return build_sparse_form_t(AccA{A, lda, N, nullptr}, N, Np, group, pre_bits, w, s, alloc, actx, launches);
 }
 
 cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
                                     int64_t *launches)
 {
-    return build_sparse_form_t(AccWords{words, N, (1u << n) - 1u, nullptr}, N, Np, group, w, s, alloc, actx,
+    return build_sparse_form_t(AccWords{words, N, (1u << n) - 1u, nullptr}, N, Np, group, nullptr, w, s, alloc, actx,
                                launches);
 }
 
@@ -1745,6 +1851,44 @@ cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_
                                  int64_t w, uint16_t *X1, int64_t ldx, cudaStream_t s)
 {
     k_x1_from_words<<<grid_for(Np * ldx, 256), 256, 0, s>>>(words, N, (1u << n) - 1u, Np, c0, gcol, w, X1, ldx);
+    return cudaGetLastError();
+}
+
+// X_1 from the row lists of A (the grouped path; A is < 1 % finite): fill with +inf, then
+// scatter each finite a_il whose column l is local (loc[l] >= 0) to X1[i][loc[l]].  The value
+// comes from A (matrix sources) or is the label zeros(l) (words source).
+__global__ void k_x1_fill(uint16_t *__restrict__ X1, int64_t n16)
+{
+    uint4 *p = reinterpret_cast<uint4 *>(X1);
+    const uint4 inf = make_uint4(0x7FFF7FFFu, 0x7FFF7FFFu, 0x7FFF7FFFu, 0x7FFF7FFFu);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n16; q += (int64_t)gridDim.x * blockDim.x)
+        p[q] = inf;
+}
+__global__ void k_x1_scatter(const int64_t *__restrict__ off, const int32_t *__restrict__ idx, int64_t N,
+                             const uint16_t *__restrict__ A, int64_t lda, const WordMask *__restrict__ words,
+                             const int32_t *__restrict__ loc, uint16_t *__restrict__ X1, int64_t ldx)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        for (int64_t q = off[i] + lane; q < off[i + 1]; q += 32) {
+            const int32_t l = idx[q];
+            const int32_t j = loc[l];
+            if (j < 0) continue;
+            uint16_t v = A ? A[i * lda + l] : words[l].zeros;
+            if (v > kFiniteMax) v = kDevInf;
+            X1[i * ldx + j] = v;
+        }
+    }
+}
+
+cudaError_t launch_x1_csr(const int64_t *off, const int32_t *idx, int64_t N, const uint16_t *A, int64_t lda,
+                          const WordMask *words, const int32_t *loc, uint16_t *X1, int64_t ldx, int64_t Np,
+                          cudaStream_t s)
+{
+    const int64_t n16 = Np * ldx / 8; // ldx is a multiple of 512
+    k_x1_fill<<<grid_for(n16, 256), 256, 0, s>>>(X1, n16);
+    k_x1_scatter<<<grid_for(N * 32, 256), 256, 0, s>>>(off, idx, N, A, lda, words, loc, X1, ldx);
     return cudaGetLastError();
 }
 
@@ -1777,14 +1921,17 @@ cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, c
 // Range check of A (row-major, boundary encoding) and, if occ != null, the occupancy of its
 // 128 x 32 tiles (occ zeroed by the caller): one warp per (row, 32-column tile).
 __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N, int64_t Kt, uint8_t *__restrict__ occ,
-                          int *__restrict__ range_flag, const int32_t *__restrict__ sigma, int *__restrict__ sym_flag)
+                          int *__restrict__ range_flag, const int32_t *__restrict__ sigma, int *__restrict__ sym_flag,
+                          uint32_t *__restrict__ bits, int64_t nw)
 {
-    const int lane = threadIdx.x & 31;
+    // blocks stride over rows, warps over the row's 32-column words (= the tile columns of occ)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     bool bad = false, asym = false;
     for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
         const uint16_t *row = A + i * lda;
-        for (int64_t j0 = 0; j0 < Kt * 16; j0 += blockDim.x) { // column pairs; a warp = 2 tiles
-            const int64_t j = j0 + threadIdx.x, c = 2 * j;
+        const int64_t si = sigma ? (int64_t)sigma[i] : 0;
+        for (int64_t k = warp; k < nw; k += nwarps) {
+            const int64_t c = k * 32 + lane;
             bool f = false;
             if (c < N) {
                 const uint16_t x = row[c];
@@ -1792,20 +1939,15 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
                 bad |= f && x > kFiniteMax;
                 // symmetry hint: every finite entry must reappear at (sigma i, sigma j); sigma x
                 // sigma is a bijection, so the +inf entries then map onto +inf entries too
-                if (sigma && f) asym |= A[(int64_t)sigma[i] * lda + sigma[c]] != x;
+                if (sigma && f) asym |= A[si * lda + sigma[c]] != x;
             }
-            if (c + 1 < N) {
-                const uint16_t x = row[c + 1];
-                f |= x != kBndInf;
-                bad |= x != kBndInf && x > kFiniteMax;
-                if (sigma && x != kBndInf) asym |= A[(int64_t)sigma[i] * lda + sigma[c + 1]] != x;
-            }
-            const uint32_t b = __ballot_sync(0xFFFFFFFFu, f);
-            if (occ && lane == 0) {
-                const int64_t kt = (j - lane) / 16;
-                uint8_t *o = occ + (i / kBM) * Kt + kt;
-                if ((b & 0xFFFFu) && kt < Kt && !o[0]) o[0] = 1;
-                if ((b >> 16) && kt + 1 < Kt && !o[1]) o[1] = 1;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+            if (lane == 0) {
+                if (bits) bits[i * nw + k] = m;
+                if (occ && m && k < Kt) {
+                    uint8_t *o = occ + (i / kBM) * Kt + k;
+                    if (!*o) *o = 1;
+                }
             }
         }
     }
@@ -1814,11 +1956,12 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
 }
 
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
-                           const int32_t *sigma, int *sym_flag, cudaStream_t s)
+                           const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s)
 {
+    static_assert(kBK == 32, "occupancy tiles are the 32-column words");
     const int64_t Kt = Np / kBK;
     k_check_a<<<(unsigned)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
-        A, lda, N, Kt, occ, range_flag, sigma, sym_flag);
+        A, lda, N, Kt, occ, range_flag, sigma, sym_flag, bits, (N + 31) / 32);
     return cudaGetLastError();
 }
 

@@ -42,6 +42,9 @@ struct SparseWork {
     int64_t *tptr = nullptr, *tch = nullptr, *eoff = nullptr;
     uint4 *E = nullptr;
     int32_t *rows = nullptr; // row grouping (null: consecutive rows)
+    uint32_t *bits = nullptr; // support bitsets (grouped path)
+    int64_t *off = nullptr;   // row lists of A's support (grouped path): CSR offsets ...
+    int32_t *idx = nullptr;   // ... and column indices
     int group_rows = 0;      // rows per group: issued steps = entries * group_rows * ld
     int64_t total_union = 0, total_chunks = 0, entries = 0;
 };
@@ -49,15 +52,21 @@ cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint1
                         int64_t ncols_p, cudaStream_t s);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
-cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group, SparseWork &w,
-                              cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
-                              int64_t *launches);
+// pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).
+cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group,
+                              const uint32_t *pre_bits, SparseWork &w, cudaStream_t s,
+                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);
 cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
                                     int64_t *launches);
 // gcol (may be null): the global column of each local column (else c0 + j).
 cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, const int32_t *gcol,
                                  int64_t w, uint16_t *X1, int64_t ldx, cudaStream_t s);
+// X_1 from the row lists of A: +inf everywhere, then each finite a_il with loc[l] >= 0 at
+// X1[i][loc[l]] (value from A, or the label zeros(l) of the words source if A is null).
+cudaError_t launch_x1_csr(const int64_t *off, const int32_t *idx, int64_t N, const uint16_t *A, int64_t lda,
+                          const WordMask *words, const int32_t *loc, uint16_t *X1, int64_t ldx, int64_t Np,
+                          cudaStream_t s);
 // X_1 on a column list: dst[i][j] = enc(src[i][gcol[j]]).
 cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, const int32_t *gcol, int64_t w,
                                uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s);
@@ -67,8 +76,10 @@ cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int
 // Range check of a row-major A (flag set if an entry lies in (0x7FFE, 0xFFFF)) and, if occ is
 // not null, the occupancy of its 128 x 32 tiles (occ zeroed by the caller).
 // If sigma is not null, sym_flag is set when some finite A_ij != A_(sigma i, sigma j).
+// If bits is not null it receives A's support bitsets (bit b of bits[i * ceil(N/32) + k] =
+// A_(i, 32k + b) finite).
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
-                           const int32_t *sigma, int *sym_flag, cudaStream_t s);
+                           const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s);
 cudaError_t launch_tile_occupancy(const uint32_t *AT2, int64_t Mp, int64_t Kp, uint8_t *occ, cudaStream_t s);
 
 } // namespace mp
