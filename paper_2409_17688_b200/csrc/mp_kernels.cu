@@ -908,19 +908,33 @@ __global__ void k_group_masks(Acc acc, int64_t Np, uint8_t *__restrict__ m8)
 __global__ void k_group_masks_bits(const uint32_t *__restrict__ bits, int64_t nw, int64_t N,
                                    const int32_t *__restrict__ rows, int64_t Np, uint8_t *__restrict__ m8)
 {
-    const int64_t G = Np / kG;
-    const int64_t total = G * Np;
+    // one thread per (group, 32-column word): 4 bitset words in, 32 mask bytes out
+    const int64_t G = Np / kG, nk = Np / 32;
+    const int64_t total = G * nk;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t g = t / Np, l = t - g * Np;
-        unsigned m = 0;
-        if (l < N) {
+        const int64_t g = t / nk, k = t - g * nk;
+        uint32_t wr[kG];
 #pragma unroll
-            for (int r = 0; r < kG; ++r) {
-                const int64_t i = rows[g * kG + r];
-                if (i < N) m |= ((bits[i * nw + (l >> 5)] >> (l & 31)) & 1u) << r;
-            }
+        for (int r = 0; r < kG; ++r) {
+            const int64_t i = rows[g * kG + r];
+            wr[r] = (i < N && k < nw) ? bits[i * nw + k] : 0u;
         }
-        m8[t] = (uint8_t)m;
+        uint32_t out[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                unsigned m = 0;
+#pragma unroll
+                for (int r = 0; r < kG; ++r) m |= ((wr[r] >> (4 * q + b)) & 1u) << r;
+                v |= m << (8 * b);
+            }
+            out[q] = v;
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(m8 + g * Np + k * 32);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
     }
 }
 
@@ -1771,7 +1785,8 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     SP_ALLOC(w.nch, (size_t)Mt * 4);
     SP_ALLOC(w.tch, (size_t)(Mt + 1) * 8);
     if (group)
-        SP_LAUNCH((k_group_masks_bits<<<grid_for(G * Np, 256), 256, 0, s>>>(w.bits, (N + 31) / 32, N, w.rows, Np, w.m8)));
+        SP_LAUNCH((k_group_masks_bits<<<grid_for(G * (Np / 32), 256), 256, 0, s>>>(w.bits, (N + 31) / 32, N, w.rows, Np,
+                                                                                   w.m8)));
     else
         SP_LAUNCH((k_group_masks<<<grid_for(G * Np, 256), 256, 0, s>>>(AT2, Np, w.m8)));
     SP_LAUNCH((k_tile_union<<<(unsigned)Mt, 1024, 0, s>>>(w.m8, Np, nullptr, w.tcnt, nullptr)));
@@ -1930,23 +1945,31 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
     for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
         const uint16_t *row = A + i * lda;
         const int64_t si = sigma ? (int64_t)sigma[i] : 0;
-        for (int64_t k = warp; k < nw; k += nwarps) {
-            const int64_t c = k * 32 + lane;
-            bool f = false;
-            if (c < N) {
-                const uint16_t x = row[c];
-                f = x != kBndInf;
+        for (int64_t k0 = warp; k0 < nw; k0 += 4 * nwarps) { // 4 words' loads in flight
+            uint16_t xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t c = (k0 + (int64_t)u * nwarps) * 32 + lane;
+                xv[u] = c < N ? row[c] : kBndInf;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t k = k0 + (int64_t)u * nwarps;
+                if (k >= nw) break;
+                const int64_t c = k * 32 + lane;
+                const uint16_t x = xv[u];
+                const bool f = x != kBndInf;
                 bad |= f && x > kFiniteMax;
                 // symmetry hint: every finite entry must reappear at (sigma i, sigma j); sigma x
                 // sigma is a bijection, so the +inf entries then map onto +inf entries too
                 if (sigma && f) asym |= A[si * lda + sigma[c]] != x;
-            }
-            const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
-            if (lane == 0) {
-                if (bits) bits[i * nw + k] = m;
-                if (occ && m && k < Kt) {
-                    uint8_t *o = occ + (i / kBM) * Kt + k;
-                    if (!*o) *o = 1;
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+                if (lane == 0) {
+                    if (bits) bits[i * nw + k] = m;
+                    if (occ && m && k < Kt) {
+                        uint8_t *o = occ + (i / kBM) * Kt + k;
+                        if (!*o) *o = 1;
+                    }
                 }
             }
         }
