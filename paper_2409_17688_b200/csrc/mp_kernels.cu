@@ -508,7 +508,11 @@ constexpr int kSpGroups = kSpRows / kG;
 constexpr int kSpChunk = MP_SP_CHUNK;
 constexpr int kSpCols = 512;            // columns per CTA (32 lanes x 16)
 constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
-constexpr int kSpConsumers = kSpGroups;  // warp j < kSpGroups computes group j
+#ifndef MP_SP_GPW
+#define MP_SP_GPW 1
+#endif
+constexpr int kSpGpw = MP_SP_GPW;                  // groups per consumer warp
+constexpr int kSpConsumers = kSpGroups / kSpGpw;   // consumer warp w computes groups w*kSpGpw ..
 constexpr int kSpThreads = 32 * (kSpConsumers + 1); // + one producer warp
 constexpr int kSpStages = MP_SP_STAGES;
 // One ring stage: X rows | entries (+3 look-ahead records) | the chunk's kSpGroups + 1 entry
@@ -1353,12 +1357,14 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
         return;
     }
 
-    // consumer warp: group j = warp
-    uint32_t acc[kG][8];
+    // consumer warp: groups warp * kSpGpw + gg
+    uint32_t acc[kSpGpw][kG][8];
 #pragma unroll
-    for (int r = 0; r < kG; ++r)
+    for (int gg = 0; gg < kSpGpw; ++gg)
 #pragma unroll
-        for (int p = 0; p < 8; ++p) acc[r][p] = 0xFFFFFFFFu;
+        for (int r = 0; r < kG; ++r)
+#pragma unroll
+            for (int p = 0; p < 8; ++p) acc[gg][r][p] = 0xFFFFFFFFu;
     for (int c = 0; c < nch; ++c) {
         const int st = c % kSpStages;
         mbar_wait(bar_full + st * 8, (c / kSpStages) & 1);
@@ -1366,7 +1372,6 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
         const uint4 *Es = reinterpret_cast<const uint4 *>(stage_p + XB);
         const int64_t *Bs = reinterpret_cast<const int64_t *>(stage_p + XB + EB);
         const int64_t eb = Bs[0];
-        const int e0 = (int)(Bs[warp] - eb), e1 = (int)(Bs[warp + 1] - eb);
         // Entries walked with values and X rows one entry ahead (ping-pong A/B) and row offsets
         // two ahead.  Look-ahead reads past the group's end read the next group's records or a
         // zero/stale record of the entry area, whose row offset is a valid one.  Row offsets
@@ -1377,6 +1382,10 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
 #pragma unroll
             for (int u = 0; u < kG / 4; ++u) v[u] = Es[kEntU4 * q + u];
         };
+#pragma unroll
+        for (int gg = 0; gg < kSpGpw; ++gg) {
+        const int jg = warp * kSpGpw + gg;
+        const int e0 = (int)(Bs[jg] - eb), e1 = (int)(Bs[jg + 1] - eb);
         if (e0 < e1) {
             int e = e0;
             uint4 pa[kG / 4], pb[kG / 4];
@@ -1389,9 +1398,9 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
                 const uint4 xb0 = lds128(Xl + s), xb1 = lds128(Xl + s + 512);
                 s = row(e + 2);
 #if !MP_SP_NOCOMPUTE
-                dpx_group(acc, pa, xa0, xa1);
+                dpx_group(acc[gg], pa, xa0, xa1);
 #else // diagnostic build: the data path alone (results are not meaningful)
-                acc[0][0] ^= pa[0].x ^ xa0.x ^ xa1.y;
+                acc[gg][0][0] ^= pa[0].x ^ xa0.x ^ xa1.y;
 #endif
                 if (e + 1 >= e1) break;
                 vals(e + 2, pa);
@@ -1399,13 +1408,14 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
                 xa1 = lds128(Xl + s + 512);
                 s = row(e + 3);
 #if !MP_SP_NOCOMPUTE
-                dpx_group(acc, pb, xb0, xb1);
+                dpx_group(acc[gg], pb, xb0, xb1);
 #else
-                acc[0][1] ^= pb[0].x ^ xb0.x ^ xb1.y;
+                acc[gg][0][1] ^= pb[0].x ^ xb0.x ^ xb1.y;
 #endif
                 e += 2;
                 if (e >= e1) break;
             }
+        }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty + st * 8);
@@ -1415,20 +1425,21 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
     // (The a4 statistics stay in k_stats: fused here they cost more, 9 ms vs 5.7 ms per n = 12
     // power, because only this CTA's warps run the hashing while it holds its SM slot.)
 #pragma unroll
-    for (int r = 0; r < kG; ++r) {
-        const int64_t slot = (int64_t)t * kSpRows + kG * warp + r;
+    for (int q = 0; q < kSpGpw * kG; ++q) {
+        const int gg = q / kG, r = q % kG;
+        const int64_t slot = (int64_t)t * kSpRows + kG * (warp * kSpGpw + gg) + r;
         const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
         uint16_t *crow = C + i * ldc + col0 + 8 * lane;
         uint4 v;
-        v.x = __vminu2(acc[r][0], 0x7FFF7FFFu);
-        v.y = __vminu2(acc[r][1], 0x7FFF7FFFu);
-        v.z = __vminu2(acc[r][2], 0x7FFF7FFFu);
-        v.w = __vminu2(acc[r][3], 0x7FFF7FFFu);
+        v.x = __vminu2(acc[gg][r][0], 0x7FFF7FFFu);
+        v.y = __vminu2(acc[gg][r][1], 0x7FFF7FFFu);
+        v.z = __vminu2(acc[gg][r][2], 0x7FFF7FFFu);
+        v.w = __vminu2(acc[gg][r][3], 0x7FFF7FFFu);
         *reinterpret_cast<uint4 *>(crow) = v;
-        v.x = __vminu2(acc[r][4], 0x7FFF7FFFu);
-        v.y = __vminu2(acc[r][5], 0x7FFF7FFFu);
-        v.z = __vminu2(acc[r][6], 0x7FFF7FFFu);
-        v.w = __vminu2(acc[r][7], 0x7FFF7FFFu);
+        v.x = __vminu2(acc[gg][r][4], 0x7FFF7FFFu);
+        v.y = __vminu2(acc[gg][r][5], 0x7FFF7FFFu);
+        v.z = __vminu2(acc[gg][r][6], 0x7FFF7FFFu);
+        v.w = __vminu2(acc[gg][r][7], 0x7FFF7FFFu);
         *reinterpret_cast<uint4 *>(crow + 256) = v;
     }
 }
