@@ -92,6 +92,23 @@ mp_status minplus_mul_device(const uint16_t *dA, int64_t lda, const uint16_t *dB
                              uint16_t *dC, int64_t ldc, int64_t M, int64_t K, int64_t N,
                              void *stream);
 
+/* NEXT-4: general products through the same kernel.
+ *   minplus_mul_strided_batched_device: C_b = A_b x B_b for b < batch, with A_b = dA +
+ *     b*strideA (elements; likewise B_b, C_b), each as in minplus_mul_device, in order on
+ *     `stream`.  Errors as minplus_mul_device, plus MP_ERR_DOMAIN for batch <= 0, a negative
+ *     stride, C matrices overlapping each other or any A_b / B_b.
+ *   minplus_closure: D = (I (+) W)^(2^t) with 2^t >= N-1 (t squarings; *squarings_out = t if
+ *     not NULL): for a weighted adjacency W (N x N host, boundary encoding, W_ij = arc
+ *     length) the all-pairs shortest path lengths, +inf if unreachable, path lengths >= 0x7FFF
+ *     saturating to +inf (G6).  I (+) W = W with a zero diagonal.  Host buffers, caller-owned.
+ *     Errors: MP_ERR_DOMAIN (NULL, N <= 0, D overlapping W), MP_ERR_RANGE, MP_ERR_RESOURCE,
+ *     MP_ERR_CUDA. */
+mp_status minplus_mul_strided_batched_device(const uint16_t *dA, int64_t lda, int64_t strideA,
+                                             const uint16_t *dB, int64_t ldb, int64_t strideB,
+                                             uint16_t *dC, int64_t ldc, int64_t strideC, int64_t M,
+                                             int64_t K, int64_t N, int64_t batch, void *stream);
+mp_status minplus_closure(const uint16_t *W, int64_t N, uint16_t *D, int32_t *squarings_out);
+
 /* ----------------------------------------------------------------------------------------
  * a3-a5  Power sequence until it is quasi-periodic
  * ------------------------------------------------------------------------------------- */

@@ -31,7 +31,8 @@ EXPORTS = [
     "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
     "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_gamma2_formula", "mp_gamma2_record",
-    "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal",
+    "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal", "minplus_mul_strided_batched_device",
+    "minplus_closure",
 ]
 
 
@@ -103,6 +104,8 @@ def _load() -> ctypes.CDLL:
         "mp_set_options": ([i32, i64], i32),
         "mp_set_grouping": ([i32], i32),
         "mp_set_symmetry": ([ctypes.c_void_p, i64], i32),
+        "minplus_mul_strided_batched_device": ([P, i64, i64, P, i64, i64, P, i64, i64, i64, i64, i64, i64, P], i32),
+        "minplus_closure": ([P, i64, P, ctypes.c_void_p], i32),
         "mp_set_word_symmetry": ([i32], i32),
         "mp_word_reversal": ([i32, ctypes.c_void_p, i64], i32),
         "mp_gamma2_formula": ([P, P], i32),
@@ -174,6 +177,40 @@ def minplus_mul_device(A, B, C=None, stream=None):
         _check(lib.minplus_mul_device(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
                                       C.data_ptr(), C.stride(0), M, K, N, stream.cuda_stream))
     return C
+
+
+def minplus_mul_batched_device(A, B, C=None, stream=None):
+    """C[b] = A[b] (x) B[b] for 3-D torch CUDA tensors (batch, rows, cols), 16-bit storage,
+    row-major matrices (stride(2) == 1); one library call (strided batch)."""
+    import torch
+    for t in (A, B):
+        if not t.is_cuda or t.element_size() != 2 or t.dim() != 3 or t.stride(2) != 1:
+            raise MinplusError(1, "expected 3-D 16-bit CUDA tensors with contiguous rows")
+    nb, M, K = A.shape
+    nb2, K2, N = B.shape
+    if nb != nb2 or K != K2:
+        raise MinplusError(1, f"shape mismatch {tuple(A.shape)} x {tuple(B.shape)}")
+    if C is None:
+        C = torch.empty((nb, M, N), dtype=A.dtype, device=A.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    with torch.cuda.device(A.device):
+        _check(lib.minplus_mul_strided_batched_device(
+            A.data_ptr(), A.stride(1), A.stride(0), B.data_ptr(), B.stride(1), B.stride(0),
+            C.data_ptr(), C.stride(1), C.stride(0), M, K, N, nb, stream.cuda_stream))
+    return C
+
+
+def minplus_closure(W: np.ndarray):
+    """(D, t): D = (I (+) W)^(2^t), the all-pairs shortest path lengths of the weighted
+    adjacency W (uint16, 0xFFFF = no arc), t = the number of squarings."""
+    W = np.ascontiguousarray(W, dtype=np.uint16)
+    if W.ndim != 2 or W.shape[0] != W.shape[1]:
+        raise MinplusError(1, "expected a square matrix")
+    D = np.empty_like(W)
+    t = ctypes.c_int32(0)
+    _check(lib.minplus_closure(W.ctypes.data, W.shape[0], D.ctypes.data, ctypes.byref(t)))
+    return D, t.value
 
 
 # ----------------------------------------------------------------------------- a3-a5

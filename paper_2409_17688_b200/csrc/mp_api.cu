@@ -880,6 +880,56 @@ mp_status minplus_mul_device(const uint16_t *dA, int64_t lda, const uint16_t *dB
     return mul_device_impl(*st, dA, lda, dB, ldb, dC, ldc, M, K, N, (cudaStream_t)stream);
 }
 
+mp_status minplus_mul_strided_batched_device(const uint16_t *dA, int64_t lda, int64_t strideA, const uint16_t *dB,
+                                             int64_t ldb, int64_t strideB, uint16_t *dC, int64_t ldc, int64_t strideC,
+                                             int64_t M, int64_t K, int64_t N, int64_t batch, void *stream)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!dA || !dB || !dC || M <= 0 || K <= 0 || N <= 0 || batch <= 0 || lda < K || ldb < N || ldc < N ||
+        strideA < 0 || strideB < 0 || strideC < 0)
+        return fail(MP_ERR_DOMAIN, "minplus_mul_strided_batched_device: NULL pointer, non-positive dimension, "
+                                   "ld < cols or negative stride");
+    const size_t cspan = span_bytes(M, N, ldc);
+    if (batch > 1 && (size_t)strideC * 2 < cspan)
+        return fail(MP_ERR_DOMAIN, "minplus_mul_strided_batched_device: the C matrices overlap (strideC too small)");
+    const size_t ca = (size_t)(batch - 1) * (size_t)strideC * 2 + cspan;
+    if (overlaps(dC, ca, dA, (size_t)(batch - 1) * (size_t)strideA * 2 + span_bytes(M, K, lda)) ||
+        overlaps(dC, ca, dB, (size_t)(batch - 1) * (size_t)strideB * 2 + span_bytes(K, N, ldb)))
+        return fail(MP_ERR_DOMAIN, "minplus_mul_strided_batched_device: C overlaps A or B");
+    int dev = 0;
+    DevState *st = nullptr;
+    TRY(current_device(&dev, &st));
+    for (int64_t b = 0; b < batch; ++b)
+        TRY(mul_device_impl(*st, dA + b * strideA, lda, dB + b * strideB, ldb, dC + b * strideC, ldc, M, K, N,
+                            (cudaStream_t)stream));
+    return MP_OK;
+}
+
+mp_status minplus_closure(const uint16_t *W, int64_t N, uint16_t *D, int32_t *squarings_out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!W || !D || N <= 0) return fail(MP_ERR_DOMAIN, "minplus_closure: NULL pointer or N <= 0");
+    if (overlaps(D, (size_t)N * N * 2, W, (size_t)N * N * 2)) return fail(MP_ERR_DOMAIN, "minplus_closure: D overlaps W");
+    int dev = 0;
+    DevState *st = nullptr;
+    TRY(current_device(&dev, &st));
+    cudaStream_t s = st->stream;
+    TRY(st->stage_a.ensure((size_t)N * N * 2, "closure buffer"));
+    TRY(st->stage_b.ensure((size_t)N * N * 2, "closure buffer"));
+    uint16_t *X = st->stage_a.as<uint16_t>(), *Y = st->stage_b.as<uint16_t>();
+    COPY(X, W, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+    LAUNCH(launch_set_diag_zero(X, N, N, s)); // I (+) W: every vertex reaches itself at cost 0
+    int32_t t = 0;
+    for (int64_t reach = 1; reach < N - 1; reach *= 2, ++t) { // (I + W)^(2^t) covers paths of 2^t arcs
+        TRY(mul_device_impl(*st, X, N, X, N, Y, N, N, N, N, s));
+        std::swap(X, Y);
+    }
+    COPY(D, X, (size_t)N * N * 2, cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (squarings_out) *squarings_out = t;
+    return MP_OK;
+}
+
 mp_status minplus_power_until_periodic(const uint16_t *A, int64_t N, int max_k, mp_periodic_result *out)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);

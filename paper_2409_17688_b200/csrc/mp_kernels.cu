@@ -1674,6 +1674,19 @@ cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int6
     return cudaGetLastError();
 }
 
+// X[i][i] = 0 for i < n (boundary encoding; the identity of the (min,+) semiring on the diagonal)
+__global__ void k_set_diag_zero(uint16_t *__restrict__ X, int64_t ld, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        X[i * ld + i] = 0;
+}
+
+cudaError_t launch_set_diag_zero(uint16_t *X, int64_t ld, int64_t n, cudaStream_t s)
+{
+    k_set_diag_zero<<<grid_for(n, 256), 256, 0, s>>>(X, ld, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
                           int64_t ldd, cudaStream_t s)
 {

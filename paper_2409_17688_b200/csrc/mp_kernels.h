@@ -24,6 +24,8 @@ cudaError_t launch_build_from_words(const WordMask *words, int64_t N, int n, uin
                                     cudaStream_t s);
 cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int64_t w, uint16_t *X1,
                                int64_t ldx, cudaStream_t s);
+// X[i][i] = 0 for i < n.
+cudaError_t launch_set_diag_zero(uint16_t *X, int64_t ld, int64_t n, cudaStream_t s);
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
                           int64_t ldd, cudaStream_t s);
 // Grouped sparse form of A for the SpMM product (see k_spmm in mp_kernels.cu).

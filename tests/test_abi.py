@@ -152,6 +152,17 @@ def test_symmetry_hint_domain_errors():
         _native._check(_native.lib.mp_word_reversal(4, np.zeros(3, dtype=np.int32).ctypes.data, 3))
 
 
+def test_next4_argument_errors():
+    lib = _native.lib
+    a = np.zeros((4, 4), dtype=np.uint16)
+    assert lib.minplus_closure(None, 4, a.ctypes.data, None) == 1
+    assert lib.minplus_closure(a.ctypes.data, 0, a.ctypes.data, None) == 1
+    assert lib.minplus_closure(a.ctypes.data, 4, a.ctypes.data, None) == 1  # D overlaps W
+    assert lib.minplus_mul_strided_batched_device(None, 4, 16, None, 4, 16, None, 4, 16, 4, 4, 4, 2, None) == 1
+    assert lib.minplus_mul_strided_batched_device(a.ctypes.data, 4, 16, a.ctypes.data, 4, 16, 8, 4, 16,
+                                                  4, 4, 4, 0, None) == 1  # batch <= 0
+
+
 def test_argument_errors_before_device():
     with pytest.raises(mp.MinplusError) as e:
         mp.minplus_mul(np.zeros((2, 3)), np.zeros((2, 3)))

@@ -102,6 +102,48 @@ def test_minplus_mul_device_strided(mp, oracle_mod):
     assert np.array_equal(got, oracle_mod.minplus(A, B))
 
 
+# ----------------------------------------------------------------- NEXT-4: batched, closure
+def test_minplus_mul_batched(mp, oracle_mod):
+    """Strided batch: every C_b equals the oracle's product of its own A_b, B_b."""
+    import torch
+    nb, M, K, N = 3, 130, 70, 300
+    As = [synth.transfer_like(M, K, 0.5, salt=900 + b) for b in range(nb)]
+    Bs = [synth.power_like(K, N, salt=910 + b) for b in range(nb)]
+    dA = torch.from_numpy(np.stack(As).view(np.int16)).cuda()
+    dB = torch.from_numpy(np.stack(Bs).view(np.int16)).cuda()
+    dC = mp.minplus_mul_batched_device(dA, dB)
+    torch.cuda.synchronize()
+    got = dC.cpu().numpy().view(np.uint16)
+    for b in range(nb):
+        assert np.array_equal(got[b], oracle_mod.minplus(As[b], Bs[b])), b
+
+
+@pytest.mark.parametrize("N,density", [(1, 0.5), (2, 0.5), (96, 0.04), (700, 0.01)])
+def test_minplus_closure_all_pairs_shortest_paths(mp, oracle_mod, N, density):
+    """(I + W)^(2^t) on the GPU equals scipy's Dijkstra all-pairs shortest paths (an
+    independent library) and, for small N, the oracle's repeated squaring."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import shortest_path
+    g = synth.rng(synth.SEED, 70 + N)
+    W = np.full((N, N), INF, dtype=np.uint16)
+    mask = g.random((N, N)) < density
+    W[mask] = g.integers(0, 40, size=int(mask.sum()))
+    D, t = mp.minplus_closure(W)
+    assert 2 ** t >= N - 1
+    Wz = W.copy()
+    np.fill_diagonal(Wz, 0)
+    dense = np.where(Wz == INF, 0.0, np.where(Wz == 0, 1e-12, Wz.astype(float)))
+    np.fill_diagonal(dense, 0.0)
+    ref = shortest_path(csr_matrix(dense), method="D")
+    expect = np.where(np.isinf(ref), INF, np.rint(ref)).astype(np.uint16)
+    assert np.array_equal(D, expect)
+    if N <= 96:
+        X = Wz
+        for _ in range(t):
+            X = oracle_mod.minplus(X, X)
+        assert np.array_equal(D, X)
+
+
 # ------------------------------------------------------------------- power sequences
 @pytest.mark.parametrize("kernel", ["tiles", "spmm", "spmm-greedy"])
 @pytest.mark.parametrize("n", range(2, 10))
