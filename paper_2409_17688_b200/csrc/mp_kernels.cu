@@ -594,7 +594,10 @@ struct AccWords { // straight from the word masks (A(D_n) without materialising 
 // gives the same product; this one only lowers the issued steps and the staged X rows
 // (DESIGN.md "Row grouping").
 // ---------------------------------------------------------------------------------------
-constexpr int kGrpWin = 256; // 512 gave 1 % fewer staged X rows at twice the pass-2 time
+#ifndef MP_GRP_WIN
+#define MP_GRP_WIN 256
+#endif
+constexpr int kGrpWin = MP_GRP_WIN; // rows per grouping window (also pass 2's CTA size)
 constexpr int kRefThreads = 128;
 constexpr int kRefRows = 32; // pass 3 refines 32-row blocks of a tile into groups of kG
 constexpr int kRefGroups = kRefRows / kG;
