@@ -1,7 +1,7 @@
 # round-1 final measurement sweep (after the row grouping, 4-row-group SpMM, symmetry)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-T=r1w
+T=${1:-r1w}
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
 timeout 900 python bench.py > gpurun_out/${T}_bench_default.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_bench_default.log
 timeout 600 python bench.py --impl reference > gpurun_out/${T}_bench_reference.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_bench_reference.log
