@@ -176,6 +176,7 @@ struct PowerRun {
     bool bits_ok = false;
     std::vector<int32_t> sigma, gcol, loc; // loc[g] = local column of domain column g (cap path)
     DBuf dsig, dgcol, dloc; // dloc[g] = local column of global column g, or -1
+    DBuf drw;               // row weights s(2i), then s(2 sigma i) (symmetric statistics)
     int64_t cols_rep = 0;
     const uint16_t *a_src = nullptr; // matrix sources: A (boundary encoding; the caller's buffer or
     int64_t a_ld = 0;                // stage_raw), valid for the duration of the run
@@ -475,6 +476,8 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         TRY(R.dsig.ensure((size_t)N * 4, "symmetry"));
         TRY(R.dgcol.ensure(std::max<size_t>(R.gcol.size(), 1) * 4, "column list"));
         COPY(R.dsig.p, R.sigma.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s);
+        TRY(R.drw.ensure((size_t)N * 16, "row weights"));
+        LAUNCH(launch_row_weights(N, R.dsig.as<int32_t>(), R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, s));
         if (!R.gcol.empty())
             COPY(R.dgcol.p, R.gcol.data(), R.gcol.size() * 4, cudaMemcpyHostToDevice, s);
     } else {
@@ -670,7 +673,8 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             }
             if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s)); // stats start
             if (R.sym)
-                LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.w,
+                LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(),
+                                        R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
                                         reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
             else

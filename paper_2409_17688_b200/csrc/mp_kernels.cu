@@ -1509,8 +1509,8 @@ cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, i
 // entry (r, r) of the full matrix equals (sigma r, sigma r), which some local column holds).
 __global__ void __launch_bounds__(256)
     k_stats_sym(const uint16_t *__restrict__ X, int64_t ld, int64_t N, const int32_t *__restrict__ gcol,
-                const int32_t *__restrict__ sigma, int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum,
-                unsigned long long *__restrict__ out_min)
+                const int32_t *__restrict__ sigma, const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm,
+                int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
 {
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
@@ -1570,7 +1570,7 @@ __global__ void __launch_bounds__(256)
                     rm += bm[e] * x;
                 }
             }
-            h += mix64(2 * (uint64_t)i) * rs + mix64(2 * (uint64_t)si) * rm;
+            h += rw[i] * rs + rwm[i] * rm; // row weights s(2i), s(2 sigma i), precomputed
             if (i >= g[0] && i <= glast) { // the diagonal entry (i, i), if this slice holds it
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
@@ -1628,12 +1628,30 @@ __global__ void __launch_bounds__(256)
 }
 
 cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
-                             int64_t w, unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s)
+                             const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
+                             unsigned long long *out_min, cudaStream_t s)
 {
     const int64_t gx = std::max<int64_t>(1, (w + kStCols - 1) / kStCols);
     const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t)num_sms() * 8 / gx));
     const int64_t rpb = (N + gy - 1) / gy;
-    k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(X, ld, N, gcol, sigma, w, rpb, out_sum, out_min);
+    k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb, out_sum,
+                                                                 out_min);
+    return cudaGetLastError();
+}
+
+// rw[i] = s(2i), rwm[i] = s(2 sigma i): the row weights of the fingerprint (once per run)
+__global__ void k_row_weights(int64_t N, const int32_t *__restrict__ sigma, uint64_t *__restrict__ rw,
+                              uint64_t *__restrict__ rwm)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        rw[i] = mix64(2 * (uint64_t)i);
+        rwm[i] = mix64(2 * (uint64_t)sigma[i]);
+    }
+}
+
+cudaError_t launch_row_weights(int64_t N, const int32_t *sigma, uint64_t *rw, uint64_t *rwm, cudaStream_t s)
+{
+    k_row_weights<<<grid_for(N, 256), 256, 0, s>>>(N, sigma, rw, rwm);
     return cudaGetLastError();
 }
 

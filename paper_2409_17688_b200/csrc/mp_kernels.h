@@ -73,8 +73,12 @@ cudaError_t launch_x1_csr(const int64_t *off, const int32_t *idx, int64_t N, con
 cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, const int32_t *gcol, int64_t w,
                                uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s);
 // Statistics of the full matrix from its columns gcol[0..w) under the symmetry sigma.
+// rw / rwm: the row weights of launch_row_weights.
 cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
-                             int64_t w, unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s);
+                             const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
+                             unsigned long long *out_min, cudaStream_t s);
+// rw[i] = s(2i), rwm[i] = s(2 sigma i) for i < N.
+cudaError_t launch_row_weights(int64_t N, const int32_t *sigma, uint64_t *rw, uint64_t *rwm, cudaStream_t s);
 // Range check of a row-major A (flag set if an entry lies in (0x7FFE, 0xFFFF)) and, if occ is
 // not null, the occupancy of its 128 x 32 tiles (occ zeroed by the caller).
 // If sigma is not null, sym_flag is set when some finite A_ij != A_(sigma i, sigma j).
