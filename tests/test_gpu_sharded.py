@@ -219,10 +219,15 @@ def test_dist_torch_nccl_world1(oracle_mod):
     try:
         mp.dist_set_torch()
         A = oracle_mod.transition_matrix(6)
-        g = mp.minplus_power_until_periodic(A)
         o = oracle_mod.power_until_periodic(A)
-        assert (g.mu, g.lam, g.offset) == (o.mu, o.lam, o.offset)
-        assert g.fingerprint == o.fingerprint and g.diag_min == o.diag_min
+        for sym in (False, True):
+            mp.set_symmetry(mp.word_reversal(6) if sym else None)
+            try:
+                g = mp.minplus_power_until_periodic(A)
+            finally:
+                mp.set_symmetry(None)
+            assert (g.mu, g.lam, g.offset) == (o.mu, o.lam, o.offset)
+            assert g.fingerprint == o.fingerprint and g.diag_min == o.diag_min
     finally:
         mp.dist_set(0, 1, None)
         dist.destroy_process_group()
