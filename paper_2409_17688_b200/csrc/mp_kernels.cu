@@ -470,19 +470,19 @@ __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, i
 // ---------------------------------------------------------------------------------------
 // a3, sparse form (NEXT-1 ii, exact): grouped (min,+) SpMM.
 //
-// Rows of A are taken in groups of kG = 8.  A group "entry" is an inner index l at which at
-// least one of its 8 rows has a finite A_il; it carries the 8 values {a, a} (+inf for rows
-// without an arc).  A CTA owns kSpRows = 32 rows (4 groups) x kSpCols = 512 columns.  The
-// union U_t of its groups' l indices, in increasing order, is cut into chunks of kSpChunk =
-// 16; per chunk the CTA stages the 16 rows X[l, cols] (16 KB) and the chunk's entries
-// (grouped by group) in shared memory with cp.async.  Warp j owns group j over all 512
-// columns (8 packed pairs per lane): per entry two broadcast LDS.128 of the values, two
-// LDS.128 of X and 64 VIADDMNMX.U16x2 (8 rows x 8 pairs), so the shared-memory and loop
-// instructions per DPX are half those of a 4-pair layout.  The groups' entry counts per
-// chunk differ, so a warp may wait at the chunk barrier; 4 CTAs (16 warps) per SM cover it.
-// Issued steps = 8 * entries * ld; every skipped term is an all-+inf one, so the result is
-// the same product.
-// Entry layout (3 x uint4): {a0..a3}, {a4..a7}, {s * kSpRowBytes, 0, 0, 0}, s = row in the chunk.
+// Rows of A are taken in groups of kG = 4 (the slot -> row map of the row grouping below).  A
+// group "entry" is an inner index l at which at least one of the group's rows has a finite
+// A_il; it carries the kG values {a, a} (+inf for rows without an arc) and l's X row offset in
+// its chunk: a 32-byte record {a0..a3}, {s * kSpRowBytes, 0, 0, 0}.  A CTA owns kSpRows = 32
+// rows (8 groups) x kSpCols = 512 columns.  The union U_t of its groups' l indices, in
+// increasing order, is cut into chunks of kSpChunk = 16; per chunk the CTA stages the 16 rows
+// X[l, cols] (16 KB), the chunk's entries (grouped by group) and its entry offsets in one
+// stage of a kSpStages-deep ring, filled by a producer warp with bulk copies and mbarriers.
+// Consumer warp j owns group j over all 512 columns (8 packed column pairs per lane): per
+// entry one broadcast LDS.128 of the values, one LDS of the row offset, two LDS.128 of X and
+// 32 VIADDMNMX.U16x2 (4 rows x 8 pairs).  Issued steps = kG * entries * ld; every skipped term
+// is an all-+inf one, so the result is the same product.  (kG = 8 builds too: 48-byte
+// records, 4 consumer warps; DESIGN.md section 5 compares them.)
 // ---------------------------------------------------------------------------------------
 #ifndef MP_SP_G
 #define MP_SP_G 4
