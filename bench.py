@@ -64,6 +64,57 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- clocks
+class NvmlClockSampler:
+    """SM clock and clock-event reasons read through NVML every 5 ms in a thread during the
+    timed region (enough samples even for the millisecond-long small-n runs); falls back to
+    the nvidia-smi sampler below if NVML is unavailable."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, cuda_index: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        import torch
+        p = torch.cuda.get_device_properties(cuda_index)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.sm, self.reasons, self.run = [], set(), False
+
+    def _loop(self):
+        nv = self.nv
+        while self.run:
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) \
+                    if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001 - a failed sample is skipped, not fatal
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        self.run = True
+        self.thread = threading.Thread(target=self._loop, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        self.run = False
+        self.thread.join(timeout=2)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 5 ms"}
+
+
+def make_clock_sampler(cuda_index: int):
+    try:
+        return NvmlClockSampler(cuda_index)
+    except Exception:  # noqa: BLE001 - no NVML: nvidia-smi
+        return ClockSampler(cuda_index)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 500 ms during the timed region (a
     tighter period measurably slowed the many short synchronisations of the small-n runs)."""
@@ -233,7 +284,7 @@ def run_mine(args):
         res = mp.minplus_power_until_periodic_device(dA)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = make_clock_sampler(local)
     clocks.start()
     barrier()
     torch.cuda.synchronize()
