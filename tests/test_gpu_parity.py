@@ -345,19 +345,29 @@ def test_gamma2_cylinder_small(mp, oracle_mod):
             assert mp.gamma2_cylinder(n, m) == o.gamma2(m), (n, m)
 
 
+@pytest.mark.parametrize("sym", [False, True])
 @pytest.mark.parametrize("n", [10, 11, 12])
-def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n):
-    """Full-size cases: sampled rows of every power up to k_last against the oracle's
-    vector-matrix recurrence; (mu, lambda, b) against Table 5; gamma_2 against the paper's
-    closed formula (Table 7 with the exception rows) for every m <= 200 and m = 1000."""
+def test_large_n_sampled_rows_and_tables(mp, oracle_mod, n, sym):
+    """Full-size cases, in the configuration bench.py times (sym: the word-reversal symmetry,
+    only the domain columns computed) and on all columns: sampled rows of every power up to
+    k_last against the oracle's vector-matrix recurrence; (mu, lambda, b) against Table 5;
+    gamma_2 against the paper's closed formula (Table 7 with the exception rows) for every
+    m <= 200 and m = 1000."""
     t5 = {int(r[0]): tuple(map(int, r[1:])) for r in golden("table5_recurrence.txt")}
     A = mp.build_transition_matrix(n)
     N = A.shape[0]
-    g = mp.minplus_power_until_periodic(A)
+    mp.set_symmetry(mp.word_reversal(n) if sym else None)
+    try:
+        g = mp.minplus_power_until_periodic(A)
+        rows = [0, 1, N // 3, N // 2 + 7, N - 1]
+        got = mp.minplus_power_rows(A, rows, g.k_last)
+    finally:
+        mp.set_symmetry(None)
     assert (g.mu, g.lam, g.offset) == t5[n]
     assert g.dense_from == 3
-    rows = [0, 1, N // 3, N // 2 + 7, N - 1]
-    got = mp.minplus_power_rows(A, rows, g.k_last)
+    if sym:  # every full-matrix fingerprint and diagonal minimum equals the all-columns run's
+        full = mp.minplus_power_until_periodic(A)
+        assert g.fingerprint == full.fingerprint and g.diag_min == full.diag_min
     for r_i, r in enumerate(rows):
         ref = oracle_mod.power_rows(A, r, g.k_last)
         assert np.array_equal(got[:, r_i, :], ref), r
