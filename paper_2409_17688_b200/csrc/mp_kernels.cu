@@ -474,13 +474,14 @@ __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, i
 // group "entry" is an inner index l at which at least one of the group's rows has a finite
 // A_il; it carries the kG values {a, a} (+inf for rows without an arc) and l's X row offset in
 // its chunk: a 32-byte record {a0..a3}, {s * kSpRowBytes, 0, 0, 0}.  A CTA owns kSpRows = 32
-// rows (8 groups) x kSpCols = 512 columns.  The union U_t of its groups' l indices, in
+// rows (8 groups) x kSpCols = 1024 columns.  The union U_t of its groups' l indices, in
 // increasing order, is cut into chunks of kSpChunk = 16; per chunk the CTA stages the 16 rows
-// X[l, cols] (16 KB), the chunk's entries (grouped by group) and its entry offsets in one
+// X[l, cols] (32 KB), the chunk's entries (grouped by group) and its entry offsets in one
 // stage of a kSpStages-deep ring, filled by a producer warp with bulk copies and mbarriers.
-// Consumer warp j owns group j over all 512 columns (8 packed column pairs per lane): per
-// entry one broadcast LDS.128 of the values, one LDS of the row offset, two LDS.128 of X and
-// 32 VIADDMNMX.U16x2 (4 rows x 8 pairs).  Issued steps = kG * entries * ld; every skipped term
+// Consumer warp j owns group j over all 1024 columns (16 packed column pairs per lane): per
+// entry one broadcast LDS.128 of the values, one LDS of the row offset, four LDS.128 of X and
+// 64 VIADDMNMX.U16x2 (4 rows x 16 pairs).  (MP_SP_PPL = 8 builds the 512-column CTA: two
+// LDS.128 and 32 DPX per entry, 3 CTAs per SM.)  Issued steps = kG * entries * ld; every skipped term
 // is an all-+inf one, so the result is the same product.  (kG = 8 builds too: 48-byte
 // records, 4 consumer warps; DESIGN.md section 5 compares them.)
 // ---------------------------------------------------------------------------------------
@@ -489,6 +490,7 @@ __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, i
 #endif
 constexpr int kG = MP_SP_G;             // rows per group (4 or 8)
 static_assert(kG == 4 || kG == 8, "group size");
+static_assert(kG * MP_SP_PPL <= 64, "accumulators: kG x pairs per lane registers");
 constexpr int kEntU4 = kG / 4 + 1;      // entry record: kG values {a, a}, then {row offset, 0, 0, 0}
 constexpr int kEntBytes = 16 * kEntU4;
 #ifndef MP_SP_ROWS
@@ -503,10 +505,13 @@ constexpr int kSpGroups = kSpRows / kG;
 #define MP_SP_STAGES 3
 #endif
 #ifndef MP_SP_CTAS
-#define MP_SP_CTAS 3
+#define MP_SP_CTAS (MP_SP_PPL == 16 ? 2 : 3) // resident CTAs per SM (registers: 96 / 72 per thread)
 #endif
 constexpr int kSpChunk = MP_SP_CHUNK;
-constexpr int kSpCols = 512;            // columns per CTA (32 lanes x 16)
+constexpr int kSpPpl = MP_SP_PPL;       // packed column pairs per lane (8 or 16)
+static_assert(kSpPpl == 8 || kSpPpl == 16, "pairs per lane");
+constexpr int kSpXq = kSpPpl / 4;       // LDS.128 of X per entry and lane (one per 256 columns)
+constexpr int kSpCols = 64 * kSpPpl;    // columns per CTA (32 lanes x 2 * kSpPpl)
 constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
 #ifndef MP_SP_GPW
 #define MP_SP_GPW 1
@@ -1219,22 +1224,21 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
 }
 
 // acc[r][p] = min(a_r + x_p, acc[r][p]) for the kG rows of a group entry and this lane's
-// eight packed column pairs.
-__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][8], const uint4 (&av)[kG / 4], const uint4 &x0,
-                                          const uint4 &x1)
+// kSpPpl packed column pairs (x[q] = the lane's 8 columns of the q-th 256-column slice).
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][kSpPpl], const uint4 (&av)[kG / 4],
+                                          const uint4 (&x)[kSpXq])
 {
 #pragma unroll
     for (int r = 0; r < kG; ++r) {
         const uint4 &q = av[r / 4];
         const uint32_t a = (r % 4 == 0) ? q.x : (r % 4 == 1) ? q.y : (r % 4 == 2) ? q.z : q.w;
-        acc[r][0] = __viaddmin_u16x2(a, x0.x, acc[r][0]);
-        acc[r][1] = __viaddmin_u16x2(a, x0.y, acc[r][1]);
-        acc[r][2] = __viaddmin_u16x2(a, x0.z, acc[r][2]);
-        acc[r][3] = __viaddmin_u16x2(a, x0.w, acc[r][3]);
-        acc[r][4] = __viaddmin_u16x2(a, x1.x, acc[r][4]);
-        acc[r][5] = __viaddmin_u16x2(a, x1.y, acc[r][5]);
-        acc[r][6] = __viaddmin_u16x2(a, x1.z, acc[r][6]);
-        acc[r][7] = __viaddmin_u16x2(a, x1.w, acc[r][7]);
+#pragma unroll
+        for (int h = 0; h < kSpXq; ++h) {
+            acc[r][4 * h + 0] = __viaddmin_u16x2(a, x[h].x, acc[r][4 * h + 0]);
+            acc[r][4 * h + 1] = __viaddmin_u16x2(a, x[h].y, acc[r][4 * h + 1]);
+            acc[r][4 * h + 2] = __viaddmin_u16x2(a, x[h].z, acc[r][4 * h + 2]);
+            acc[r][4 * h + 3] = __viaddmin_u16x2(a, x[h].w, acc[r][4 * h + 3]);
+        }
     }
 }
 
@@ -1342,8 +1346,8 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
             for (int r = 0; r < nrows; ++r) {
                 const int32_t lr = __shfl_sync(0xFFFFFFFFu, l, r);
                 const uint16_t *src = X + (int64_t)lr * ldx + col0;
-                cp_async16(sX + r * kSpRowBytes + lane * 16, src + lane * 8);
-                cp_async16(sX + r * kSpRowBytes + 512 + lane * 16, src + 256 + lane * 8);
+#pragma unroll
+                for (int h = 0; h < kSpXq; ++h) cp_async16(sX + r * kSpRowBytes + 512 * h + lane * 16, src + 256 * h + lane * 8);
             }
             for (uint32_t q = lane; q < ebytes / 16; q += 32) cp_async16(sX + XB + q * 16, E + kEntU4 * e0 + q);
             if (lane < kSpOffBytes / 16) cp_async16(sX + XB + EB + lane * 16, eoff + gc * kSpGroups + 2 * lane);
@@ -1361,13 +1365,13 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
     }
 
     // consumer warp: groups warp * kSpGpw + gg
-    uint32_t acc[kSpGpw][kG][8];
+    uint32_t acc[kSpGpw][kG][kSpPpl];
 #pragma unroll
     for (int gg = 0; gg < kSpGpw; ++gg)
 #pragma unroll
         for (int r = 0; r < kG; ++r)
 #pragma unroll
-            for (int p = 0; p < 8; ++p) acc[gg][r][p] = 0xFFFFFFFFu;
+            for (int p = 0; p < kSpPpl; ++p) acc[gg][r][p] = 0xFFFFFFFFu;
     for (int c = 0; c < nch; ++c) {
         const int st = c % kSpStages;
         mbar_wait(bar_full + st * 8, (c / kSpStages) & 1);
@@ -1385,35 +1389,38 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
 #pragma unroll
             for (int u = 0; u < kG / 4; ++u) v[u] = Es[kEntU4 * q + u];
         };
+        auto xrow = [&](uint32_t off, uint4(&x)[kSpXq]) {
+#pragma unroll
+            for (int h = 0; h < kSpXq; ++h) x[h] = lds128(Xl + off + 512 * h);
+        };
 #pragma unroll
         for (int gg = 0; gg < kSpGpw; ++gg) {
         const int jg = warp * kSpGpw + gg;
         const int e0 = (int)(Bs[jg] - eb), e1 = (int)(Bs[jg + 1] - eb);
         if (e0 < e1) {
             int e = e0;
-            uint4 pa[kG / 4], pb[kG / 4];
+            uint4 pa[kG / 4], pb[kG / 4], xa[kSpXq], xb[kSpXq];
             vals(e, pa);
             uint32_t s = row(e);
-            uint4 xa0 = lds128(Xl + s), xa1 = lds128(Xl + s + 512);
+            xrow(s, xa);
             s = row(e + 1);
             for (;;) {
                 vals(e + 1, pb);
-                const uint4 xb0 = lds128(Xl + s), xb1 = lds128(Xl + s + 512);
+                xrow(s, xb);
                 s = row(e + 2);
 #if !MP_SP_NOCOMPUTE
-                dpx_group(acc[gg], pa, xa0, xa1);
+                dpx_group(acc[gg], pa, xa);
 #else // diagnostic build: the data path alone (results are not meaningful)
-                acc[gg][0][0] ^= pa[0].x ^ xa0.x ^ xa1.y;
+                acc[gg][0][0] ^= pa[0].x ^ xa[0].x ^ xa[kSpXq - 1].y;
 #endif
                 if (e + 1 >= e1) break;
                 vals(e + 2, pa);
-                xa0 = lds128(Xl + s);
-                xa1 = lds128(Xl + s + 512);
+                xrow(s, xa);
                 s = row(e + 3);
 #if !MP_SP_NOCOMPUTE
-                dpx_group(acc[gg], pb, xb0, xb1);
+                dpx_group(acc[gg], pb, xb);
 #else
-                acc[gg][0][1] ^= pb[0].x ^ xb0.x ^ xb1.y;
+                acc[gg][0][1] ^= pb[0].x ^ xb[0].x ^ xb[kSpXq - 1].y;
 #endif
                 e += 2;
                 if (e >= e1) break;
@@ -1433,17 +1440,15 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
         const int64_t slot = (int64_t)t * kSpRows + kG * (warp * kSpGpw + gg) + r;
         const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
         uint16_t *crow = C + i * ldc + col0 + 8 * lane;
-        uint4 v;
-        v.x = __vminu2(acc[gg][r][0], 0x7FFF7FFFu);
-        v.y = __vminu2(acc[gg][r][1], 0x7FFF7FFFu);
-        v.z = __vminu2(acc[gg][r][2], 0x7FFF7FFFu);
-        v.w = __vminu2(acc[gg][r][3], 0x7FFF7FFFu);
-        *reinterpret_cast<uint4 *>(crow) = v;
-        v.x = __vminu2(acc[gg][r][4], 0x7FFF7FFFu);
-        v.y = __vminu2(acc[gg][r][5], 0x7FFF7FFFu);
-        v.z = __vminu2(acc[gg][r][6], 0x7FFF7FFFu);
-        v.w = __vminu2(acc[gg][r][7], 0x7FFF7FFFu);
-        *reinterpret_cast<uint4 *>(crow + 256) = v;
+#pragma unroll
+        for (int h = 0; h < kSpXq; ++h) {
+            uint4 v;
+            v.x = __vminu2(acc[gg][r][4 * h + 0], 0x7FFF7FFFu);
+            v.y = __vminu2(acc[gg][r][4 * h + 1], 0x7FFF7FFFu);
+            v.z = __vminu2(acc[gg][r][4 * h + 2], 0x7FFF7FFFu);
+            v.w = __vminu2(acc[gg][r][4 * h + 3], 0x7FFF7FFFu);
+            *reinterpret_cast<uint4 *>(crow + 256 * h) = v;
+        }
     }
 }
 

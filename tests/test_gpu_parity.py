@@ -230,7 +230,8 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     recompute path for evicted A^j: n = 7 has lambda = 18, so the partner of the first repeat
     has left the ring."""
     A = mp.build_transition_matrix(7)
-    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 511) // 512) * 512) * 2  # Np x ld x 2 B
+    # Np x ld x 2 B; ld = the column pitch kLdAlign = 1024 of the default build (mp_internal.h)
+    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 1023) // 1024) * 1024) * 2
     mp.set_options("auto", device_budget_bytes=19 * slot)  # 19 - 2 reserved = 17 ring slots
     try:
         g = mp.minplus_power_until_periodic(A)
