@@ -305,6 +305,7 @@ def run_mine(args):
         prod_ms += p["product_ms"]
         prod_launches += p["product_launches"]
         kernel_used = p["kernel"]
+        spmm_cols = p["spmm_cols"]
         dense += p["dense_steps"]
         issued += p["issued_steps"]
         setup_ms = p["setup_ms"]
@@ -386,7 +387,7 @@ def run_mine(args):
         "data": "synthetic: deterministic transfer matrix A(D_n) built on the host (no randomness, no datasets)",
         "config": dict(workload_config(args.n, N, world), products_per_step=products,
                        mu_lambda_b=[res.mu, res.lam, res.offset], gamma2_m1000=res.gamma2(1000),
-                       kernel=args.kernel,
+                       kernel=args.kernel, spmm_cta_cols=spmm_cols or None,
                        symmetry="none" if args.no_symmetry else "word reversal (columns g <= sigma g computed)"),
         "seconds_to_gamma2": ms / args.steps / 1e3,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,

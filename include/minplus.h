@@ -270,6 +270,7 @@ typedef struct {
     int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
     int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,
                                  2 grouped SpMM                                              */
+    int32_t spmm_cols;        /* SpMM CTA width used (512 or 1024 columns; 0 if kernel != 2) */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
 
@@ -304,11 +305,18 @@ mp_status mp_set_symmetry(const int32_t *sigma, int64_t N);
 mp_status mp_set_word_symmetry(int on);
 mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N);
 
-/* Row grouping of the SpMM kernel (sparsity 2): 0 = groups of 8 consecutive rows; 1 = rows
- * grouped greedily by support overlap in windows of 512 rows (fewer issued steps, same
+/* Row grouping of the SpMM kernel (sparsity 2): 0 = groups of 4 consecutive rows; 1 = rows
+ * grouped greedily by support overlap in windows of 256 rows (fewer issued steps, same
  * product); -1 = automatic (the default: greedy from N >= 8192).
  * Process-wide.  Errors: MP_ERR_DOMAIN. */
 mp_status mp_set_grouping(int mode);
+
+/* CTA width of the SpMM kernel (sparsity 2), in columns: 512 (8 packed column pairs per
+ * lane, 3 CTAs per SM), 1024 (16 pairs per lane, 2 CTAs per SM: half the per-entry
+ * overhead, half the CTAs), or 0 = automatic (the default: 1024 when the grid still has at
+ * least 24 CTAs per SM, i.e. n >= 11 for A(D_n)).  The power pitch ld is padded to a
+ * multiple of the width.  Same product either way.  Process-wide.  Errors: MP_ERR_DOMAIN. */
+mp_status mp_set_spmm_width(int cols);
 
 #ifdef __cplusplus
 }

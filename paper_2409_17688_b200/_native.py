@@ -30,7 +30,7 @@ EXPORTS = [
     "gamma2_cylinder",
     "mp_gamma2_readoff", "mp_dist_set", "mp_shard_range", "mp_fingerprint_unit",
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
-    "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_gamma2_formula", "mp_gamma2_record",
+    "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_set_spmm_width", "mp_gamma2_formula", "mp_gamma2_record",
     "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal", "minplus_mul_strided_batched_device",
     "minplus_closure",
 ]
@@ -67,7 +67,7 @@ class _Profile(ctypes.Structure):
                 ("dense_steps", ctypes.c_double), ("issued_steps", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("setup_ms", ctypes.c_double), ("stats_ms", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
-                ("kernel", ctypes.c_int32)]
+                ("kernel", ctypes.c_int32), ("spmm_cols", ctypes.c_int32)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
@@ -103,6 +103,7 @@ def _load() -> ctypes.CDLL:
         "mp_last_profile": ([P], i32),
         "mp_set_options": ([i32, i64], i32),
         "mp_set_grouping": ([i32], i32),
+        "mp_set_spmm_width": ([i32], i32),
         "mp_set_symmetry": ([ctypes.c_void_p, i64], i32),
         "minplus_mul_strided_batched_device": ([P, i64, i64, P, i64, i64, P, i64, i64, i64, i64, i64, i64, P], i32),
         "minplus_closure": ([P, i64, P, ctypes.c_void_p], i32),
@@ -372,7 +373,7 @@ def last_profile() -> dict:
     return {"product_ms": p.product_ms, "product_launches": p.product_launches,
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
             "setup_ms": p.setup_ms, "stats_ms": p.stats_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
-            "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?")}
+            "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols}
 
 
 SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}
@@ -412,6 +413,11 @@ GROUPING = {"auto": -1, "consecutive": 0, "greedy": 1}
 def set_grouping(mode: str = "auto") -> None:
     """Row grouping of the SpMM kernel: "auto" | "consecutive" | "greedy" (same product)."""
     _check(lib.mp_set_grouping(GROUPING[mode]))
+
+
+def set_spmm_width(cols: int = 0) -> None:
+    """CTA width of the SpMM kernel: 0 (automatic), 512 or 1024 columns (same product)."""
+    _check(lib.mp_set_spmm_width(int(cols)))
 
 
 def version() -> str:

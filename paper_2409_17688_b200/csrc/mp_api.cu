@@ -167,6 +167,7 @@ struct DBuf {
 // do not pay cudaMalloc/cudaFree; released by mp_shutdown().
 struct PowerRun {
     int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
+    int spmm_cols = 512; // k_spmm CTA width of this run (spmm_cols); ld is a multiple of it
     DBuf at2, words, tmp0, tmp1, ktp, kti, occ, stats, flag, stage_raw;
     bool has_at2 = false; // only the tile kernels stage AT2; SpMM reads A or the word masks
     // symmetry: local column jj holds global column gcol[jj] (g <= sigma g) and stands for g and
@@ -329,6 +330,7 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
 {
     R.sp_next = 0;
     R.sp = SparseWork();
+    R.sp.cols = R.spmm_cols; // entry row offsets are bytes of a staged X row of this width
     int64_t launches = 0;
     const bool group = g_opts.grouping == 1 || (g_opts.grouping < 0 && R.N >= kGroupMinN);
     const cudaError_t e =
@@ -358,7 +360,7 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
         sa.eoff = R.sp.eoff;
         sa.E = R.sp.E;
         sa.rows = R.sp.rows;
-        LAUNCH(launch_spmm(sa, X, R.ld, C, R.ld, R.Np, R.ld, s));
+        LAUNCH(launch_spmm(sa, R.sp.cols, X, R.ld, C, R.ld, R.Np, R.ld, s));
         return MP_OK;
     }
     LAUNCH(launch_minplus(R.at2.as<uint32_t>(), R.Np, X, R.ld, C, R.ld, R.Np, R.ld, R.Np,
@@ -491,7 +493,8 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         }
         R.cols_rep = R.w;
     }
-    R.ld = pad_cols(R.w);
+    R.spmm_cols = spmm_cols(R.Np, R.w); // the SpMM CTA width of this run
+    R.ld = round_up(R.w > 0 ? R.w : 1, R.spmm_cols);
     {
         std::vector<int32_t> dl((size_t)N, -1);
         if (R.sym)
@@ -792,6 +795,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.h2d_bytes = g_h2d.load() - h2d0;
     g_prof.d2h_bytes = g_d2h.load() - d2h0;
     g_prof.kernel = R.spmm ? 2 : (R.sparse ? 1 : 0);
+    g_prof.spmm_cols = R.spmm ? R.sp.cols : 0;
 
     if (!found) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
     *out = res;
@@ -1203,6 +1207,15 @@ mp_status mp_set_grouping(int mode)
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (mode < -1 || mode > 1) return fail(MP_ERR_DOMAIN, "mp_set_grouping: mode %d outside [-1, 1]", mode);
     g_opts.grouping = mode;
+    return MP_OK;
+}
+
+mp_status mp_set_spmm_width(int cols)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (cols != 0 && cols != 512 && cols != 1024)
+        return fail(MP_ERR_DOMAIN, "mp_set_spmm_width: %d is not 0, 512 or 1024", cols);
+    g_spmm_width = cols;
     return MP_OK;
 }
 

@@ -32,11 +32,9 @@ constexpr int kThreads = 256; // 8 warps, 8x16 outputs per thread
 // Pitches: every device matrix is padded with +inf to these multiples.
 MP_HD int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 MP_HD int64_t pad_rows(int64_t n) { return round_up(n > 0 ? n : 1, kBM); } // multiple of kBM and kBK
-#ifndef MP_SP_PPL
-#define MP_SP_PPL 16 // packed column pairs per lane in k_spmm (16: 1024-column CTAs, default; 8: 512)
-#endif
-// column pitch of every device power: a multiple of both CTA widths (k_minplus 256, k_spmm 64 * MP_SP_PPL)
-constexpr int kLdAlign = MP_SP_PPL * 64 > 512 ? MP_SP_PPL * 64 : 512;
+// column pitch of every device power: a multiple of both CTA widths (k_minplus 256, k_spmm 512);
+// a run on the 1024-column SpMM CTA pads its powers to 1024 (spmm_cols in mp_kernels.h)
+constexpr int kLdAlign = 512;
 MP_HD int64_t pad_cols(int64_t n) { return round_up(n > 0 ? n : 1, kLdAlign); }
 
 // ---------------------------------------------------------------------------------------

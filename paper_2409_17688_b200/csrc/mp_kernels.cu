@@ -473,15 +473,15 @@ __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, i
 // Rows of A are taken in groups of kG = 4 (the slot -> row map of the row grouping below).  A
 // group "entry" is an inner index l at which at least one of the group's rows has a finite
 // A_il; it carries the kG values {a, a} (+inf for rows without an arc) and l's X row offset in
-// its chunk: a 32-byte record {a0..a3}, {s * kSpRowBytes, 0, 0, 0}.  A CTA owns kSpRows = 32
-// rows (8 groups) x kSpCols = 1024 columns.  The union U_t of its groups' l indices, in
-// increasing order, is cut into chunks of kSpChunk = 16; per chunk the CTA stages the 16 rows
-// X[l, cols] (32 KB), the chunk's entries (grouped by group) and its entry offsets in one
+// its chunk: a 32-byte record {a0..a3}, {s * row bytes, 0, 0, 0} (built for one CTA width).  A CTA owns kSpRows = 32 rows
+// (8 groups) x 64 * PPL columns, PPL = 16 or 8 packed column pairs per lane (SpCfg; the run
+// picks the width with spmm_cols).  The union U_t of its groups' l indices, in increasing
+// order, is cut into chunks of kSpChunk = 16; per chunk the CTA stages the 16 rows X[l, cols]
+// (32 KB at PPL = 16), the chunk's entries (grouped by group) and its entry offsets in one
 // stage of a kSpStages-deep ring, filled by a producer warp with bulk copies and mbarriers.
-// Consumer warp j owns group j over all 1024 columns (16 packed column pairs per lane): per
-// entry one broadcast LDS.128 of the values, one LDS of the row offset, four LDS.128 of X and
-// 64 VIADDMNMX.U16x2 (4 rows x 16 pairs).  (MP_SP_PPL = 8 builds the 512-column CTA: two
-// LDS.128 and 32 DPX per entry, 3 CTAs per SM.)  Issued steps = kG * entries * ld; every skipped term
+// Consumer warp j owns group j over all the CTA's columns (PPL pairs per lane): per entry one
+// broadcast LDS.128 of the values, one LDS of the row offset, PPL / 4 LDS.128 of X and 4 * PPL
+// VIADDMNMX.U16x2 (64 at PPL = 16).  Issued steps = kG * entries * ld; every skipped term
 // is an all-+inf one, so the result is the same product.  (kG = 8 builds too: 48-byte
 // records, 4 consumer warps; DESIGN.md section 5 compares them.)
 // ---------------------------------------------------------------------------------------
@@ -490,7 +490,6 @@ __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, i
 #endif
 constexpr int kG = MP_SP_G;             // rows per group (4 or 8)
 static_assert(kG == 4 || kG == 8, "group size");
-static_assert(kG * MP_SP_PPL <= 64, "accumulators: kG x pairs per lane registers");
 constexpr int kEntU4 = kG / 4 + 1;      // entry record: kG values {a, a}, then {row offset, 0, 0, 0}
 constexpr int kEntBytes = 16 * kEntU4;
 #ifndef MP_SP_ROWS
@@ -504,15 +503,7 @@ constexpr int kSpGroups = kSpRows / kG;
 #ifndef MP_SP_STAGES
 #define MP_SP_STAGES 3
 #endif
-#ifndef MP_SP_CTAS
-#define MP_SP_CTAS (MP_SP_PPL == 16 ? 2 : 3) // resident CTAs per SM (registers: 96 / 72 per thread)
-#endif
 constexpr int kSpChunk = MP_SP_CHUNK;
-constexpr int kSpPpl = MP_SP_PPL;       // packed column pairs per lane (8 or 16)
-static_assert(kSpPpl == 8 || kSpPpl == 16, "pairs per lane");
-constexpr int kSpXq = kSpPpl / 4;       // LDS.128 of X per entry and lane (one per 256 columns)
-constexpr int kSpCols = 64 * kSpPpl;    // columns per CTA (32 lanes x 2 * kSpPpl)
-constexpr int kSpRowBytes = kSpCols * 2; // one staged X row, in bytes
 #ifndef MP_SP_GPW
 #define MP_SP_GPW 1
 #endif
@@ -524,9 +515,22 @@ constexpr int kSpStages = MP_SP_STAGES;
 // offsets (copied as a 16-byte multiple).
 constexpr int kSpEntryBytes = (kSpGroups * kSpChunk + 3) * kEntBytes;
 constexpr int kSpOffBytes = ((kSpGroups + 1) * 8 + 15) / 16 * 16;
-constexpr int kSpStageBytes = kSpChunk * kSpRowBytes + kSpEntryBytes + kSpOffBytes;
-constexpr int kSpSmemBytes = kSpStages * kSpStageBytes + 2 * kSpStages * 8;
-constexpr int kSpCtasPerSm = MP_SP_CTAS;
+// The CTA width: PPL packed column pairs per lane (8: 512 columns, 3 CTAs per SM at 72
+// registers; 16: 1024 columns, 2 CTAs per SM at 96 registers; spmm_cols picks one per run).
+template <int PPL> struct SpCfg {
+    static_assert(PPL == 8 || PPL == 16, "pairs per lane");
+    static_assert(kG * PPL <= 64, "accumulators: kG x pairs per lane registers");
+    static constexpr int Xq = PPL / 4;          // LDS.128 of X per entry and lane (one per 256 columns)
+    static constexpr int Cols = 64 * PPL;       // columns per CTA (32 lanes x 2 * PPL)
+    static constexpr int RowBytes = Cols * 2;   // one staged X row, in bytes
+#ifdef MP_SP_CTAS
+    static constexpr int Ctas = MP_SP_CTAS;
+#else
+    static constexpr int Ctas = PPL == 16 ? 2 : 3;
+#endif
+    static constexpr int StageBytes = kSpChunk * RowBytes + kSpEntryBytes + kSpOffBytes;
+    static constexpr int SmemBytes = kSpStages * StageBytes + 2 * kSpStages * 8;
+};
 #ifndef MP_SP_LDGSTS
 #define MP_SP_LDGSTS 0
 #endif
@@ -540,7 +544,6 @@ constexpr int kSpCtasPerSm = MP_SP_CTAS;
 #define MP_SP_BAND 1000000
 #endif
 constexpr int kSpBand = MP_SP_BAND; // column blocks per band of the CTA order
-static_assert(kSpCols % kLdAlign == 0 || kLdAlign % kSpCols == 0, "shard pitch must tile the SpMM CTA width");
 
 // How the sparse-form builders read A: the kG duplicated values (device encoding) of the rows
 // in group slots kG*g .. kG*g + kG-1 at column l; finite(i, l) for i, l < N.  `rows` (may be
@@ -1094,7 +1097,8 @@ template <class Acc>
 __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t Np,
                                 const int32_t *__restrict__ L, const int64_t *__restrict__ tptr,
                                 const int64_t *__restrict__ tch, const int32_t *__restrict__ chunk_tile, int64_t TC,
-                                int32_t *__restrict__ ecnt, const int64_t *__restrict__ eoff, uint4 *__restrict__ E)
+                                int32_t *__restrict__ ecnt, const int64_t *__restrict__ eoff, uint4 *__restrict__ E,
+                                uint32_t row_bytes)
 {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < TC * kSpGroups;
          q += (int64_t)gridDim.x * blockDim.x) {
@@ -1119,7 +1123,7 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
 #pragma unroll
                 for (int u = 0; u < kG / 4; ++u)
                     E[kEntU4 * e + u] = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-                E[kEntU4 * e + kG / 4] = make_uint4((unsigned)s * (unsigned)kSpRowBytes, 0u, 0u, 0u); // X row (bytes)
+                E[kEntU4 * e + kG / 4] = make_uint4((unsigned)s * row_bytes, 0u, 0u, 0u); // X row (bytes)
                 ++e;
             }
             ++cnt;
@@ -1224,16 +1228,16 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
 }
 
 // acc[r][p] = min(a_r + x_p, acc[r][p]) for the kG rows of a group entry and this lane's
-// kSpPpl packed column pairs (x[q] = the lane's 8 columns of the q-th 256-column slice).
-__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][kSpPpl], const uint4 (&av)[kG / 4],
-                                          const uint4 (&x)[kSpXq])
+// PPL packed column pairs (x[h] = the lane's 8 columns of the h-th 256-column slice).
+template <int PPL>
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][PPL], const uint4 (&av)[kG / 4], const uint4 (&x)[PPL / 4])
 {
 #pragma unroll
     for (int r = 0; r < kG; ++r) {
         const uint4 &q = av[r / 4];
         const uint32_t a = (r % 4 == 0) ? q.x : (r % 4 == 1) ? q.y : (r % 4 == 2) ? q.z : q.w;
 #pragma unroll
-        for (int h = 0; h < kSpXq; ++h) {
+        for (int h = 0; h < PPL / 4; ++h) {
             acc[r][4 * h + 0] = __viaddmin_u16x2(a, x[h].x, acc[r][4 * h + 0]);
             acc[r][4 * h + 1] = __viaddmin_u16x2(a, x[h].y, acc[r][4 * h + 1]);
             acc[r][4 * h + 2] = __viaddmin_u16x2(a, x[h].z, acc[r][4 * h + 2]);
@@ -1267,19 +1271,22 @@ __device__ __forceinline__ int64_t ldg_nc_s64(const int64_t *p)
 }
 
 // Warp-specialised ring (kSpStages deep): the producer warp fills a stage with bulk copies
-// (16 X rows of 1 KB, the chunk's entries, its entry offsets) that complete on the stage's
+// (16 X rows of 2 or 1 KB, the chunk's entries, its entry offsets) that complete on the stage's
 // "full" mbarrier; consumer warp j waits on it, walks group j's entries, and arrives on the
 // stage's "empty" mbarrier.  No CTA-wide barrier in the loop, so a warp whose group has few
 // entries in one chunk runs ahead into the next (up to the ring depth) instead of idling.
-__global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
+template <int PPL>
+__global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
     k_spmm(const int32_t *__restrict__ L, const int64_t *__restrict__ tptr, const int64_t *__restrict__ tch,
            const int64_t *__restrict__ eoff, const uint4 *__restrict__ E, const uint16_t *__restrict__ X, int64_t ldx,
            uint16_t *__restrict__ C, int64_t ldc, const int32_t *__restrict__ rowmap)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int XB = kSpChunk * kSpRowBytes; // 16 KB of X rows
-    constexpr int EB = kSpEntryBytes;           // up to 64 entries + 3 look-ahead records
-    constexpr int STAGE = kSpStageBytes;
+    using Cfg = SpCfg<PPL>;
+    constexpr int kSpRowBytes = Cfg::RowBytes, kSpCols = Cfg::Cols, kSpXq = Cfg::Xq;
+    constexpr int XB = kSpChunk * kSpRowBytes; // 16 (32) KB of X rows
+    constexpr int EB = kSpEntryBytes;           // up to 128 entries + 3 look-ahead records
+    constexpr int STAGE = Cfg::StageBytes;
     static_assert(STAGE % 16 == 0 && XB % 16 == 0 && EB % 16 == 0, "stage layout");
     // CTA order: bands of kSpBand column blocks, row tiles fastest within a band, so the CTAs
     // resident at once read X rows of few column blocks (L2 reuse of the staged X rows).
@@ -1365,13 +1372,13 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
     }
 
     // consumer warp: groups warp * kSpGpw + gg
-    uint32_t acc[kSpGpw][kG][kSpPpl];
+    uint32_t acc[kSpGpw][kG][PPL];
 #pragma unroll
     for (int gg = 0; gg < kSpGpw; ++gg)
 #pragma unroll
         for (int r = 0; r < kG; ++r)
 #pragma unroll
-            for (int p = 0; p < kSpPpl; ++p) acc[gg][r][p] = 0xFFFFFFFFu;
+            for (int p = 0; p < PPL; ++p) acc[gg][r][p] = 0xFFFFFFFFu;
     for (int c = 0; c < nch; ++c) {
         const int st = c % kSpStages;
         mbar_wait(bar_full + st * 8, (c / kSpStages) & 1);
@@ -1409,7 +1416,7 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
                 xrow(s, xb);
                 s = row(e + 2);
 #if !MP_SP_NOCOMPUTE
-                dpx_group(acc[gg], pa, xa);
+                dpx_group<PPL>(acc[gg], pa, xa);
 #else // diagnostic build: the data path alone (results are not meaningful)
                 acc[gg][0][0] ^= pa[0].x ^ xa[0].x ^ xa[kSpXq - 1].y;
 #endif
@@ -1418,7 +1425,7 @@ __global__ void __launch_bounds__(kSpThreads, kSpCtasPerSm)
                 xrow(s, xa);
                 s = row(e + 3);
 #if !MP_SP_NOCOMPUTE
-                dpx_group(acc[gg], pb, xb);
+                dpx_group<PPL>(acc[gg], pb, xb);
 #else
                 acc[gg][0][1] ^= pb[0].x ^ xb[0].x ^ xb[kSpXq - 1].y;
 #endif
@@ -1720,18 +1727,43 @@ cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_
     return cudaGetLastError();
 }
 
-cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
-                        int64_t ncols_p, cudaStream_t s)
+int g_spmm_width = 0;
+
+int spmm_cols(int64_t Np, int64_t w)
 {
+#ifdef MP_SP_WIDTH
+    if (MP_SP_WIDTH) return MP_SP_WIDTH;
+#endif
+    if (g_spmm_width) return g_spmm_width;
+    // 1024-column CTAs halve the per-entry overhead but also the CTA count: keep them for
+    // grids of at least 24 CTAs per SM (n = 11, 12), 512 columns below (n <= 10)
+    const int64_t ctas = (Np / kSpRows) * ((w + 1023) / 1024);
+    return ctas >= 24LL * num_sms() ? 1024 : 512;
+}
+
+template <int PPL>
+static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
+                                 int64_t Mp, int64_t ncols_p, cudaStream_t s)
+{
+    using Cfg = SpCfg<PPL>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_spmm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(k_spmm<PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)(Mp / kSpRows), (unsigned)(ncols_p / kSpCols)); // x: tiles, y: column blocks (remapped)
-    k_spmm<<<grid, kSpThreads, kSpSmemBytes, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
+    if (ncols_p % Cfg::Cols || ldx % 8 || ldc % 8) return cudaErrorInvalidValue;
+    dim3 grid((unsigned)(Mp / kSpRows), (unsigned)(ncols_p / Cfg::Cols)); // x: tiles, y: column blocks (remapped)
+    k_spmm<PPL><<<grid, kSpThreads, Cfg::SmemBytes, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
     return cudaGetLastError();
+}
+
+cudaError_t launch_spmm(const SparseA &sa, int cols, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
+                        int64_t Mp, int64_t ncols_p, cudaStream_t s)
+{
+    if (cols == 1024) return launch_spmm_t<16>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
+    if (cols == 512) return launch_spmm_t<8>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
+    return cudaErrorInvalidValue;
 }
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
@@ -1864,7 +1896,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
 #endif
     SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
-        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], w.ecnt, nullptr, nullptr)));
+        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], w.ecnt, nullptr, nullptr, 0u)));
     SP_SCAN(w.ecnt, tot[1] * kSpGroups, w.eoff);
     int64_t ne = 0;
     if ((e = cudaMemcpyAsync(&ne, w.eoff + tot[1] * kSpGroups, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
@@ -1873,7 +1905,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     SP_ALLOC(w.E, (size_t)std::max<int64_t>(ne, 1) * kEntBytes);
     w.group_rows = kG;
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
-        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E)));
+        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E, (uint32_t)(2 * w.cols))));
 #undef SP_SCAN
 #undef SP_LAUNCH
 #undef SP_ALLOC

@@ -48,10 +48,15 @@ struct SparseWork {
     int64_t *off = nullptr;   // row lists of A's support (grouped path): CSR offsets ...
     int32_t *idx = nullptr;   // ... and column indices
     int group_rows = 0;      // rows per group: issued steps = entries * group_rows * ld
+    int cols = 512;          // set by the caller: the k_spmm CTA width the entries are built for
     int64_t total_union = 0, total_chunks = 0, entries = 0;
 };
-cudaError_t launch_spmm(const SparseA &sa, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc, int64_t Mp,
-                        int64_t ncols_p, cudaStream_t s);
+// cols = the CTA width, 512 or 1024 (ncols_p must be a multiple of it): spmm_cols(Np, w) picks
+// it per run from the grid size (or the mp_set_spmm_width override in g_spmm_width).
+int spmm_cols(int64_t Np, int64_t w);
+extern int g_spmm_width;
+cudaError_t launch_spmm(const SparseA &sa, int cols, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
+                        int64_t Mp, int64_t ncols_p, cudaStream_t s);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
 // pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).

@@ -48,6 +48,16 @@ def test_count_words_table1(oracle_mod):
     assert e.value.status == 1
 
 
+def test_spmm_width_option():
+    """The SpMM CTA width accepts 0 (automatic), 512 and 1024 columns, nothing else."""
+    for cols in (512, 1024, 0):
+        mp.set_spmm_width(cols)
+    for cols in (-1, 256, 768, 2048):
+        with pytest.raises(mp.MinplusError) as e:
+            mp.set_spmm_width(cols)
+        assert e.value.status == 1
+
+
 @pytest.mark.parametrize("n", range(2, 11))
 def test_transition_matrix_equals_oracle(oracle_mod, n):
     """a1 parity: the bitmask/DFS construction equals the letter-by-letter oracle bit for bit."""

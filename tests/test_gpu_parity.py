@@ -181,6 +181,48 @@ def test_power_rows_full_matrices(mp, oracle_mod, sparse):
         reset_kernel(mp)
 
 
+@pytest.mark.parametrize("width", [512, 1024])
+@pytest.mark.parametrize("sym", [False, True])
+def test_spmm_width_full_matrices(mp, oracle_mod, width, sym):
+    """Both SpMM CTA widths (512 / 1024 columns; automatic choice picks 1024 only for n >= 11)
+    forced on n = 7 (N = 558: one ragged 1024-column block): every entry of A^1..A^10."""
+    A = mp.build_transition_matrix(7)
+    use_kernel(mp, "spmm-greedy")
+    mp.set_spmm_width(width)
+    if sym:
+        mp.set_symmetry(mp.word_reversal(7))
+    try:
+        got = mp.minplus_power_rows(A, np.arange(A.shape[0]), 10)
+    finally:
+        mp.set_symmetry(None)
+        mp.set_spmm_width(0)
+        reset_kernel(mp)
+    X = A.copy()
+    for k in range(1, 11):
+        if k > 1:
+            X = oracle_mod.minplus(A, X)
+        assert np.array_equal(got[k - 1], X), k
+
+
+@pytest.mark.parametrize("width", [512, 1024])
+@pytest.mark.parametrize("n", [2, 5, 8, 9])
+def test_spmm_width_power_until_periodic(mp, oracle_mod, n, width):
+    """Whole runs with each forced SpMM width (symmetric columns, greedy rows) = the oracle."""
+    A = mp.build_transition_matrix(n)
+    use_kernel(mp, "spmm-greedy")
+    mp.set_spmm_width(width)
+    mp.set_symmetry(mp.word_reversal(n))
+    try:
+        g = mp.minplus_power_until_periodic(A)
+    finally:
+        mp.set_symmetry(None)
+        mp.set_spmm_width(0)
+        reset_kernel(mp)
+    o = oracle_mod.power_until_periodic(A)
+    assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+    assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
+
+
 @pytest.mark.parametrize("kernel", ["dense", "tiles", "spmm", "spmm-greedy", "auto"])
 @pytest.mark.parametrize("seed", range(5))
 def test_power_until_periodic_random(mp, oracle_mod, seed, kernel):
@@ -230,8 +272,8 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     recompute path for evicted A^j: n = 7 has lambda = 18, so the partner of the first repeat
     has left the ring."""
     A = mp.build_transition_matrix(7)
-    # Np x ld x 2 B; ld = the column pitch kLdAlign = 1024 of the default build (mp_internal.h)
-    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 1023) // 1024) * 1024) * 2
+    # Np x ld x 2 B; ld = a multiple of the SpMM CTA width, 512 at this size (spmm_cols)
+    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 511) // 512) * 512) * 2
     mp.set_options("auto", device_budget_bytes=19 * slot)  # 19 - 2 reserved = 17 ring slots
     try:
         g = mp.minplus_power_until_periodic(A)
