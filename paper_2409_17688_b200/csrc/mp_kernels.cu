@@ -26,6 +26,14 @@ template <int N> __device__ __forceinline__ void cp_async_wait()
 {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
+// 16-byte shared load from a 32-bit shared-window address (lane base + uniform offset folds
+// into one LDS [R + UR]).
+__device__ __forceinline__ uint4 lds128(uint32_t addr)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 
 // mbarrier + bulk-copy (TMA, non-tensor) helpers
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
@@ -192,10 +200,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 // row weight.
 // ---------------------------------------------------------------------------------------
 constexpr int kStCols = 256 * 8;
+#ifndef MP_ST_DEPTH
+#define MP_ST_DEPTH 8
+#endif
+#if MP_ST_DEPTH > 1
+constexpr int kStDepth = MP_ST_DEPTH; // depth of k_stats_sym's per-thread cp.async ring (4 KB per row)
+#else
 #ifndef MP_ST_ROWS
 #define MP_ST_ROWS 4
 #endif
-constexpr int kStRows = MP_ST_ROWS; // rows whose loads k_stats_sym keeps in flight
+constexpr int kStRows = MP_ST_ROWS; // rows whose loads k_stats_sym keeps in flight (MP_ST_DEPTH <= 1)
+#endif
+// d = a * b + c with a 64-bit addend: one IMAD.WIDE.U32 (the C++ form compiles to two)
+__device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c)
+{
+    uint64_t d;
+    asm("mad.wide.u32 %0, %1, %2, %3;\n" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
+}
 __device__ __forceinline__ uint4 ldg_nc_v4(const void *p)
 {
     uint4 v;
@@ -1246,14 +1268,6 @@ __device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][PPL], const uint4 
     }
 }
 
-// 16-byte shared load from a 32-bit shared-window address (lane base + uniform offset folds
-// into one LDS [R + UR]).
-__device__ __forceinline__ uint4 lds128(uint32_t addr)
-{
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
 
 // Non-coherent global loads kept at their program position (asm volatile), so a prefetch
 // issued one chunk ahead is not sunk next to its use by the scheduler.
@@ -1530,41 +1544,67 @@ __global__ void __launch_bounds__(256)
     const int64_t i0 = (int64_t)blockIdx.y * rpb, i1 = min(N, i0 + rpb);
     if (j0 < w) {
         const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
-        uint64_t b[8], bm[8];
+        // column weights split in 32-bit halves: b * x = b.lo * x + (b.hi * x) << 32 (mod 2^64),
+        // so an entry costs one IMAD.WIDE.U32 (64-bit accumulate) and one 32-bit IMAD per sum
+        uint32_t blo[8], bhi[8], bmlo[8], bmhi[8];
         int32_t g[8], m[8];
         unsigned two = 0; // bit e: column e stands for two global columns
         int32_t mmin = INT32_MAX;
+        int emin = 0;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             g[e] = e < nc ? gcol[j0 + e] : 0;
             m[e] = e < nc ? sigma[g[e]] : 0;
-            b[e] = e < nc ? mix64(2 * (uint64_t)g[e] + 1) : 0;
-            bm[e] = (e < nc && m[e] != g[e]) ? mix64(2 * (uint64_t)m[e] + 1) : 0;
+            const uint64_t b = e < nc ? mix64(2 * (uint64_t)g[e] + 1) : 0;
+            const uint64_t bm = (e < nc && m[e] != g[e]) ? mix64(2 * (uint64_t)m[e] + 1) : 0;
+            blo[e] = (uint32_t)b;
+            bhi[e] = (uint32_t)(b >> 32);
+            bmlo[e] = (uint32_t)bm;
+            bmhi[e] = (uint32_t)(bm >> 32);
             if (e < nc && m[e] != g[e]) two |= 1u << e;
-            if (e < nc) mmin = min(mmin, m[e]);
+            if (e < nc && m[e] < mmin) {
+                mmin = m[e];
+                emin = e;
+            }
         }
         const int32_t glast = g[nc - 1];
+        // Keys of the all-finite rows: among (i, g_e) the smallest is at the first such row and
+        // e = 0 (gcol ascending); among the mirrors (sigma i, m_e) at the row of smallest
+        // sigma i and e = emin.  Tracked here, folded into ref after the loop.
+        int64_t fi = INT64_MAX, fsi = INT64_MAX;
+        uint32_t fx = 0, fxm = 0;
         auto row = [&](int64_t i, int64_t si, const uint4 &v) {
             const uint32_t words[4] = {v.x, v.y, v.z, v.w};
-            const uint32_t anyinf = __vcmpeq2(v.x, 0x7FFF7FFFu) | __vcmpeq2(v.y, 0x7FFF7FFFu) |
-                                    __vcmpeq2(v.z, 0x7FFF7FFFu) | __vcmpeq2(v.w, 0x7FFF7FFFu);
-            uint64_t rs = 0, rm = 0;
+            // any half >= 0x7FFF (the device +inf; stored values never exceed it)
+            const uint32_t anyinf = (((v.x & 0x7FFF7FFFu) + 0x00010001u) | ((v.y & 0x7FFF7FFFu) + 0x00010001u) |
+                                     ((v.z & 0x7FFF7FFFu) + 0x00010001u) | ((v.w & 0x7FFF7FFFu) + 0x00010001u) |
+                                     v.x | v.y | v.z | v.w) & 0x80008000u;
+            uint64_t rs, rm;
             if (nc == 8 && !anyinf) {
-                // the smallest key among (i, g_e) is e = 0 (gcol ascending); among the mirrors
-                // (sigma i, m_e) the one at the smallest m_e
-                unsigned long long key = ((uint64_t)(i * N + g[0]) << 16) | (v.x & 0xFFFFu);
-                if (key < ref) ref = key;
-                uint32_t xm = 0;
+                uint64_t lo = 0, lom = 0;
+                uint32_t hi = 0, him = 0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                    rs += b[e] * x;
-                    rm += bm[e] * x;
-                    if (m[e] == mmin) xm = x;
+                    lo = madw(blo[e], x, lo);
+                    hi += bhi[e] * x;
+                    lom = madw(bmlo[e], x, lom);
+                    him += bmhi[e] * x;
                 }
-                key = ((uint64_t)(si * N + mmin) << 16) | xm;
-                if (key < ref) ref = key;
+                rs = lo + ((uint64_t)hi << 32);
+                rm = lom + ((uint64_t)him << 32);
+                if (i < fi) {
+                    fi = i;
+                    fx = v.x & 0xFFFFu;
+                }
+                if (si < fsi) {
+                    fsi = si;
+                    const uint32_t wd = (emin & 4) ? ((emin & 2) ? v.w : v.z) : ((emin & 2) ? v.y : v.x);
+                    fxm = (wd >> ((emin & 1) * 16)) & 0xFFFFu;
+                }
             } else {
+                rs = 0;
+                rm = 0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     if (e >= nc) break;
@@ -1578,8 +1618,10 @@ __global__ void __launch_bounds__(256)
                         key = ((uint64_t)(si * N + m[e]) << 16) | x;
                         if (key < ref) ref = key;
                     }
-                    rs += b[e] * x;
-                    rm += bm[e] * x;
+                    const uint64_t b = ((uint64_t)bhi[e] << 32) | blo[e];
+                    const uint64_t bm = ((uint64_t)bmhi[e] << 32) | bmlo[e];
+                    rs += b * x;
+                    rm += bm * x;
                 }
             }
             h += rw[i] * rs + rwm[i] * rm; // row weights s(2i), s(2 sigma i), precomputed
@@ -1592,6 +1634,30 @@ __global__ void __launch_bounds__(256)
                     }
             }
         };
+#if MP_ST_DEPTH > 1
+        // kStDepth-deep per-thread cp.async ring: the thread's 16 bytes of rows i .. i+D-1 are
+        // in flight while row i is hashed (no block barrier: each thread reads only its slots)
+        __shared__ __align__(16) uint4 ring[kStDepth][256];
+        const uint32_t slot0 = smem_addr(&ring[0][threadIdx.x]);
+        const uint16_t *src = X + i0 * ld + j0;
+#pragma unroll
+        for (int d = 0; d < kStDepth - 1; ++d) {
+            if (i0 + d < i1) cp_async16(slot0 + d * 4096, src + d * ld);
+            cp_async_commit();
+        }
+        int slot = 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const int64_t ip = i + kStDepth - 1; // refills the slot row i - 1 used
+            const int pslot = slot == 0 ? kStDepth - 1 : slot - 1;
+            if (ip < i1) cp_async16(slot0 + pslot * 4096, X + ip * ld + j0);
+            cp_async_commit();
+            const int32_t si = sigma[i];
+            cp_async_wait<kStDepth - 1>();
+            row(i, si, lds128(slot0 + slot * 4096));
+            slot = slot == kStDepth - 1 ? 0 : slot + 1;
+        }
+        cp_async_wait<0>();
+#else
         int64_t i = i0;
         for (; i + kStRows <= i1; i += kStRows) { // kStRows rows' loads in flight
             uint4 vv[kStRows];
@@ -1605,6 +1671,13 @@ __global__ void __launch_bounds__(256)
             for (int u = 0; u < kStRows; ++u) row(i + u, ss[u], vv[u]);
         }
         for (; i < i1; ++i) row(i, sigma[i], *reinterpret_cast<const uint4 *>(X + i * ld + j0));
+#endif
+        if (fi != INT64_MAX) {
+            unsigned long long key = ((uint64_t)(fi * N + g[0]) << 16) | fx;
+            if (key < ref) ref = key;
+            key = ((uint64_t)(fsi * N + mmin) << 16) | fxm;
+            if (key < ref) ref = key;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
