@@ -13,6 +13,7 @@ torch.cuda.set_device(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 A = mp.build_transition_matrix(n)
 mp.set_symmetry(mp.word_reversal(n))
+mp.set_spmm_width(int(os.environ.get("MP_WIDTH", "0")))  # 0: the automatic choice
 for _ in range(2):
     mp.minplus_power_rows(A, np.array([0]), 6)
 p = mp.last_profile()

@@ -270,7 +270,7 @@ typedef struct {
     int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
     int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,
                                  2 grouped SpMM                                              */
-    int32_t spmm_cols;        /* SpMM CTA width used (512 or 1024 columns; 0 if kernel != 2) */
+    int32_t spmm_cols;        /* SpMM CTA width used (256, 512 or 1024 columns; 0 if kernel != 2) */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
 
@@ -311,10 +311,11 @@ mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N);
  * Process-wide.  Errors: MP_ERR_DOMAIN. */
 mp_status mp_set_grouping(int mode);
 
-/* CTA width of the SpMM kernel (sparsity 2), in columns: 512 (8 packed column pairs per
- * lane, 3 CTAs per SM), 1024 (16 pairs per lane, 2 CTAs per SM: half the per-entry
+/* CTA width of the SpMM kernel (sparsity 2), in columns: 256 (4 packed column pairs per
+ * lane, 3 CTAs per SM), 512 (8 pairs per lane, 3 CTAs per SM), 1024 (16 pairs per lane, 2 CTAs per SM: half the per-entry
  * overhead, half the CTAs), or 0 = automatic (the default: 1024 when the grid still has at
- * least 24 CTAs per SM, i.e. n >= 11 for A(D_n)).  The power pitch ld is padded to a
+ * least 24 CTAs per SM, i.e. n >= 11 for A(D_n); else 512 when that grid has at least 8 CTAs
+ * per SM, i.e. n = 10; else 256).  The power pitch ld is padded to a
  * multiple of the width.  Same product either way.  Process-wide.  Errors: MP_ERR_DOMAIN. */
 mp_status mp_set_spmm_width(int cols);
 

@@ -416,7 +416,7 @@ def set_grouping(mode: str = "auto") -> None:
 
 
 def set_spmm_width(cols: int = 0) -> None:
-    """CTA width of the SpMM kernel: 0 (automatic), 512 or 1024 columns (same product)."""
+    """CTA width of the SpMM kernel: 0 (automatic), 256, 512 or 1024 columns (same product)."""
     _check(lib.mp_set_spmm_width(int(cols)))
 
 

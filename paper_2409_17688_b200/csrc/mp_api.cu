@@ -1213,8 +1213,8 @@ mp_status mp_set_grouping(int mode)
 mp_status mp_set_spmm_width(int cols)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
-    if (cols != 0 && cols != 512 && cols != 1024)
-        return fail(MP_ERR_DOMAIN, "mp_set_spmm_width: %d is not 0, 512 or 1024", cols);
+    if (cols != 0 && cols != 256 && cols != 512 && cols != 1024)
+        return fail(MP_ERR_DOMAIN, "mp_set_spmm_width: %d is not 0, 256, 512 or 1024", cols);
     g_spmm_width = cols;
     return MP_OK;
 }

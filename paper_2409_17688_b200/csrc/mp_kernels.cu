@@ -537,10 +537,10 @@ constexpr int kSpStages = MP_SP_STAGES;
 // offsets (copied as a 16-byte multiple).
 constexpr int kSpEntryBytes = (kSpGroups * kSpChunk + 3) * kEntBytes;
 constexpr int kSpOffBytes = ((kSpGroups + 1) * 8 + 15) / 16 * 16;
-// The CTA width: PPL packed column pairs per lane (8: 512 columns, 3 CTAs per SM at 72
-// registers; 16: 1024 columns, 2 CTAs per SM at 96 registers; spmm_cols picks one per run).
+// The CTA width: PPL packed column pairs per lane (4: 256 columns, 8: 512 columns, 3 CTAs per
+// SM; 16: 1024 columns, 2 CTAs per SM at 96 registers; spmm_cols picks one per run).
 template <int PPL> struct SpCfg {
-    static_assert(PPL == 8 || PPL == 16, "pairs per lane");
+    static_assert(PPL == 4 || PPL == 8 || PPL == 16, "pairs per lane");
     static_assert(kG * PPL <= 64, "accumulators: kG x pairs per lane registers");
     static constexpr int Xq = PPL / 4;          // LDS.128 of X per entry and lane (one per 256 columns)
     static constexpr int Cols = 64 * PPL;       // columns per CTA (32 lanes x 2 * PPL)
@@ -1809,9 +1809,11 @@ int spmm_cols(int64_t Np, int64_t w)
 #endif
     if (g_spmm_width) return g_spmm_width;
     // 1024-column CTAs halve the per-entry overhead but also the CTA count: keep them for
-    // grids of at least 24 CTAs per SM (n = 11, 12), 512 columns below (n <= 10)
-    const int64_t ctas = (Np / kSpRows) * ((w + 1023) / 1024);
-    return ctas >= 24LL * num_sms() ? 1024 : 512;
+    // grids of at least 24 CTAs per SM (n = 11, 12), 512 columns for at least 8 CTAs per SM at
+    // that width (n = 10), 256 below (n <= 9; n = 9: 0.110 -> 0.089 ms per product)
+    const int64_t tiles = Np / kSpRows;
+    if (tiles * ((w + 1023) / 1024) >= 24LL * num_sms()) return 1024;
+    return tiles * ((w + 511) / 512) >= 8LL * num_sms() ? 512 : 256;
 }
 
 template <int PPL>
@@ -1836,6 +1838,7 @@ cudaError_t launch_spmm(const SparseA &sa, int cols, const uint16_t *X, int64_t 
 {
     if (cols == 1024) return launch_spmm_t<16>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
     if (cols == 512) return launch_spmm_t<8>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
+    if (cols == 256) return launch_spmm_t<4>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
     return cudaErrorInvalidValue;
 }
 

@@ -49,10 +49,10 @@ def test_count_words_table1(oracle_mod):
 
 
 def test_spmm_width_option():
-    """The SpMM CTA width accepts 0 (automatic), 512 and 1024 columns, nothing else."""
-    for cols in (512, 1024, 0):
+    """The SpMM CTA width accepts 0 (automatic), 256, 512 and 1024 columns, nothing else."""
+    for cols in (256, 512, 1024, 0):
         mp.set_spmm_width(cols)
-    for cols in (-1, 256, 768, 2048):
+    for cols in (-1, 128, 768, 2048):
         with pytest.raises(mp.MinplusError) as e:
             mp.set_spmm_width(cols)
         assert e.value.status == 1

@@ -181,10 +181,10 @@ def test_power_rows_full_matrices(mp, oracle_mod, sparse):
         reset_kernel(mp)
 
 
-@pytest.mark.parametrize("width", [512, 1024])
+@pytest.mark.parametrize("width", [256, 512, 1024])
 @pytest.mark.parametrize("sym", [False, True])
 def test_spmm_width_full_matrices(mp, oracle_mod, width, sym):
-    """Both SpMM CTA widths (512 / 1024 columns; automatic choice picks 1024 only for n >= 11)
+    """Every SpMM CTA width (256 / 512 / 1024 columns; the automatic choice: 256 for n <= 9)
     forced on n = 7 (N = 558: one ragged 1024-column block): every entry of A^1..A^10."""
     A = mp.build_transition_matrix(7)
     use_kernel(mp, "spmm-greedy")
@@ -204,7 +204,7 @@ def test_spmm_width_full_matrices(mp, oracle_mod, width, sym):
         assert np.array_equal(got[k - 1], X), k
 
 
-@pytest.mark.parametrize("width", [512, 1024])
+@pytest.mark.parametrize("width", [256, 512, 1024])
 @pytest.mark.parametrize("n", [2, 5, 8, 9])
 def test_spmm_width_power_until_periodic(mp, oracle_mod, n, width):
     """Whole runs with each forced SpMM width (symmetric columns, greedy rows) = the oracle."""
@@ -272,8 +272,8 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     recompute path for evicted A^j: n = 7 has lambda = 18, so the partner of the first repeat
     has left the ring."""
     A = mp.build_transition_matrix(7)
-    # Np x ld x 2 B; ld = a multiple of the SpMM CTA width, 512 at this size (spmm_cols)
-    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 511) // 512) * 512) * 2
+    # Np x ld x 2 B; ld = a multiple of the SpMM CTA width, 256 at this size (spmm_cols)
+    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 255) // 256) * 256) * 2
     mp.set_options("auto", device_budget_bytes=19 * slot)  # 19 - 2 reserved = 17 ring slots
     try:
         g = mp.minplus_power_until_periodic(A)
