@@ -200,6 +200,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // row weight.
 // ---------------------------------------------------------------------------------------
 constexpr int kStCols = 256 * 8;
+#ifndef MP_ST_MIN_ROWS
+#define MP_ST_MIN_ROWS 16
+#endif
+constexpr int64_t kStMinRows = MP_ST_MIN_ROWS; // fewest rows per k_stats_sym block
 #ifndef MP_ST_DEPTH
 #define MP_ST_DEPTH 8
 #endif
@@ -1717,7 +1721,12 @@ cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int
                              unsigned long long *out_min, cudaStream_t s)
 {
     const int64_t gx = std::max<int64_t>(1, (w + kStCols - 1) / kStCols);
-    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t)num_sms() * 8 / gx));
+    // at least kStMinRows rows per block while that still leaves one block per SM: a thread's
+    // setup (16 column weights, gcol and sigma loads) costs about as much as hashing 10 rows
+    // (n = 9: 16 instead of 3 rows per block; n <= 6 keeps one or two rows per block)
+    const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms() * 8 / gx);
+    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>((N + kStMinRows - 1) / kStMinRows,
+                                                                                      std::min<int64_t>(N, num_sms()))));
     const int64_t rpb = (N + gy - 1) / gy;
     k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb, out_sum,
                                                                  out_min);
