@@ -1530,6 +1530,11 @@ cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, i
     return cudaGetLastError();
 }
 
+#ifndef MP_ST_THREADS
+#define MP_ST_THREADS 128
+#endif
+constexpr int kSymThreads = MP_ST_THREADS;    // k_stats_sym block: kSymThreads x 8 columns
+constexpr int kSymCols = kSymThreads * 8;
 // Statistics of a power stored on a column list under a symmetry sigma (an involution with
 // A_(sigma i, sigma j) = A_ij, so every power has X_(sigma i, sigma j) = X_ij): local column jj
 // holds global column g = gcol[jj] (g <= sigma g) and stands for g and its mirror sigma g.
@@ -1537,14 +1542,14 @@ cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, i
 // s(2i) s(2g+1) x + [sigma g != g] s(2 sigma i) s(2 sigma g + 1) x to H, one or two +inf
 // counts, the keys of (i, g) and (sigma i, sigma g), and the diagonal (g, g) (every diagonal
 // entry (r, r) of the full matrix equals (sigma r, sigma r), which some local column holds).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSymThreads)
     k_stats_sym(const uint16_t *__restrict__ X, int64_t ld, int64_t N, const int32_t *__restrict__ gcol,
                 const int32_t *__restrict__ sigma, const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm,
                 int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
 {
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
-    const int64_t j0 = (int64_t)blockIdx.x * kStCols + (int64_t)threadIdx.x * 8;
+    const int64_t j0 = (int64_t)blockIdx.x * kSymCols + (int64_t)threadIdx.x * 8;
     const int64_t i0 = (int64_t)blockIdx.y * rpb, i1 = min(N, i0 + rpb);
     if (j0 < w) {
         const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
@@ -1641,23 +1646,23 @@ __global__ void __launch_bounds__(256)
 #if MP_ST_DEPTH > 1
         // kStDepth-deep per-thread cp.async ring: the thread's 16 bytes of rows i .. i+D-1 are
         // in flight while row i is hashed (no block barrier: each thread reads only its slots)
-        __shared__ __align__(16) uint4 ring[kStDepth][256];
+        __shared__ __align__(16) uint4 ring[kStDepth][kSymThreads];
         const uint32_t slot0 = smem_addr(&ring[0][threadIdx.x]);
         const uint16_t *src = X + i0 * ld + j0;
 #pragma unroll
         for (int d = 0; d < kStDepth - 1; ++d) {
-            if (i0 + d < i1) cp_async16(slot0 + d * 4096, src + d * ld);
+            if (i0 + d < i1) cp_async16(slot0 + d * kSymThreads * 16, src + d * ld);
             cp_async_commit();
         }
         int slot = 0;
         for (int64_t i = i0; i < i1; ++i) {
             const int64_t ip = i + kStDepth - 1; // refills the slot row i - 1 used
             const int pslot = slot == 0 ? kStDepth - 1 : slot - 1;
-            if (ip < i1) cp_async16(slot0 + pslot * 4096, X + ip * ld + j0);
+            if (ip < i1) cp_async16(slot0 + pslot * kSymThreads * 16, X + ip * ld + j0);
             cp_async_commit();
             const int32_t si = sigma[i];
             cp_async_wait<kStDepth - 1>();
-            row(i, si, lds128(slot0 + slot * 4096));
+            row(i, si, lds128(slot0 + slot * kSymThreads * 16));
             slot = slot == kStDepth - 1 ? 0 : slot + 1;
         }
         cp_async_wait<0>();
@@ -1720,15 +1725,15 @@ cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int
                              const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
                              unsigned long long *out_min, cudaStream_t s)
 {
-    const int64_t gx = std::max<int64_t>(1, (w + kStCols - 1) / kStCols);
+    const int64_t gx = std::max<int64_t>(1, (w + kSymCols - 1) / kSymCols);
     // at least kStMinRows rows per block while that still leaves one block per SM: a thread's
     // setup (16 column weights, gcol and sigma loads) costs about as much as hashing 10 rows
     // (n = 9: 16 instead of 3 rows per block; n <= 6 keeps one or two rows per block)
-    const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms() * 8 / gx);
+    const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms() * 8 * (256 / kSymThreads) / gx);
     const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>((N + kStMinRows - 1) / kStMinRows,
                                                                                       std::min<int64_t>(N, num_sms()))));
     const int64_t rpb = (N + gy - 1) / gy;
-    k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb, out_sum,
+    k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), kSymThreads, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb, out_sum,
                                                                  out_min);
     return cudaGetLastError();
 }
