@@ -155,6 +155,21 @@ mp_status minplus_power_until_periodic_device(const uint16_t *dA, int64_t lda, i
 mp_status minplus_power_rows(const uint16_t *A, int64_t N, int kmax, const int64_t *rows, int nrows,
                              uint16_t *out);
 
+/* Parity observer.  While set (fn != NULL), every power run of this process (the matrix
+ * sources, the device source and the words source of gamma2_cylinder / mp_gamma2_record; not
+ * minplus_power_rows) calls fn(ctx, k, power, N) once per power k = 1 .. k_last, in order, on
+ * the calling thread, after A^k and its statistics are computed and before the repeat search
+ * looks at it.  power = the WHOLE N x N matrix A^k (Algorithm 2), row-major,
+ * boundary encoding (MP_INF = +inf), in a library-owned pinned host buffer valid only during
+ * the call; with a symmetry the columns the run does not compute are filled in from their
+ * mirrors.  The run itself is unchanged (same kernels, same ring) apart
+ * from the extra device buffer of 2 N^2 bytes and the copy.  fn returns 0 to continue; any
+ * other value stops the run with MP_ERR_DOMAIN.  fn = NULL clears it.  A run with an observer
+ * and a distributed context of world > 1 fails with MP_ERR_DOMAIN (a rank holds only its
+ * shard).  Process-wide.  Errors: none (always MP_OK). */
+typedef int (*mp_power_observer_fn)(void *ctx, int k, const uint16_t *power, int64_t N);
+mp_status mp_set_power_observer(mp_power_observer_fn fn, void *ctx);
+
 /* ----------------------------------------------------------------------------------------
  * a6  gamma_2(P_n x C_m) (Theorem 2; Theorem 3; solving procedure P:219-222)
  * ------------------------------------------------------------------------------------- */
@@ -216,6 +231,15 @@ mp_status mp_dist_set(int rank, int world, mp_allreduce_fn fn, void *ctx);
  * Errors: MP_ERR_DOMAIN. */
 mp_status mp_shard_range(int64_t N, int world, int rank, int64_t *c0, int64_t *c1);
 
+/* Column plan of the SpMM product for a rank computing w columns of an N x N power (DESIGN.md
+ * section 6): CTA columns of the run's main width (*main_cols: 1024, 512 or 256 by the grid
+ * size, or the mp_set_spmm_width override) and the remainder, rounded up to 64 columns, in up
+ * to three narrower CTA columns of 768 / 512 / 256 / 128 / 64 columns (*tail_cols = their
+ * total; 0 if none), so *ld (the padded width = the pitch of the powers) exceeds w by less
+ * than 64 columns unless a width is forced.  Pure host function
+ * (assumes 148 SMs when no device is present).  Errors: MP_ERR_DOMAIN. */
+mp_status mp_column_plan(int64_t N, int64_t w, int64_t *ld, int32_t *main_cols, int32_t *tail_cols);
+
 /* ----------------------------------------------------------------------------------------
  * Periodicity bookkeeping (pure host functions; exported so the multi-rank logic is
  * testable without a GPU)
@@ -271,6 +295,9 @@ typedef struct {
     int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,
                                  2 grouped SpMM                                              */
     int32_t spmm_cols;        /* SpMM CTA width used (256, 512 or 1024 columns; 0 if kernel != 2) */
+    int64_t local_cols;       /* columns this rank computes per power (its shard; with a symmetry
+                                 a shard of the domain g <= sigma g)                          */
+    int64_t ld;               /* pitch of the device powers (local_cols padded to the CTA width) */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
 
@@ -312,11 +339,13 @@ mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N);
 mp_status mp_set_grouping(int mode);
 
 /* CTA width of the SpMM kernel (sparsity 2), in columns: 256 (4 packed column pairs per
- * lane, 3 CTAs per SM), 512 (8 pairs per lane, 3 CTAs per SM), 1024 (16 pairs per lane, 2 CTAs per SM: half the per-entry
- * overhead, half the CTAs), or 0 = automatic (the default: 1024 when the grid still has at
- * least 24 CTAs per SM, i.e. n >= 11 for A(D_n); else 512 when that grid has at least 8 CTAs
- * per SM, i.e. n = 10; else 256).  The power pitch ld is padded to a
- * multiple of the width.  Same product either way.  Process-wide.  Errors: MP_ERR_DOMAIN. */
+ * lane, 3 CTAs per SM), 512 (8 pairs per lane, 3 CTAs per SM), 1024 (16 pairs per lane, 2 CTAs
+ * per SM: half the per-entry overhead, half the CTAs) for every CTA, the power pitch padded to a
+ * multiple of it; the negative values -256, -512, -1024 set the main width but keep the
+ * narrower CTA columns for the remainder (mp_column_plan); 0 = automatic (the default: main
+ * width 1024 when the grid still has at least 24 CTAs per SM, i.e. n >= 11 for A(D_n); else 512
+ * when that grid has at least 8 CTAs per SM, i.e. n = 10; else 256; plus the remainder
+ * columns).  Same product either way.  Process-wide.  Errors: MP_ERR_DOMAIN. */
 mp_status mp_set_spmm_width(int cols);
 
 #ifdef __cplusplus

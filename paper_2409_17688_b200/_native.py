@@ -32,7 +32,7 @@ EXPORTS = [
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
     "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_set_spmm_width", "mp_gamma2_formula", "mp_gamma2_record",
     "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal", "minplus_mul_strided_batched_device",
-    "minplus_closure",
+    "minplus_closure", "mp_set_power_observer", "mp_column_plan",
 ]
 
 
@@ -67,17 +67,26 @@ class _Profile(ctypes.Structure):
                 ("dense_steps", ctypes.c_double), ("issued_steps", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("setup_ms", ctypes.c_double), ("stats_ms", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
-                ("kernel", ctypes.c_int32), ("spmm_cols", ctypes.c_int32)]
+                ("kernel", ctypes.c_int32), ("spmm_cols", ctypes.c_int32),
+                ("local_cols", ctypes.c_int64), ("ld", ctypes.c_int64)]
 
 
+OBSERVER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64)
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                 ctypes.c_int64, ctypes.c_void_p)
 
 
+def _so_path() -> str:
+    """The product library, or a diagnostic build named by MP_LIB_PATH (bench_tools variants
+    are loaded this way; nothing ever overwrites the product .so)."""
+    return os.environ.get("MP_LIB_PATH") or _build.SO
+
+
 def _load() -> ctypes.CDLL:
-    if not os.path.exists(_build.SO):
-        raise ImportError(f"{_build.SO} is missing: run __graft_entry__.build() (no CPU fallback)")
-    L = ctypes.CDLL(_build.SO)
+    so = _so_path()
+    if not os.path.exists(so):
+        raise ImportError(f"{so} is missing: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(so)
     P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     sig = {
         "mp_count_words": ([i32, P], i32),
@@ -111,6 +120,8 @@ def _load() -> ctypes.CDLL:
         "mp_word_reversal": ([i32, ctypes.c_void_p, i64], i32),
         "mp_gamma2_formula": ([P, P], i32),
         "mp_gamma2_record": ([i32, P], i32),
+        "mp_set_power_observer": ([OBSERVER_FN, P], i32),
+        "mp_column_plan": ([i64, i64, P, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -263,15 +274,26 @@ def minplus_power_until_periodic_device(dA, max_k: int = 64) -> PeriodicResult:
         raise MinplusError(1, "expected a square row-major 16-bit CUDA tensor")
     import torch
     r = _PeriodicResult()
+    # the run is enqueued on the library stream of this device: unless that is torch's current
+    # stream (set_stream), wait for whatever torch still has in flight on dA
+    cur = torch.cuda.current_stream(dA.device)
+    if _lib_stream.get(dA.device.index) != cur.cuda_stream:
+        cur.synchronize()
     with torch.cuda.device(dA.device):
         _check(lib.minplus_power_until_periodic_device(dA.data_ptr(), dA.stride(0), dA.shape[0],
                                                        max_k, ctypes.byref(r)))
     return _result(r)
 
 
+_lib_stream = {}  # device index -> the cudaStream_t the power runs use (set_stream)
+
+
 def set_stream(stream) -> None:
-    """Run power sequences on `stream` (torch.cuda.Stream or None for the library's own)."""
+    """Run power sequences on `stream` (torch.cuda.Stream or None for the library's own),
+    on the current device."""
+    import torch
     _check(lib.mp_set_stream(None if stream is None else stream.cuda_stream))
+    _lib_stream[torch.cuda.current_device()] = None if stream is None else stream.cuda_stream
 
 
 def minplus_power_rows(A, rows, kmax: int) -> np.ndarray:
@@ -296,6 +318,32 @@ def gamma2_record(n: int) -> PeriodicResult:
     r = _PeriodicResult()
     _check(lib.mp_gamma2_record(n, ctypes.byref(r)))
     return _result(r)
+
+
+_observer_keep = []
+
+
+def set_power_observer(fn=None) -> None:
+    """Parity hook: fn(k, power) is called for every power A^k of every following run, power
+    = the whole N x N matrix (uint16 numpy view of a library buffer, valid only during the
+    call: copy what you keep).  fn returning True stops the run (MP_ERR_DOMAIN).  None clears."""
+    if fn is None:
+        _check(lib.mp_set_power_observer(OBSERVER_FN(), None))
+        _observer_keep.clear()
+        return
+
+    def cb(ctx, k, ptr, N):
+        try:
+            buf = (ctypes.c_uint16 * (N * N)).from_address(ptr)
+            return 1 if fn(int(k), np.frombuffer(buf, dtype=np.uint16).reshape(N, N)) else 0
+        except Exception:  # noqa: BLE001 -- reported to C as a stopped run
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    c = OBSERVER_FN(cb)
+    _observer_keep[:] = [c]
+    _check(lib.mp_set_power_observer(c, None))
 
 
 # -------------------------------------------------------------------------- multi-GPU
@@ -348,6 +396,13 @@ def shard_range(N: int, world: int, rank: int):
     return c0.value, c1.value
 
 
+def column_plan(N: int, w: int) -> dict:
+    """SpMM column plan for w local columns of an N x N power: {ld, main_cols, tail_cols}."""
+    ld, mc, tc = ctypes.c_int64(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib.mp_column_plan(N, w, ctypes.byref(ld), ctypes.byref(mc), ctypes.byref(tc)))
+    return {"ld": ld.value, "main_cols": mc.value, "tail_cols": tc.value}
+
+
 def fingerprint_unit(N: int) -> int:
     return int(lib.mp_fingerprint_unit(N))
 
@@ -373,7 +428,8 @@ def last_profile() -> dict:
     return {"product_ms": p.product_ms, "product_launches": p.product_launches,
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
             "setup_ms": p.setup_ms, "stats_ms": p.stats_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
-            "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols}
+            "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols,
+            "local_cols": p.local_cols, "ld": p.ld}
 
 
 SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}
@@ -416,7 +472,8 @@ def set_grouping(mode: str = "auto") -> None:
 
 
 def set_spmm_width(cols: int = 0) -> None:
-    """CTA width of the SpMM kernel: 0 (automatic), 256, 512 or 1024 columns (same product)."""
+    """CTA width of the SpMM kernel: 0 (automatic), 256, 512 or 1024 columns everywhere, or
+    -256 / -512 / -1024 = that main width plus narrower remainder columns (same product)."""
     _check(lib.mp_set_spmm_width(int(cols)))
 
 
@@ -426,3 +483,4 @@ def version() -> str:
 
 def shutdown() -> None:
     lib.mp_shutdown()
+    _lib_stream.clear()  # the per-device state, stream choice included, is gone

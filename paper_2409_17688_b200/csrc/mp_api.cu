@@ -55,6 +55,12 @@ std::vector<int32_t> g_sym;
 bool g_word_sym = true;
 
 mp_profile g_prof{};
+
+// Parity observer (mp_set_power_observer): sees every power of every run in full.
+struct Observer {
+    mp_power_observer_fn fn = nullptr;
+    void *ctx = nullptr;
+} g_obs;
 std::map<std::tuple<int, int, int>, mp_periodic_result> g_cache; // (n, world, rank)
 
 // MP_TRACE=1: phase timings of each power run on stderr (the stream is synchronised at every
@@ -167,7 +173,8 @@ struct DBuf {
 // do not pay cudaMalloc/cudaFree; released by mp_shutdown().
 struct PowerRun {
     int64_t N = 0, Np = 0, c0 = 0, w = 0, ld = 0;
-    int spmm_cols = 512; // k_spmm CTA width of this run (spmm_cols); ld is a multiple of it
+    int spmm_cols = 512; // main k_spmm CTA width of this run (spmm_cols)
+    SpmmPlan plan;       // its column segments; ld = plan.ld
     DBuf at2, words, tmp0, tmp1, ktp, kti, occ, stats, flag, stage_raw;
     bool has_at2 = false; // only the tile kernels stage AT2; SpMM reads A or the word masks
     // symmetry: local column jj holds global column gcol[jj] (g <= sigma g) and stands for g and
@@ -190,15 +197,21 @@ struct PowerRun {
     bool spmm = false;    // grouped SpMM kernel
     double issued_per_product = 0.0;
     double issued_tiles = 0.0, issued_spmm = 0.0;
+    int64_t tiles_nonempty = 0; // non-empty 128 x 32 tiles of A (block-sparse tile kernel)
     // grouped sparse form of A (k_spmm): buffers handed out in order by sp_alloc
     std::vector<DBuf> sp_bufs;
     size_t sp_next = 0;
     SparseWork sp;
     std::vector<cudaEvent_t> events; // per-power product start/stop
+    // observer path: the whole power, unfolded on the device and copied to pinned host memory
+    DBuf full_dev;
+    uint16_t *full_host = nullptr;
+    size_t full_host_bytes = 0;
     ~PowerRun()
     {
         for (auto ev : events)
             if (ev) cudaEventDestroy(ev);
+        if (full_host) cudaFreeHost(full_host);
     }
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
@@ -208,6 +221,9 @@ struct DevState {
     cudaStream_t stream = nullptr;      // the library's own non-blocking stream
     cudaStream_t user_stream = nullptr; // mp_set_stream override for power runs
     DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c;
+    // last use of the product scratch (at2, xb, cb, flag): the next user, on whatever stream,
+    // waits on it, so a call on another stream cannot overwrite scratch still being read
+    cudaEvent_t scratch_ev = nullptr;
     std::unique_ptr<PowerRun> pr;
 };
 std::map<int, DevState> g_dev;
@@ -232,6 +248,7 @@ mp_status current_device(int *dev_out, DevState **st)
                         prop.name, prop.major, prop.minor);
         DevState ds;
         CUDA_TRY(cudaStreamCreateWithFlags(&ds.stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ds.scratch_ev, cudaEventDisableTiming));
         it = g_dev.emplace(dev, std::move(ds)).first;
     }
     *dev_out = dev;
@@ -264,6 +281,7 @@ mp_status mul_device_impl(DevState &st, const uint16_t *dA, int64_t lda, const u
     TRY(st.xb.ensure((size_t)Kp * Np * 2, "B (padded)"));
     TRY(st.cb.ensure((size_t)Mp * Np * 2, "C (padded)"));
     TRY(st.flag.ensure(16, "range flag"));
+    CUDA_TRY(cudaStreamWaitEvent(s, st.scratch_ev, 0)); // the previous user of the scratch is done
     CUDA_TRY(cudaMemsetAsync(st.flag.p, 0, sizeof(int), s));
     LAUNCH(launch_make_at2(dA, lda, M, K, st.at2.as<uint32_t>(), Mp, Kp, st.flag.as<int>(), s));
     LAUNCH(launch_encode(dB, ldb, K, N, st.xb.as<uint16_t>(), Np, Kp, st.flag.as<int>(), s));
@@ -274,6 +292,7 @@ mp_status mul_device_impl(DevState &st, const uint16_t *dA, int64_t lda, const u
     LAUNCH(launch_minplus(st.at2.as<uint32_t>(), Mp, st.xb.as<uint16_t>(), Np, st.cb.as<uint16_t>(), Np, Mp, Np,
                           Kp, nullptr, nullptr, s));
     LAUNCH(launch_decode(st.cb.as<uint16_t>(), Np, M, N, dC, ldc, s));
+    CUDA_TRY(cudaEventRecord(st.scratch_ev, s));
     return MP_OK;
 }
 
@@ -311,7 +330,8 @@ mp_status build_tile_lists(PowerRun &R, cudaStream_t s)
     COPY(R.ktp.p, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice, s);
     COPY(R.kti.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s);
     CUDA_TRY(cudaStreamSynchronize(s));
-    R.issued_tiles = (double)ptr[(size_t)Mt] * kBK * kBM * (double)R.ld;
+    R.tiles_nonempty = ptr[(size_t)Mt];
+    R.issued_tiles = (double)R.tiles_nonempty * kBK * kBM * (double)R.ld;
     return MP_OK;
 }
 
@@ -330,7 +350,7 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
 {
     R.sp_next = 0;
     R.sp = SparseWork();
-    R.sp.cols = R.spmm_cols; // entry row offsets are bytes of a staged X row of this width
+    R.sp.cols = R.spmm_cols; // reported width (the entries carry row offsets for every width)
     int64_t launches = 0;
     const bool group = g_opts.grouping == 1 || (g_opts.grouping < 0 && R.N >= kGroupMinN);
     const cudaError_t e =
@@ -360,7 +380,13 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
         sa.eoff = R.sp.eoff;
         sa.E = R.sp.E;
         sa.rows = R.sp.rows;
-        LAUNCH(launch_spmm(sa, R.sp.cols, X, R.ld, C, R.ld, R.Np, R.ld, s));
+        int nl = 0;
+        const cudaError_t e = launch_spmm(sa, R.plan, X, R.ld, C, R.ld, R.Np, s, &nl);
+        g_launches.fetch_add(nl);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MP_ERR_CUDA, "kernel k_spmm failed: %s", cudaGetErrorString(e));
+        }
         return MP_OK;
     }
     LAUNCH(launch_minplus(R.at2.as<uint32_t>(), R.Np, X, R.ld, C, R.ld, R.Np, R.ld, R.Np,
@@ -415,6 +441,31 @@ mp_status power_buffer(PowerRun &R, int j, const uint16_t **out, cudaStream_t s)
     return MP_OK;
 }
 
+// Hands the whole power A^k (boundary encoding, host memory) to the observer.
+mp_status observe(PowerRun &R, const uint16_t *X, int k, cudaStream_t s)
+{
+    const size_t bytes = (size_t)R.N * (size_t)R.N * 2;
+    TRY(R.full_dev.ensure(bytes, "observer copy of a power"));
+    if (R.full_host_bytes < bytes) {
+        if (R.full_host) cudaFreeHost(R.full_host);
+        R.full_host = nullptr;
+        R.full_host_bytes = 0;
+        if (cudaMallocHost((void **)&R.full_host, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            R.full_host = nullptr;
+            return fail(MP_ERR_RESOURCE, "pinned host allocation of %zu bytes for the power observer failed", bytes);
+        }
+        R.full_host_bytes = bytes;
+    }
+    LAUNCH(launch_unfold(X, R.ld, R.N, R.dloc.as<int32_t>(), R.sym ? R.dsig.as<int32_t>() : nullptr,
+                         R.full_dev.as<uint16_t>(), s));
+    COPY(R.full_host, R.full_dev.p, bytes, cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (g_obs.fn(g_obs.ctx, k, R.full_host, R.N) != 0)
+        return fail(MP_ERR_DOMAIN, "the power observer stopped the run at k = %d", k);
+    return MP_OK;
+}
+
 // Source of A: either a host matrix or the word masks of path order n.
 struct ASource {
     const uint16_t *host = nullptr; // host matrix, pitch N
@@ -436,6 +487,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     int dev = 0;
     DevState *st = nullptr;
     TRY(current_device(&dev, &st));
+    if (g_obs.fn && !cap && g_dist.world > 1)
+        return fail(MP_ERR_DOMAIN, "the power observer needs the whole power: single rank only (world = %d)",
+                    g_dist.world);
     cudaStream_t s = st->user_stream ? st->user_stream : st->stream;
     const int64_t h2d0 = g_h2d.load(), d2h0 = g_d2h.load();
     cudaEvent_t ev_all0, ev_all1;
@@ -493,8 +547,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         }
         R.cols_rep = R.w;
     }
-    R.spmm_cols = spmm_cols(R.Np, R.w); // the SpMM CTA width of this run
-    R.ld = round_up(R.w > 0 ? R.w : 1, R.spmm_cols);
+    R.plan = spmm_plan(R.Np, R.w); // SpMM CTA widths of this run (DESIGN.md sections 5, 6)
+    R.spmm_cols = R.plan.main_cols;
+    R.ld = R.plan.ld;
     {
         std::vector<int32_t> dl((size_t)N, -1);
         if (R.sym)
@@ -571,7 +626,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 R.issued_per_product = R.issued_spmm;
             }
         }
-        if (!R.spmm) { // the tile kernels: stage AT2
+        if (!R.spmm) { // the tile kernels: stage AT2; their CTA is 256 columns wide
+            R.ld = round_up(R.ld, kBN);
+            R.issued_tiles = (double)R.tiles_nonempty * kBK * kBM * (double)R.ld;
             TRY(R.at2.ensure((size_t)R.Np * R.Np * 4, "A (transposed, duplicated)"));
             if (words_src) {
                 LAUNCH(launch_build_from_words(R.words.as<WordMask>(), N, src.n, R.at2.as<uint32_t>(), R.Np, s));
@@ -604,11 +661,14 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         const double cap_bytes = std::max((double)kDefaultRingBytes, 4.0 * (double)R.slot_bytes());
         int64_t budget = g_opts.budget > 0 ? g_opts.budget : (int64_t)std::min(avail, cap_bytes);
         int64_t slots = budget / (int64_t)R.slot_bytes();
-        slots = std::min<int64_t>(slots, std::max(max_k, 2));
+        // an explicit budget also covers the two recompute buffers of an evicted partner
         if (g_opts.budget > 0) slots -= 2;
-        // a batched run (small N) needs the whole batch resident; the batch size depends on N
-        // only, so every rank of a sharded run issues the same collective calls
-        const int64_t need = (N <= kBatchMaxN && !cap) ? std::min(kBatch, max_k) + 1 : 2;
+        // a batched run (small N) needs the whole batch resident (one more slot if the run can
+        // go past the first batch); the batch size depends on N only, so every rank of a
+        // sharded run issues the same collective calls
+        const int64_t bsz = (N <= kBatchMaxN && !cap) ? std::min(kBatch, max_k) : 1;
+        const int64_t need = bsz + (max_k > bsz ? 1 : 0) > 2 ? bsz + (max_k > bsz ? 1 : 0) : 2;
+        slots = std::min<int64_t>(slots, std::max<int64_t>(max_k, need));
         if (slots < need)
             return fail(MP_ERR_RESOURCE, "power store needs at least %lld slots of %zu bytes (budget %lld bytes)",
                         (long long)need, R.slot_bytes(), (long long)budget);
@@ -711,6 +771,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             res.fingerprint[k] = (uint64_t)cs.fingerprint;
             if (!res.dense_from && cs.inf_count == 0) res.dense_from = k;
             const uint16_t *cur = buf[(size_t)k];
+            if (g_obs.fn && !cap) TRY(observe(R, cur, k, s));
 
             if (cap) {
                 DBuf rowbuf;
@@ -796,6 +857,8 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.d2h_bytes = g_d2h.load() - d2h0;
     g_prof.kernel = R.spmm ? 2 : (R.sparse ? 1 : 0);
     g_prof.spmm_cols = R.spmm ? R.sp.cols : 0;
+    g_prof.local_cols = R.w;
+    g_prof.ld = R.ld;
 
     if (!found) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
     *out = res;
@@ -1086,6 +1149,20 @@ mp_status mp_shard_range(int64_t N, int world, int rank, int64_t *c0, int64_t *c
     return MP_OK;
 }
 
+mp_status mp_column_plan(int64_t N, int64_t w, int64_t *ld, int32_t *main_cols, int32_t *tail_cols)
+{
+    if (!ld || !main_cols || !tail_cols || N <= 0 || w < 0)
+        return fail(MP_ERR_DOMAIN, "mp_column_plan: invalid arguments");
+    const SpmmPlan P = spmm_plan(pad_rows(N), w);
+    *ld = P.ld;
+    *main_cols = P.main_cols;
+    int32_t tail = 0;
+    for (int g = 0; g < P.nseg; ++g)
+        if (P.seg[g].cols != P.main_cols) tail += (int32_t)P.seg[g].ncols;
+    *tail_cols = tail;
+    return MP_OK;
+}
+
 uint64_t mp_fingerprint_unit(int64_t N)
 {
     // S(N) = sum over i, j < N of s(2i) s(2j+1) = (sum_i s(2i)) (sum_j s(2j+1))  (mod 2^64)
@@ -1127,6 +1204,8 @@ void mp_shutdown(void)
         cudaGetDevice(&cur);
         cudaSetDevice(kv.first);
         kv.second.pr.reset();
+        if (kv.second.scratch_ev) cudaEventDestroy(kv.second.scratch_ev);
+        kv.second.scratch_ev = nullptr;
         if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
         kv.second.stream = nullptr;
         cudaSetDevice(cur);
@@ -1202,6 +1281,14 @@ mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N)
     return MP_OK;
 }
 
+mp_status mp_set_power_observer(mp_power_observer_fn fn, void *ctx)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_obs.fn = fn;
+    g_obs.ctx = fn ? ctx : nullptr;
+    return MP_OK;
+}
+
 mp_status mp_set_grouping(int mode)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
@@ -1213,8 +1300,9 @@ mp_status mp_set_grouping(int mode)
 mp_status mp_set_spmm_width(int cols)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
-    if (cols != 0 && cols != 256 && cols != 512 && cols != 1024)
-        return fail(MP_ERR_DOMAIN, "mp_set_spmm_width: %d is not 0, 256, 512 or 1024", cols);
+    const int a = cols < 0 ? -cols : cols;
+    if (a != 0 && a != 256 && a != 512 && a != 1024)
+        return fail(MP_ERR_DOMAIN, "mp_set_spmm_width: %d is not 0, +-256, +-512 or +-1024", cols);
     g_spmm_width = cols;
     return MP_OK;
 }

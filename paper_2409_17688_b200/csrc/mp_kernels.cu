@@ -4,6 +4,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <algorithm>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "mp_internal.h"
 #include "mp_kernels.h"
@@ -32,6 +35,18 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr)
 {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
     return v;
 }
 
@@ -469,6 +484,22 @@ __global__ void k_decode(const uint16_t *__restrict__ src, int64_t lds, int64_t 
     }
 }
 
+// The whole N x N power in the boundary encoding from the columns a run keeps: column g is local
+// column loc[g] if loc[g] >= 0, else (symmetry) X_(i, g) = X_(sigma i,
+// sigma g) with sigma g local.  Parity / observer path only.
+__global__ void k_unfold(const uint16_t *__restrict__ X, int64_t ld, int64_t N, const int32_t *__restrict__ loc,
+                         const int32_t *__restrict__ sigma, uint16_t *__restrict__ out)
+{
+    for (int64_t i = blockIdx.y; i < N; i += gridDim.y) {
+        const int64_t si = sigma ? (int64_t)sigma[i] : i;
+        for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < N; g += (int64_t)gridDim.x * blockDim.x) {
+            const int32_t jj = loc[g];
+            const uint16_t v = jj >= 0 ? X[i * ld + jj] : X[si * ld + loc[sigma[g]]];
+            out[i * N + g] = v >= kDevInf ? kBndInf : v;
+        }
+    }
+}
+
 // occ[bm * Ktiles + kt] = 1 if the kBM x kBK tile of A (read through AT2) has a finite entry.
 __global__ void k_tile_occupancy(const uint32_t *__restrict__ AT2, int64_t Mp, int64_t Kp,
                                  uint8_t *__restrict__ occ)
@@ -544,22 +575,24 @@ constexpr int kSpOffBytes = ((kSpGroups + 1) * 8 + 15) / 16 * 16;
 // The CTA width: PPL packed column pairs per lane (4: 256 columns, 8: 512 columns, 3 CTAs per
 // SM; 16: 1024 columns, 2 CTAs per SM at 96 registers; spmm_cols picks one per run).
 template <int PPL> struct SpCfg {
-    static_assert(PPL == 4 || PPL == 8 || PPL == 16, "pairs per lane");
+    static_assert(PPL == 1 || PPL == 2 || PPL == 4 || PPL == 8 || PPL == 12 || PPL == 16, "pairs per lane");
+    // which field of an entry's offset record holds the X row offset for this width (PPL 2
+    // and 1 shift the 256-column field right by 1 and 2)
+    static constexpr int OffField = PPL == 16 ? 0 : PPL == 8 ? 1 : PPL == 12 ? 3 : 2;
+    static constexpr int OffShift = PPL == 2 ? 1 : PPL == 1 ? 2 : 0;
     static_assert(kG * PPL <= 64, "accumulators: kG x pairs per lane registers");
     static constexpr int Xq = PPL / 4;          // LDS.128 of X per entry and lane (one per 256 columns)
     static constexpr int Cols = 64 * PPL;       // columns per CTA (32 lanes x 2 * PPL)
     static constexpr int RowBytes = Cols * 2;   // one staged X row, in bytes
+    static constexpr int LaneBytes = PPL >= 4 ? 16 : 4 * PPL; // a lane's part of a 256-column slice
 #ifdef MP_SP_CTAS
     static constexpr int Ctas = MP_SP_CTAS;
 #else
-    static constexpr int Ctas = PPL == 16 ? 2 : 3;
+    static constexpr int Ctas = PPL >= 12 ? 2 : 3;
 #endif
     static constexpr int StageBytes = kSpChunk * RowBytes + kSpEntryBytes + kSpOffBytes;
     static constexpr int SmemBytes = kSpStages * StageBytes + 2 * kSpStages * 8;
 };
-#ifndef MP_SP_LDGSTS
-#define MP_SP_LDGSTS 0
-#endif
 #ifndef MP_SP_NOCOMPUTE
 #define MP_SP_NOCOMPUTE 0
 #endif
@@ -1149,7 +1182,10 @@ __global__ void k_chunk_entries(const uint8_t *__restrict__ m8, Acc acc, int64_t
 #pragma unroll
                 for (int u = 0; u < kG / 4; ++u)
                     E[kEntU4 * e + u] = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-                E[kEntU4 * e + kG / 4] = make_uint4((unsigned)s * row_bytes, 0u, 0u, 0u); // X row (bytes)
+                // X row offset in bytes for each CTA width (SpCfg<PPL>::OffField picks one):
+                // 1024, 512, 256 and 768 columns (rows of 2048, 1024, 512, 1536 bytes)
+                E[kEntU4 * e + kG / 4] = make_uint4((unsigned)s * 2048u, (unsigned)s * 1024u, (unsigned)s * 512u,
+                                                    (unsigned)s * 1536u);
                 ++e;
             }
             ++cnt;
@@ -1256,18 +1292,18 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
 // acc[r][p] = min(a_r + x_p, acc[r][p]) for the kG rows of a group entry and this lane's
 // PPL packed column pairs (x[h] = the lane's 8 columns of the h-th 256-column slice).
 template <int PPL>
-__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][PPL], const uint4 (&av)[kG / 4], const uint4 (&x)[PPL / 4])
+__device__ __forceinline__ void dpx_group(uint32_t (&acc)[kG][PPL], const uint4 (&av)[kG / 4],
+                                          const uint4 (&x)[PPL >= 4 ? PPL / 4 : 1])
 {
 #pragma unroll
     for (int r = 0; r < kG; ++r) {
         const uint4 &q = av[r / 4];
         const uint32_t a = (r % 4 == 0) ? q.x : (r % 4 == 1) ? q.y : (r % 4 == 2) ? q.z : q.w;
 #pragma unroll
-        for (int h = 0; h < PPL / 4; ++h) {
-            acc[r][4 * h + 0] = __viaddmin_u16x2(a, x[h].x, acc[r][4 * h + 0]);
-            acc[r][4 * h + 1] = __viaddmin_u16x2(a, x[h].y, acc[r][4 * h + 1]);
-            acc[r][4 * h + 2] = __viaddmin_u16x2(a, x[h].z, acc[r][4 * h + 2]);
-            acc[r][4 * h + 3] = __viaddmin_u16x2(a, x[h].w, acc[r][4 * h + 3]);
+        for (int p = 0; p < PPL; ++p) {
+            const uint4 &xh = x[p / 4];
+            const uint32_t xv = (p % 4 == 0) ? xh.x : (p % 4 == 1) ? xh.y : (p % 4 == 2) ? xh.z : xh.w;
+            acc[r][p] = __viaddmin_u16x2(a, xv, acc[r][p]);
         }
     }
 }
@@ -1301,7 +1337,7 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     using Cfg = SpCfg<PPL>;
-    constexpr int kSpRowBytes = Cfg::RowBytes, kSpCols = Cfg::Cols, kSpXq = Cfg::Xq;
+    constexpr int kSpRowBytes = Cfg::RowBytes, kSpCols = Cfg::Cols, kSpXq = PPL >= 4 ? Cfg::Xq : 1;
     constexpr int XB = kSpChunk * kSpRowBytes; // 16 (32) KB of X rows
     constexpr int EB = kSpEntryBytes;           // up to 128 entries + 3 look-ahead records
     constexpr int STAGE = Cfg::StageBytes;
@@ -1333,7 +1369,7 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
         reinterpret_cast<uint4 *>(smem + (q / (EB / 16)) * STAGE + XB)[q % (EB / 16)] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         for (int st = 0; st < kSpStages; ++st) {
-            mbar_init(bar_full + st * 8, MP_SP_LDGSTS ? 32 : 1);
+            mbar_init(bar_full + st * 8, 1);
             mbar_init(bar_empty + st * 8, kSpConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1365,26 +1401,12 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
             const int nrows = min(kSpChunk, U - c * kSpChunk);
             const uint32_t ebytes = (uint32_t)(e1 - e0) * kEntBytes;
             const uint32_t sX = sbase + st * STAGE;
-#if MP_SP_LDGSTS
-            // 16-byte cp.async by all 32 lanes; each lane's completion arrives on "full"
-            // (initialised with 32 arrivals) through cp.async.mbarrier.arrive.noinc
-            for (int r = 0; r < nrows; ++r) {
-                const int32_t lr = __shfl_sync(0xFFFFFFFFu, l, r);
-                const uint16_t *src = X + (int64_t)lr * ldx + col0;
-#pragma unroll
-                for (int h = 0; h < kSpXq; ++h) cp_async16(sX + r * kSpRowBytes + 512 * h + lane * 16, src + 256 * h + lane * 8);
-            }
-            for (uint32_t q = lane; q < ebytes / 16; q += 32) cp_async16(sX + XB + q * 16, E + kEntU4 * e0 + q);
-            if (lane < kSpOffBytes / 16) cp_async16(sX + XB + EB + lane * 16, eoff + gc * kSpGroups + 2 * lane);
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_full + st * 8) : "memory");
-#else
             if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + kSpOffBytes);
             __syncwarp();
             if (lane < nrows)
                 bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
             if (lane == 0 && ebytes) bulk_g2s(sX + XB, E + kEntU4 * e0, ebytes, bar_full + st * 8);
             if (lane == 1) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, kSpOffBytes, bar_full + st * 8);
-#endif
         }
         return;
     }
@@ -1408,15 +1430,27 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
         // two ahead.  Look-ahead reads past the group's end read the next group's records or a
         // zero/stale record of the entry area, whose row offset is a valid one.  Row offsets
         // are bytes, so an X load is one LDS [lane base + offset].
-        const uint32_t Xl = sbase + st * STAGE + lane * 16;
-        auto row = [&](int q) { return Es[kEntU4 * q + kG / 4].x; };
+        const uint32_t Xl = sbase + st * STAGE + lane * Cfg::LaneBytes;
+        auto row = [&](int q) {
+            const uint4 o = Es[kEntU4 * q + kG / 4];
+            return (Cfg::OffField == 0 ? o.x : Cfg::OffField == 1 ? o.y : Cfg::OffField == 2 ? o.z : o.w) >>
+                   Cfg::OffShift;
+        };
         auto vals = [&](int q, uint4(&v)[kG / 4]) {
 #pragma unroll
             for (int u = 0; u < kG / 4; ++u) v[u] = Es[kEntU4 * q + u];
         };
         auto xrow = [&](uint32_t off, uint4(&x)[kSpXq]) {
+            if constexpr (PPL >= 4) {
 #pragma unroll
-            for (int h = 0; h < kSpXq; ++h) x[h] = lds128(Xl + off + 512 * h);
+                for (int h = 0; h < kSpXq; ++h) x[h] = lds128(Xl + off + 512 * h);
+            } else if constexpr (PPL == 2) {
+                const uint2 v = lds64(Xl + off);
+                x[0].x = v.x;
+                x[0].y = v.y;
+            } else {
+                x[0].x = lds32(Xl + off);
+            }
         };
 #pragma unroll
         for (int gg = 0; gg < kSpGpw; ++gg) {
@@ -1464,9 +1498,18 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
         const int gg = q / kG, r = q % kG;
         const int64_t slot = (int64_t)t * kSpRows + kG * (warp * kSpGpw + gg) + r;
         const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
+        if constexpr (PPL < 4) { // lane owns columns 2 PPL lane .. + 2 PPL - 1
+            uint16_t *crow = C + i * ldc + col0 + 2 * PPL * lane;
+            if constexpr (PPL == 2)
+                *reinterpret_cast<uint2 *>(crow) =
+                    make_uint2(__vminu2(acc[gg][r][0], 0x7FFF7FFFu), __vminu2(acc[gg][r][1], 0x7FFF7FFFu));
+            else
+                *reinterpret_cast<uint32_t *>(crow) = __vminu2(acc[gg][r][0], 0x7FFF7FFFu);
+            continue;
+        }
         uint16_t *crow = C + i * ldc + col0 + 8 * lane;
 #pragma unroll
-        for (int h = 0; h < kSpXq; ++h) {
+        for (int h = 0; h < Cfg::Xq; ++h) {
             uint4 v;
             v.x = __vminu2(acc[gg][r][4 * h + 0], 0x7FFF7FFFu);
             v.y = __vminu2(acc[gg][r][4 * h + 1], 0x7FFF7FFFu);
@@ -1480,16 +1523,37 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
 // ---------------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------------
-static int g_num_sms = 0;
+// Per-device caches: the SM count, and which kernels had their dynamic shared-memory limit
+// raised (cudaFuncSetAttribute applies to the current device only).
+constexpr int kMaxDevices = 64;
+static int g_num_sms[kMaxDevices] = {};
+static int current_dev()
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
 static int num_sms()
 {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+    const int dev = current_dev();
+    if (!g_num_sms[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = n > 0 ? n : 148;
     }
-    return g_num_sms;
+    return g_num_sms[dev];
+}
+template <class Kernel>
+static cudaError_t smem_limit(Kernel *k, int bytes)
+{
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    const std::pair<const void *, int> key{(const void *)k, current_dev()};
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(key)) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
 }
 
 static int grid_for(int64_t work, int per_block)
@@ -1507,13 +1571,9 @@ cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, 
                            int64_t ldc, int64_t Mp, int64_t ncols_p, int64_t Kp, const int32_t *kt_ptr,
                            const int32_t *kt_idx, cudaStream_t s)
 {
-    static bool attr_set = false;
     const int smem = kStages * (kBK * kBM * 4 + kBK * kBN * 2);
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_minplus<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    const cudaError_t e = smem_limit(k_minplus<kStages>, smem);
+    if (e != cudaSuccess) return e;
     dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kBM));
     k_minplus<kStages><<<grid, kThreads, smem, s>>>(AT2, lda, X, ldx, C, ldc, kt_ptr, kt_idx,
                                                     (int)(Kp / kBK));
@@ -1814,6 +1874,14 @@ cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_
     return cudaGetLastError();
 }
 
+cudaError_t launch_unfold(const uint16_t *X, int64_t ld, int64_t N, const int32_t *loc, const int32_t *sigma,
+                          uint16_t *out, cudaStream_t s)
+{
+    const dim3 grid((unsigned)std::min<int64_t>((N + 255) / 256, 64), (unsigned)std::min<int64_t>(N, 16384));
+    k_unfold<<<grid, 256, 0, s>>>(X, ld, N, loc, sigma, out);
+    return cudaGetLastError();
+}
+
 int g_spmm_width = 0;
 
 int spmm_cols(int64_t Np, int64_t w)
@@ -1821,7 +1889,7 @@ int spmm_cols(int64_t Np, int64_t w)
 #ifdef MP_SP_WIDTH
     if (MP_SP_WIDTH) return MP_SP_WIDTH;
 #endif
-    if (g_spmm_width) return g_spmm_width;
+    if (g_spmm_width) return g_spmm_width > 0 ? g_spmm_width : -g_spmm_width;
     // 1024-column CTAs halve the per-entry overhead but also the CTA count: keep them for
     // grids of at least 24 CTAs per SM (n = 11, 12), 512 columns for at least 8 CTAs per SM at
     // that width (n = 10), 256 below (n <= 9; n = 9: 0.110 -> 0.089 ms per product)
@@ -1835,25 +1903,75 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
                                  int64_t Mp, int64_t ncols_p, cudaStream_t s)
 {
     using Cfg = SpCfg<PPL>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_spmm<PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    const cudaError_t e = smem_limit(k_spmm<PPL>, Cfg::SmemBytes);
+    if (e != cudaSuccess) return e;
     if (ncols_p % Cfg::Cols || ldx % 8 || ldc % 8) return cudaErrorInvalidValue;
     dim3 grid((unsigned)(Mp / kSpRows), (unsigned)(ncols_p / Cfg::Cols)); // x: tiles, y: column blocks (remapped)
     k_spmm<PPL><<<grid, kSpThreads, Cfg::SmemBytes, s>>>(sa.L, sa.tptr, sa.tch, sa.eoff, sa.E, X, ldx, C, ldc, sa.rows);
     return cudaGetLastError();
 }
 
-cudaError_t launch_spmm(const SparseA &sa, int cols, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
-                        int64_t Mp, int64_t ncols_p, cudaStream_t s)
+SpmmPlan spmm_plan(int64_t Np, int64_t w)
 {
-    if (cols == 1024) return launch_spmm_t<16>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
-    if (cols == 512) return launch_spmm_t<8>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
-    if (cols == 256) return launch_spmm_t<4>(sa, X, ldx, C, ldc, Mp, ncols_p, s);
+    SpmmPlan P;
+    const int main = spmm_cols(Np, w);
+    P.main_cols = main;
+    const int64_t q = std::max<int64_t>(w, 1) / main;
+    int64_t col = 0;
+    if (q > 0) {
+        P.seg[P.nseg++] = {col, main, q * main};
+        col += q * main;
+    }
+    if (g_spmm_width > 0) { // a forced width everywhere (experiments)
+        if (col < w) {
+            if (P.nseg) P.seg[0].ncols += main;
+            else P.seg[P.nseg++] = {col, main, (int64_t)main};
+            col += main;
+        }
+    } else {
+        // the remainder, rounded up to 64 columns (one DPX instruction spans 32 lanes x 2
+        // columns), in CTA columns of decreasing width: 768, 512, 256, 128, 64 (at most three)
+        int64_t r = round_up(std::max<int64_t>(w - col, 0), 64);
+        if (r == main) { // a whole main-width column after all
+            if (P.nseg) P.seg[0].ncols += main;
+            else P.seg[P.nseg++] = {col, main, (int64_t)main};
+            col += main;
+            r = 0;
+        }
+        static const int widths[] = {768, 512, 256, 128, 64};
+        for (int cw : widths)
+            if (cw < main && r >= cw) {
+                P.seg[P.nseg++] = {col, cw, (int64_t)cw};
+                col += cw;
+                r -= cw;
+            }
+    }
+    P.ld = col;
+    return P;
+}
+
+static cudaError_t launch_width(const SparseA &sa, int cols, const uint16_t *X, int64_t ldx, uint16_t *C,
+                                int64_t ldc, int64_t Mp, int64_t ncols, cudaStream_t s)
+{
+    if (cols == 1024) return launch_spmm_t<16>(sa, X, ldx, C, ldc, Mp, ncols, s);
+    if (cols == 768) return launch_spmm_t<12>(sa, X, ldx, C, ldc, Mp, ncols, s);
+    if (cols == 512) return launch_spmm_t<8>(sa, X, ldx, C, ldc, Mp, ncols, s);
+    if (cols == 256) return launch_spmm_t<4>(sa, X, ldx, C, ldc, Mp, ncols, s);
+    if (cols == 128) return launch_spmm_t<2>(sa, X, ldx, C, ldc, Mp, ncols, s);
+    if (cols == 64) return launch_spmm_t<1>(sa, X, ldx, C, ldc, Mp, ncols, s);
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_spmm(const SparseA &sa, const SpmmPlan &P, const uint16_t *X, int64_t ldx, uint16_t *C,
+                        int64_t ldc, int64_t Mp, cudaStream_t s, int *launches)
+{
+    for (int g = 0; g < P.nseg; ++g) {
+        const SpmmPlan::Seg &sg = P.seg[g];
+        const cudaError_t e = launch_width(sa, sg.cols, X + sg.col0, ldx, C + sg.col0, ldc, Mp, sg.ncols, s);
+        if (launches) ++*launches;
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // Builds the grouped sparse form (all device work; two host reads of totals).
@@ -1995,7 +2113,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     SP_ALLOC(w.E, (size_t)std::max<int64_t>(ne, 1) * kEntBytes);
     w.group_rows = kG;
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
-        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E, (uint32_t)(2 * w.cols))));
+        w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E, 0u)));
 #undef SP_SCAN
 #undef SP_LAUNCH
 #undef SP_ALLOC

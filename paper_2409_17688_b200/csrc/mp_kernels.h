@@ -28,6 +28,11 @@ cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int6
 cudaError_t launch_set_diag_zero(uint16_t *X, int64_t ld, int64_t n, cudaStream_t s);
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
                           int64_t ldd, cudaStream_t s);
+// out (N x N, boundary encoding) = the whole power from the local columns of X: column g is
+// local column loc[g] if loc[g] >= 0, else X_(sigma i, loc[sigma g]) (sigma may be null only if
+// every column is local).
+cudaError_t launch_unfold(const uint16_t *X, int64_t ld, int64_t N, const int32_t *loc, const int32_t *sigma,
+                          uint16_t *out, cudaStream_t s);
 // Grouped sparse form of A for the SpMM product (see k_spmm in mp_kernels.cu).
 struct SparseA {
     const int32_t *L = nullptr;    // concatenated per-tile (32-row) ordered union lists of l
@@ -55,8 +60,26 @@ struct SparseWork {
 // it per run from the grid size (or the mp_set_spmm_width override in g_spmm_width).
 int spmm_cols(int64_t Np, int64_t w);
 extern int g_spmm_width;
-cudaError_t launch_spmm(const SparseA &sa, int cols, const uint16_t *X, int64_t ldx, uint16_t *C, int64_t ldc,
-                        int64_t Mp, int64_t ncols_p, cudaStream_t s);
+// Column plan of one SpMM product over w local columns: CTA columns of the run's main width
+// (spmm_cols) and, for the remainder rounded up to 64 columns, up to three narrower CTA columns
+// (768, 512, 256, 128, 64), so a shard is padded by less than 64 columns instead of up to
+// main - 1.
+// ld = the padded width = the pitch of the powers.
+struct SpmmPlan {
+    struct Seg {
+        int64_t col0; // first local column
+        int cols;     // CTA width (1024, 768, 512, 256, 128 or 64)
+        int64_t ncols; // columns of this segment (a multiple of cols)
+    };
+    Seg seg[4];
+    int nseg = 0;
+    int main_cols = 0;
+    int64_t ld = 0;
+};
+SpmmPlan spmm_plan(int64_t Np, int64_t w);
+// One launch per segment of the plan (*launches counts them).
+cudaError_t launch_spmm(const SparseA &sa, const SpmmPlan &P, const uint16_t *X, int64_t ldx, uint16_t *C,
+                        int64_t ldc, int64_t Mp, cudaStream_t s, int *launches);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
 // pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).

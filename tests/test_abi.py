@@ -49,10 +49,10 @@ def test_count_words_table1(oracle_mod):
 
 
 def test_spmm_width_option():
-    """The SpMM CTA width accepts 0 (automatic), 256, 512 and 1024 columns, nothing else."""
-    for cols in (256, 512, 1024, 0):
+    """The SpMM CTA width accepts 0 (automatic), +-256, +-512 and +-1024 columns, nothing else."""
+    for cols in (256, 512, 1024, -256, -512, -1024, 0):
         mp.set_spmm_width(cols)
-    for cols in (-1, 128, 768, 2048):
+    for cols in (-1, 128, 768, 2048, -768):
         with pytest.raises(mp.MinplusError) as e:
             mp.set_spmm_width(cols)
         assert e.value.status == 1
@@ -95,6 +95,35 @@ def test_shard_ranges_cover():
             assert w % 8 == 0 or w == N
     with pytest.raises(mp.MinplusError):
         mp.shard_range(10, 2, 2)
+
+
+@pytest.mark.parametrize("n", [9, 10, 11, 12, 13])
+def test_column_plan_padding(n):
+    """Shard quantisation: for every rank of G = 1..8 column shards of the
+    symmetric domain of A(D_n), the SpMM column plan pads its shard by less than 64 columns (one
+    DPX instruction spans 64), and covers it with at most four CTA widths."""
+    N = mp.count_words(n)
+    sg = mp.word_reversal(n)
+    D = int(np.sum(np.arange(N) <= sg))
+    for G in range(1, 9):
+        for r in range(G):
+            c0, c1 = mp.shard_range(D, G, r)
+            p = mp.column_plan(N, c1 - c0)
+            assert c1 - c0 <= p["ld"] < max(c1 - c0, 1) + 64, (n, G, r, p)
+            assert p["ld"] % 64 == 0 and p["main_cols"] in (256, 512, 1024)
+    # a forced width pads to a multiple of it; a negative one keeps the remainder columns
+    mp.set_spmm_width(1024)
+    try:
+        assert mp.column_plan(N, 3328)["ld"] == 4096
+    finally:
+        mp.set_spmm_width(-1024)
+    try:
+        p = mp.column_plan(N, 3328)
+        assert (p["ld"], p["main_cols"], p["tail_cols"]) == (3328, 1024, 256)
+        assert mp.column_plan(N, 960) == {"ld": 960, "main_cols": 1024, "tail_cols": 960}
+        assert mp.column_plan(N, 1800) == {"ld": 1856, "main_cols": 1024, "tail_cols": 832}
+    finally:
+        mp.set_spmm_width(0)
 
 
 def test_fingerprint_unit_matches_oracle(oracle_mod):

@@ -223,6 +223,29 @@ def test_spmm_width_power_until_periodic(mp, oracle_mod, n, width):
     assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
 
 
+@pytest.mark.parametrize("main", [-1024, -512, -256, 0])
+@pytest.mark.parametrize("N", [100, 700, 960, 1500, 1800])
+def test_spmm_remainder_columns(mp, oracle_mod, N, main):
+    """Column plans with narrower remainder CTA columns (mp_column_plan: 768 / 512 / 256 / 128
+    / 64 wide after the main width; e.g. N = 960 at main 1024 -> 768 + 128 + 64): every entry
+    of A^1..A^4 of a random sparse matrix through the SpMM kernel equals the oracle's."""
+    A = synth.transfer_like(N, N, 0.97, salt=700 + N)
+    use_kernel(mp, "spmm-greedy")
+    mp.set_spmm_width(main)
+    try:
+        got = mp.minplus_power_rows(A, np.arange(N), 4)
+        plan = mp.column_plan(N, N)
+    finally:
+        mp.set_spmm_width(0)
+        reset_kernel(mp)
+    assert N <= plan["ld"] < N + 64
+    X = A.copy()
+    for k in range(1, 5):
+        if k > 1:
+            X = oracle_mod.minplus(A, X)
+        assert np.array_equal(got[k - 1], X), k
+
+
 @pytest.mark.parametrize("kernel", ["dense", "tiles", "spmm", "spmm-greedy", "auto"])
 @pytest.mark.parametrize("seed", range(5))
 def test_power_until_periodic_random(mp, oracle_mod, seed, kernel):
