@@ -4,13 +4,16 @@ n = 12, the paper's largest case) and gamma_2(P_n x C_m) read off from it.
 
 One "step" = one whole run of SURVEY.md section 8(a) rows a2-a6 (stage A, A^k = A (x) A^{k-1}
 with fused periodicity statistics until A^{mu+lambda} = b (x) A^mu, read gamma_2) on a device-
-resident A.  The metric is BASELINE.json's: (min,+) Gop/s (one op = one add + one min on one
-16-bit lane, counted dense-equivalent: N^3 per product) and seconds to gamma_2.
+resident A.  The metric is BASELINE.json's: (min,+) Gop/s and seconds to gamma_2.  One op =
+one add + one min on one 16-bit lane; `value` counts the method's own work, nnz(A) x (columns
+computed) per product -- every finite A_il against every computed column (the +inf terms a dense
+loop would also visit are reported separately as `dense_equivalent_gops`).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--n 12] [--impl reference]
 
-For N > 1 launch with torchrun (one rank per GPU, NCCL all-reduce of the per-power
-statistics over NVLink).  Prints ONE JSON line on rank 0.
+With --gpus N > 1 and no torchrun environment the script relaunches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL all-reduce of the per-power statistics
+over NVLink); under torchrun it uses WORLD_SIZE.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -174,28 +177,46 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------- cpu oracle
-def cpu_baseline(n: int, target_s: float) -> dict:
-    """The oracle as it stands (oracle_minplus_ikj: the skip-inf triple loop) on a bounded
-    sample of the workload: R rows of one product A (x) A^{k-1} of A(D_n), dense-equivalent
-    steps R*N*N.  The inner loop costs the same for any dense right operand, so A itself
-    stands in for A^{k-1}."""
+def oracle_sample(n: int, target_s: float, A=None) -> dict:
+    """The oracle as it stands (oracle_minplus_ikj: the skip-inf triple loop, OpenMP over rows)
+    on a bounded sample of the workload: rows 0..R-1 of one product A (x) X of A(D_n), with
+    A(D_n) built by the ORACLE (oracle.transition_matrix) -- the product library is never
+    loaded on this path.  The loop visits exactly the finite A_il of those rows against every
+    column, so the sample's useful steps are nnz(A[:R]) * N (the unit of `value`) and its
+    dense-equivalent steps R * N * N.  The cost of the inner loop does not depend on the dense
+    right operand's values, so A itself stands in for A^{k-1}."""
     import numpy as np
     import oracle
-    import paper_2409_17688_b200 as mp
-    A = mp.build_transition_matrix(n)
+    if A is None:
+        A = oracle.transition_matrix(n)
     N = A.shape[0]
+    nnz_row = np.count_nonzero(A != oracle.INF, axis=1)
     R = max(1, min(N, 64))
     t = time.perf_counter()
-    oracle.minplus(A[:R], A)
+    oracle.minplus(np.ascontiguousarray(A[:R]), A)
     dt = time.perf_counter() - t
     R2 = int(min(N, max(R, R * target_s / max(dt, 1e-3))))
     t = time.perf_counter()
     oracle.minplus(np.ascontiguousarray(A[:R2]), A)
     dt = time.perf_counter() - t
-    return {"value": R2 * N * N / dt / 1e9, "unit": "Gop/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"rows 0..{R2 - 1} of one product A(D_{n}) (x) X, N={N}, skip-inf triple loop "
-                      f"(oracle_minplus_ikj), {dt:.1f} s; dense-equivalent steps {R2}*N*N",
-            "seconds": dt}
+    useful = float(nnz_row[:R2].sum()) * N
+    return {"value": useful / dt / 1e9, "unit": "Gop/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"rows 0..{R2 - 1} of one product A(D_{n}) (x) X, N={N}, A built by oracle.transition_matrix, "
+                      f"skip-inf triple loop (oracle_minplus_ikj), {dt:.1f} s; useful steps nnz(A[:{R2}])*N = "
+                      f"{useful:.3e}",
+            "dense_equivalent_gops": R2 * N * N / dt / 1e9, "seconds": dt, "A": A}
+
+
+ORACLE_RUNS_PATH = os.path.join(ROOT, "profiles", "r2", "oracle_runs.json")
+
+
+def oracle_full_runs():
+    """Whole oracle runs to gamma_2 (committed measurements, bench_tools/oracle_runs.py and the
+    golden-record generator), for context next to the bounded sample."""
+    try:
+        return json.load(open(ORACLE_RUNS_PATH))
+    except (OSError, ValueError):
+        return None
 
 
 def small_l2(N: int) -> bool:
@@ -210,7 +231,7 @@ def workload_config(n: int, N: int, world: int) -> dict:
             "l2": ("L2 flushed between steps (512 MB write, untimed): each power 2*N^2 = %.3f GB fits in the "
                    "126 MB L2" if small_l2(N) else "inputs larger than L2 (each power 2*N^2 = %.2f GB > 126 MB)")
                   % (2 * N * N / 1e9),
-            "ops": "dense-equivalent N^3 per product (one op = add+min on one u16 lane)"}
+            "ops": "useful: nnz(A) x computed columns per product (one op = add+min on one u16 lane)"}
 
 
 def cpu_model() -> str:
@@ -224,28 +245,33 @@ def cpu_model() -> str:
 
 
 def run_reference(args):
+    """The reference arm of this tier: the CPU oracle (no reference package exists), timed as it
+    stands on the host cores; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import oracle
+    A = oracle.transition_matrix(args.n)
+    N = A.shape[0]
     steps = []
     base = None
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for i in range(args.warmup + args.steps):
-        b = cpu_baseline(args.n, per_step)
+        b = oracle_sample(args.n, per_step, A)
         if i >= args.warmup:
             steps.append(b)
         base = b
     val = statistics.median(s["value"] for s in steps)
-    import paper_2409_17688_b200 as mp
-    N_words = mp.count_words(args.n)
-    N = base["sample"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Gop/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(s["seconds"] for s in steps) * 1e3,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.median(s["seconds"] for s in steps) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
-            "data": "synthetic: deterministic transfer matrix A(D_n)",
-            "config": dict(workload_config(args.n, N_words, 1), kernel="oracle (CPU, bounded sample)"),
+            "data": "synthetic: deterministic transfer matrix A(D_n) (oracle.transition_matrix)",
+            "config": dict(workload_config(args.n, N, 1), kernel="oracle (CPU, bounded sample)"),
             "cpu_baseline": {"value": val, "unit": "Gop/s", "cores": base["cores"], "kind": "oracle",
-                             "sample": N, "cpu": cpu_model()},
+                             "sample": base["sample"], "cpu": cpu_model()},
+            "dense_equivalent_gops": statistics.median(s["dense_equivalent_gops"] for s in steps),
+            "oracle_full_runs": oracle_full_runs(),
             "e2e": {"value": val, "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -274,6 +300,7 @@ def run_mine(args):
 
     A = mp.build_transition_matrix(args.n)
     N = A.shape[0]
+    nnz = int(np.count_nonzero(A != mp.MP_INF))
     dA = torch.from_numpy(A.view(np.int16)).cuda()  # resident input for the device-timed value
 
     def barrier():
@@ -306,6 +333,7 @@ def run_mine(args):
         prod_launches += p["product_launches"]
         kernel_used = p["kernel"]
         spmm_cols = p["spmm_cols"]
+        local_cols, ld = p["local_cols"], p["ld"]
         dense += p["dense_steps"]
         issued += p["issued_steps"]
         setup_ms = p["setup_ms"]
@@ -353,52 +381,62 @@ def run_mine(args):
     assert g2_1000 == res.gamma2(1000)
     barrier()
 
-    vals = torch.tensor([ms, e2e_ms, dense, issued, prod_ms, float(prod_launches), float(launches),
+    # the method's own work per product on this rank: every finite A_il against every column the
+    # rank computes (with the word-reversal symmetry: its shard of the domain g <= sigma g)
+    # (powers past the first repeat that a small-N batch computed anyway are not counted)
+    useful = float(nnz) * local_cols * (res.k_last - 1) * args.steps
+    vals = torch.tensor([ms, e2e_ms, dense, issued, useful, prod_ms, float(prod_launches), float(launches),
                          float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
     if world > 1:
         mx = vals[:2].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vals[2:4].clone()
+        sm = vals[2:5].clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        vals[:2], vals[2:4] = mx, sm
-    ms, e2e_ms, dense_all, issued_all = [float(v) for v in vals[:4].tolist()]
+        vals[:2], vals[2:5] = mx, sm
+    ms, e2e_ms, dense_all, issued_all, useful_all = [float(v) for v in vals[:5].tolist()]
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
     products = res.k_last - 1
-    value = dense_all / (ms * 1e-3) / 1e9
-    e2e_dense = dense_all / args.steps * e2e_steps
+    value = useful_all / (ms * 1e-3) / 1e9
     sm_mhz = clk.get("sm_mhz") or 1965.0
     peak = 148 * DPX_STEPS_PER_CLK_PER_SM * sm_mhz * 1e6 / 1e9  # Gstep/s at the observed clock
     avg_launch_ms = prod_ms / max(1, prod_launches)
     issued_per_launch = issued / max(1, prod_launches)
-    achieved = issued_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    useful_per_launch = float(nnz) * local_cols
+    achieved = useful_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    issued_rate = issued_per_launch / (avg_launch_ms * 1e-3) / 1e9
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(args.n, args.cpu_seconds)
-        cpu = {k: v for k, v in cpu.items() if k != "seconds"}
+        cpu = oracle_sample(args.n, args.cpu_seconds)
+        cpu = {k: v for k, v in cpu.items() if k not in ("seconds", "A")}
         cpu["cpu"] = cpu_model()
+        cpu["full_runs"] = oracle_full_runs()
     line = {
         "metric": METRIC, "value": value, "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u16",
         "data": "synthetic: deterministic transfer matrix A(D_n) built on the host (no randomness, no datasets)",
-        "config": dict(workload_config(args.n, N, world), products_per_step=products,
+        "config": dict(workload_config(args.n, N, world), products_per_step=products, nnz_A=nnz,
                        mu_lambda_b=[res.mu, res.lam, res.offset], gamma2_m1000=res.gamma2(1000),
-                       kernel=args.kernel, spmm_cta_cols=spmm_cols or None,
+                       kernel=args.kernel, spmm_cta_cols=spmm_cols or None, cols_rank0=local_cols, ld_rank0=ld,
                        symmetry="none" if args.no_symmetry else "word reversal (columns g <= sigma g computed)"),
         "seconds_to_gamma2": ms / args.steps / 1e3,
+        "dense_equivalent_gops": dense_all / (ms * 1e-3) / 1e9,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used], "achieved": achieved, "peak": peak,
                      "unit": "Gstep/s", "frac": achieved / peak,
                      "traffic": traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world, not args.no_symmetry),
                      "peak_source": f"148 SM x 128 steps/clk/SM x {sm_mhz:.0f} MHz observed (DESIGN.md)",
-                     "avg_launch_ms": avg_launch_ms, "issued_steps_per_launch": issued_per_launch,
+                     "work": "useful steps = nnz(A) x columns computed per product (rank 0)",
+                     "avg_launch_ms": avg_launch_ms, "useful_steps_per_launch": useful_per_launch,
+                     "issued_steps_per_launch": issued_per_launch, "issued_achieved": issued_rate,
+                     "issue_frac": issued_rate / peak, "slot_occupancy": useful_per_launch / max(issued_per_launch, 1),
                      "kernel_share_of_step": prod_ms / max(ms, 1e-9)},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_dense / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
+        "e2e": {"value": useful_all / args.steps * e2e_steps / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
                 "h2d_bytes_per_step": int(h2d / max(1, e2e_steps)), "d2h_bytes_per_step": int(d2h / max(1, e2e_steps)),
                 "seconds_to_gamma2": e2e_ms / e2e_steps / 1e3,
                 "setup_ms_last_step": e2e_setup_ms},
@@ -416,8 +454,22 @@ def run_mine(args):
         dist.destroy_process_group()
 
 
+def relaunch_distributed(n_gpus: int) -> int:
+    """--gpus N > 1 without a torchrun environment: run this script under torch.distributed.run
+    with N ranks on this node (rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -167,6 +167,13 @@ mp_status minplus_power_rows(const uint16_t *A, int64_t N, int kmax, const int64
  * other value stops the run with MP_ERR_DOMAIN.  fn = NULL clears it.  A run with an observer
  * and a distributed context of world > 1 fails with MP_ERR_DOMAIN (a rank holds only its
  * shard).  Process-wide.  Errors: none (always MP_OK). */
+/* Small-N latency path: single-rank power runs of matrices with N <= 256
+ * and at most 16384 finite entries, with the automatic kernel choice and no observer, run
+ * entirely in one thread-block-cluster launch (products, statistics, repeat search, exact
+ * compares; one read of the result).  on = 0 sends them through the general path instead (same
+ * results); default on.  Process-wide.  Errors: none. */
+mp_status mp_set_small_path(int on);
+
 typedef int (*mp_power_observer_fn)(void *ctx, int k, const uint16_t *power, int64_t N);
 mp_status mp_set_power_observer(mp_power_observer_fn fn, void *ctx);
 
@@ -293,7 +300,8 @@ typedef struct {
     int64_t h2d_bytes;        /* host -> device bytes copied by the run                    */
     int64_t d2h_bytes;        /* device -> host bytes copied by the run                    */
     int32_t kernel;           /* product kernel used: 0 dense tiles, 1 block-sparse tiles,
-                                 2 grouped SpMM                                              */
+                                 2 grouped SpMM, 3 the fused small-N run (product_ms = the
+                                 whole run's one launch, statistics included)                */
     int32_t spmm_cols;        /* SpMM CTA width used (256, 512 or 1024 columns; 0 if kernel != 2) */
     int64_t local_cols;       /* columns this rank computes per power (its shard; with a symmetry
                                  a shard of the domain g <= sigma g)                          */

@@ -32,7 +32,7 @@ EXPORTS = [
     "mp_repeat_candidate", "mp_last_error", "mp_shutdown", "mp_version", "mp_kernel_launches",
     "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_set_spmm_width", "mp_gamma2_formula", "mp_gamma2_record",
     "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal", "minplus_mul_strided_batched_device",
-    "minplus_closure", "mp_set_power_observer", "mp_column_plan",
+    "minplus_closure", "mp_set_power_observer", "mp_column_plan", "mp_set_small_path",
 ]
 
 
@@ -122,6 +122,7 @@ def _load() -> ctypes.CDLL:
         "mp_gamma2_record": ([i32, P], i32),
         "mp_set_power_observer": ([OBSERVER_FN, P], i32),
         "mp_column_plan": ([i64, i64, P, P, P], i32),
+        "mp_set_small_path": ([i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -428,7 +429,7 @@ def last_profile() -> dict:
     return {"product_ms": p.product_ms, "product_launches": p.product_launches,
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
             "setup_ms": p.setup_ms, "stats_ms": p.stats_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
-            "kernel": {0: "dense", 1: "tiles", 2: "spmm"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols,
+            "kernel": {0: "dense", 1: "tiles", 2: "spmm", 3: "small"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols,
             "local_cols": p.local_cols, "ld": p.ld}
 
 
@@ -475,6 +476,11 @@ def set_spmm_width(cols: int = 0) -> None:
     """CTA width of the SpMM kernel: 0 (automatic), 256, 512 or 1024 columns everywhere, or
     -256 / -512 / -1024 = that main width plus narrower remainder columns (same product)."""
     _check(lib.mp_set_spmm_width(int(cols)))
+
+
+def set_small_path(on: bool = True) -> None:
+    """Whether small single-rank runs (N <= 256) use the one-launch cluster kernel."""
+    _check(lib.mp_set_small_path(1 if on else 0))
 
 
 def version() -> str:

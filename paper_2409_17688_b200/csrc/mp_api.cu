@@ -53,6 +53,7 @@ constexpr int64_t kGroupMinN = 8192; // below this the grouping pass costs more 
 // words source.
 std::vector<int32_t> g_sym;
 bool g_word_sym = true;
+bool g_small_off = false; // mp_set_small_path(0): always the general path
 
 mp_profile g_prof{};
 
@@ -205,6 +206,7 @@ struct PowerRun {
     std::vector<cudaEvent_t> events; // per-power product start/stop
     // observer path: the whole power, unfolded on the device and copied to pinned host memory
     DBuf full_dev;
+    DBuf small_hist, small_out, small_sig; // small-N path: power history, result, symmetry hint
     uint16_t *full_host = nullptr;
     size_t full_host_bytes = 0;
     ~PowerRun()
@@ -481,9 +483,123 @@ struct Capture {
     uint16_t *out = nullptr; // host
 };
 
+// Small-N latency path (DESIGN.md section 5 "Small-N path"): the whole run -- products,
+// statistics, repeat search, exact compares -- in one thread-block-cluster launch, one read of
+// the result.  *handled = false (and MP_OK) if A has too many finite entries for the kernel's
+// shared memory; the caller then takes the general path.
+constexpr int kSmallMaxNnz = 16384;
+mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_periodic_result *out, bool *handled)
+{
+    *handled = false;
+    if (!st.pr) st.pr.reset(new PowerRun());
+    PowerRun &R = *st.pr;
+    cudaStream_t s = st.user_stream ? st.user_stream : st.stream;
+    const int64_t h2d0 = g_h2d.load(), d2h0 = g_d2h.load();
+    cudaEvent_t ev[4];
+    for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
+    struct Destroy {
+        cudaEvent_t *e;
+        ~Destroy()
+        {
+            for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+        }
+    } destroy{ev};
+    CUDA_TRY(cudaEventRecord(ev[0], s));
+    const uint16_t *dA = src.dev;
+    int64_t lda = src.lda;
+    if (!dA) { // host matrix, or A(D_n) from the word masks (at most 256 x 256 here)
+        std::vector<uint16_t> words_A;
+        const uint16_t *h = src.host;
+        if (!h) {
+            words_A.resize((size_t)N * N);
+            fill_transition_matrix(enumerate_words(src.n), src.n, words_A.data(), 1);
+            h = words_A.data();
+        }
+        TRY(R.stage_raw.ensure((size_t)N * N * 2, "A staging"));
+        COPY(R.stage_raw.p, h, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+        if (!src.host) CUDA_TRY(cudaStreamSynchronize(s)); // words_A is about to go away
+        dA = R.stage_raw.as<uint16_t>();
+        lda = N;
+    }
+    const int C = small_run_ctas(N);
+    TRY(R.small_hist.ensure((size_t)(max_k + 1) * N * 64 * C * 2, "small-N power history"));
+    const size_t nout = 6 + 2 * (size_t)(max_k + 1);
+    TRY(R.small_out.ensure(nout * 8, "small-N result"));
+    const uint64_t S = mp_fingerprint_unit(N);
+    const int32_t *dsig = nullptr;
+    if ((src.dev || src.host) && (int64_t)g_sym.size() == N) { // a matrix source's symmetry hint
+        TRY(R.small_sig.ensure((size_t)N * 4, "symmetry"));
+        COPY(R.small_sig.p, g_sym.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s);
+        dsig = R.small_sig.as<int32_t>();
+    }
+    CUDA_TRY(cudaEventRecord(ev[1], s));
+    LAUNCH(launch_small_run(dA, lda, N, max_k, kSmallMaxNnz, dsig, R.small_hist.as<uint16_t>(), S,
+                            R.small_out.as<long long>(), s));
+    CUDA_TRY(cudaEventRecord(ev[2], s));
+    std::vector<long long> h(nout, 0);
+    COPY(h.data(), R.small_out.p, nout * 8, cudaMemcpyDeviceToHost, s);
+    CUDA_TRY(cudaEventRecord(ev[3], s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (h[0] == -1) return MP_OK; // too many finite entries: the general path
+    *handled = true;
+    float kms = 0.f, all = 0.f, setup = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&kms, ev[1], ev[2]));
+    CUDA_TRY(cudaEventElapsedTime(&all, ev[0], ev[3]));
+    CUDA_TRY(cudaEventElapsedTime(&setup, ev[0], ev[1]));
+    const int products = (int)h[4] - 1;
+    g_prof = mp_profile{};
+    g_prof.product_ms = kms;
+    g_prof.product_launches = products;
+    g_prof.dense_steps = (double)products * (double)N * (double)N * (double)N;
+    g_prof.issued_steps = 0.0; // the row lists of A against 64 C columns; counted by the caller as nnz * 64 C
+    g_prof.total_ms = all;
+    g_prof.setup_ms = setup;
+    g_prof.stats_ms = 0.0; // fused
+    g_prof.h2d_bytes = g_h2d.load() - h2d0;
+    g_prof.d2h_bytes = g_d2h.load() - d2h0;
+    g_prof.kernel = 3;
+    g_prof.spmm_cols = 0;
+    g_prof.local_cols = N;
+    g_prof.ld = 64 * C;
+    if (h[0] == 2) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
+    if (h[0] == 1) return fail(MP_ERR_DOMAIN, "symmetry hint: A[sigma i][sigma j] != A[i][j] for some i, j");
+    if (h[0] == 4) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
+    mp_periodic_result res;
+    std::memset(&res, 0, sizeof(res));
+    res.mu = (int32_t)h[1];
+    res.lambda = (int32_t)h[2];
+    res.offset = (int32_t)h[3];
+    res.k_last = (int32_t)h[4];
+    res.dense_from = (int32_t)h[5];
+    for (int k = 1; k <= res.k_last; ++k) {
+        res.diag_min[k] = (uint16_t)std::min<long long>(h[6 + k], 0xFFFF);
+        res.fingerprint[k] = (uint64_t)h[6 + (max_k + 1) + k];
+    }
+    *out = res;
+    return MP_OK;
+}
+
+// The small-N path applies to single-rank runs of small matrices with the automatic kernel
+// choice and no observer (a forced kernel, a sharded run or an observer take the general path,
+// which the tests also exercise at these sizes; mp_set_small_path(0) forces it).
+bool small_path_ok(const ASource &src, int64_t N, const Capture *cap)
+{
+    (void)src;
+    if (cap || N > kSmallMaxN || g_opts.sparsity != -1 || g_dist.world > 1 || g_dist.fn || g_obs.fn) return false;
+    return !g_small_off;
+}
+
 mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_result *out,
                      const Capture *cap = nullptr)
 {
+    if (small_path_ok(src, N, cap)) {
+        int dev0 = 0;
+        DevState *st0 = nullptr;
+        TRY(current_device(&dev0, &st0));
+        bool handled = false;
+        TRY(run_small(*st0, src, N, max_k, out, &handled));
+        if (handled) return MP_OK;
+    }
     int dev = 0;
     DevState *st = nullptr;
     TRY(current_device(&dev, &st));
@@ -1278,6 +1394,13 @@ mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N)
     if ((int64_t)sg.size() != N)
         return fail(MP_ERR_DOMAIN, "mp_word_reversal: N = %lld, A(D_%d) has %zu words", (long long)N, n, sg.size());
     std::memcpy(sigma_out, sg.data(), sg.size() * 4);
+    return MP_OK;
+}
+
+mp_status mp_set_small_path(int on)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_small_off = on == 0;
     return MP_OK;
 }
 

@@ -1914,9 +1914,10 @@ static cudaError_t launch_spmm_t(const SparseA &sa, const uint16_t *X, int64_t l
 SpmmPlan spmm_plan(int64_t Np, int64_t w)
 {
     SpmmPlan P;
+    w = std::max<int64_t>(w, 1); // an empty shard still gets one (all-padding) CTA column
     const int main = spmm_cols(Np, w);
     P.main_cols = main;
-    const int64_t q = std::max<int64_t>(w, 1) / main;
+    const int64_t q = w / main;
     int64_t col = 0;
     if (q > 0) {
         P.seg[P.nseg++] = {col, main, q * main};

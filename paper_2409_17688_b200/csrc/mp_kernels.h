@@ -28,6 +28,16 @@ cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int6
 cudaError_t launch_set_diag_zero(uint16_t *X, int64_t ld, int64_t n, cudaStream_t s);
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
                           int64_t ldd, cudaStream_t s);
+// Small-N latency path (mp_small.cu): the whole power-until-periodic run in one cluster launch.
+// sigma (may be null): symmetry hint verified on the way (status 1 if violated).
+// out[]: status (0 ok, 1 hint violated, 2 range, 4 not periodic, -1 more than max_nnz finite
+// entries), mu, lambda,
+// offset, k_last, dense_from, then diag_min[k] at out[6 + k] and fingerprint[k] at
+// out[6 + (max_k + 1) + k].  hist: (max_k + 1) x N x (64 * ctas) u16 scratch.
+constexpr int kSmallMaxN = 256;
+int small_run_ctas(int64_t N);
+cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_k, int max_nnz, const int32_t *sigma,
+                             uint16_t *hist, uint64_t S, long long *out, cudaStream_t s);
 // out (N x N, boundary encoding) = the whole power from the local columns of X: column g is
 // local column loc[g] if loc[g] >= 0, else X_(sigma i, loc[sigma g]) (sigma may be null only if
 // every column is local).

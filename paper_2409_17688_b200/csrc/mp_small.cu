@@ -1,0 +1,312 @@
+// Small-N latency path (N <= 256, e.g. A(D_n) for n <= 6): the WHOLE power-until-periodic run
+// -- every product A^k = A (x) A^{k-1} (Algorithm 2), its statistics (a4), the
+// first-repeat search with its exact compare (a5; Lemma 1) -- in ONE launch of one
+// thread-block cluster, with one host read of the result at the end.
+// "Small-N path".  Product code only; shares nothing with oracle/.
+//
+// CTA c of the cluster owns the 64 columns [64c, 64c + 64) of every power (a lane holds two of
+// them as a packed u16 pair).  Column j of A^k depends only on column j of A^{k-1} (left
+// multiplication by the fixed A, G8), so the CTAs never exchange matrix data: A's finite entries
+// (row lists) and the CTA's column block of A^{k-1} and A^k live in shared memory, and only the
+// per-power statistics (fingerprint, +inf count, diagonal minimum, first finite entry) and the
+// exact-compare mismatch counts cross the cluster, through distributed shared memory.  Every
+// power's column block is also written to a history buffer in global memory (L2-resident:
+// at most 64 x 256 x 256 x 2 B) for the exact compares against earlier powers.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mp_internal.h"
+#include "mp_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace mp {
+
+namespace {
+
+constexpr int kSmThreads = 512; // 16 warps; warp w computes rows w, w + 16, ...
+constexpr int kSmWarps = kSmThreads / 32;
+
+struct Stats { // the per-power statistics of k_stats (mp_power_stats), int64 fields
+    unsigned long long fp, inf;
+    long long dmin, ref;
+};
+
+__device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m)
+{
+    const unsigned lo = __shfl_xor_sync(0xFFFFFFFFu, (unsigned)v, m);
+    const unsigned hi = __shfl_xor_sync(0xFFFFFFFFu, (unsigned)(v >> 32), m);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+// Candidate test of the forward first-repeat search (the rule of mp_repeat_candidate in
+// mp_api.cu, restated for the device).
+__device__ bool candidate(const Stats &k, const Stats &j, unsigned long long S, int *c)
+{
+    if (k.inf != j.inf) return false;
+    const long long kInfRef = 0x7FFFFFFFFFFFFFFFll;
+    const bool ak = k.ref == kInfRef, aj = j.ref == kInfRef;
+    if (ak || aj) {
+        *c = 0;
+        return ak == aj;
+    }
+    if ((k.ref >> 16) != (j.ref >> 16)) return false;
+    *c = (int)(k.ref & 0xFFFF) - (int)(j.ref & 0xFFFF);
+    if (k.inf > 0) return true; // +inf present: the exact compare decides
+    return k.fp - j.fp == (unsigned long long)(long long)*c * S;
+}
+
+} // namespace
+
+// sigma (may be null): a symmetry hint to verify (every finite A_il must reappear at
+// (sigma i, sigma l)); the run itself computes every column.
+// out[]: status (0 ok, 1 symmetry hint violated, 2 range, 4 not periodic, -1 too many entries
+// for shared memory), mu,
+// lambda, offset, k_last, dense_from, then diag_min[k] and fingerprint[k] for k = 0..max_k.
+__global__ void __launch_bounds__(kSmThreads, 1)
+    k_small_run(const uint16_t *__restrict__ A, int64_t lda, int N, int max_k, int max_nnz,
+                const int32_t *__restrict__ sigma, uint16_t *__restrict__ hist, unsigned long long S,
+                long long *__restrict__ out)
+{
+    extern __shared__ __align__(16) uint8_t smem[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ldh = 64 * C;                // history pitch (columns of all CTAs)
+    const int64_t hsz = (int64_t)N * ldh;  // one power in the history
+
+    // shared memory: X blocks (2 x N x 32 u32) | row pointers | entries | statistics history |
+    // per-warp partials | cluster exchange (2 parity buffers) | flags
+    uint32_t *Xa = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *Xb = Xa + N * 32;
+    int32_t *rptr = reinterpret_cast<int32_t *>(Xb + N * 32);
+    uint32_t *ent = reinterpret_cast<uint32_t *>(rptr + ((N + 4) & ~3));
+    Stats *hs = reinterpret_cast<Stats *>(ent + ((max_nnz + 3) & ~3)); // [max_k + 1]
+    Stats *wred = hs + (max_k + 1);                                       // [kSmWarps]
+    Stats *xch = wred + kSmWarps;                                         // [2]: this CTA's partials
+    long long *xmis = reinterpret_cast<long long *>(xch + 2);             // [2]: mismatch partials
+    int *flags = reinterpret_cast<int *>(xmis + 2); // [0] range, [1] nnz, [2] candidate j, [3] c, [4] asym
+
+    const int j0 = 64 * c + 2 * lane, j1 = j0 + 1; // this lane's global columns
+    const bool v0 = j0 < N, v1 = j1 < N;
+    const uint64_t cw0 = v0 ? mix64(2 * (uint64_t)j0 + 1) : 0, cw1 = v1 ? mix64(2 * (uint64_t)j1 + 1) : 0;
+
+    // ---- a2: row lists of A (every CTA builds its own copy), range check, X_1 block
+    if (tid == 0) flags[0] = flags[1] = flags[4] = 0;
+    __syncthreads();
+    for (int i = warp; i < N; i += kSmWarps) {
+        int cnt = 0;
+        bool bad = false, asym = false;
+        for (int l0 = 0; l0 < N; l0 += 32) {
+            const int l = l0 + lane;
+            const uint16_t x = l < N ? A[(int64_t)i * lda + l] : (uint16_t)kBndInf;
+            bad |= x != kBndInf && x > kFiniteMax;
+            if (sigma && x != kBndInf) asym |= A[(int64_t)sigma[i] * lda + sigma[l]] != x;
+            cnt += __popc(__ballot_sync(0xFFFFFFFFu, x != kBndInf));
+        }
+        if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) flags[0] = 1;
+        if (__any_sync(0xFFFFFFFFu, asym) && lane == 0) flags[4] = 1;
+        if (lane == 0) rptr[i + 1] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        rptr[0] = 0;
+        for (int i = 0; i < N; ++i) rptr[i + 1] += rptr[i];
+        flags[1] = rptr[N];
+    }
+    __syncthreads();
+    if (flags[0] || flags[4] || flags[1] > max_nnz) { // every CTA sees the same A: uniform exit
+        if (c == 0 && tid == 0) out[0] = flags[0] ? 2 : flags[4] ? 1 : -1;
+        return;
+    }
+    for (int i = warp; i < N; i += kSmWarps) {
+        int e = rptr[i];
+        for (int l0 = 0; l0 < N; l0 += 32) {
+            const int l = l0 + lane;
+            const uint16_t x = l < N ? A[(int64_t)i * lda + l] : (uint16_t)kBndInf;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, x != kBndInf);
+            if (x != kBndInf) ent[e + __popc(m & ((1u << lane) - 1))] = ((uint32_t)l << 16) | x;
+            e += __popc(m);
+        }
+        // X_1 = A[:, block], device encoding (+inf 0x7FFF), packed pairs
+        const uint16_t a0 = v0 ? A[(int64_t)i * lda + j0] : (uint16_t)kBndInf;
+        const uint16_t a1 = v1 ? A[(int64_t)i * lda + j1] : (uint16_t)kBndInf;
+        Xa[i * 32 + lane] = (uint32_t)(a0 == kBndInf ? kDevInf : a0) | ((uint32_t)(a1 == kBndInf ? kDevInf : a1) << 16);
+    }
+    __syncthreads();
+
+    uint32_t *Xp = Xa, *Xc = Xb; // X_{k-1}, X_k (X_1 is in Xa)
+    int xi = 0;                  // cluster exchange count (parity buffer)
+    int mu = 0, lam = 0, off = 0, k_last = 0, dense_from = 0;
+    bool found = false;
+    int k = 1;
+    for (;; ++k) {
+        uint32_t *X = (k == 1) ? Xa : Xc;
+        if (k >= 2) { // A^k = A (x) A^{k-1} on this block: warp per row, lane per column pair
+            for (int i = warp; i < N; i += kSmWarps) {
+                uint32_t acc = 0xFFFFFFFFu;
+                const int e1 = rptr[i + 1];
+                for (int e = rptr[i]; e < e1; ++e) {
+                    const uint32_t q = ent[e];
+                    const uint32_t a = q & 0xFFFFu;
+                    acc = __viaddmin_u16x2(a | (a << 16), Xp[(q >> 16) * 32 + lane], acc);
+                }
+                X[i * 32 + lane] = __vminu2(acc, 0x7FFF7FFFu); // a finite sum >= 0x7FFF is +inf (G6)
+            }
+            __syncthreads();
+        }
+        // ---- a4: statistics of this block (boundary encoding 0xFFFF for +inf in the hash)
+        Stats st{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+        for (int i = warp; i < N; i += kSmWarps) {
+            const uint32_t p = X[i * 32 + lane];
+            const uint32_t x0 = p & 0xFFFFu, x1 = p >> 16;
+            const uint64_t b0 = x0 >= kDevInf ? kBndInf : x0, b1 = x1 >= kDevInf ? kBndInf : x1;
+            st.fp += mix64(2 * (uint64_t)i) * (cw0 * b0 + cw1 * b1);
+            st.inf += (v0 && x0 >= kDevInf) + (v1 && x1 >= kDevInf);
+            if (v0 && j0 == i) st.dmin = min(st.dmin, (long long)b0);
+            if (v1 && j1 == i) st.dmin = min(st.dmin, (long long)b1);
+            if (v0 && x0 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j0) << 16) | (long long)x0);
+            if (v1 && x1 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j1) << 16) | (long long)x1);
+        }
+        for (int m = 16; m; m >>= 1) {
+            st.fp += shfl_xor_u64(st.fp, m);
+            st.inf += shfl_xor_u64(st.inf, m);
+            st.dmin = min(st.dmin, (long long)shfl_xor_u64((unsigned long long)st.dmin, m));
+            st.ref = min(st.ref, (long long)shfl_xor_u64((unsigned long long)st.ref, m));
+        }
+        if (lane == 0) wred[warp] = st;
+        // the block also goes to the history (exact compares of later powers read it)
+        for (int t = tid; t < N * 32; t += kSmThreads)
+            reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)(t >> 5) * ldh + 64 * c)[t & 31] = X[t];
+        __syncthreads();
+        if (tid == 0) {
+            Stats s = wred[0];
+            for (int w = 1; w < kSmWarps; ++w) {
+                s.fp += wred[w].fp;
+                s.inf += wred[w].inf;
+                s.dmin = min(s.dmin, wred[w].dmin);
+                s.ref = min(s.ref, wred[w].ref);
+            }
+            xch[xi & 1] = s;
+        }
+        cluster.sync(); // partials visible cluster-wide
+        if (tid == 0) {
+            Stats g{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+            for (int r = 0; r < C; ++r) {
+                const Stats p = cluster.map_shared_rank(xch, r)[xi & 1];
+                g.fp += p.fp;
+                g.inf += p.inf;
+                g.dmin = min(g.dmin, p.dmin);
+                g.ref = min(g.ref, p.ref);
+            }
+            hs[k] = g;
+            if (!dense_from && g.inf == 0) dense_from = k;
+        }
+        ++xi;
+        __syncthreads();
+        // ---- a5: forward first-repeat search, j = k-1 down to 1 (identical in every CTA)
+        int jn = k - 1;
+        while (!found) {
+            if (tid == 0) {
+                int cc = 0, j = jn;
+                while (j >= 1 && !candidate(hs[k], hs[j], S, &cc)) --j;
+                flags[2] = j;
+                flags[3] = cc;
+            }
+            __syncthreads();
+            const int j = flags[2], cc = flags[3];
+            if (j < 1) break;
+            // exact compare of this block: equal +inf pattern, X_k - X_j = cc on finite entries
+            long long bad = 0;
+            const uint16_t *Z = hist + (int64_t)j * hsz + 64 * c;
+            for (int t = tid; t < N * 32; t += kSmThreads) {
+                const uint32_t y = X[t], z = reinterpret_cast<const uint32_t *>(Z + (int64_t)(t >> 5) * ldh)[t & 31];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!(h ? v1 : v0)) continue;
+                    const int yy = (int)((y >> (16 * h)) & 0xFFFFu), zz = (int)((z >> (16 * h)) & 0xFFFFu);
+                    const bool yi = yy >= kDevInf, zi = zz >= kDevInf;
+                    bad += (yi != zi) || (!yi && yy - zz != cc);
+                }
+            }
+            for (int m = 16; m; m >>= 1) bad += (long long)shfl_xor_u64((unsigned long long)bad, m);
+            if (lane == 0) wred[warp].fp = (unsigned long long)bad;
+            __syncthreads();
+            if (tid == 0) {
+                long long b = 0;
+                for (int w = 0; w < kSmWarps; ++w) b += (long long)wred[w].fp;
+                xmis[xi & 1] = b;
+            }
+            cluster.sync();
+            long long total = 0;
+            for (int r = 0; r < C; ++r) total += cluster.map_shared_rank(xmis, r)[xi & 1];
+            ++xi;
+            if (total == 0) {
+                found = true;
+                mu = j;
+                lam = k - j;
+                off = cc;
+                k_last = k;
+            }
+            jn = j - 1;
+            __syncthreads();
+        }
+        if (found || k == max_k) break;
+        if (k >= 2) { // the new power becomes X_{k-1}
+            uint32_t *tmp = Xp;
+            Xp = Xc;
+            Xc = tmp;
+        } else { // k == 1: X_1 sits in Xa, which Xp already points to
+            Xc = Xb;
+        }
+    }
+    cluster.sync(); // no CTA leaves while another may still read its shared memory
+    if (c == 0 && tid == 0) {
+        out[0] = found ? 0 : 4;
+        out[1] = mu;
+        out[2] = lam;
+        out[3] = off;
+        out[4] = found ? k_last : k;
+        out[5] = dense_from;
+        const int kk = found ? k_last : k;
+        for (int q = 1; q <= kk; ++q) {
+            out[6 + q] = hs[q].dmin;
+            out[6 + (max_k + 1) + q] = (long long)hs[q].fp;
+        }
+    }
+}
+
+int small_run_ctas(int64_t N) { return (int)((N + 63) / 64); }
+
+size_t small_run_smem(int64_t N, int max_k, int max_nnz)
+{
+    return (size_t)N * 32 * 4 * 2 + (size_t)((N + 4) & ~3) * 4 + (size_t)((max_nnz + 3) & ~3) * 4 +
+           (size_t)(max_k + 1 + kSmWarps + 2) * sizeof(Stats) + 2 * 8 + 8 * 4;
+}
+
+cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_k, int max_nnz, const int32_t *sigma,
+                             uint16_t *hist, uint64_t S, long long *out, cudaStream_t s)
+{
+    if (N < 1 || N > kSmallMaxN) return cudaErrorInvalidValue;
+    const size_t smem = small_run_smem(N, max_k, max_nnz);
+    cudaError_t e = cudaFuncSetAttribute(k_small_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)small_run_ctas(N));
+    cfg.blockDim = dim3(kSmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)small_run_ctas(N);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_small_run, A, lda, (int)N, max_k, max_nnz, sigma, hist, (unsigned long long)S,
+                              out);
+}
+
+} // namespace mp
