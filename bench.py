@@ -34,7 +34,8 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 DPX_STEPS_PER_CLK_PER_SM = 128  # 64 VIADDMNMX.U16x2 lanes / clk / SM x 2 steps
 KERNEL_NAMES = {"dense": "k_minplus (dense tiles, VIADDMNMX.U16x2)",
                 "tiles": "k_minplus (block-sparse tiles, VIADDMNMX.U16x2)",
-                "spmm": "k_spmm (grouped SpMM, VIADDMNMX.U16x2)"}
+                "spmm": "k_spmm (grouped SpMM, VIADDMNMX.U16x2)",
+                "small": "k_small_run (the whole run in one thread-block-cluster launch, VIADDMNMX.U16x2)"}
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
@@ -61,6 +62,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-row-reuse", action="store_true",
+                    help="do not use the row-inclusion reuse of A(D_n) (the SpMM over every finite entry)")
     ap.add_argument("--no-symmetry", action="store_true",
                     help="do not pass the word-reversal symmetry of A(D_n) (compute every column)")
     return ap.parse_args()
@@ -295,6 +298,10 @@ def run_mine(args):
     # A(D_n) is invariant under reversing every word (the path's reflection): the library
     # then computes only the columns g <= sigma(g) and verifies the hint on the device
     mp.set_symmetry(None if args.no_symmetry else mp.word_reversal(args.n))
+    # A is A(D_n): the library verifies that on the device and then uses the row-inclusion
+    # reuse; --no-row-reuse times the plain grouped SpMM instead
+    mp.set_transfer_hint(args.n)
+    mp.set_row_reuse(not args.no_row_reuse)
     stream = torch.cuda.current_stream()
     mp.set_stream(stream)
 
@@ -316,7 +323,7 @@ def run_mine(args):
     barrier()
     torch.cuda.synchronize()
     launches0 = mp.kernel_launches()
-    prod_ms, prod_launches, dense, issued = 0.0, 0, 0.0, 0.0
+    prod_ms, prod_launches, dense, issued, spmm_ms = 0.0, 0, 0.0, 0.0, 0.0
     stats_ms, total_lib_ms, setup_ms = 0.0, 0.0, 0.0
     # Small powers fit in the 126 MB L2: flush it between steps (a 512 MB write, excluded from
     # the timing by per-step events); large powers exceed it anyway.
@@ -330,10 +337,12 @@ def run_mine(args):
         ev[s_i][1].record(stream)
         p = mp.last_profile()
         prod_ms += p["product_ms"]
+        spmm_ms += p["spmm_ms"]
         prod_launches += p["product_launches"]
         kernel_used = p["kernel"]
         spmm_cols = p["spmm_cols"]
         local_cols, ld = p["local_cols"], p["ld"]
+        row_levels, row_parents = p["row_levels"], p["row_parents"]
         dense += p["dense_steps"]
         issued += p["issued_steps"]
         setup_ms = p["setup_ms"]
@@ -403,11 +412,14 @@ def run_mine(args):
     value = useful_all / (ms * 1e-3) / 1e9
     sm_mhz = clk.get("sm_mhz") or 1965.0
     peak = 148 * DPX_STEPS_PER_CLK_PER_SM * sm_mhz * 1e6 / 1e9  # Gstep/s at the observed clock
-    avg_launch_ms = prod_ms / max(1, prod_launches)
+    avg_launch_ms = prod_ms / max(1, prod_launches)        # one product: SpMM (+ fold passes)
+    avg_kernel_ms = spmm_ms / max(1, prod_launches)        # the product kernel alone
     issued_per_launch = issued / max(1, prod_launches)
     useful_per_launch = float(nnz) * local_cols
-    achieved = useful_per_launch / (avg_launch_ms * 1e-3) / 1e9
-    issued_rate = issued_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    # physical roofline: DPX steps the kernel issued per launch / its duration
+    achieved = issued_per_launch / (avg_kernel_ms * 1e-3) / 1e9 if issued_per_launch else None
+    # the method's work (every finite A_il x every computed column) / the whole product's time
+    useful_rate = useful_per_launch / (avg_launch_ms * 1e-3) / 1e9
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = oracle_sample(args.n, args.cpu_seconds)
@@ -422,19 +434,26 @@ def run_mine(args):
         "config": dict(workload_config(args.n, N, world), products_per_step=products, nnz_A=nnz,
                        mu_lambda_b=[res.mu, res.lam, res.offset], gamma2_m1000=res.gamma2(1000),
                        kernel=args.kernel, spmm_cta_cols=spmm_cols or None, cols_rank0=local_cols, ld_rank0=ld,
-                       symmetry="none" if args.no_symmetry else "word reversal (columns g <= sigma g computed)"),
+                       symmetry="none" if args.no_symmetry else "word reversal (columns g <= sigma g computed)",
+                       row_reuse=(f"{row_levels} levels, {row_parents} parent links" if row_levels else "off")),
         "seconds_to_gamma2": ms / args.steps / 1e3,
         "dense_equivalent_gops": dense_all / (ms * 1e-3) / 1e9,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
-        "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used], "achieved": achieved, "peak": peak,
-                     "unit": "Gstep/s", "frac": achieved / peak,
+        "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used],
+                     "achieved": achieved if achieved else useful_rate, "peak": peak, "unit": "Gstep/s",
+                     "frac": (achieved if achieved else useful_rate) / peak,
                      "traffic": traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world, not args.no_symmetry),
                      "peak_source": f"148 SM x 128 steps/clk/SM x {sm_mhz:.0f} MHz observed (DESIGN.md)",
-                     "work": "useful steps = nnz(A) x columns computed per product (rank 0)",
-                     "avg_launch_ms": avg_launch_ms, "useful_steps_per_launch": useful_per_launch,
-                     "issued_steps_per_launch": issued_per_launch, "issued_achieved": issued_rate,
-                     "issue_frac": issued_rate / peak, "slot_occupancy": useful_per_launch / max(issued_per_launch, 1),
-                     "kernel_share_of_step": prod_ms / max(ms, 1e-9)},
+                     "work": ("issued DPX steps of the product kernel per launch (4-row groups x extra/finite "
+                              "entries x columns) / its CUDA-event duration" if achieved else
+                              "useful steps / kernel duration (the fused small-N run)"),
+                     "avg_kernel_ms": avg_kernel_ms, "issued_steps_per_launch": issued_per_launch or None,
+                     "useful_steps_per_product": useful_per_launch, "avg_product_ms": avg_launch_ms,
+                     "useful_achieved": useful_rate, "useful_frac": useful_rate / peak,
+                     "useful_note": "nnz(A) x computed columns per product / product time (kernel + fold passes); "
+                                    "above 1 only when the row-inclusion reuse skips redundant terms",
+                     "kernel_share_of_step": spmm_ms / max(ms, 1e-9),
+                     "product_share_of_step": prod_ms / max(ms, 1e-9)},
         "cpu_baseline": cpu,
         "e2e": {"value": useful_all / args.steps * e2e_steps / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
                 "h2d_bytes_per_step": int(h2d / max(1, e2e_steps)), "d2h_bytes_per_step": int(d2h / max(1, e2e_steps)),
@@ -443,7 +462,8 @@ def run_mine(args):
         "gamma2_cylinder": {"n": args.n, "m": 1000, "gamma2": g2_1000, "seconds_cold_wall": g2_seconds,
                             "note": "words source, word-reversal symmetry, includes allocation"},
         "setup_ms": setup_ms,
-        "breakdown_ms_per_step": {"products": prod_ms / args.steps, "stats": stats_ms / args.steps,
+        "breakdown_ms_per_step": {"products": prod_ms / args.steps, "product_kernel": spmm_ms / args.steps,
+                                  "folds": (prod_ms - spmm_ms) / args.steps, "stats": stats_ms / args.steps,
                                   "setup": setup_ms, "library_total": total_lib_ms / args.steps,
                                   "step": ms / args.steps},
         "gpu_launches": int(launches),

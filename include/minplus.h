@@ -167,6 +167,23 @@ mp_status minplus_power_rows(const uint16_t *A, int64_t N, int kmax, const int64
  * other value stops the run with MP_ERR_DOMAIN.  fn = NULL clears it.  A run with an observer
  * and a distributed context of world > 1 fails with MP_ERR_DOMAIN (a rank holds only its
  * shard).  Process-wide.  Errors: none (always MP_OK). */
+/* Row-inclusion reuse for the transfer matrix (not in the paper).  Row q'
+ * of A(D_n) is row q restricted to a subset of its support whenever q' is q with one letter 1
+ * turned into a 2 (can-follow, depends on q only through its 0- and 2-positions; the
+ * label, only on the column), so every power satisfies (A^k)_q = min((A^k)_q over the
+ * extra entries of row q, (A^k)_q' over the parents q') -- the same minimum regrouped.  The SpMM
+ * then runs on the extra entries (0.23 of nnz(A) at n = 12) and one fold pass per level of the
+ * parent DAG adds the parents' rows.  Used for the words source (gamma2_cylinder) and for matrix
+ * sources announced by mp_set_transfer_hint(n): the run then verifies on the device that A is
+ * A(D_n) entry by entry (MP_ERR_DOMAIN if not) -- wherever the grouped SpMM runs (N >= 8192
+ * with the automatic options).
+ *   mp_set_transfer_hint: n = 0 clears; applies to matrix sources of order |C_n|.
+ *     Errors: MP_ERR_DOMAIN (n outside {0} u [2, MP_MAX_N]).
+ *   mp_set_row_reuse: on = 0 switches the reuse off (same results); default on.  Errors: none.
+ * Both process-wide. */
+mp_status mp_set_transfer_hint(int n);
+mp_status mp_set_row_reuse(int on);
+
 /* Small-N latency path: single-rank power runs of matrices with N <= 256
  * and at most 16384 finite entries, with the automatic kernel choice and no observer, run
  * entirely in one thread-block-cluster launch (products, statistics, repeat search, exact
@@ -306,6 +323,10 @@ typedef struct {
     int64_t local_cols;       /* columns this rank computes per power (its shard; with a symmetry
                                  a shard of the domain g <= sigma g)                          */
     int64_t ld;               /* pitch of the device powers (local_cols padded to the CTA width) */
+    double spmm_ms;           /* of product_ms, the product kernel itself (without the fold
+                                 passes of the row-inclusion reuse)                          */
+    int32_t row_levels;       /* row-inclusion reuse: levels of the parent DAG (0 = not used)   */
+    int64_t row_parents;      /*   and its number of parent links                               */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
 

@@ -10,6 +10,6 @@ from ._native import (  # noqa: F401
     gamma2_cylinder, gamma2_record, kernel_launches, last_error, last_profile, minplus_closure, minplus_mul,
     minplus_mul_batched_device, minplus_mul_device,
     minplus_power_rows, minplus_power_until_periodic, minplus_power_until_periodic_device,
-    repeat_candidate, set_grouping, set_power_observer, set_small_path, set_spmm_width, set_options, set_stream, set_symmetry, set_word_symmetry,
+    repeat_candidate, set_grouping, set_power_observer, set_small_path, set_transfer_hint, set_row_reuse, set_spmm_width, set_options, set_stream, set_symmetry, set_word_symmetry,
     word_reversal, shard_range, shutdown, version, column_plan,
 )

@@ -33,6 +33,7 @@ EXPORTS = [
     "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_set_spmm_width", "mp_gamma2_formula", "mp_gamma2_record",
     "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal", "minplus_mul_strided_batched_device",
     "minplus_closure", "mp_set_power_observer", "mp_column_plan", "mp_set_small_path",
+    "mp_set_transfer_hint", "mp_set_row_reuse",
 ]
 
 
@@ -68,7 +69,8 @@ class _Profile(ctypes.Structure):
                 ("total_ms", ctypes.c_double), ("setup_ms", ctypes.c_double), ("stats_ms", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("kernel", ctypes.c_int32), ("spmm_cols", ctypes.c_int32),
-                ("local_cols", ctypes.c_int64), ("ld", ctypes.c_int64)]
+                ("local_cols", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("spmm_ms", ctypes.c_double), ("row_levels", ctypes.c_int32), ("row_parents", ctypes.c_int64)]
 
 
 OBSERVER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64)
@@ -123,6 +125,8 @@ def _load() -> ctypes.CDLL:
         "mp_set_power_observer": ([OBSERVER_FN, P], i32),
         "mp_column_plan": ([i64, i64, P, P, P], i32),
         "mp_set_small_path": ([i32], i32),
+        "mp_set_transfer_hint": ([i32], i32),
+        "mp_set_row_reuse": ([i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -430,7 +434,8 @@ def last_profile() -> dict:
             "dense_steps": p.dense_steps, "issued_steps": p.issued_steps, "total_ms": p.total_ms,
             "setup_ms": p.setup_ms, "stats_ms": p.stats_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
             "kernel": {0: "dense", 1: "tiles", 2: "spmm", 3: "small"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols,
-            "local_cols": p.local_cols, "ld": p.ld}
+            "local_cols": p.local_cols, "ld": p.ld, "row_levels": p.row_levels, "row_parents": p.row_parents,
+            "spmm_ms": p.spmm_ms}
 
 
 SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}
@@ -476,6 +481,17 @@ def set_spmm_width(cols: int = 0) -> None:
     """CTA width of the SpMM kernel: 0 (automatic), 256, 512 or 1024 columns everywhere, or
     -256 / -512 / -1024 = that main width plus narrower remainder columns (same product)."""
     _check(lib.mp_set_spmm_width(int(cols)))
+
+
+def set_transfer_hint(n: int = 0) -> None:
+    """Matrix sources of order |C_n| are claimed to be A(D_n) (verified on the device by every
+    run): enables the row-inclusion reuse for them.  0 clears."""
+    _check(lib.mp_set_transfer_hint(int(n)))
+
+
+def set_row_reuse(on: bool = True) -> None:
+    """Row-inclusion reuse for A(D_n) on (default) or off (same results)."""
+    _check(lib.mp_set_row_reuse(1 if on else 0))
 
 
 def set_small_path(on: bool = True) -> None:

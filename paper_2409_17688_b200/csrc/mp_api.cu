@@ -54,6 +54,8 @@ constexpr int64_t kGroupMinN = 8192; // below this the grouping pass costs more 
 std::vector<int32_t> g_sym;
 bool g_word_sym = true;
 bool g_small_off = false; // mp_set_small_path(0): always the general path
+int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be A(D_n)
+bool g_row_reuse = true;   // mp_set_row_reuse: row-inclusion reuse for A(D_n)
 
 mp_profile g_prof{};
 
@@ -196,6 +198,8 @@ struct PowerRun {
     size_t cached_slot = 0; // slot size the cached buffers were allocated for
     bool sparse = false;  // tile kernel with l-tile lists
     bool spmm = false;    // grouped SpMM kernel
+    int dag_n = 0;        // row-inclusion reuse (A = A(D_dag_n)); 0 = off
+    RowDag rdag;
     double issued_per_product = 0.0;
     double issued_tiles = 0.0, issued_spmm = 0.0;
     int64_t tiles_nonempty = 0; // non-empty 128 x 32 tiles of A (block-sparse tile kernel)
@@ -355,11 +359,21 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
     R.sp.cols = R.spmm_cols; // reported width (the entries carry row offsets for every width)
     int64_t launches = 0;
     const bool group = g_opts.grouping == 1 || (g_opts.grouping < 0 && R.N >= kGroupMinN);
-    const cudaError_t e =
-        R.a_src ? build_sparse_form(R.a_src, R.a_ld, R.N, R.Np, group, group && R.bits_ok ? R.bits.as<uint32_t>() : nullptr,
-                                    R.sp, s, sp_alloc, &R, &launches)
-                : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, group, R.sp, s, sp_alloc,
-                                            &R, &launches);
+    cudaError_t e = cudaSuccess;
+    const RowDag *dag = nullptr;
+    if (R.dag_n && group) { // row-inclusion reuse: parents and levels
+        R.rdag = RowDag();
+        e = build_row_dag(R.words.as<WordMask>(), R.N, R.dag_n, R.rdag, s, sp_alloc, &R, &launches);
+        dag = &R.rdag;
+    } else {
+        R.dag_n = 0;
+    }
+    if (e == cudaSuccess)
+        e = R.a_src ? build_sparse_form(R.a_src, R.a_ld, R.N, R.Np, group,
+                                        group && R.bits_ok ? R.bits.as<uint32_t>() : nullptr, R.sp, s, sp_alloc, &R,
+                                        &launches, dag)
+                    : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, group, R.sp, s, sp_alloc,
+                                              &R, &launches, dag);
     g_launches.fetch_add(launches);
     g_d2h.fetch_add(24);
     if (e == cudaErrorMemoryAllocation) return MP_ERR_RESOURCE; // message set by DBuf::alloc
@@ -372,7 +386,8 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
 }
 
 // C = A (x) X with the selected kernel.
-mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
+// mid (may be null): recorded between the SpMM and the fold passes of the row-inclusion reuse.
+mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, cudaEvent_t mid = nullptr)
 {
     if (R.spmm) {
         SparseA sa;
@@ -383,7 +398,9 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s)
         sa.E = R.sp.E;
         sa.rows = R.sp.rows;
         int nl = 0;
-        const cudaError_t e = launch_spmm(sa, R.plan, X, R.ld, C, R.ld, R.Np, s, &nl);
+        cudaError_t e = launch_spmm(sa, R.plan, X, R.ld, C, R.ld, R.Np, s, &nl);
+        if (e == cudaSuccess && mid) e = cudaEventRecord(mid, s);
+        if (e == cudaSuccess && R.dag_n) e = launch_folds(R.rdag, C, R.ld, R.ld, s, &nl); // parents' rows
         g_launches.fetch_add(nl);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -549,6 +566,7 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     const int products = (int)h[4] - 1;
     g_prof = mp_profile{};
     g_prof.product_ms = kms;
+    g_prof.spmm_ms = kms;
     g_prof.product_launches = products;
     g_prof.dense_steps = (double)products * (double)N * (double)N * (double)N;
     g_prof.issued_steps = 0.0; // the row lists of A against 64 C columns; counted by the caller as nnz * 64 C
@@ -714,16 +732,30 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.bits_ok = (g_opts.sparsity == 2 || g_opts.sparsity < 0) &&
                     (g_opts.grouping == 1 || (g_opts.grouping < 0 && N >= kGroupMinN));
         if (R.bits_ok) TRY(R.bits.ensure((size_t)N * ((N + 31) / 32) * 4, "support bitsets"));
-        CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, 2 * sizeof(int), s));
+        // a transfer-matrix hint (mp_set_transfer_hint) brings the word masks along, verified below
+        const bool hint = g_transfer_n >= 2 && count_words(g_transfer_n) == N;
+        if (hint) {
+            std::vector<WordMask> words = enumerate_words(g_transfer_n);
+            TRY(R.words.ensure(words.size() * sizeof(WordMask), "word masks"));
+            COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
+        }
+        CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, 3 * sizeof(int), s));
         LAUNCH(launch_check_a(R.a_src, R.a_ld, N, R.Np, need_occ ? R.occ.as<uint8_t>() : nullptr, R.flag.as<int>(),
                               R.sym ? R.dsig.as<int32_t>() : nullptr, R.flag.as<int>() + 1,
                               R.bits_ok ? R.bits.as<uint32_t>() : nullptr, s));
-        int hflag[2] = {0, 0};
-        COPY(hflag, R.flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (hint)
+            LAUNCH(launch_verify_transfer(R.a_src, R.a_ld, R.words.as<WordMask>(), N, g_transfer_n,
+                                          R.flag.as<int>() + 2, s));
+        int hflag[3] = {0, 0, 0};
+        COPY(hflag, R.flag.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));
         if (hflag[0]) return fail(MP_ERR_RANGE, "an entry of A lies in (0x7FFE, 0xFFFF)");
         if (hflag[1]) return fail(MP_ERR_DOMAIN, "symmetry hint: A[sigma i][sigma j] != A[i][j] for some i, j");
+        if (hflag[2]) return fail(MP_ERR_DOMAIN, "transfer hint: A is not A(D_%d)", g_transfer_n);
+        if (hint) R.n_words = g_transfer_n; // the rows' word structure is now known
     }
+    // row-inclusion reuse needs the word structure and the grouped SpMM
+    R.dag_n = (g_row_reuse && R.n_words && (g_opts.sparsity == 2 || g_opts.sparsity < 0)) ? R.n_words : 0;
     tr.mark("a2 stage A");
 
     // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
@@ -813,15 +845,15 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // depends only on N, so every rank of a sharded run makes the same collective calls.
     const int B = (N <= kBatchMaxN && !cap) ? std::min(kBatch, max_k) : 1; // ring >= B + 1 (above)
     // events: [0, 2(max_k+1)) product start/stop per power, then stats start, stats stop
-    if ((int)R.events.size() < 4 * (max_k + 1)) {
+    if ((int)R.events.size() < 5 * (max_k + 1)) {
         for (auto ev : R.events) cudaEventDestroy(ev);
-        R.events.assign((size_t)4 * (max_k + 1), nullptr);
+        R.events.assign((size_t)5 * (max_k + 1), nullptr);
         for (auto &ev : R.events) CUDA_TRY(cudaEventCreate(&ev));
     }
 
     std::vector<mp_power_stats> hs((size_t)max_k + 1);
     const uint64_t S = mp_fingerprint_unit(N); // O(N) on the host
-    double prod_ms = 0.0, stats_ms = 0.0;
+    double prod_ms = 0.0, stats_ms = 0.0, spmm_ms = 0.0;
     int64_t launches = 0;
     cudaEvent_t ev_setup;
     CUDA_TRY(cudaEventCreate(&ev_setup));
@@ -846,7 +878,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 TRY(make_power1(R, dst, s)); // X_1 = A[:, shard]
             } else {
                 CUDA_TRY(cudaEventRecord(R.events[2 * k], s));
-                TRY(product(R, prev, dst, s)); // A^k = A (x) A^{k-1}
+                TRY(product(R, prev, dst, s, R.events[4 * (max_k + 1) + k])); // A^k = A (x) A^{k-1}
                 CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
                 ++launches;
             }
@@ -875,6 +907,10 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 float ms = 0.f;
                 CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[2 * k + 1]));
                 prod_ms += ms;
+                if (R.spmm) {
+                    CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[4 * (max_k + 1) + k]));
+                    spmm_ms += ms;
+                }
                 CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * (max_k + 1) + k], R.events[3 * (max_k + 1) + k]));
                 stats_ms += ms;
             }
@@ -945,6 +981,10 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 float ms = 0.f;
                 CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[2 * k + 1]));
                 prod_ms += ms;
+                if (R.spmm) {
+                    CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[4 * (max_k + 1) + k]));
+                    spmm_ms += ms;
+                }
             }
     }
     CUDA_TRY(cudaEventRecord(ev_all1, s));
@@ -975,6 +1015,9 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.spmm_cols = R.spmm ? R.sp.cols : 0;
     g_prof.local_cols = R.w;
     g_prof.ld = R.ld;
+    g_prof.spmm_ms = R.spmm ? spmm_ms : prod_ms;
+    g_prof.row_levels = R.spmm && R.dag_n ? R.rdag.levels : 0;
+    g_prof.row_parents = R.spmm && R.dag_n ? R.rdag.parents : 0;
 
     if (!found) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
     *out = res;
@@ -1394,6 +1437,23 @@ mp_status mp_word_reversal(int n, int32_t *sigma_out, int64_t N)
     if ((int64_t)sg.size() != N)
         return fail(MP_ERR_DOMAIN, "mp_word_reversal: N = %lld, A(D_%d) has %zu words", (long long)N, n, sg.size());
     std::memcpy(sigma_out, sg.data(), sg.size() * 4);
+    return MP_OK;
+}
+
+mp_status mp_set_transfer_hint(int n)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (n != 0 && (n < 2 || n > MP_MAX_N))
+        return fail(MP_ERR_DOMAIN, "mp_set_transfer_hint: n = %d outside {0} u [2, %d]", n, MP_MAX_N);
+    g_transfer_n = n;
+    return MP_OK;
+}
+
+mp_status mp_set_row_reuse(int on)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_row_reuse = on != 0;
+    g_cache.clear(); // records of the words source were computed either way
     return MP_OK;
 }
 

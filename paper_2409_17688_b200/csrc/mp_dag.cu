@@ -1,0 +1,265 @@
+// Row-inclusion reuse for the transfer matrix A(D_n) (DESIGN.md section 5 "Row-inclusion
+// reuse").  Product code only; shares nothing with oracle/.
+//
+// Whether p can follow q depends on q only through its zero positions z(q) and its
+// 2-positions t(q): rule (1) asks p_i = 0 wherever q_i = 2, rules (2)-(3) count q_i = 0 among
+// the neighbours of p_i.  The label of the arc q -> p is the number of zeros of p, a
+// function of p alone.  So if q' is q with one letter 1 turned into a 2 (same zeros, one more
+// 2), every p that can follow q' can follow q with the same label: row q' of A is row q
+// restricted to a subset of its support.  For every power,
+//     (A^k)_(q, j) = min( min over parents q' of (A^k)_(q', j),
+//                         min over l in extra(q) of a_ql + (A^{k-1})_(l, j) ),
+// extra(q) = supp(q) minus the union of the parents' supports -- the same minimum over the same
+// terms (min is idempotent), regrouped.  The SpMM kernel runs on the extra entries only
+// (0.227 of nnz(A) at n = 12) and a fold pass per level of the parent DAG (a parent has one
+// more 2, so levels are at most n) takes the minimum with the parents' finished rows.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "mp_internal.h"
+#include "mp_kernels.h"
+
+namespace mp {
+
+namespace {
+
+// Base-3 value of a word with letter 0 (the top row) most significant: the lexicographic order
+// of A(D_n) (G5) is the order of these keys.
+__device__ __forceinline__ uint32_t word_key(const WordMask &w, int n)
+{
+    uint32_t k = 0;
+    for (int i = 0; i < n; ++i) k = 3 * k + ((w.o >> i) & 1u) + 2 * ((w.t >> i) & 1u);
+    return k;
+}
+
+__global__ void k_word_keys(const WordMask *__restrict__ w, int64_t N, int n, uint32_t *__restrict__ keys)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = word_key(w[i], n);
+}
+
+__device__ __forceinline__ int64_t find_key(const uint32_t *__restrict__ keys, int64_t N, uint32_t k)
+{
+    int64_t lo = 0, hi = N;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < k) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < N && keys[lo] == k) ? lo : -1;
+}
+
+// parents of q: the words q with one letter 1 turned into 2 that are correct words
+// (count pass if pidx == nullptr, else fill from off[q])
+__global__ void k_dag_parents(const WordMask *__restrict__ w, const uint32_t *__restrict__ keys, int64_t N, int n,
+                              const int64_t *__restrict__ off, int32_t *__restrict__ cnt, int32_t *__restrict__ pidx)
+{
+    uint32_t pw3[16];
+    pw3[0] = 1;
+    for (int i = 1; i < 16; ++i) pw3[i] = 3 * pw3[i - 1];
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t kq = keys[q];
+        int c = 0;
+        int64_t o = pidx ? off[q] : 0;
+        for (int b = 0; b < n; ++b) {
+            if (!((w[q].o >> b) & 1u)) continue;
+            const int64_t p = find_key(keys, N, kq + pw3[n - 1 - b]); // letter b: 1 -> 2
+            if (p < 0) continue;
+            if (pidx) pidx[o++] = (int32_t)p;
+            ++c;
+        }
+        if (!pidx) cnt[q] = c;
+    }
+}
+
+// level[q] = 0 without parents, else 1 + max level of the parents (one relaxation pass; n + 1
+// passes reach the fixed point: a parent has one more 2)
+__global__ void k_dag_level(const int64_t *__restrict__ off, const int32_t *__restrict__ pidx, int64_t N,
+                            int32_t *__restrict__ level)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+        int l = 0;
+        for (int64_t e = off[q]; e < off[q + 1]; ++e) l = max(l, level[pidx[e]] + 1);
+        level[q] = l;
+    }
+}
+
+__global__ void k_level_hist(const int32_t *__restrict__ level, int64_t N, int32_t *__restrict__ hist)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hist[level[q]], 1);
+}
+
+// rows grouped by level (order inside a level: ascending row, from a per-level ballot scan)
+__global__ void k_level_scatter(const int32_t *__restrict__ level, int64_t N, int L,
+                                const int64_t *__restrict__ lptr, int32_t *__restrict__ lrows)
+{
+    // one block; the block walks the rows in order, per level a running offset
+    __shared__ int64_t pos[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int l = threadIdx.x; l < L; l += blockDim.x) pos[l] = lptr[l];
+    __syncthreads();
+    for (int64_t base = 0; base < N; base += 32 * nwarps) {
+        // warp w handles rows base + 32 w .. + 31; warps take turns to keep the order
+        for (int turn = 0; turn < nwarps; ++turn) {
+            if (warp == turn) {
+                const int64_t q = base + 32 * warp + lane;
+                const int lv = q < N ? level[q] : -1;
+                for (int l = 0; l < L; ++l) {
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, lv == l);
+                    if (!m) continue;
+                    if (lv == l) lrows[pos[l] + __popc(m & ((1u << lane) - 1))] = (int32_t)q;
+                    __syncwarp();
+                    if (lane == 0) pos[l] += __popc(m);
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// extra(q) = supp(q) minus the parents' supports, as bitsets (warp per row, lanes over words)
+__global__ void k_extra_bits(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, const int64_t *__restrict__ off,
+                             const int32_t *__restrict__ pidx, uint32_t *__restrict__ ebits)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < N;
+         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t e0 = off[q], e1 = off[q + 1];
+        for (int64_t k = lane; k < nw; k += 32) {
+            uint32_t m = bits[q * nw + k];
+            for (int64_t e = e0; e < e1 && m; ++e) m &= ~bits[(int64_t)pidx[e] * nw + k];
+            ebits[q * nw + k] = m;
+        }
+    }
+}
+
+// (A^k)_(q, :) = min((A^k)_(q, :), (A^k)_(p, :)) over the parents p of the rows q of one level
+// (8 columns per thread; the parents' rows are final: they belong to earlier levels)
+__global__ void k_fold(const int32_t *__restrict__ lrows, int64_t nrows, const int64_t *__restrict__ off,
+                       const int32_t *__restrict__ pidx, uint16_t *__restrict__ C, int64_t ldc, int64_t c8)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nrows * c8; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / c8, c = t - r * c8;
+        const int64_t q = lrows[r];
+        uint4 *dst = reinterpret_cast<uint4 *>(C + q * ldc) + c;
+        uint4 v = *dst;
+        for (int64_t e = off[q]; e < off[q + 1]; ++e) {
+            const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(C + (int64_t)pidx[e] * ldc) + c);
+            v.x = __vminu2(v.x, u.x);
+            v.y = __vminu2(v.y, u.y);
+            v.z = __vminu2(v.z, u.z);
+            v.w = __vminu2(v.w, u.w);
+        }
+        *dst = v;
+    }
+}
+
+// A (matrix source) equals A(D_n) built from the words: flag set on the first difference
+__global__ void k_verify_transfer(const uint16_t *__restrict__ A, int64_t lda, const WordMask *__restrict__ w, int64_t N,
+                                  unsigned full, int *__restrict__ flag)
+{
+    bool bad = false;
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
+        const WordMask q = w[i];
+        for (int64_t l = threadIdx.x; l < N; l += blockDim.x) {
+            const WordMask p = w[l];
+            const uint16_t want = can_follow_mask(q, p, full) ? (uint16_t)p.zeros : (uint16_t)kBndInf;
+            bad |= A[i * lda + l] != want;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+int grid_rows(int64_t work, int per_block)
+{
+    const int64_t g = (work + per_block - 1) / per_block;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+} // namespace
+
+cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cudaStream_t s,
+                          cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
+{
+    cudaError_t e;
+    auto A = [&](auto *&p, size_t bytes) { return alloc((void **)&p, std::max<size_t>(bytes, 16), actx); };
+    uint32_t *keys = nullptr;
+    int32_t *cnt = nullptr, *hist = nullptr;
+    if ((e = A(keys, (size_t)N * 4)) != cudaSuccess) return e;
+    if ((e = A(cnt, (size_t)N * 4)) != cudaSuccess) return e;
+    if ((e = A(d.off, (size_t)(N + 1) * 8)) != cudaSuccess) return e;
+    if ((e = A(d.level, (size_t)N * 4)) != cudaSuccess) return e;
+    if ((e = A(d.lrows, (size_t)N * 4)) != cudaSuccess) return e;
+    if ((e = A(hist, 32 * 4)) != cudaSuccess) return e;
+    if ((e = A(d.lptr_dev, 33 * 8)) != cudaSuccess) return e;
+    const int gb = grid_rows(N, 256);
+    k_word_keys<<<gb, 256, 0, s>>>(words, N, n, keys);
+    k_dag_parents<<<gb, 256, 0, s>>>(words, keys, N, n, nullptr, cnt, nullptr);
+    *launches += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // offsets on the host (N <= 131562 counts): one copy each way
+    std::vector<int32_t> hc((size_t)N);
+    if ((e = cudaMemcpyAsync(hc.data(), cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    std::vector<int64_t> ho((size_t)N + 1, 0);
+    for (int64_t q = 0; q < N; ++q) ho[(size_t)q + 1] = ho[(size_t)q] + hc[(size_t)q];
+    d.parents = ho[(size_t)N];
+    if ((e = A(d.idx, (size_t)d.parents * 4)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(d.off, ho.data(), ho.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    k_dag_parents<<<gb, 256, 0, s>>>(words, keys, N, n, d.off, nullptr, d.idx);
+    if ((e = cudaMemsetAsync(d.level, 0, (size_t)N * 4, s)) != cudaSuccess) return e;
+    for (int pass = 0; pass <= n; ++pass) k_dag_level<<<gb, 256, 0, s>>>(d.off, d.idx, N, d.level);
+    if ((e = cudaMemsetAsync(hist, 0, 32 * 4, s)) != cudaSuccess) return e;
+    k_level_hist<<<gb, 256, 0, s>>>(d.level, N, hist);
+    *launches += (int64_t)n + 3;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int32_t hh[32];
+    if ((e = cudaMemcpyAsync(hh, hist, sizeof(hh), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    d.levels = 0;
+    d.lptr.assign(1, 0);
+    for (int l = 0; l < 32 && hh[l] > 0; ++l) {
+        d.lptr.push_back(d.lptr.back() + hh[l]);
+        d.levels = l + 1;
+    }
+    if (d.lptr.back() != N) return cudaErrorUnknown; // levels are contiguous from 0
+    if ((e = cudaMemcpyAsync(d.lptr_dev, d.lptr.data(), d.lptr.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return e;
+    k_level_scatter<<<1, 1024, 0, s>>>(d.level, N, d.levels, d.lptr_dev, d.lrows);
+    *launches += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaStreamSynchronize(s); // d.lptr (host) and ho go out of scope safely
+}
+
+cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const RowDag &d, uint32_t *ebits,
+                              cudaStream_t s)
+{
+    k_extra_bits<<<grid_rows(N * 32, 256), 256, 0, s>>>(bits, nw, N, d.off, d.idx, ebits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncols, cudaStream_t s, int *launches)
+{
+    const int64_t c8 = (ncols + 7) / 8;
+    for (int l = 1; l < d.levels; ++l) {
+        const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
+        k_fold<<<grid_rows(nr * c8, 256), 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc, c8);
+        if (launches) ++*launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_verify_transfer(const uint16_t *A, int64_t lda, const WordMask *words, int64_t N, int n, int *flag,
+                                   cudaStream_t s)
+{
+    k_verify_transfer<<<grid_rows(N, 1), 256, 0, s>>>(A, lda, words, N, (1u << n) - 1u, flag);
+    return cudaGetLastError();
+}
+
+} // namespace mp

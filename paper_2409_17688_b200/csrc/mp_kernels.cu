@@ -1979,7 +1979,7 @@ cudaError_t launch_spmm(const SparseA &sa, const SpmmPlan &P, const uint16_t *X,
 template <class Acc>
 cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, const uint32_t *pre_bits, SparseWork &w,
                                 cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
-                                int64_t *launches)
+                                int64_t *launches, const RowDag *dag)
 {
     const int64_t G = Np / kG, Mt = Np / kSpRows;
     cudaError_t e;
@@ -2026,6 +2026,13 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
             SP_ALLOC(bits, (size_t)N * nw * 4);
             SP_LAUNCH(
                 (k_support_bits<<<(unsigned)std::min<int64_t>(N, (int64_t)num_sms() * 8), 256, 0, s>>>(AT2, N, nw, bits)));
+        }
+        if (dag) { // row-inclusion reuse: each row keeps only the entries its parents lack
+            uint32_t *ebits = nullptr;
+            SP_ALLOC(ebits, (size_t)N * nw * 4);
+            if ((e = launch_extra_bits(bits, nw, N, *dag, ebits, s)) != cudaSuccess) return e;
+            ++*launches;
+            bits = ebits;
         }
         w.bits = bits;
         SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, cnt)));
@@ -2115,6 +2122,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     w.group_rows = kG;
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E, 0u)));
+    if (dag) w.off = nullptr, w.idx = nullptr; // row lists of the extra entries only: not A's
 #undef SP_SCAN
 #undef SP_LAUNCH
 #undef SP_ALLOC
@@ -2123,17 +2131,18 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
 
 cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group,
                               const uint32_t *pre_bits, SparseWork &w, cudaStream_t s,
-                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches)
+                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches,
+                              const RowDag *dag)
 {
-    return build_sparse_form_t(AccA{A, lda, N, nullptr}, N, Np, group, pre_bits, w, s, alloc, actx, launches);
+    return build_sparse_form_t(AccA{A, lda, N, nullptr}, N, Np, group, pre_bits, w, s, alloc, actx, launches, dag);
 }
 
 cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
-                                    int64_t *launches)
+                                    int64_t *launches, const RowDag *dag)
 {
     return build_sparse_form_t(AccWords{words, N, (1u << n) - 1u, nullptr}, N, Np, group, nullptr, w, s, alloc, actx,
-                               launches);
+                               launches, dag);
 }
 
 // X1[i][j] = A_(i, c0+j) from the word masks, +inf padding (rows >= N, columns >= w).

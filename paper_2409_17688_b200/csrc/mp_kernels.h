@@ -90,15 +90,39 @@ SpmmPlan spmm_plan(int64_t Np, int64_t w);
 // One launch per segment of the plan (*launches counts them).
 cudaError_t launch_spmm(const SparseA &sa, const SpmmPlan &P, const uint16_t *X, int64_t ldx, uint16_t *C,
                         int64_t ldc, int64_t Mp, cudaStream_t s, int *launches);
+// Row-inclusion reuse for A(D_n) (mp_dag.cu): parents of row q = the
+// words q with one letter 1 turned into 2 (their rows are restrictions of row q); rows by level.
+struct RowDag {
+    int64_t *off = nullptr;     // [N + 1] parent lists (CSR)
+    int32_t *idx = nullptr;     // parents
+    int32_t *level = nullptr;   // [N] 0 without parents, else 1 + max level of the parents
+    int32_t *lrows = nullptr;   // [N] rows grouped by level
+    int64_t *lptr_dev = nullptr;
+    std::vector<int64_t> lptr;  // [levels + 1] level offsets into lrows (host copy)
+    int levels = 0;
+    int64_t parents = 0;
+};
+cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cudaStream_t s,
+                          cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);
+// ebits = bits minus the union of the parents' bits, row by row (N x nw words each)
+cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const RowDag &d, uint32_t *ebits,
+                              cudaStream_t s);
+// C_q = min(C_q, C_p) over the parents p, level by level (levels 1 .. levels-1), ncols columns
+cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncols, cudaStream_t s, int *launches);
+// *flag |= 1 unless A (row-major, boundary encoding) equals A(D_n)
+cudaError_t launch_verify_transfer(const uint16_t *A, int64_t lda, const WordMask *words, int64_t N, int n, int *flag,
+                                   cudaStream_t s);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
 // pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).
+// dag (may be null; needs group): build the form on the extra entries of each row only.
 cudaError_t build_sparse_form(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, bool group,
                               const uint32_t *pre_bits, SparseWork &w, cudaStream_t s,
-                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);
+                              cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches,
+                              const RowDag *dag = nullptr);
 cudaError_t build_sparse_form_words(const WordMask *words, int64_t N, int n, int64_t Np, bool group, SparseWork &w,
                                     cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *), void *actx,
-                                    int64_t *launches);
+                                    int64_t *launches, const RowDag *dag = nullptr);
 // gcol (may be null): the global column of each local column (else c0 + j).
 cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_t Np, int64_t c0, const int32_t *gcol,
                                  int64_t w, uint16_t *X1, int64_t ldx, cudaStream_t s);

@@ -67,17 +67,33 @@ def check_result(g, rec):
 
 def run_config(mp, A, n, config):
     import torch
-    if config == "bench":  # exactly what bench.py times: device-resident A, its stream
+    if config == "bench":  # exactly what bench.py times: device-resident A, its stream, hints
         mp.set_symmetry(mp.word_reversal(n))
+        mp.set_transfer_hint(n)
         dA = torch.from_numpy(A.view(np.int16)).cuda()
         mp.set_stream(torch.cuda.current_stream())
         try:
-            return mp.minplus_power_until_periodic_device(dA)
+            g = mp.minplus_power_until_periodic_device(dA)
+            assert mp.last_profile()["row_levels"] > 1  # the row-inclusion reuse ran
+            return g
         finally:
             mp.set_stream(None)
             mp.set_symmetry(None)
+            mp.set_transfer_hint(0)
     if config == "allcols":
         return mp.minplus_power_until_periodic(A)
+    if config == "noreuse":  # the benchmarked options without the row-inclusion reuse
+        mp.set_symmetry(mp.word_reversal(n))
+        mp.set_transfer_hint(n)
+        mp.set_row_reuse(False)
+        try:
+            g = mp.minplus_power_until_periodic(A)
+            assert mp.last_profile()["row_levels"] == 0
+            return g
+        finally:
+            mp.set_row_reuse(True)
+            mp.set_symmetry(None)
+            mp.set_transfer_hint(0)
     if config == "tiles":
         mp.set_options("tiles")
         try:
@@ -87,7 +103,7 @@ def run_config(mp, A, n, config):
     raise ValueError(config)
 
 
-@pytest.mark.parametrize("config", ["bench", "allcols", "tiles"])
+@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse"])
 @pytest.mark.parametrize("n", SIZES)
 def test_power_records(mp, n, config):
     """Every power's fingerprint and diagonal minimum, (mu, lambda, b) and dense_from equal the

@@ -223,6 +223,44 @@ def test_spmm_width_power_until_periodic(mp, oracle_mod, n, width):
     assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
 
 
+@pytest.mark.parametrize("sym", [False, True])
+@pytest.mark.parametrize("n", [4, 6, 7, 8, 9])
+def test_row_reuse_transfer_hint(mp, oracle_mod, n, sym):
+    """Row-inclusion reuse (SpMM on each row's extra entries, then one fold pass per level of
+    the parent DAG) on A(D_n) announced by the transfer hint, greedy grouping forced so the
+    grouped SpMM runs at these sizes: every entry of A^1..A^8 and the whole periodic record
+    equal the oracle's; a matrix that is not A(D_n) is refused."""
+    A = mp.build_transition_matrix(n)
+    o = oracle_mod.power_until_periodic(A)
+    use_kernel(mp, "spmm-greedy")
+    mp.set_transfer_hint(n)
+    mp.set_small_path(False)
+    if sym:
+        mp.set_symmetry(mp.word_reversal(n))
+    try:
+        got = mp.minplus_power_rows(A, np.arange(A.shape[0]), 8)
+        g = mp.minplus_power_until_periodic(A)
+        assert mp.last_profile()["row_levels"] > 1
+        bad = A.copy()
+        i, j = np.argwhere(A != INF)[3]
+        bad[i, j] = INF
+        with pytest.raises(mp.MinplusError) as e:
+            mp.minplus_power_until_periodic(bad)
+        assert e.value.name == "MP_ERR_DOMAIN"
+    finally:
+        mp.set_symmetry(None)
+        mp.set_transfer_hint(0)
+        mp.set_small_path(True)
+        reset_kernel(mp)
+    assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+    assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
+    X = A.copy()
+    for k in range(1, 9):
+        if k > 1:
+            X = oracle_mod.minplus(A, X)
+        assert np.array_equal(got[k - 1], X), k
+
+
 @pytest.mark.parametrize("main", [-1024, -512, -256, 0])
 @pytest.mark.parametrize("N", [100, 700, 960, 1500, 1800])
 def test_spmm_remainder_columns(mp, oracle_mod, N, main):
