@@ -94,13 +94,15 @@ mp_status minplus_mul_device(const uint16_t *dA, int64_t lda, const uint16_t *dB
 
 /* NEXT-4: general products through the same kernel.
  *   minplus_mul_strided_batched_device: C_b = A_b x B_b for b < batch, with A_b = dA +
- *     b*strideA (elements; likewise B_b, C_b), each as in minplus_mul_device, in order on
- *     `stream`.  Errors as minplus_mul_device, plus MP_ERR_DOMAIN for batch <= 0, a negative
+ *     b*strideA (elements; likewise B_b, C_b; a stride may be 0 to reuse one operand), each as
+ *     in minplus_mul_device; every kernel runs once for all items (the batch index is the grid's
+ *     z dimension; items are taken in chunks of at most 8 GB of scratch), on `stream`.  Errors as minplus_mul_device, plus MP_ERR_DOMAIN for batch <= 0, a negative
  *     stride, C matrices overlapping each other or any A_b / B_b.
  *   minplus_closure: D = (I (+) W)^(2^t) with 2^t >= N-1 (t squarings; *squarings_out = t if
  *     not NULL): for a weighted adjacency W (N x N host, boundary encoding, W_ij = arc
  *     length) the all-pairs shortest path lengths, +inf if unreachable, path lengths >= 0x7FFF
  *     saturating to +inf (G6).  I (+) W = W with a zero diagonal.  Host buffers, caller-owned.
+ *     Sharded over the ranks like minplus_mul when an all-gather is registered.
  *     Errors: MP_ERR_DOMAIN (NULL, N <= 0, D overlapping W), MP_ERR_RANGE, MP_ERR_RESOURCE,
  *     MP_ERR_CUDA. */
 mp_status minplus_mul_strided_batched_device(const uint16_t *dA, int64_t lda, int64_t strideA,
@@ -248,6 +250,21 @@ typedef int (*mp_allreduce_fn)(void *ctx, int op, int64_t *dev_buf, int64_t coun
  * process-wide distributed context used by minplus_power_until_periodic.
  * Errors: MP_ERR_DOMAIN. */
 mp_status mp_dist_set(int rank, int world, mp_allreduce_fn fn, void *ctx);
+
+/* The all-gather the general products call when sharded (minplus_mul, minplus_closure): every
+ * rank contributes `bytes` bytes at send_dev (DEVICE memory) and receives the world blocks in
+ * rank order at recv_dev (world * bytes; already ordered after the library's work on `stream`,
+ * which the library synchronises before the call).  Returns 0 on success. */
+typedef int (*mp_allgather_fn)(void *ctx, const void *send_dev, void *recv_dev, int64_t bytes, void *stream);
+
+/* Registers (fn != NULL) or clears the all-gather of the distributed context.  With a context
+ * of world > 1 and an all-gather, minplus_mul and minplus_closure run column-sharded: every
+ * rank passes the same host inputs, rank r computes the column block C[:, J_r] = A (x) B[:, J_r]
+ * (J_r = mp_shard_range(N, world, r); A replicated -- the partitioning the paper proposes as
+ * future work), the blocks are all-gathered, and every rank's output receives the whole
+ * product (the closure all-gathers after every squaring: both of its operands change).
+ * Errors: none (always MP_OK). */
+mp_status mp_dist_set_allgather(mp_allgather_fn fn, void *ctx);
 
 /* Column shard [*c0, *c1) of rank `rank` among `world` for an N x N power: width
  * w = roundup(ceil(N / world), 8), c0 = min(N, rank*w), c1 = min(N, c0 + w) (the last

@@ -6,7 +6,7 @@ The computation lives in ``libminplus.so`` (CUDA kernels behind the C ABI of
 """
 from ._native import (  # noqa: F401
     MP_FINITE_MAX, MP_INF, MP_MAX_K, MP_MAX_N, MinplusError, PeriodicResult, PowerStats,
-    build_transition_matrix, count_words, dist_set, dist_set_torch, fingerprint_unit,
+    build_transition_matrix, count_words, dist_set, dist_set_allgather, dist_set_torch, fingerprint_unit,
     gamma2_cylinder, gamma2_record, kernel_launches, last_error, last_profile, minplus_closure, minplus_mul,
     minplus_mul_batched_device, minplus_mul_device,
     minplus_power_rows, minplus_power_until_periodic, minplus_power_until_periodic_device,

@@ -33,7 +33,7 @@ EXPORTS = [
     "mp_last_profile", "mp_set_options", "mp_set_grouping", "mp_set_spmm_width", "mp_gamma2_formula", "mp_gamma2_record",
     "mp_set_symmetry", "mp_set_word_symmetry", "mp_word_reversal", "minplus_mul_strided_batched_device",
     "minplus_closure", "mp_set_power_observer", "mp_column_plan", "mp_set_small_path",
-    "mp_set_transfer_hint", "mp_set_row_reuse",
+    "mp_set_transfer_hint", "mp_set_row_reuse", "mp_dist_set_allgather",
 ]
 
 
@@ -74,6 +74,8 @@ class _Profile(ctypes.Structure):
 
 
 OBSERVER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                ctypes.c_void_p)
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                 ctypes.c_int64, ctypes.c_void_p)
 
@@ -127,6 +129,7 @@ def _load() -> ctypes.CDLL:
         "mp_set_small_path": ([i32], i32),
         "mp_set_transfer_hint": ([i32], i32),
         "mp_set_row_reuse": ([i32], i32),
+        "mp_dist_set_allgather": ([ALLGATHER_FN, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -361,6 +364,7 @@ def dist_set(rank: int, world: int, allreduce) -> None:
     if allreduce is None:
         _check(lib.mp_dist_set(0, 1, ALLREDUCE_FN(), None))
         _keep_alive.clear()
+        _gather_keep.clear()
         return
 
     def cb(ctx, op, dev_ptr, count, stream):
@@ -377,22 +381,63 @@ def dist_set(rank: int, world: int, allreduce) -> None:
     _check(lib.mp_dist_set(rank, world, fn, None))
 
 
+def dist_set_allgather(allgather) -> None:
+    """Registers allgather(send_ptr, recv_ptr, nbytes) -> None (device pointers; recv holds
+    world * nbytes, rank order) for the sharded general products; None clears it."""
+    if allgather is None:
+        _check(lib.mp_dist_set_allgather(ALLGATHER_FN(), None))
+        _gather_keep.clear()
+        return
+
+    def cb(ctx, send, recv, nbytes, stream):
+        try:
+            allgather(int(send), int(recv), int(nbytes))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to C as MP_ERR_COMM
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    fn = ALLGATHER_FN(cb)
+    _gather_keep[:] = [fn]
+    _check(lib.mp_dist_set_allgather(fn, None))
+
+
+_gather_keep = []
+
+
 def dist_set_torch(group=None) -> None:
-    """Column sharding over torch.distributed (backend nccl: NVLink/NVSwitch)."""
+    """Column sharding over torch.distributed (backend nccl: NVLink/NVSwitch): the per-power
+    statistics all-reduce of the power runs and the all-gather of the general products."""
     import torch
     import torch.distributed as dist
 
     class _Dev:
-        def __init__(self, ptr, n):
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+        def __init__(self, ptr, n, typestr="<i8"):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                              "version": 3, "strides": None, "stream": None}
 
+    def dev():
+        return torch.device("cuda", torch.cuda.current_device())
+
     def allreduce(op, ptr, count):
-        t = torch.as_tensor(_Dev(ptr, count), device=torch.device("cuda", torch.cuda.current_device()))
+        t = torch.as_tensor(_Dev(ptr, count), device=dev())
         dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MIN, group=group)
         torch.cuda.synchronize()
 
-    dist_set(dist.get_rank(group), dist.get_world_size(group), allreduce)
+    world = dist.get_world_size(group)
+
+    def allgather(send, recv, nbytes):
+        src = torch.as_tensor(_Dev(send, nbytes, "|u1"), device=dev())
+        dst = torch.as_tensor(_Dev(recv, nbytes * world, "|u1"), device=dev())
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(dst, src, group=group)
+        else:  # gloo (tests on one GPU): the list form
+            dist.all_gather(list(dst.view(world, nbytes).unbind(0)), src, group=group)
+        torch.cuda.synchronize()
+
+    dist_set(dist.get_rank(group), world, allreduce)
+    dist_set_allgather(allgather)
 
 
 def shard_range(N: int, world: int, rank: int):

@@ -40,6 +40,8 @@ struct Dist {
     int rank = 0, world = 1;
     mp_allreduce_fn fn = nullptr;
     void *ctx = nullptr;
+    mp_allgather_fn gather = nullptr; // general products: column blocks of C to every rank
+    void *gctx = nullptr;
 } g_dist;
 
 struct Opts {
@@ -226,7 +228,7 @@ struct PowerRun {
 struct DevState {
     cudaStream_t stream = nullptr;      // the library's own non-blocking stream
     cudaStream_t user_stream = nullptr; // mp_set_stream override for power runs
-    DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c;
+    DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c, shard_c, gathered;
     // last use of the product scratch (at2, xb, cb, flag): the next user, on whatever stream,
     // waits on it, so a call on another stream cannot overwrite scratch still being read
     cudaEvent_t scratch_ev = nullptr;
@@ -279,26 +281,67 @@ int host_threads()
 // ---------------------------------------------------------------------------------------
 // Product on device buffers (boundary encoding in and out).
 // ---------------------------------------------------------------------------------------
+// C_b = A_b (x) B_b for b < batch (strides in elements; batch 1 = one product).  The items go
+// through the tile kernel together -- one launch of each kernel per chunk of items, the chunk as
+// large as 8 GB of scratch allows -- with one read of the range flag per chunk.
+mp_status mul_device_impl(DevState &st, const uint16_t *dA, int64_t lda, int64_t sA, const uint16_t *dB, int64_t ldb,
+                          int64_t sB, uint16_t *dC, int64_t ldc, int64_t sC, int64_t M, int64_t K, int64_t N,
+                          int64_t batch, cudaStream_t s)
+{
+    const int64_t Mp = pad_rows(M), Kp = pad_rows(K), Np = pad_cols(N);
+    const int64_t at_i = Kp * Mp, xb_i = Kp * Np, cb_i = Mp * Np; // scratch elements per item
+    const int64_t per = at_i * 4 + xb_i * 2 + cb_i * 2;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>({batch, (int64_t)(8LL << 30) / per, 65535}));
+    TRY(st.at2.ensure((size_t)(chunk * at_i) * 4, "A (transposed, duplicated)"));
+    TRY(st.xb.ensure((size_t)(chunk * xb_i) * 2, "B (padded)"));
+    TRY(st.cb.ensure((size_t)(chunk * cb_i) * 2, "C (padded)"));
+    TRY(st.flag.ensure(16, "range flag"));
+    CUDA_TRY(cudaStreamWaitEvent(s, st.scratch_ev, 0)); // the previous user of the scratch is done
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int nb = (int)std::min<int64_t>(chunk, batch - b0);
+        CUDA_TRY(cudaMemsetAsync(st.flag.p, 0, sizeof(int), s));
+        LAUNCH(launch_make_at2(dA + b0 * sA, lda, M, K, st.at2.as<uint32_t>(), Mp, Kp, st.flag.as<int>(), s, nb, sA,
+                               at_i));
+        LAUNCH(launch_encode(dB + b0 * sB, ldb, K, N, st.xb.as<uint16_t>(), Np, Kp, st.flag.as<int>(), s, nb, sB,
+                             xb_i));
+        int flag = 0;
+        COPY(&flag, st.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (flag) return fail(MP_ERR_RANGE, "an input entry lies in (0x7FFE, 0xFFFF)");
+        LAUNCH(launch_minplus(st.at2.as<uint32_t>(), Mp, st.xb.as<uint16_t>(), Np, st.cb.as<uint16_t>(), Np, Mp, Np,
+                              Kp, nullptr, nullptr, s, nb, at_i, xb_i, cb_i));
+        LAUNCH(launch_decode(st.cb.as<uint16_t>(), Np, M, N, dC + b0 * sC, ldc, s, nb, cb_i, sC));
+    }
+    CUDA_TRY(cudaEventRecord(st.scratch_ev, s));
+    return MP_OK;
+}
+
 mp_status mul_device_impl(DevState &st, const uint16_t *dA, int64_t lda, const uint16_t *dB, int64_t ldb,
                           uint16_t *dC, int64_t ldc, int64_t M, int64_t K, int64_t N, cudaStream_t s)
 {
-    const int64_t Mp = pad_rows(M), Kp = pad_rows(K), Np = pad_cols(N);
-    TRY(st.at2.ensure((size_t)Kp * Mp * 4, "A (transposed, duplicated)"));
-    TRY(st.xb.ensure((size_t)Kp * Np * 2, "B (padded)"));
-    TRY(st.cb.ensure((size_t)Mp * Np * 2, "C (padded)"));
-    TRY(st.flag.ensure(16, "range flag"));
-    CUDA_TRY(cudaStreamWaitEvent(s, st.scratch_ev, 0)); // the previous user of the scratch is done
-    CUDA_TRY(cudaMemsetAsync(st.flag.p, 0, sizeof(int), s));
-    LAUNCH(launch_make_at2(dA, lda, M, K, st.at2.as<uint32_t>(), Mp, Kp, st.flag.as<int>(), s));
-    LAUNCH(launch_encode(dB, ldb, K, N, st.xb.as<uint16_t>(), Np, Kp, st.flag.as<int>(), s));
-    int flag = 0;
-    COPY(&flag, st.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+    return mul_device_impl(st, dA, lda, 0, dB, ldb, 0, dC, ldc, 0, M, K, N, 1, s);
+}
+
+// Column-sharded product over the ranks of the distributed context (one GPU each; SURVEY.md
+// section 8(b)/(e)): A replicated, rank r computes C[:, J_r] = A (x) B[:, J_r] on its
+// column shard J_r = mp_shard_range(N, world, r), and the all-gather callback hands every rank
+// every block, which k_unshard places into the whole C (device, pitch N).
+bool sharded_products() { return g_dist.world > 1 && g_dist.gather != nullptr; }
+
+mp_status mul_sharded(DevState &st, const uint16_t *dA, const uint16_t *dB, int64_t ldb, uint16_t *dC, int64_t M,
+                      int64_t K, int64_t N, cudaStream_t s)
+{
+    int64_t c0 = 0, c1 = 0;
+    mp_shard_range(N, g_dist.world, g_dist.rank, &c0, &c1);
+    const int64_t w = round_up((N + g_dist.world - 1) / g_dist.world, 8); // every rank's block width
+    const size_t blk = (size_t)M * w * 2;
+    TRY(st.shard_c.ensure(blk, "C column block"));
+    TRY(st.gathered.ensure(blk * g_dist.world, "gathered C blocks"));
+    if (c1 > c0) TRY(mul_device_impl(st, dA, K, dB + c0, ldb, st.shard_c.as<uint16_t>(), w, M, K, c1 - c0, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    if (flag) return fail(MP_ERR_RANGE, "an input entry lies in (0x7FFE, 0xFFFF)");
-    LAUNCH(launch_minplus(st.at2.as<uint32_t>(), Mp, st.xb.as<uint16_t>(), Np, st.cb.as<uint16_t>(), Np, Mp, Np,
-                          Kp, nullptr, nullptr, s));
-    LAUNCH(launch_decode(st.cb.as<uint16_t>(), Np, M, N, dC, ldc, s));
-    CUDA_TRY(cudaEventRecord(st.scratch_ev, s));
+    if (g_dist.gather(g_dist.gctx, st.shard_c.p, st.gathered.p, (int64_t)blk, (void *)s) != 0)
+        return fail(MP_ERR_COMM, "all-gather callback failed (%zu bytes per rank)", blk);
+    LAUNCH(launch_unshard(st.gathered.as<uint16_t>(), g_dist.world, M, w, N, dC, N, s));
     return MP_OK;
 }
 
@@ -1088,8 +1131,12 @@ mp_status minplus_mul(const uint16_t *A, const uint16_t *B, uint16_t *C, int64_t
     TRY(st->stage_c.ensure((size_t)M * N * 2, "C staging"));
     COPY(st->stage_a.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice, s);
     COPY(st->stage_b.p, B, (size_t)K * N * 2, cudaMemcpyHostToDevice, s);
-    TRY(mul_device_impl(*st, st->stage_a.as<uint16_t>(), K, st->stage_b.as<uint16_t>(), N,
-                        st->stage_c.as<uint16_t>(), N, M, K, N, s));
+    if (sharded_products())
+        TRY(mul_sharded(*st, st->stage_a.as<uint16_t>(), st->stage_b.as<uint16_t>(), N, st->stage_c.as<uint16_t>(),
+                        M, K, N, s));
+    else
+        TRY(mul_device_impl(*st, st->stage_a.as<uint16_t>(), K, st->stage_b.as<uint16_t>(), N,
+                            st->stage_c.as<uint16_t>(), N, M, K, N, s));
     COPY(C, st->stage_c.p, (size_t)M * N * 2, cudaMemcpyDeviceToHost, s);
     CUDA_TRY(cudaStreamSynchronize(s));
     return MP_OK;
@@ -1129,10 +1176,8 @@ mp_status minplus_mul_strided_batched_device(const uint16_t *dA, int64_t lda, in
     int dev = 0;
     DevState *st = nullptr;
     TRY(current_device(&dev, &st));
-    for (int64_t b = 0; b < batch; ++b)
-        TRY(mul_device_impl(*st, dA + b * strideA, lda, dB + b * strideB, ldb, dC + b * strideC, ldc, M, K, N,
-                            (cudaStream_t)stream));
-    return MP_OK;
+    return mul_device_impl(*st, dA, lda, strideA, dB, ldb, strideB, dC, ldc, strideC, M, K, N, batch,
+                           (cudaStream_t)stream);
 }
 
 mp_status minplus_closure(const uint16_t *W, int64_t N, uint16_t *D, int32_t *squarings_out)
@@ -1151,7 +1196,10 @@ mp_status minplus_closure(const uint16_t *W, int64_t N, uint16_t *D, int32_t *sq
     LAUNCH(launch_set_diag_zero(X, N, N, s)); // I (+) W: every vertex reaches itself at cost 0
     int32_t t = 0;
     for (int64_t reach = 1; reach < N - 1; reach *= 2, ++t) { // (I + W)^(2^t) covers paths of 2^t arcs
-        TRY(mul_device_impl(*st, X, N, X, N, Y, N, N, N, N, s));
+        if (sharded_products()) // X is replicated: each rank squares its column block, then all-gather
+            TRY(mul_sharded(*st, X, X, N, Y, N, N, N, s));
+        else
+            TRY(mul_device_impl(*st, X, N, X, N, Y, N, N, N, N, s));
         std::swap(X, Y);
     }
     COPY(D, X, (size_t)N * N * 2, cudaMemcpyDeviceToHost, s);
@@ -1289,12 +1337,24 @@ mp_status mp_dist_set(int rank, int world, mp_allreduce_fn fn, void *ctx)
         g_dist = Dist();
         return MP_OK;
     }
+    const mp_allgather_fn keep = g_dist.gather;
+    void *keep_ctx = g_dist.gctx;
     if (world < 1 || rank < 0 || rank >= world)
         return fail(MP_ERR_DOMAIN, "mp_dist_set: rank %d / world %d invalid", rank, world);
     g_dist.rank = rank;
     g_dist.world = world;
     g_dist.fn = fn;
     g_dist.ctx = ctx;
+    g_dist.gather = keep;
+    g_dist.gctx = keep_ctx;
+    return MP_OK;
+}
+
+mp_status mp_dist_set_allgather(mp_allgather_fn fn, void *ctx)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_dist.gather = fn;
+    g_dist.gctx = fn ? ctx : nullptr;
     return MP_OK;
 }
 

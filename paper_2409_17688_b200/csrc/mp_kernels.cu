@@ -103,8 +103,12 @@ template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_minplus(const uint32_t *__restrict__ AT2, int64_t lda, const uint16_t *__restrict__ X,
               int64_t ldx, uint16_t *__restrict__ C, int64_t ldc, const int32_t *__restrict__ kt_ptr,
-              const int32_t *__restrict__ kt_idx, int num_kt)
+              const int32_t *__restrict__ kt_idx, int num_kt, int64_t sA, int64_t sX, int64_t sC)
 {
+    // batch item blockIdx.z (strided batches: one launch for every item)
+    AT2 += (int64_t)blockIdx.z * sA;
+    X += (int64_t)blockIdx.z * sX;
+    C += (int64_t)blockIdx.z * sC;
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int A_STAGE = kBK * kBM * 4; // 16 KB
     constexpr int B_STAGE = kBK * kBN * 2; // 16 KB
@@ -385,8 +389,10 @@ __device__ __forceinline__ uint32_t enc_dev(uint16_t s, bool &bad)
 // rows, threads over column pairs (one u32 store each).
 __global__ void k_encode(const uint16_t *__restrict__ src, int64_t lds, int64_t rows, int64_t cols,
                          uint16_t *__restrict__ dst, int64_t ldd, int64_t rows_p,
-                         int *__restrict__ range_flag)
+                         int *__restrict__ range_flag, int64_t ss, int64_t sd)
 {
+    src += (int64_t)blockIdx.y * ss; // batch item
+    dst += (int64_t)blockIdx.y * sd;
     bool bad = false;
     for (int64_t i = blockIdx.x; i < rows_p; i += gridDim.x) {
         uint32_t *d = reinterpret_cast<uint32_t *>(dst + i * ldd);
@@ -407,8 +413,11 @@ __global__ void k_encode(const uint16_t *__restrict__ src, int64_t lds, int64_t 
 // AT2 [Kp][Mp] u32: AT2[l][i] = {enc(a_il), enc(a_il)}; +inf padding.  32x32 tiles through
 // shared memory so both the read of A (row-major) and the write of AT2 are coalesced.
 __global__ void k_make_at2(const uint16_t *__restrict__ A, int64_t lda, int64_t M, int64_t K,
-                           uint32_t *__restrict__ AT2, int64_t Mp, int64_t Kp, int *__restrict__ range_flag)
+                           uint32_t *__restrict__ AT2, int64_t Mp, int64_t Kp, int *__restrict__ range_flag,
+                           int64_t sa, int64_t sat)
 {
+    A += (int64_t)blockIdx.z * sa; // batch item
+    AT2 += (int64_t)blockIdx.z * sat;
     __shared__ uint16_t tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.y * 32, l0 = (int64_t)blockIdx.x * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -473,8 +482,10 @@ __global__ void k_x1_from_at2(const uint32_t *__restrict__ AT2, int64_t Np, int6
 
 // dst (rows x cols, ldd, boundary encoding) = dec(src[i][j]) for the valid region.
 __global__ void k_decode(const uint16_t *__restrict__ src, int64_t lds, int64_t rows, int64_t cols,
-                         uint16_t *__restrict__ dst, int64_t ldd)
+                         uint16_t *__restrict__ dst, int64_t ldd, int64_t ss, int64_t sd)
 {
+    src += (int64_t)blockIdx.y * ss; // batch item
+    dst += (int64_t)blockIdx.y * sd;
     const int64_t total = rows * cols;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -1569,14 +1580,14 @@ constexpr int kStages = 4;
 
 cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, int64_t ldx, uint16_t *C,
                            int64_t ldc, int64_t Mp, int64_t ncols_p, int64_t Kp, const int32_t *kt_ptr,
-                           const int32_t *kt_idx, cudaStream_t s)
+                           const int32_t *kt_idx, cudaStream_t s, int batch, int64_t sA, int64_t sX, int64_t sC)
 {
     const int smem = kStages * (kBK * kBM * 4 + kBK * kBN * 2);
     const cudaError_t e = smem_limit(k_minplus<kStages>, smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kBM));
+    dim3 grid((unsigned)(ncols_p / kBN), (unsigned)(Mp / kBM), (unsigned)batch);
     k_minplus<kStages><<<grid, kThreads, smem, s>>>(AT2, lda, X, ldx, C, ldc, kt_ptr, kt_idx,
-                                                    (int)(Kp / kBK));
+                                                    (int)(Kp / kBK), sA, sX, sC);
     return cudaGetLastError();
 }
 
@@ -1823,19 +1834,21 @@ cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int
 }
 
 cudaError_t launch_encode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
-                          int64_t ldd, int64_t rows_p, int *range_flag, cudaStream_t s)
+                          int64_t ldd, int64_t rows_p, int *range_flag, cudaStream_t s, int batch, int64_t ss,
+                          int64_t sd)
 {
-    if (ldd % 2) return cudaErrorInvalidValue; // padded pitches are multiples of 512
-    k_encode<<<(unsigned)std::min<int64_t>(std::max<int64_t>(rows_p, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
-        src, lds, rows, cols, dst, ldd, rows_p, range_flag);
+    if (ldd % 2) return cudaErrorInvalidValue; // padded pitches are multiples of 64
+    const dim3 grid((unsigned)std::min<int64_t>(std::max<int64_t>(rows_p, 1), (int64_t)num_sms() * 8 / batch + 1),
+                    (unsigned)batch);
+    k_encode<<<grid, 256, 0, s>>>(src, lds, rows, cols, dst, ldd, rows_p, range_flag, ss, sd);
     return cudaGetLastError();
 }
 
 cudaError_t launch_make_at2(const uint16_t *A, int64_t lda, int64_t M, int64_t K, uint32_t *AT2, int64_t Mp,
-                            int64_t Kp, int *range_flag, cudaStream_t s)
+                            int64_t Kp, int *range_flag, cudaStream_t s, int batch, int64_t sa, int64_t sat)
 {
-    dim3 grid((unsigned)((Kp + 31) / 32), (unsigned)((Mp + 31) / 32));
-    k_make_at2<<<grid, dim3(32, 8), 0, s>>>(A, lda, M, K, AT2, Mp, Kp, range_flag);
+    dim3 grid((unsigned)((Kp + 31) / 32), (unsigned)((Mp + 31) / 32), (unsigned)batch);
+    k_make_at2<<<grid, dim3(32, 8), 0, s>>>(A, lda, M, K, AT2, Mp, Kp, range_flag, sa, sat);
     return cudaGetLastError();
 }
 
@@ -1868,9 +1881,10 @@ cudaError_t launch_set_diag_zero(uint16_t *X, int64_t ld, int64_t n, cudaStream_
 }
 
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
-                          int64_t ldd, cudaStream_t s)
+                          int64_t ldd, cudaStream_t s, int batch, int64_t ss, int64_t sd)
 {
-    k_decode<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, lds, rows, cols, dst, ldd);
+    const dim3 grid((unsigned)std::max(1, grid_for(rows * cols, 256) / batch), (unsigned)batch);
+    k_decode<<<grid, 256, 0, s>>>(src, lds, rows, cols, dst, ldd, ss, sd);
     return cudaGetLastError();
 }
 
@@ -1879,6 +1893,25 @@ cudaError_t launch_unfold(const uint16_t *X, int64_t ld, int64_t N, const int32_
 {
     const dim3 grid((unsigned)std::min<int64_t>((N + 255) / 256, 64), (unsigned)std::min<int64_t>(N, 16384));
     k_unfold<<<grid, 256, 0, s>>>(X, ld, N, loc, sigma, out);
+    return cudaGetLastError();
+}
+
+// C[i][r w + j] = G[r][i][j] (j < w, r w + j < N): the all-gathered column blocks of a sharded
+// product placed into the whole matrix (pitch ldc)
+__global__ void k_unshard(const uint16_t *__restrict__ G, int world, int64_t M, int64_t w, int64_t N,
+                          uint16_t *__restrict__ C, int64_t ldc)
+{
+    const int64_t total = M * N;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / N, c = t - i * N, r = c / w, j = c - r * w;
+        C[i * ldc + c] = G[(r * M + i) * w + j];
+    }
+}
+
+cudaError_t launch_unshard(const uint16_t *G, int world, int64_t M, int64_t w, int64_t N, uint16_t *C, int64_t ldc,
+                           cudaStream_t s)
+{
+    k_unshard<<<grid_for(M * N, 256), 256, 0, s>>>(G, world, M, w, N, C, ldc);
     return cudaGetLastError();
 }
 

@@ -9,25 +9,32 @@ namespace mp {
 
 // C[Mp][ldc] = AT2 (x) X over Kp inner steps, for the column tiles [0, ncols_p).
 // kt_ptr/kt_idx: optional per-row-tile list of l-tiles with a finite A entry.
+// batch > 1: items b < batch at AT2 + b sA, X + b sX, C + b sC, all in one launch (grid z).
 cudaError_t launch_minplus(const uint32_t *AT2, int64_t lda, const uint16_t *X, int64_t ldx, uint16_t *C,
                            int64_t ldc, int64_t Mp, int64_t ncols_p, int64_t Kp, const int32_t *kt_ptr,
-                           const int32_t *kt_idx, cudaStream_t s);
+                           const int32_t *kt_idx, cudaStream_t s, int batch = 1, int64_t sA = 0, int64_t sX = 0,
+                           int64_t sC = 0);
 cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, int64_t w,
                          unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s);
 cudaError_t launch_compare(const uint16_t *Y, const uint16_t *Z, int64_t ld, int64_t N, int64_t w, int32_t c,
                            unsigned long long *out, cudaStream_t s);
 cudaError_t launch_encode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
-                          int64_t ldd, int64_t rows_p, int *range_flag, cudaStream_t s);
+                          int64_t ldd, int64_t rows_p, int *range_flag, cudaStream_t s, int batch = 1,
+                          int64_t ss = 0, int64_t sd = 0);
 cudaError_t launch_make_at2(const uint16_t *A, int64_t lda, int64_t M, int64_t K, uint32_t *AT2, int64_t Mp,
-                            int64_t Kp, int *range_flag, cudaStream_t s);
+                            int64_t Kp, int *range_flag, cudaStream_t s, int batch = 1, int64_t sa = 0,
+                            int64_t sat = 0);
 cudaError_t launch_build_from_words(const WordMask *words, int64_t N, int n, uint32_t *AT2, int64_t Np,
                                     cudaStream_t s);
 cudaError_t launch_x1_from_at2(const uint32_t *AT2, int64_t Np, int64_t c0, int64_t w, uint16_t *X1,
                                int64_t ldx, cudaStream_t s);
+// C[i][r w + j] = G[r][i][j]: world all-gathered M x w column blocks into the M x N matrix C.
+cudaError_t launch_unshard(const uint16_t *G, int world, int64_t M, int64_t w, int64_t N, uint16_t *C, int64_t ldc,
+                           cudaStream_t s);
 // X[i][i] = 0 for i < n.
 cudaError_t launch_set_diag_zero(uint16_t *X, int64_t ld, int64_t n, cudaStream_t s);
 cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_t cols, uint16_t *dst,
-                          int64_t ldd, cudaStream_t s);
+                          int64_t ldd, cudaStream_t s, int batch = 1, int64_t ss = 0, int64_t sd = 0);
 // Small-N latency path (mp_small.cu): the whole power-until-periodic run in one cluster launch.
 // sigma (may be null): symmetry hint verified on the way (status 1 if violated).
 // out[]: status (0 ok, 1 hint violated, 2 range, 4 not periodic, -1 more than max_nnz finite

@@ -333,14 +333,31 @@ def test_ring_eviction_recompute(mp, oracle_mod):
     recompute path for evicted A^j: n = 7 has lambda = 18, so the partner of the first repeat
     has left the ring."""
     A = mp.build_transition_matrix(7)
-    # Np x ld x 2 B; ld = a multiple of the SpMM CTA width, 256 at this size (spmm_cols)
-    slot = (((A.shape[0] + 127) // 128) * 128) * (((A.shape[0] + 255) // 256) * 256) * 2
+    # Np x ld x 2 B; ld = the SpMM column plan's padded width (mp_column_plan)
+    slot = (((A.shape[0] + 127) // 128) * 128) * mp.column_plan(A.shape[0], A.shape[0])["ld"] * 2
     mp.set_options("auto", device_budget_bytes=19 * slot)  # 19 - 2 reserved = 17 ring slots
     try:
         g = mp.minplus_power_until_periodic(A)
     finally:
         mp.set_options("auto", device_budget_bytes=0)
     assert (g.mu, g.lam, g.offset) == (23, 18, 53)
+
+
+def test_resource_error_reports_bytes(mp):
+    """A device budget below the power store's minimum (17 slots for a 16-power batch at this
+    size) is MP_ERR_RESOURCE, with the slot size and the budget in the message; the
+    next run with the default budget works."""
+    A = mp.build_transition_matrix(7)
+    slot = (((A.shape[0] + 127) // 128) * 128) * mp.column_plan(A.shape[0], A.shape[0])["ld"] * 2
+    mp.set_options("auto", device_budget_bytes=8 * slot)
+    try:
+        with pytest.raises(mp.MinplusError) as e:
+            mp.minplus_power_until_periodic(A)
+    finally:
+        mp.set_options("auto", device_budget_bytes=0)
+    assert e.value.name == "MP_ERR_RESOURCE"
+    assert str(slot) in str(e.value) and str(8 * slot) in str(e.value)
+    assert mp.minplus_power_until_periodic(A).mu == 23
 
 
 # --------------------------------------------------------------------------- symmetry
