@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--spmm-width", type=int, default=0,
+                    help="SpMM CTA width override (mp_set_spmm_width; 0 = automatic)")
     ap.add_argument("--no-row-reuse", action="store_true",
                     help="do not use the row-inclusion reuse of A(D_n) (the SpMM over every finite entry)")
     ap.add_argument("--no-symmetry", action="store_true",
@@ -302,6 +304,7 @@ def run_mine(args):
     # reuse; --no-row-reuse times the plain grouped SpMM instead
     mp.set_transfer_hint(args.n)
     mp.set_row_reuse(not args.no_row_reuse)
+    mp.set_spmm_width(args.spmm_width)
     stream = torch.cuda.current_stream()
     mp.set_stream(stream)
 

@@ -187,7 +187,7 @@ mp_status mp_set_transfer_hint(int n);
 mp_status mp_set_row_reuse(int on);
 
 /* Small-N latency path: single-rank power runs of matrices with N <= 256
- * and at most 16384 finite entries, with the automatic kernel choice and no observer, run
+ * and at most 8192 finite entries, with the automatic kernel choice and no observer, run
  * entirely in one thread-block-cluster launch (products, statistics, repeat search, exact
  * compares; one read of the result).  on = 0 sends them through the general path instead (same
  * results); default on.  Process-wide.  Errors: none. */

@@ -213,6 +213,8 @@ struct PowerRun {
     // observer path: the whole power, unfolded on the device and copied to pinned host memory
     DBuf full_dev;
     DBuf small_hist, small_out, small_sig; // small-N path: power history, result, symmetry hint
+    cudaEvent_t small_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::vector<long long> small_host; // the result's host copy
     uint16_t *full_host = nullptr;
     size_t full_host_bytes = 0;
     ~PowerRun()
@@ -220,6 +222,8 @@ struct PowerRun {
         for (auto ev : events)
             if (ev) cudaEventDestroy(ev);
         if (full_host) cudaFreeHost(full_host);
+        for (auto ev : small_ev)
+            if (ev) cudaEventDestroy(ev);
     }
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
@@ -547,7 +551,7 @@ struct Capture {
 // statistics, repeat search, exact compares -- in one thread-block-cluster launch, one read of
 // the result.  *handled = false (and MP_OK) if A has too many finite entries for the kernel's
 // shared memory; the caller then takes the general path.
-constexpr int kSmallMaxNnz = 16384;
+constexpr int kSmallMaxNnz = 8192; // 64 KB of {offset, value} entries in shared memory
 mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_periodic_result *out, bool *handled)
 {
     *handled = false;
@@ -555,15 +559,9 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     PowerRun &R = *st.pr;
     cudaStream_t s = st.user_stream ? st.user_stream : st.stream;
     const int64_t h2d0 = g_h2d.load(), d2h0 = g_d2h.load();
-    cudaEvent_t ev[4];
-    for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
-    struct Destroy {
-        cudaEvent_t *e;
-        ~Destroy()
-        {
-            for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
-        }
-    } destroy{ev};
+    cudaEvent_t *ev = R.small_ev;
+    if (!ev[0])
+        for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&ev[i]));
     CUDA_TRY(cudaEventRecord(ev[0], s));
     const uint16_t *dA = src.dev;
     int64_t lda = src.lda;
@@ -596,8 +594,9 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     LAUNCH(launch_small_run(dA, lda, N, max_k, kSmallMaxNnz, dsig, R.small_hist.as<uint16_t>(), S,
                             R.small_out.as<long long>(), s));
     CUDA_TRY(cudaEventRecord(ev[2], s));
-    std::vector<long long> h(nout, 0);
-    COPY(h.data(), R.small_out.p, nout * 8, cudaMemcpyDeviceToHost, s);
+    if (R.small_host.size() < nout) R.small_host.assign(nout, 0);
+    long long *h = R.small_host.data();
+    COPY(h, R.small_out.p, nout * 8, cudaMemcpyDeviceToHost, s);
     CUDA_TRY(cudaEventRecord(ev[3], s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (h[0] == -1) return MP_OK; // too many finite entries: the general path

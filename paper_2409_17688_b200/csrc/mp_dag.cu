@@ -147,7 +147,13 @@ __global__ void k_fold(const int32_t *__restrict__ lrows, int64_t nrows, const i
         const int64_t q = lrows[r];
         uint4 *dst = reinterpret_cast<uint4 *>(C + q * ldc) + c;
         uint4 v = *dst;
+#if MP_DEBUG_CHECKS
+        if (q < 0 || (int64_t)c * 8 >= ldc) __trap();
+#endif
         for (int64_t e = off[q]; e < off[q + 1]; ++e) {
+#if MP_DEBUG_CHECKS
+            if (pidx[e] < 0 || pidx[e] == q) __trap();
+#endif
             const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(C + (int64_t)pidx[e] * ldc) + c);
             v.x = __vminu2(v.x, u.x);
             v.y = __vminu2(v.y, u.y);

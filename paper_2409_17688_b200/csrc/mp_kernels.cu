@@ -2,6 +2,7 @@
 // with its roofline; the citations name the paper passage each one implements.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <algorithm>
 #include <mutex>
@@ -12,6 +13,25 @@
 #include "mp_kernels.h"
 
 namespace mp {
+
+// Debug build (-DMP_DEBUG_CHECKS=1, bench_tools/r2/gpu_debug.sh): device-side bounds checks of
+// the indices the kernels derive from their own data structures, trapping on the first
+// violation.  The pool's compute-sanitizer is closed, so this build runs the GPU tests instead.
+#ifndef MP_DEBUG_CHECKS
+#define MP_DEBUG_CHECKS 0
+#endif
+#if MP_DEBUG_CHECKS
+#define MP_CHECK(cond)                                                                                                  \
+    do {                                                                                                                \
+        if (!(cond)) {                                                                                                  \
+            printf("MP_CHECK failed: %s (%s:%d) block (%d,%d) thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x,     \
+                   blockIdx.y, threadIdx.x);                                                                            \
+            __trap();                                                                                                   \
+        }                                                                                                               \
+    } while (0)
+#else
+#define MP_CHECK(cond) ((void)0)
+#endif
 
 // ---------------------------------------------------------------------------------------
 // small PTX helpers
@@ -1411,6 +1431,8 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
             const int64_t gc = c0 + c;
             const int nrows = min(kSpChunk, U - c * kSpChunk);
             const uint32_t ebytes = (uint32_t)(e1 - e0) * kEntBytes;
+            MP_CHECK(e1 >= e0 && ebytes <= (uint32_t)(kSpGroups * kSpChunk) * kEntBytes && nrows >= 1);
+            MP_CHECK(lane >= nrows || (l >= 0 && (int64_t)l < (int64_t)gridDim.x * kSpRows));
             const uint32_t sX = sbase + st * STAGE;
             if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + kSpOffBytes);
             __syncwarp();
@@ -1467,6 +1489,10 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
         for (int gg = 0; gg < kSpGpw; ++gg) {
         const int jg = warp * kSpGpw + gg;
         const int e0 = (int)(Bs[jg] - eb), e1 = (int)(Bs[jg + 1] - eb);
+        MP_CHECK(e0 >= 0 && e0 <= e1 && e1 <= kSpGroups * kSpChunk);
+#if MP_DEBUG_CHECKS
+        for (int q = e0; q < e1; ++q) MP_CHECK(row(q) < (uint32_t)XB && row(q) % kSpRowBytes == 0);
+#endif
         if (e0 < e1) {
             int e = e0;
             uint4 pa[kG / 4], pb[kG / 4], xa[kSpXq], xb[kSpXq];
@@ -1509,6 +1535,7 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
         const int gg = q / kG, r = q % kG;
         const int64_t slot = (int64_t)t * kSpRows + kG * (warp * kSpGpw + gg) + r;
         const int64_t i = rowmap ? (int64_t)rowmap[slot] : slot;
+        MP_CHECK(i >= 0 && i < (int64_t)gridDim.x * kSpRows && col0 + kSpCols <= ldc);
         if constexpr (PPL < 4) { // lane owns columns 2 PPL lane .. + 2 PPL - 1
             uint16_t *crow = C + i * ldc + col0 + 2 * PPL * lane;
             if constexpr (PPL == 2)

@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     uint32_t *Xa = reinterpret_cast<uint32_t *>(smem);
     uint32_t *Xb = Xa + N * 32;
     int32_t *rptr = reinterpret_cast<int32_t *>(Xb + N * 32);
-    uint32_t *ent = reinterpret_cast<uint32_t *>(rptr + ((N + 4) & ~3));
-    Stats *hs = reinterpret_cast<Stats *>(ent + ((max_nnz + 3) & ~3)); // [max_k + 1]
+    // entry e of row i: {byte offset of X row l in a 32 x u32 block, a_il duplicated in both halves}
+    uint2 *ent = reinterpret_cast<uint2 *>(rptr + ((N + 4) & ~3));
+    Stats *hs = reinterpret_cast<Stats *>(ent + ((max_nnz + 1) & ~1)); // [max_k + 1]
     Stats *wred = hs + (max_k + 1);                                       // [kSmWarps]
     Stats *xch = wred + kSmWarps;                                         // [2]: this CTA's partials
     long long *xmis = reinterpret_cast<long long *>(xch + 2);             // [2]: mismatch partials
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             const int l = l0 + lane;
             const uint16_t x = l < N ? A[(int64_t)i * lda + l] : (uint16_t)kBndInf;
             const unsigned m = __ballot_sync(0xFFFFFFFFu, x != kBndInf);
-            if (x != kBndInf) ent[e + __popc(m & ((1u << lane) - 1))] = ((uint32_t)l << 16) | x;
+            if (x != kBndInf) ent[e + __popc(m & ((1u << lane) - 1))] = make_uint2((uint32_t)l * 128u, (uint32_t)x * 0x10001u);
             e += __popc(m);
         }
         // X_1 = A[:, block], device encoding (+inf 0x7FFF), packed pairs
@@ -144,23 +145,44 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     int k = 1;
     for (;; ++k) {
         uint32_t *X = (k == 1) ? Xa : Xc;
-        if (k >= 2) { // A^k = A (x) A^{k-1} on this block: warp per row, lane per column pair
-            for (int i = warp; i < N; i += kSmWarps) {
-                uint32_t acc = 0xFFFFFFFFu;
-                const int e1 = rptr[i + 1];
-                for (int e = rptr[i]; e < e1; ++e) {
-                    const uint32_t q = ent[e];
-                    const uint32_t a = q & 0xFFFFu;
-                    acc = __viaddmin_u16x2(a | (a << 16), Xp[(q >> 16) * 32 + lane], acc);
-                }
-                X[i * 32 + lane] = __vminu2(acc, 0x7FFF7FFFu); // a finite sum >= 0x7FFF is +inf (G6)
-            }
-            __syncthreads();
-        }
-        // ---- a4: statistics of this block (boundary encoding 0xFFFF for +inf in the hash)
+        // ---- A^k = A (x) A^{k-1} on this block (k >= 2) with its a4 statistics: warp per row, lane
+        // per column pair, the row's entries walked four at a time into independent chains.
         Stats st{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
         for (int i = warp; i < N; i += kSmWarps) {
-            const uint32_t p = X[i * 32 + lane];
+            uint32_t p;
+            if (k >= 2) {
+                // broadcast LDS.64 of the entry, LDS of the X pair, DPX: four independent chains
+                uint32_t acc0 = 0xFFFFFFFFu, acc1 = 0xFFFFFFFFu, acc2 = 0xFFFFFFFFu, acc3 = 0xFFFFFFFFu;
+                const uint8_t *xb = reinterpret_cast<const uint8_t *>(Xp) + 4 * lane;
+                const int e0 = rptr[i], e1 = rptr[i + 1];
+#if MP_DEBUG_CHECKS
+                if (e0 < 0 || e1 < e0 || e1 > max_nnz) __trap();
+                for (int q = e0; q < e1; ++q)
+                    if (ent[q].x >= (uint32_t)N * 128u) __trap();
+#endif
+                int e = e0;
+                for (; e + 4 <= e1; e += 4) {
+                    const uint2 q0 = ent[e], q1 = ent[e + 1], q2 = ent[e + 2], q3 = ent[e + 3];
+                    acc0 = __viaddmin_u16x2(q0.y, *reinterpret_cast<const uint32_t *>(xb + q0.x), acc0);
+                    acc1 = __viaddmin_u16x2(q1.y, *reinterpret_cast<const uint32_t *>(xb + q1.x), acc1);
+                    acc2 = __viaddmin_u16x2(q2.y, *reinterpret_cast<const uint32_t *>(xb + q2.x), acc2);
+                    acc3 = __viaddmin_u16x2(q3.y, *reinterpret_cast<const uint32_t *>(xb + q3.x), acc3);
+                }
+                for (; e < e1; ++e) {
+                    const uint2 q0 = ent[e];
+                    acc0 = __viaddmin_u16x2(q0.y, *reinterpret_cast<const uint32_t *>(xb + q0.x), acc0);
+                }
+                acc0 = __vminu2(acc0, acc1);
+                acc2 = __vminu2(acc2, acc3);
+                acc1 = acc0;
+                acc0 = acc2;
+                p = __vminu2(__vminu2(acc0, acc1), 0x7FFF7FFFu); // a finite sum >= 0x7FFF is +inf (G6)
+                X[i * 32 + lane] = p;
+            } else {
+                p = X[i * 32 + lane];
+            }
+            // a4: fingerprint, +inf count, diagonal minimum, first finite entry (boundary
+            // encoding 0xFFFF for +inf in the hash)
             const uint32_t x0 = p & 0xFFFFu, x1 = p >> 16;
             const uint64_t b0 = x0 >= kDevInf ? kBndInf : x0, b1 = x1 >= kDevInf ? kBndInf : x1;
             st.fp += mix64(2 * (uint64_t)i) * (cw0 * b0 + cw1 * b1);
@@ -169,6 +191,8 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             if (v1 && j1 == i) st.dmin = min(st.dmin, (long long)b1);
             if (v0 && x0 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j0) << 16) | (long long)x0);
             if (v1 && x1 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j1) << 16) | (long long)x1);
+            // the block also goes to the history (exact compares of later powers read it)
+            reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)i * ldh + 64 * c)[lane] = p;
         }
         for (int m = 16; m; m >>= 1) {
             st.fp += shfl_xor_u64(st.fp, m);
@@ -177,31 +201,27 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             st.ref = min(st.ref, (long long)shfl_xor_u64((unsigned long long)st.ref, m));
         }
         if (lane == 0) wred[warp] = st;
-        // the block also goes to the history (exact compares of later powers read it)
-        for (int t = tid; t < N * 32; t += kSmThreads)
-            reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)(t >> 5) * ldh + 64 * c)[t & 31] = X[t];
         __syncthreads();
-        if (tid == 0) {
-            Stats s = wred[0];
-            for (int w = 1; w < kSmWarps; ++w) {
-                s.fp += wred[w].fp;
-                s.inf += wred[w].inf;
-                s.dmin = min(s.dmin, wred[w].dmin);
-                s.ref = min(s.ref, wred[w].ref);
+        if (warp == 0) { // the block's partial: lanes < 16 hold the warps' partials
+            Stats s = lane < kSmWarps ? wred[lane] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+            for (int m = 16; m; m >>= 1) {
+                s.fp += shfl_xor_u64(s.fp, m);
+                s.inf += shfl_xor_u64(s.inf, m);
+                s.dmin = min(s.dmin, (long long)shfl_xor_u64((unsigned long long)s.dmin, m));
+                s.ref = min(s.ref, (long long)shfl_xor_u64((unsigned long long)s.ref, m));
             }
-            xch[xi & 1] = s;
+            if (lane == 0) xch[xi & 1] = s;
         }
         cluster.sync(); // partials visible cluster-wide
-        if (tid == 0) {
-            Stats g{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
-            for (int r = 0; r < C; ++r) {
-                const Stats p = cluster.map_shared_rank(xch, r)[xi & 1];
-                g.fp += p.fp;
-                g.inf += p.inf;
-                g.dmin = min(g.dmin, p.dmin);
-                g.ref = min(g.ref, p.ref);
+        if (warp == 0) { // lane r < C reads CTA r's partial; every lane ends with the sum
+            Stats g = lane < C ? cluster.map_shared_rank(xch, lane)[xi & 1] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+            for (int m = 16; m; m >>= 1) {
+                g.fp += shfl_xor_u64(g.fp, m);
+                g.inf += shfl_xor_u64(g.inf, m);
+                g.dmin = min(g.dmin, (long long)shfl_xor_u64((unsigned long long)g.dmin, m));
+                g.ref = min(g.ref, (long long)shfl_xor_u64((unsigned long long)g.ref, m));
             }
-            hs[k] = g;
+            if (lane == 0) hs[k] = g;
             if (!dense_from && g.inf == 0) dense_from = k;
         }
         ++xi;
@@ -209,11 +229,25 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         // ---- a5: forward first-repeat search, j = k-1 down to 1 (identical in every CTA)
         int jn = k - 1;
         while (!found) {
-            if (tid == 0) {
-                int cc = 0, j = jn;
-                while (j >= 1 && !candidate(hs[k], hs[j], S, &cc)) --j;
-                flags[2] = j;
-                flags[3] = cc;
+            if (warp == 0) { // lane t tests j = jn - t (32 at a time, descending): the highest hit
+                const Stats sk = hs[k];
+                int j = 0, cc = 0;
+                for (int top = jn; top >= 1; top -= 32) {
+                    const int jj = top - lane;
+                    int c1 = 0;
+                    const bool hit = jj >= 1 && candidate(sk, hs[jj], S, &c1);
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
+                    if (m) {
+                        const int src = __ffs(m) - 1; // the lowest lane = the highest j
+                        j = __shfl_sync(0xFFFFFFFFu, jj, src);
+                        cc = __shfl_sync(0xFFFFFFFFu, c1, src);
+                        break;
+                    }
+                }
+                if (lane == 0) {
+                    flags[2] = j;
+                    flags[3] = cc;
+                }
             }
             __syncthreads();
             const int j = flags[2], cc = flags[3];
@@ -234,10 +268,10 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             for (int m = 16; m; m >>= 1) bad += (long long)shfl_xor_u64((unsigned long long)bad, m);
             if (lane == 0) wred[warp].fp = (unsigned long long)bad;
             __syncthreads();
-            if (tid == 0) {
-                long long b = 0;
-                for (int w = 0; w < kSmWarps; ++w) b += (long long)wred[w].fp;
-                xmis[xi & 1] = b;
+            if (warp == 0) {
+                long long b = lane < kSmWarps ? (long long)wred[lane].fp : 0;
+                for (int m = 16; m; m >>= 1) b += (long long)shfl_xor_u64((unsigned long long)b, m);
+                if (lane == 0) xmis[xi & 1] = b;
             }
             cluster.sync();
             long long total = 0;
@@ -282,7 +316,7 @@ int small_run_ctas(int64_t N) { return (int)((N + 63) / 64); }
 
 size_t small_run_smem(int64_t N, int max_k, int max_nnz)
 {
-    return (size_t)N * 32 * 4 * 2 + (size_t)((N + 4) & ~3) * 4 + (size_t)((max_nnz + 3) & ~3) * 4 +
+    return (size_t)N * 32 * 4 * 2 + (size_t)((N + 4) & ~3) * 4 + (size_t)((max_nnz + 1) & ~1) * 8 +
            (size_t)(max_k + 1 + kSmWarps + 2) * sizeof(Stats) + 2 * 8 + 8 * 4;
 }
 
@@ -291,8 +325,16 @@ cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_
 {
     if (N < 1 || N > kSmallMaxN) return cudaErrorInvalidValue;
     const size_t smem = small_run_smem(N, max_k, max_nnz);
-    cudaError_t e = cudaFuncSetAttribute(k_small_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    // the shared-memory limit is per device; raise it once per device to the largest size used
+    static size_t limit[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (limit[dev] < smem) {
+        const cudaError_t e = cudaFuncSetAttribute(k_small_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        limit[dev] = smem;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)small_run_ctas(N));
     cfg.blockDim = dim3(kSmThreads);
