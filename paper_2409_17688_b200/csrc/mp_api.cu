@@ -428,6 +428,12 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
         cudaGetLastError();
         return fail(MP_ERR_CUDA, "building the sparse form of A failed: %s", cudaGetErrorString(e));
     }
+    if (dag) { // every parent's support must lie inside its child's
+        int bad = 0;
+        COPY(&bad, R.rdag.bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (bad) return fail(MP_ERR_CUDA, "internal: a row-inclusion parent is not a subset of its row");
+    }
     R.issued_spmm = (double)R.sp.entries * (double)R.sp.group_rows * (double)R.ld;
     return MP_OK;
 }

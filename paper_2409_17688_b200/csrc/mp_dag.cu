@@ -4,15 +4,16 @@
 // Whether p can follow q depends on q only through its zero positions z(q) and its
 // 2-positions t(q): rule (1) asks p_i = 0 wherever q_i = 2, rules (2)-(3) count q_i = 0 among
 // the neighbours of p_i.  The label of the arc q -> p is the number of zeros of p, a
-// function of p alone.  So if q' is q with one letter 1 turned into a 2 (same zeros, one more
-// 2), every p that can follow q' can follow q with the same label: row q' of A is row q
-// restricted to a subset of its support.  For every power,
+// function of p alone.  Let q' be q with ONE letter q_i in {0, 1} turned into a 2.  Every p that
+// can follow q' has p_i = 0 (rule 1), so no rule applies at position i, and at every other
+// position the rules read the same letters of q and q'; hence p can follow q, with the same
+// label: row q' of A is row q restricted to a subset of its support.  For every power,
 //     (A^k)_(q, j) = min( min over parents q' of (A^k)_(q', j),
 //                         min over l in extra(q) of a_ql + (A^{k-1})_(l, j) ),
 // extra(q) = supp(q) minus the union of the parents' supports -- the same minimum over the same
 // terms (min is idempotent), regrouped.  The SpMM kernel runs on the extra entries only
-// (0.227 of nnz(A) at n = 12) and a fold pass per level of the parent DAG (a parent has one
-// more 2, so levels are at most n) takes the minimum with the parents' finished rows.
+// (about 3 % of nnz(A) for n >= 10) and a fold pass per level of the parent DAG (a parent has one
+// more 2, so there are at most n + 1 levels) takes the minimum with the parents' finished rows.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,7 +52,7 @@ __device__ __forceinline__ int64_t find_key(const uint32_t *__restrict__ keys, i
     return (lo < N && keys[lo] == k) ? lo : -1;
 }
 
-// parents of q: the words q with one letter 1 turned into 2 that are correct words
+// parents of q: the words q with one letter 0 or 1 turned into a 2 that are correct words
 // (count pass if pidx == nullptr, else fill from off[q])
 __global__ void k_dag_parents(const WordMask *__restrict__ w, const uint32_t *__restrict__ keys, int64_t N, int n,
                               const int64_t *__restrict__ off, int32_t *__restrict__ cnt, int32_t *__restrict__ pidx)
@@ -64,8 +65,9 @@ __global__ void k_dag_parents(const WordMask *__restrict__ w, const uint32_t *__
         int c = 0;
         int64_t o = pidx ? off[q] : 0;
         for (int b = 0; b < n; ++b) {
-            if (!((w[q].o >> b) & 1u)) continue;
-            const int64_t p = find_key(keys, N, kq + pw3[n - 1 - b]); // letter b: 1 -> 2
+            if ((w[q].t >> b) & 1u) continue;
+            const uint32_t up = ((w[q].o >> b) & 1u) ? 1u : 2u;         // letter b: 1 -> 2 or 0 -> 2
+            const int64_t p = find_key(keys, N, kq + up * pw3[n - 1 - b]);
             if (p < 0) continue;
             if (pidx) pidx[o++] = (int32_t)p;
             ++c;
@@ -121,20 +123,29 @@ __global__ void k_level_scatter(const int32_t *__restrict__ level, int64_t N, in
     }
 }
 
-// extra(q) = supp(q) minus the parents' supports, as bitsets (warp per row, lanes over words)
+// extra(q) = supp(q) minus the parents' supports, as bitsets (warp per row, lanes over words);
+// *bad is set if some parent's support is not inside supp(q) (impossible for A(D_n), whose
+// identity the run has verified; the check keeps a wrong structure from ever changing a result)
 __global__ void k_extra_bits(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, const int64_t *__restrict__ off,
-                             const int32_t *__restrict__ pidx, uint32_t *__restrict__ ebits)
+                             const int32_t *__restrict__ pidx, uint32_t *__restrict__ ebits, int *__restrict__ bad)
 {
     const int lane = threadIdx.x & 31;
+    bool wrong = false;
     for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < N;
          q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t e0 = off[q], e1 = off[q + 1];
         for (int64_t k = lane; k < nw; k += 32) {
-            uint32_t m = bits[q * nw + k];
-            for (int64_t e = e0; e < e1 && m; ++e) m &= ~bits[(int64_t)pidx[e] * nw + k];
+            const uint32_t s = bits[q * nw + k];
+            uint32_t m = s;
+            for (int64_t e = e0; e < e1; ++e) {
+                const uint32_t pb = bits[(int64_t)pidx[e] * nw + k];
+                wrong |= (pb & ~s) != 0u;
+                m &= ~pb;
+            }
             ebits[q * nw + k] = m;
         }
     }
+    if (wrong) atomicOr(bad, 1);
 }
 
 // (A^k)_(q, :) = min((A^k)_(q, :), (A^k)_(p, :)) over the parents p of the rows q of one level
@@ -202,6 +213,8 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
     if ((e = A(d.lrows, (size_t)N * 4)) != cudaSuccess) return e;
     if ((e = A(hist, 32 * 4)) != cudaSuccess) return e;
     if ((e = A(d.lptr_dev, 33 * 8)) != cudaSuccess) return e;
+    if ((e = A(d.bad, 16)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(d.bad, 0, sizeof(int), s)) != cudaSuccess) return e;
     const int gb = grid_rows(N, 256);
     k_word_keys<<<gb, 256, 0, s>>>(words, N, n, keys);
     k_dag_parents<<<gb, 256, 0, s>>>(words, keys, N, n, nullptr, cnt, nullptr);
@@ -244,7 +257,7 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
 cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const RowDag &d, uint32_t *ebits,
                               cudaStream_t s)
 {
-    k_extra_bits<<<grid_rows(N * 32, 256), 256, 0, s>>>(bits, nw, N, d.off, d.idx, ebits);
+    k_extra_bits<<<grid_rows(N * 32, 256), 256, 0, s>>>(bits, nw, N, d.off, d.idx, ebits, d.bad);
     return cudaGetLastError();
 }
 

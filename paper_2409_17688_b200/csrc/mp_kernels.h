@@ -98,13 +98,15 @@ SpmmPlan spmm_plan(int64_t Np, int64_t w);
 cudaError_t launch_spmm(const SparseA &sa, const SpmmPlan &P, const uint16_t *X, int64_t ldx, uint16_t *C,
                         int64_t ldc, int64_t Mp, cudaStream_t s, int *launches);
 // Row-inclusion reuse for A(D_n) (mp_dag.cu): parents of row q = the
-// words q with one letter 1 turned into 2 (their rows are restrictions of row q); rows by level.
+// words q with one letter 0 or 1 turned into 2 (their rows are restrictions of row q); rows by
+// level.
 struct RowDag {
     int64_t *off = nullptr;     // [N + 1] parent lists (CSR)
     int32_t *idx = nullptr;     // parents
     int32_t *level = nullptr;   // [N] 0 without parents, else 1 + max level of the parents
     int32_t *lrows = nullptr;   // [N] rows grouped by level
     int64_t *lptr_dev = nullptr;
+    int *bad = nullptr;         // set by launch_extra_bits if a parent's support is not a subset
     std::vector<int64_t> lptr;  // [levels + 1] level offsets into lrows (host copy)
     int levels = 0;
     int64_t parents = 0;
