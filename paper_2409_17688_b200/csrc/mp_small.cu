@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "mp_internal.h"
@@ -25,6 +26,13 @@ namespace cg = cooperative_groups;
 namespace mp {
 
 namespace {
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
 
 constexpr int kSmThreads = 512; // 16 warps; warp w computes rows w, w + 16, ...
 constexpr int kSmWarps = kSmThreads / 32;
@@ -60,30 +68,39 @@ __device__ bool candidate(const Stats &k, const Stats &j, unsigned long long S, 
 
 } // namespace
 
+// Cluster layout: C = ceil(N / 64) column blocks x R row parts (small_run_shape); CTA (c, r)
+// (cluster rank c + C r) computes rows [r0, r1) of column block c of every power and writes
+// them into its own and its R - 1 row peers' copies of that column block (distributed shared
+// memory), so each CTA holds the whole block of A^k for the next product.
 // sigma (may be null): a symmetry hint to verify (every finite A_il must reappear at
 // (sigma i, sigma l)); the run itself computes every column.
 // out[]: status (0 ok, 1 symmetry hint violated, 2 range, 4 not periodic, -1 too many entries
-// for shared memory), mu,
-// lambda, offset, k_last, dense_from, then diag_min[k] and fingerprint[k] for k = 0..max_k.
+// for shared memory), mu, lambda, offset, k_last, dense_from, then diag_min[k] and
+// fingerprint[k] for k = 0..max_k.
 __global__ void __launch_bounds__(kSmThreads, 1)
-    k_small_run(const uint16_t *__restrict__ A, int64_t lda, int N, int max_k, int max_nnz,
+    k_small_run(const uint16_t *__restrict__ A, int64_t lda, int N, int C, int max_k, int max_nnz,
                 const int32_t *__restrict__ sigma, uint16_t *__restrict__ hist, unsigned long long S,
                 long long *__restrict__ out)
 {
     extern __shared__ __align__(16) uint8_t smem[];
     cg::cluster_group cluster = cg::this_cluster();
-    const int C = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
+    const int nct = (int)cluster.num_blocks(), rk = (int)cluster.block_rank();
+    const int R = nct / C, c = rk % C, r = rk / C;
+    const int rows_per = (N + R - 1) / R;
+    const int r0 = min(N, r * rows_per), r1 = min(N, r0 + rows_per), nr = r1 - r0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ldh = 64 * C;                // history pitch (columns of all CTAs)
-    const int64_t hsz = (int64_t)N * ldh;  // one power in the history
+    const int ldh = 64 * C;               // history pitch (columns of all CTAs)
+    const int64_t hsz = (int64_t)N * ldh; // one power in the history
 
-    // shared memory: X blocks (2 x N x 32 u32) | row pointers | entries | statistics history |
-    // per-warp partials | cluster exchange (2 parity buffers) | flags
+    // shared memory: X blocks (2 x N x 32 u32) | row weights of the own rows | row pointers |
+    // entries of the own rows | statistics history | per-warp partials | cluster exchange (2
+    // parity buffers) | mismatch exchange | flags
     uint32_t *Xa = reinterpret_cast<uint32_t *>(smem);
     uint32_t *Xb = Xa + N * 32;
-    int32_t *rptr = reinterpret_cast<int32_t *>(Xb + N * 32);
-    // entry e of row i: {byte offset of X row l in a 32 x u32 block, a_il duplicated in both halves}
-    uint2 *ent = reinterpret_cast<uint2 *>(rptr + ((N + 4) & ~3));
+    uint64_t *rw = reinterpret_cast<uint64_t *>(Xb + N * 32); // [rows_per] s(2i)
+    int32_t *rptr = reinterpret_cast<int32_t *>(rw + rows_per);
+    // entry e of an own row: {byte offset of X row l in a 32 x u32 block, a_il in both halves}
+    uint2 *ent = reinterpret_cast<uint2 *>(rptr + ((rows_per + 4) & ~3));
     Stats *hs = reinterpret_cast<Stats *>(ent + ((max_nnz + 1) & ~1)); // [max_k + 1]
     Stats *wred = hs + (max_k + 1);                                       // [kSmWarps]
     Stats *xch = wred + kSmWarps;                                         // [2]: this CTA's partials
@@ -94,10 +111,12 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     const bool v0 = j0 < N, v1 = j1 < N;
     const uint64_t cw0 = v0 ? mix64(2 * (uint64_t)j0 + 1) : 0, cw1 = v1 ? mix64(2 * (uint64_t)j1 + 1) : 0;
 
-    // ---- a2: row lists of A (every CTA builds its own copy), range check, X_1 block
+    // ---- a2: row lists of the own rows, range and symmetry checks, X_1 block (every row)
     if (tid == 0) flags[0] = flags[1] = flags[4] = 0;
+    for (int t = tid; t < nr; t += kSmThreads) rw[t] = mix64(2 * (uint64_t)(r0 + t));
     __syncthreads();
-    for (int i = warp; i < N; i += kSmWarps) {
+    for (int ii = warp; ii < nr; ii += kSmWarps) {
+        const int i = r0 + ii;
         int cnt = 0;
         bool bad = false, asym = false;
         for (int l0 = 0; l0 < N; l0 += 32) {
@@ -109,21 +128,37 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         }
         if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) flags[0] = 1;
         if (__any_sync(0xFFFFFFFFu, asym) && lane == 0) flags[4] = 1;
-        if (lane == 0) rptr[i + 1] = cnt;
+        if (lane == 0) rptr[ii + 1] = cnt;
+    }
+    for (int i = warp; i < N; i += kSmWarps) { // X_1 = A[:, block], device encoding, packed pairs
+        const uint16_t a0 = v0 ? A[(int64_t)i * lda + j0] : (uint16_t)kBndInf;
+        const uint16_t a1 = v1 ? A[(int64_t)i * lda + j1] : (uint16_t)kBndInf;
+        Xa[i * 32 + lane] = (uint32_t)(a0 == kBndInf ? kDevInf : a0) | ((uint32_t)(a1 == kBndInf ? kDevInf : a1) << 16);
     }
     __syncthreads();
     if (tid == 0) {
         rptr[0] = 0;
-        for (int i = 0; i < N; ++i) rptr[i + 1] += rptr[i];
-        flags[1] = rptr[N];
+        for (int ii = 0; ii < nr; ++ii) rptr[ii + 1] += rptr[ii];
+        flags[1] = rptr[nr] > max_nnz;
     }
-    __syncthreads();
-    if (flags[0] || flags[4] || flags[1] > max_nnz) { // every CTA sees the same A: uniform exit
-        if (c == 0 && tid == 0) out[0] = flags[0] ? 2 : flags[4] ? 1 : -1;
+    cluster.sync(); // every CTA's flags are final: one decision for the whole cluster
+    bool stop = false;
+    int status = 0;
+    for (int q = 0; q < nct; ++q) {
+        const int *f = cluster.map_shared_rank(flags, q);
+        if (f[0]) status = 2;
+        else if (f[4] && status != 2) status = 1;
+        else if (f[1] && status == 0) status = -1;
+    }
+    stop = status != 0;
+    cluster.sync(); // nobody changes its flags before every CTA has read them
+    if (stop) {
+        if (rk == 0 && tid == 0) out[0] = status;
         return;
     }
-    for (int i = warp; i < N; i += kSmWarps) {
-        int e = rptr[i];
+    for (int ii = warp; ii < nr; ii += kSmWarps) {
+        const int i = r0 + ii;
+        int e = rptr[ii];
         for (int l0 = 0; l0 < N; l0 += 32) {
             const int l = l0 + lane;
             const uint16_t x = l < N ? A[(int64_t)i * lda + l] : (uint16_t)kBndInf;
@@ -131,10 +166,6 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             if (x != kBndInf) ent[e + __popc(m & ((1u << lane) - 1))] = make_uint2((uint32_t)l * 128u, (uint32_t)x * 0x10001u);
             e += __popc(m);
         }
-        // X_1 = A[:, block], device encoding (+inf 0x7FFF), packed pairs
-        const uint16_t a0 = v0 ? A[(int64_t)i * lda + j0] : (uint16_t)kBndInf;
-        const uint16_t a1 = v1 ? A[(int64_t)i * lda + j1] : (uint16_t)kBndInf;
-        Xa[i * 32 + lane] = (uint32_t)(a0 == kBndInf ? kDevInf : a0) | ((uint32_t)(a1 == kBndInf ? kDevInf : a1) << 16);
     }
     __syncthreads();
 
@@ -143,18 +174,20 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     int mu = 0, lam = 0, off = 0, k_last = 0, dense_from = 0;
     bool found = false;
     int k = 1;
+    const uint32_t xlane = (uint32_t)__cvta_generic_to_shared(Xa) + 4 * lane; // this lane's column pair
     for (;; ++k) {
         uint32_t *X = (k == 1) ? Xa : Xc;
-        // ---- A^k = A (x) A^{k-1} on this block (k >= 2) with its a4 statistics: warp per row, lane
-        // per column pair, the row's entries walked four at a time into independent chains.
+        const uint32_t xp_s = xlane + (uint32_t)((Xp - Xa) * 4);
+        // ---- A^k = A (x) A^{k-1} on the own rows of this block (k >= 2) with the a4
+        // statistics: warp per row, lane per column pair, entries walked four at a time into
+        // independent chains; each new row also goes to the R - 1 row peers.
         Stats st{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
-        for (int i = warp; i < N; i += kSmWarps) {
+        for (int ii = warp; ii < nr; ii += kSmWarps) {
+            const int i = r0 + ii;
             uint32_t p;
             if (k >= 2) {
-                // broadcast LDS.64 of the entry, LDS of the X pair, DPX: four independent chains
                 uint32_t acc0 = 0xFFFFFFFFu, acc1 = 0xFFFFFFFFu, acc2 = 0xFFFFFFFFu, acc3 = 0xFFFFFFFFu;
-                const uint8_t *xb = reinterpret_cast<const uint8_t *>(Xp) + 4 * lane;
-                const int e0 = rptr[i], e1 = rptr[i + 1];
+                const int e0 = rptr[ii], e1 = rptr[ii + 1];
 #if MP_DEBUG_CHECKS
                 if (e0 < 0 || e1 < e0 || e1 > max_nnz) __trap();
                 for (int q = e0; q < e1; ++q)
@@ -163,21 +196,19 @@ __global__ void __launch_bounds__(kSmThreads, 1)
                 int e = e0;
                 for (; e + 4 <= e1; e += 4) {
                     const uint2 q0 = ent[e], q1 = ent[e + 1], q2 = ent[e + 2], q3 = ent[e + 3];
-                    acc0 = __viaddmin_u16x2(q0.y, *reinterpret_cast<const uint32_t *>(xb + q0.x), acc0);
-                    acc1 = __viaddmin_u16x2(q1.y, *reinterpret_cast<const uint32_t *>(xb + q1.x), acc1);
-                    acc2 = __viaddmin_u16x2(q2.y, *reinterpret_cast<const uint32_t *>(xb + q2.x), acc2);
-                    acc3 = __viaddmin_u16x2(q3.y, *reinterpret_cast<const uint32_t *>(xb + q3.x), acc3);
+                    acc0 = __viaddmin_u16x2(q0.y, lds32(xp_s + q0.x), acc0);
+                    acc1 = __viaddmin_u16x2(q1.y, lds32(xp_s + q1.x), acc1);
+                    acc2 = __viaddmin_u16x2(q2.y, lds32(xp_s + q2.x), acc2);
+                    acc3 = __viaddmin_u16x2(q3.y, lds32(xp_s + q3.x), acc3);
                 }
                 for (; e < e1; ++e) {
                     const uint2 q0 = ent[e];
-                    acc0 = __viaddmin_u16x2(q0.y, *reinterpret_cast<const uint32_t *>(xb + q0.x), acc0);
+                    acc0 = __viaddmin_u16x2(q0.y, lds32(xp_s + q0.x), acc0);
                 }
-                acc0 = __vminu2(acc0, acc1);
-                acc2 = __vminu2(acc2, acc3);
-                acc1 = acc0;
-                acc0 = acc2;
-                p = __vminu2(__vminu2(acc0, acc1), 0x7FFF7FFFu); // a finite sum >= 0x7FFF is +inf (G6)
+                p = __vminu2(__vminu2(__vminu2(acc0, acc1), __vminu2(acc2, acc3)), 0x7FFF7FFFu); // G6 clamp
                 X[i * 32 + lane] = p;
+                for (int rr = 0; rr < R; ++rr) // the row peers' copies of this column block
+                    if (rr != r) cluster.map_shared_rank(X, c + C * rr)[i * 32 + lane] = p;
             } else {
                 p = X[i * 32 + lane];
             }
@@ -185,13 +216,13 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             // encoding 0xFFFF for +inf in the hash)
             const uint32_t x0 = p & 0xFFFFu, x1 = p >> 16;
             const uint64_t b0 = x0 >= kDevInf ? kBndInf : x0, b1 = x1 >= kDevInf ? kBndInf : x1;
-            st.fp += mix64(2 * (uint64_t)i) * (cw0 * b0 + cw1 * b1);
+            st.fp += rw[ii] * (cw0 * b0 + cw1 * b1);
             st.inf += (v0 && x0 >= kDevInf) + (v1 && x1 >= kDevInf);
             if (v0 && j0 == i) st.dmin = min(st.dmin, (long long)b0);
             if (v1 && j1 == i) st.dmin = min(st.dmin, (long long)b1);
             if (v0 && x0 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j0) << 16) | (long long)x0);
             if (v1 && x1 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j1) << 16) | (long long)x1);
-            // the block also goes to the history (exact compares of later powers read it)
+            // the row also goes to the history (exact compares of later powers read it)
             reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)i * ldh + 64 * c)[lane] = p;
         }
         for (int m = 16; m; m >>= 1) {
@@ -202,7 +233,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         }
         if (lane == 0) wred[warp] = st;
         __syncthreads();
-        if (warp == 0) { // the block's partial: lanes < 16 hold the warps' partials
+        if (warp == 0) { // the CTA's partial: lanes < 16 hold the warps' partials
             Stats s = lane < kSmWarps ? wred[lane] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
             for (int m = 16; m; m >>= 1) {
                 s.fp += shfl_xor_u64(s.fp, m);
@@ -212,9 +243,10 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             }
             if (lane == 0) xch[xi & 1] = s;
         }
-        cluster.sync(); // partials visible cluster-wide
-        if (warp == 0) { // lane r < C reads CTA r's partial; every lane ends with the sum
-            Stats g = lane < C ? cluster.map_shared_rank(xch, lane)[xi & 1] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+        cluster.sync(); // partials and the peers' rows of A^k visible cluster-wide
+        if (warp == 0) { // lane q < nct reads CTA q's partial; every lane ends with the sum
+            Stats g = lane < nct ? cluster.map_shared_rank(xch, lane)[xi & 1]
+                                 : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
             for (int m = 16; m; m >>= 1) {
                 g.fp += shfl_xor_u64(g.fp, m);
                 g.inf += shfl_xor_u64(g.inf, m);
@@ -252,11 +284,13 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             __syncthreads();
             const int j = flags[2], cc = flags[3];
             if (j < 1) break;
-            // exact compare of this block: equal +inf pattern, X_k - X_j = cc on finite entries
+            // exact compare of the own rows: equal +inf pattern, X_k - X_j = cc on finite entries
             long long bad = 0;
             const uint16_t *Z = hist + (int64_t)j * hsz + 64 * c;
-            for (int t = tid; t < N * 32; t += kSmThreads) {
-                const uint32_t y = X[t], z = reinterpret_cast<const uint32_t *>(Z + (int64_t)(t >> 5) * ldh)[t & 31];
+            for (int t = tid; t < nr * 32; t += kSmThreads) {
+                const int i = r0 + (t >> 5);
+                const uint32_t y = X[i * 32 + (t & 31)];
+                const uint32_t z = reinterpret_cast<const uint32_t *>(Z + (int64_t)i * ldh)[t & 31];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!(h ? v1 : v0)) continue;
@@ -275,7 +309,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             }
             cluster.sync();
             long long total = 0;
-            for (int r = 0; r < C; ++r) total += cluster.map_shared_rank(xmis, r)[xi & 1];
+            for (int q = 0; q < nct; ++q) total += cluster.map_shared_rank(xmis, q)[xi & 1];
             ++xi;
             if (total == 0) {
                 found = true;
@@ -297,7 +331,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         }
     }
     cluster.sync(); // no CTA leaves while another may still read its shared memory
-    if (c == 0 && tid == 0) {
+    if (rk == 0 && tid == 0) {
         out[0] = found ? 0 : 4;
         out[1] = mu;
         out[2] = lam;
@@ -312,43 +346,60 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     }
 }
 
-int small_run_ctas(int64_t N) { return (int)((N + 63) / 64); }
-
-size_t small_run_smem(int64_t N, int max_k, int max_nnz)
+// C column blocks of 64 columns; R row parts (about 56 rows each) as far as a cluster of 16 allows.
+static void small_run_shape(int64_t N, int *C, int *R)
 {
-    return (size_t)N * 32 * 4 * 2 + (size_t)((N + 4) & ~3) * 4 + (size_t)((max_nnz + 1) & ~1) * 8 +
-           (size_t)(max_k + 1 + kSmWarps + 2) * sizeof(Stats) + 2 * 8 + 8 * 4;
+    *C = (int)((N + 63) / 64);
+    *R = (int)std::max<int64_t>(1, std::min<int64_t>(16 / *C, (N + 55) / 56));
+}
+
+int small_run_ctas(int64_t N)
+{
+    int C, R;
+    small_run_shape(N, &C, &R);
+    return C; // the history pitch is 64 C columns
+}
+
+size_t small_run_smem(int64_t N, int R, int max_k, int max_nnz)
+{
+    const int64_t rows_per = (N + R - 1) / R;
+    return (size_t)N * 32 * 4 * 2 + (size_t)rows_per * 8 + (size_t)((rows_per + 4) & ~3) * 4 +
+           (size_t)((max_nnz + 1) & ~1) * 8 + (size_t)(max_k + 1 + kSmWarps + 2) * sizeof(Stats) + 2 * 8 + 8 * 4;
 }
 
 cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_k, int max_nnz, const int32_t *sigma,
                              uint16_t *hist, uint64_t S, long long *out, cudaStream_t s)
 {
     if (N < 1 || N > kSmallMaxN) return cudaErrorInvalidValue;
-    const size_t smem = small_run_smem(N, max_k, max_nnz);
-    // the shared-memory limit is per device; raise it once per device to the largest size used
+    int C, R;
+    small_run_shape(N, &C, &R);
+    const size_t smem = small_run_smem(N, R, max_k, max_nnz);
+    // per-device kernel attributes: the shared-memory limit (raised to the largest size used)
+    // and clusters of up to 16 CTAs (non-portable size)
     static size_t limit[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
     if (limit[dev] < smem) {
-        const cudaError_t e = cudaFuncSetAttribute(k_small_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_small_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_small_run, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         limit[dev] = smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)small_run_ctas(N));
+    cfg.gridDim = dim3((unsigned)(C * R));
     cfg.blockDim = dim3(kSmThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)small_run_ctas(N);
+    attr[0].val.clusterDim.x = (unsigned)(C * R);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_small_run, A, lda, (int)N, max_k, max_nnz, sigma, hist, (unsigned long long)S,
-                              out);
+    return cudaLaunchKernelEx(&cfg, k_small_run, A, lda, (int)N, C, max_k, max_nnz, sigma, hist,
+                              (unsigned long long)S, out);
 }
 
 } // namespace mp
