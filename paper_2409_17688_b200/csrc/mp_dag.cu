@@ -175,6 +175,112 @@ __global__ void k_fold(const int32_t *__restrict__ lrows, int64_t nrows, const i
     }
 }
 
+// Fold and statistics of one DAG level in one pass (the a4 statistics fused into the reuse's
+// fold): thread = an 8-column slice of the power, looping over the level's rows; each row is
+// first finished (min with its parents' rows, already final: earlier levels) -- level 0 rows
+// have no parents and are only read -- and then hashed exactly as k_stats / k_stats_sym do:
+//   H += s(2i) s(2g+1) x  (+ s(2 sigma i) s(2 sigma g + 1) x for a mirrored column, SYM),
+//   +inf count (x2 for a mirrored column), diagonal minimum over (g, g), first finite entry
+//   key (t << 16) | x over t = i N + g and (with SYM) t = sigma i N + sigma g.
+// Columns: local column jj stands for g = gcol[jj] (SYM) or g = c0 + jj.  The level launches
+// of one power accumulate into the same statistics slot (atomicAdd / atomicMin per block).
+template <bool SYM>
+__global__ void __launch_bounds__(128)
+    k_fold_stats(const int32_t *__restrict__ lrows, int64_t nrows, const int64_t *__restrict__ off,
+                 const int32_t *__restrict__ pidx, uint16_t *__restrict__ C, int64_t ld, int64_t N,
+                 const int32_t *__restrict__ gcol, int64_t c0, const int32_t *__restrict__ sigma,
+                 const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t w, int64_t rpb,
+                 bool fold, unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
+{
+    unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
+    unsigned dmin = 0xFFFFu;
+    const int64_t j0 = (int64_t)blockIdx.x * 1024 + (int64_t)threadIdx.x * 8;
+    const int64_t r0 = (int64_t)blockIdx.y * rpb, r1 = min(nrows, r0 + rpb);
+    if (j0 < w && r0 < r1) {
+        const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
+        uint64_t b[8], bm[8];
+        int32_t g[8], m[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            g[e] = e < nc ? (SYM ? gcol[j0 + e] : (int32_t)(c0 + j0 + e)) : 0;
+            m[e] = (SYM && e < nc) ? sigma[g[e]] : g[e];
+            b[e] = e < nc ? mix64(2 * (uint64_t)g[e] + 1) : 0;
+            bm[e] = (SYM && e < nc && m[e] != g[e]) ? mix64(2 * (uint64_t)m[e] + 1) : 0;
+        }
+        for (int64_t r = r0; r < r1; ++r) {
+            const int64_t i = lrows[r];
+            uint4 *dst = reinterpret_cast<uint4 *>(C + i * ld + j0);
+            uint4 v = *dst;
+            if (fold) {
+                const int64_t e0 = off[i], e1 = off[i + 1];
+                for (int64_t e = e0; e < e1; ++e) {
+                    const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(C + (int64_t)pidx[e] * ld + j0));
+                    v.x = __vminu2(v.x, u.x);
+                    v.y = __vminu2(v.y, u.y);
+                    v.z = __vminu2(v.z, u.z);
+                    v.w = __vminu2(v.w, u.w);
+                }
+                if (e1 > e0) *dst = v;
+            }
+            const int64_t si = SYM ? (int64_t)sigma[i] : i;
+            const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+            uint64_t rs = 0, rm = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (e >= nc) break;
+                uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                const bool two = SYM && m[e] != g[e];
+                if (x >= kDevInf) {
+                    x = kBndInf;
+                    infc += two ? 2 : 1;
+                } else {
+                    unsigned long long key = ((uint64_t)(i * N + g[e]) << 16) | x;
+                    if (key < ref) ref = key;
+                    if (SYM) {
+                        key = ((uint64_t)(si * N + m[e]) << 16) | x;
+                        if (key < ref) ref = key;
+                    }
+                }
+                rs += b[e] * x;
+                if (SYM) rm += bm[e] * x;
+                if (g[e] == i) dmin = min(dmin, x);
+            }
+            h += rw[i] * rs + (SYM ? rwm[i] * rm : 0ull);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+        infc += __shfl_xor_sync(0xFFFFFFFFu, infc, o);
+        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
+        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, o));
+    }
+    __shared__ unsigned long long sh[4], sn[4], sr[4];
+    __shared__ unsigned sd[4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sh[warp] = h;
+        sn[warp] = infc;
+        sd[warp] = dmin;
+        sr[warp] = ref;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long H = 0, I = 0, Rf = 0x7FFFFFFFFFFFFFFFull;
+        unsigned D = 0xFFFFu;
+        for (int k = 0; k < 4; ++k) {
+            H += sh[k];
+            I += sn[k];
+            D = min(D, sd[k]);
+            Rf = min(Rf, sr[k]);
+        }
+        if (H) atomicAdd(out_sum + 0, H);
+        if (I) atomicAdd(out_sum + 1, I);
+        if (D < 0xFFFFu) atomicMin(out_min + 0, (unsigned long long)D);
+        if (Rf != 0x7FFFFFFFFFFFFFFFull) atomicMin(out_min + 1, Rf);
+    }
+}
+
 // A (matrix source) equals A(D_n) built from the words: flag set on the first difference
 __global__ void k_verify_transfer(const uint16_t *__restrict__ A, int64_t lda, const WordMask *__restrict__ w, int64_t N,
                                   unsigned full, int *__restrict__ flag)
@@ -267,6 +373,31 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
     for (int l = 1; l < d.levels; ++l) {
         const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
         k_fold<<<grid_rows(nr * c8, 256), 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc, c8);
+        if (launches) ++*launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_fold_stats(const RowDag &d, uint16_t *C, int64_t ld, int64_t N, const int32_t *gcol, int64_t c0,
+                              const int32_t *sigma, const uint64_t *rw, const uint64_t *rwm, int64_t w,
+                              unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s, int *launches)
+{
+    const int64_t gx = std::max<int64_t>(1, (w + 1023) / 1024);
+    for (int l = 0; l < d.levels; ++l) {
+        const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
+        // about 8 blocks of 128 threads per SM over the level, at least 32 rows per block (a
+        // thread's setup -- 16 column weights -- costs about as much as hashing a dozen rows)
+        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((148 * 8 + gx - 1) / gx, (nr + 31) / 32));
+        const int64_t rpb = (nr + gy - 1) / gy;
+        const dim3 grid((unsigned)gx, (unsigned)gy);
+        if (sigma)
+            k_fold_stats<true><<<grid, 128, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ld, N, gcol, c0,
+                                                    sigma, rw, rwm, w, rpb, l > 0, out_sum, out_min);
+        else
+            k_fold_stats<false><<<grid, 128, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ld, N, gcol,
+                                                     c0, sigma, rw, rwm, w, rpb, l > 0, out_sum, out_min);
         if (launches) ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -1842,7 +1842,7 @@ __global__ void k_row_weights(int64_t N, const int32_t *__restrict__ sigma, uint
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
         rw[i] = mix64(2 * (uint64_t)i);
-        rwm[i] = mix64(2 * (uint64_t)sigma[i]);
+        rwm[i] = mix64(2 * (uint64_t)(sigma ? sigma[i] : i));
     }
 }
 
