@@ -57,13 +57,17 @@ std::vector<int32_t> g_sym;
 bool g_word_sym = true;
 bool g_small_off = false; // mp_set_small_path(0): always the general path
 int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be A(D_n)
-// MP_FOLD_STATS=0: separate fold and statistics passes instead of the fused one (diagnostic)
+// MP_FOLD_STATS=1: the fold passes also compute the statistics (k_fold_stats).  Off by default:
+// measured slower at n = 12 (6.95 ms per power against 2.43 + 1.42 ms for k_fold + k_stats_sym,
+// profiles/r2/README.md) -- a thread walks its column slice down the level's rows, so each row
+// is three dependent global loads the warp waits for, where k_fold runs one thread per
+// (row, 8 columns) and hides that latency by sheer parallelism.
 bool fold_stats_on()
 {
     static int on = -1;
     if (on < 0) {
         const char *e = getenv("MP_FOLD_STATS");
-        on = (e && *e == '0') ? 0 : 1;
+        on = (e && *e == '1') ? 1 : 0;
     }
     return on == 1;
 }
