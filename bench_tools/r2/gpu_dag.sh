@@ -10,3 +10,4 @@ for n in 12 11 10; do
 done
 timeout 600 python bench.py --n 12 --steps 3 --warmup 3 --no-cpu-baseline --no-row-reuse > gpurun_out/${TAG}_bench_n12_noreuse.log 2>&1
 for n in 3 6; do timeout 600 python bench.py --n $n --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench_n$n.log 2>&1; done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_n12.csv python bench.py --n 12 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1

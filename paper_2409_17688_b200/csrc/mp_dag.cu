@@ -149,12 +149,20 @@ __global__ void k_extra_bits(const uint32_t *__restrict__ bits, int64_t nw, int6
 }
 
 // (A^k)_(q, :) = min((A^k)_(q, :), (A^k)_(p, :)) over the parents p of the rows q of one level
-// (8 columns per thread; the parents' rows are final: they belong to earlier levels)
+// (8 columns per thread; the parents' rows are final: they belong to earlier levels).  The
+// threads walk the level slab by slab (kFoldSlab columns of every row of the level, then the
+// next slab), so the threads running at one time read the parents' rows of one slab: each
+// parent row segment (read by about four children) comes from DRAM once and then from L2.
+constexpr int64_t kFoldSlab = 256; // 8-column chunks per slab: 2048 columns
 __global__ void k_fold(const int32_t *__restrict__ lrows, int64_t nrows, const int64_t *__restrict__ off,
                        const int32_t *__restrict__ pidx, uint16_t *__restrict__ C, int64_t ldc, int64_t c8)
 {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nrows * c8; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = t / c8, c = t - r * c8;
+    const int64_t per_slab = nrows * kFoldSlab;
+    const int64_t total = per_slab * ((c8 + kFoldSlab - 1) / kFoldSlab);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slab = t / per_slab, rem = t - slab * per_slab;
+        const int64_t r = rem / kFoldSlab, c = slab * kFoldSlab + (rem - r * kFoldSlab);
+        if (c >= c8) continue;
         const int64_t q = lrows[r];
         uint4 *dst = reinterpret_cast<uint4 *>(C + q * ldc) + c;
         uint4 v = *dst;
@@ -373,6 +381,8 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
     for (int l = 1; l < d.levels; ++l) {
         const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
         k_fold<<<grid_rows(nr * c8, 256), 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc, c8);
+        // (grid_rows caps the grid at 148 x 16 blocks: the slab order above needs the running
+        // threads to be a contiguous range of t)
         if (launches) ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -34,7 +34,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr)
     return v;
 }
 
-constexpr int kSmThreads = 512; // 16 warps; warp w computes rows w, w + 16, ...
+constexpr int kSmThreads = 512; // at most 16 warps; warp w computes rows w, w + nwarps, ...
 constexpr int kSmWarps = kSmThreads / 32;
 
 struct Stats { // the per-power statistics of k_stats (mp_power_stats), int64 fields
@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     const int rows_per = (N + R - 1) / R;
     const int r0 = min(N, r * rows_per), r1 = min(N, r0 + rows_per), nr = r1 - r0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nthreads = blockDim.x, nwarps = nthreads >> 5; // fewer warps for few rows
     const int ldh = 64 * C;               // history pitch (columns of all CTAs)
     const int64_t hsz = (int64_t)N * ldh; // one power in the history
 
@@ -113,9 +114,9 @@ __global__ void __launch_bounds__(kSmThreads, 1)
 
     // ---- a2: row lists of the own rows, range and symmetry checks, X_1 block (every row)
     if (tid == 0) flags[0] = flags[1] = flags[4] = 0;
-    for (int t = tid; t < nr; t += kSmThreads) rw[t] = mix64(2 * (uint64_t)(r0 + t));
+    for (int t = tid; t < nr; t += nthreads) rw[t] = mix64(2 * (uint64_t)(r0 + t));
     __syncthreads();
-    for (int ii = warp; ii < nr; ii += kSmWarps) {
+    for (int ii = warp; ii < nr; ii += nwarps) {
         const int i = r0 + ii;
         int cnt = 0;
         bool bad = false, asym = false;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         if (__any_sync(0xFFFFFFFFu, asym) && lane == 0) flags[4] = 1;
         if (lane == 0) rptr[ii + 1] = cnt;
     }
-    for (int i = warp; i < N; i += kSmWarps) { // X_1 = A[:, block], device encoding, packed pairs
+    for (int i = warp; i < N; i += nwarps) { // X_1 = A[:, block], device encoding, packed pairs
         const uint16_t a0 = v0 ? A[(int64_t)i * lda + j0] : (uint16_t)kBndInf;
         const uint16_t a1 = v1 ? A[(int64_t)i * lda + j1] : (uint16_t)kBndInf;
         Xa[i * 32 + lane] = (uint32_t)(a0 == kBndInf ? kDevInf : a0) | ((uint32_t)(a1 == kBndInf ? kDevInf : a1) << 16);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         if (rk == 0 && tid == 0) out[0] = status;
         return;
     }
-    for (int ii = warp; ii < nr; ii += kSmWarps) {
+    for (int ii = warp; ii < nr; ii += nwarps) {
         const int i = r0 + ii;
         int e = rptr[ii];
         for (int l0 = 0; l0 < N; l0 += 32) {
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         // statistics: warp per row, lane per column pair, entries walked four at a time into
         // independent chains; each new row also goes to the R - 1 row peers.
         Stats st{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
-        for (int ii = warp; ii < nr; ii += kSmWarps) {
+        for (int ii = warp; ii < nr; ii += nwarps) {
             const int i = r0 + ii;
             uint32_t p;
             if (k >= 2) {
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         if (lane == 0) wred[warp] = st;
         __syncthreads();
         if (warp == 0) { // the CTA's partial: lanes < 16 hold the warps' partials
-            Stats s = lane < kSmWarps ? wred[lane] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+            Stats s = lane < nwarps ? wred[lane] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
             for (int m = 16; m; m >>= 1) {
                 s.fp += shfl_xor_u64(s.fp, m);
                 s.inf += shfl_xor_u64(s.inf, m);
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             // exact compare of the own rows: equal +inf pattern, X_k - X_j = cc on finite entries
             long long bad = 0;
             const uint16_t *Z = hist + (int64_t)j * hsz + 64 * c;
-            for (int t = tid; t < nr * 32; t += kSmThreads) {
+            for (int t = tid; t < nr * 32; t += nthreads) {
                 const int i = r0 + (t >> 5);
                 const uint32_t y = X[i * 32 + (t & 31)];
                 const uint32_t z = reinterpret_cast<const uint32_t *>(Z + (int64_t)i * ldh)[t & 31];
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             if (lane == 0) wred[warp].fp = (unsigned long long)bad;
             __syncthreads();
             if (warp == 0) {
-                long long b = lane < kSmWarps ? (long long)wred[lane].fp : 0;
+                long long b = lane < nwarps ? (long long)wred[lane].fp : 0;
                 for (int m = 16; m; m >>= 1) b += (long long)shfl_xor_u64((unsigned long long)b, m);
                 if (lane == 0) xmis[xi & 1] = b;
             }
@@ -388,7 +389,10 @@ cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(C * R));
-    cfg.blockDim = dim3(kSmThreads);
+    // a warp per row at a time: about four rows per warp, 4 to 16 warps
+    const int64_t rows_per = (N + R - 1) / R;
+    const int warps = (int)std::max<int64_t>(4, std::min<int64_t>(kSmWarps, (rows_per + 3) / 4));
+    cfg.blockDim = dim3((unsigned)(32 * warps));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
