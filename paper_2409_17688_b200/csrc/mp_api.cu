@@ -817,12 +817,13 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
         }
         CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, 3 * sizeof(int), s));
+        // A verified equal to A(D_n) is reflection-symmetric (DESIGN.md section 4 "Symmetry"):
+        // a symmetry hint that IS the word reversal then needs no separate check
+        const bool sym_implied = hint && R.sym && R.sigma == word_reversal(g_transfer_n);
         LAUNCH(launch_check_a(R.a_src, R.a_ld, N, R.Np, need_occ ? R.occ.as<uint8_t>() : nullptr, R.flag.as<int>(),
-                              R.sym ? R.dsig.as<int32_t>() : nullptr, R.flag.as<int>() + 1,
-                              R.bits_ok ? R.bits.as<uint32_t>() : nullptr, s));
-        if (hint)
-            LAUNCH(launch_verify_transfer(R.a_src, R.a_ld, R.words.as<WordMask>(), N, g_transfer_n,
-                                          R.flag.as<int>() + 2, s));
+                              R.sym && !sym_implied ? R.dsig.as<int32_t>() : nullptr, R.flag.as<int>() + 1,
+                              R.bits_ok ? R.bits.as<uint32_t>() : nullptr, s, hint ? R.words.as<WordMask>() : nullptr,
+                              g_transfer_n, R.flag.as<int>() + 2));
         int hflag[3] = {0, 0, 0};
         COPY(hflag, R.flag.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, s);
         CUDA_TRY(cudaStreamSynchronize(s));

@@ -94,32 +94,14 @@ __global__ void k_level_hist(const int32_t *__restrict__ level, int64_t N, int32
         atomicAdd(&hist[level[q]], 1);
 }
 
-// rows grouped by level (order inside a level: ascending row, from a per-level ballot scan)
-__global__ void k_level_scatter(const int32_t *__restrict__ level, int64_t N, int L,
-                                const int64_t *__restrict__ lptr, int32_t *__restrict__ lrows)
+// rows grouped by level (the order inside a level is irrelevant: a level's rows are folded
+// independently); cursor[] zeroed by the caller
+__global__ void k_level_scatter(const int32_t *__restrict__ level, int64_t N, const int64_t *__restrict__ lptr,
+                                unsigned long long *__restrict__ cursor, int32_t *__restrict__ lrows)
 {
-    // one block; the block walks the rows in order, per level a running offset
-    __shared__ int64_t pos[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int l = threadIdx.x; l < L; l += blockDim.x) pos[l] = lptr[l];
-    __syncthreads();
-    for (int64_t base = 0; base < N; base += 32 * nwarps) {
-        // warp w handles rows base + 32 w .. + 31; warps take turns to keep the order
-        for (int turn = 0; turn < nwarps; ++turn) {
-            if (warp == turn) {
-                const int64_t q = base + 32 * warp + lane;
-                const int lv = q < N ? level[q] : -1;
-                for (int l = 0; l < L; ++l) {
-                    const unsigned m = __ballot_sync(0xFFFFFFFFu, lv == l);
-                    if (!m) continue;
-                    if (lv == l) lrows[pos[l] + __popc(m & ((1u << lane) - 1))] = (int32_t)q;
-                    __syncwarp();
-                    if (lane == 0) pos[l] += __popc(m);
-                    __syncwarp();
-                }
-            }
-            __syncthreads();
-        }
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+        const int l = level[q];
+        lrows[lptr[l] + (int64_t)atomicAdd(cursor + l, 1ull)] = (int32_t)q;
     }
 }
 
@@ -149,37 +131,59 @@ __global__ void k_extra_bits(const uint32_t *__restrict__ bits, int64_t nw, int6
 }
 
 // (A^k)_(q, :) = min((A^k)_(q, :), (A^k)_(p, :)) over the parents p of the rows q of one level
-// (8 columns per thread; the parents' rows are final: they belong to earlier levels).  The
-// threads walk the level slab by slab (kFoldSlab columns of every row of the level, then the
-// next slab), so the threads running at one time read the parents' rows of one slab: each
-// parent row segment (read by about four children) comes from DRAM once and then from L2.
-constexpr int64_t kFoldSlab = 256; // 8-column chunks per slab: 2048 columns
-__global__ void k_fold(const int32_t *__restrict__ lrows, int64_t nrows, const int64_t *__restrict__ off,
-                       const int32_t *__restrict__ pidx, uint16_t *__restrict__ C, int64_t ldc, int64_t c8)
+// (the parents' rows are final: they belong to earlier levels).  A warp takes one row segment of
+// kFoldSeg columns (32 B per lane, 4 x 16-byte loads per row read): lane e < #parents loads the
+// e-th parent index once and shuffles it to the warp, so the row's metadata costs a few
+// instructions per 1 KB of data.  Work items go segment-major (every row of the level for
+// segment 0, then segment 1, ...), so the warps running at one time read the parents' rows of
+// one segment column, which L2 then serves to the parents' other children.
+constexpr int kFoldSeg = 1024; // columns per warp item (ld is a multiple of 64: the last is partial)
+__global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows, int64_t nrows,
+                                              const int64_t *__restrict__ off, const int32_t *__restrict__ pidx,
+                                              uint16_t *__restrict__ C, int64_t ldc)
 {
-    const int64_t per_slab = nrows * kFoldSlab;
-    const int64_t total = per_slab * ((c8 + kFoldSlab - 1) / kFoldSlab);
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t slab = t / per_slab, rem = t - slab * per_slab;
-        const int64_t r = rem / kFoldSlab, c = slab * kFoldSlab + (rem - r * kFoldSlab);
-        if (c >= c8) continue;
+    const int lane = threadIdx.x & 31;
+    const int64_t nseg = (ldc + kFoldSeg - 1) / kFoldSeg, items = nrows * nseg;
+    for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
+         it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t seg = it / nrows, r = it - seg * nrows;
         const int64_t q = lrows[r];
-        uint4 *dst = reinterpret_cast<uint4 *>(C + q * ldc) + c;
-        uint4 v = *dst;
+        const int64_t e0 = off[q], np = off[q + 1] - e0;
+        const int32_t mine = lane < np ? pidx[e0 + lane] : 0;
+        uint16_t *row = C + q * ldc + seg * kFoldSeg;
+        const int ncols = (int)(ldc - seg * kFoldSeg < kFoldSeg ? ldc - seg * kFoldSeg : kFoldSeg);
 #if MP_DEBUG_CHECKS
-        if (q < 0 || (int64_t)c * 8 >= ldc) __trap();
+        if (q < 0 || np > 32) __trap();
 #endif
-        for (int64_t e = off[q]; e < off[q + 1]; ++e) {
-#if MP_DEBUG_CHECKS
-            if (pidx[e] < 0 || pidx[e] == q) __trap();
-#endif
-            const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(C + (int64_t)pidx[e] * ldc) + c);
-            v.x = __vminu2(v.x, u.x);
-            v.y = __vminu2(v.y, u.y);
-            v.z = __vminu2(v.z, u.z);
-            v.w = __vminu2(v.w, u.w);
+        uint4 v[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int col = 256 * h + 8 * lane;
+            v[h] = col < ncols ? *reinterpret_cast<const uint4 *>(row + col) : make_uint4(0, 0, 0, 0);
         }
-        *dst = v;
+        for (int e = 0; e < np; ++e) {
+            const int64_t p = __shfl_sync(0xFFFFFFFFu, mine, e);
+#if MP_DEBUG_CHECKS
+            if (p < 0 || p == q) __trap();
+#endif
+            const uint16_t *prow = C + p * ldc + seg * kFoldSeg;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int col = 256 * h + 8 * lane;
+                if (col < ncols) {
+                    const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(prow + col));
+                    v[h].x = __vminu2(v[h].x, u.x);
+                    v[h].y = __vminu2(v[h].y, u.y);
+                    v[h].z = __vminu2(v[h].z, u.z);
+                    v[h].w = __vminu2(v[h].w, u.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int col = 256 * h + 8 * lane;
+            if (col < ncols) *reinterpret_cast<uint4 *>(row + col) = v[h];
+        }
     }
 }
 
@@ -289,22 +293,6 @@ __global__ void __launch_bounds__(128)
     }
 }
 
-// A (matrix source) equals A(D_n) built from the words: flag set on the first difference
-__global__ void k_verify_transfer(const uint16_t *__restrict__ A, int64_t lda, const WordMask *__restrict__ w, int64_t N,
-                                  unsigned full, int *__restrict__ flag)
-{
-    bool bad = false;
-    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
-        const WordMask q = w[i];
-        for (int64_t l = threadIdx.x; l < N; l += blockDim.x) {
-            const WordMask p = w[l];
-            const uint16_t want = can_follow_mask(q, p, full) ? (uint16_t)p.zeros : (uint16_t)kBndInf;
-            bad |= A[i * lda + l] != want;
-        }
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
-}
-
 int grid_rows(int64_t work, int per_block)
 {
     const int64_t g = (work + per_block - 1) / per_block;
@@ -325,7 +313,7 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
     if ((e = A(d.off, (size_t)(N + 1) * 8)) != cudaSuccess) return e;
     if ((e = A(d.level, (size_t)N * 4)) != cudaSuccess) return e;
     if ((e = A(d.lrows, (size_t)N * 4)) != cudaSuccess) return e;
-    if ((e = A(hist, 32 * 4)) != cudaSuccess) return e;
+    if ((e = A(hist, 32 * 8)) != cudaSuccess) return e;
     if ((e = A(d.lptr_dev, 33 * 8)) != cudaSuccess) return e;
     if ((e = A(d.bad, 16)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(d.bad, 0, sizeof(int), s)) != cudaSuccess) return e;
@@ -362,7 +350,8 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
     if (d.lptr.back() != N) return cudaErrorUnknown; // levels are contiguous from 0
     if ((e = cudaMemcpyAsync(d.lptr_dev, d.lptr.data(), d.lptr.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return e;
-    k_level_scatter<<<1, 1024, 0, s>>>(d.level, N, d.levels, d.lptr_dev, d.lrows);
+    if ((e = cudaMemsetAsync(hist, 0, 32 * 8, s)) != cudaSuccess) return e; // reused as the cursors
+    k_level_scatter<<<gb, 256, 0, s>>>(d.level, N, d.lptr_dev, reinterpret_cast<unsigned long long *>(hist), d.lrows);
     *launches += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaStreamSynchronize(s); // d.lptr (host) and ho go out of scope safely
@@ -377,12 +366,13 @@ cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const
 
 cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncols, cudaStream_t s, int *launches)
 {
-    const int64_t c8 = (ncols + 7) / 8;
     for (int l = 1; l < d.levels; ++l) {
         const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
-        k_fold<<<grid_rows(nr * c8, 256), 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc, c8);
-        // (grid_rows caps the grid at 148 x 16 blocks: the slab order above needs the running
-        // threads to be a contiguous range of t)
+        const int64_t items = nr * ((ncols + kFoldSeg - 1) / kFoldSeg);
+        // a grid of at most 148 x 8 blocks of 8 warps: the running warps are a contiguous range
+        // of items (the segment-major order above relies on it)
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, 148 * 8));
+        k_fold<<<grid, 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc);
         if (launches) ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -415,11 +405,5 @@ cudaError_t launch_fold_stats(const RowDag &d, uint16_t *C, int64_t ld, int64_t 
     return cudaSuccess;
 }
 
-cudaError_t launch_verify_transfer(const uint16_t *A, int64_t lda, const WordMask *words, int64_t N, int n, int *flag,
-                                   cudaStream_t s)
-{
-    k_verify_transfer<<<grid_rows(N, 1), 256, 0, s>>>(A, lda, words, N, (1u << n) - 1u, flag);
-    return cudaGetLastError();
-}
 
 } // namespace mp

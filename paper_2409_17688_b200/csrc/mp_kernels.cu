@@ -2297,14 +2297,17 @@ cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, c
 // 128 x 32 tiles (occ zeroed by the caller): one warp per (row, 32-column tile).
 __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N, int64_t Kt, uint8_t *__restrict__ occ,
                           int *__restrict__ range_flag, const int32_t *__restrict__ sigma, int *__restrict__ sym_flag,
-                          uint32_t *__restrict__ bits, int64_t nw)
+                          uint32_t *__restrict__ bits, int64_t nw, const WordMask *__restrict__ words, unsigned full,
+                          int *__restrict__ xfer_flag)
 {
     // blocks stride over rows, warps over the row's 32-column words (= the tile columns of occ)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    bool bad = false, asym = false;
+    bool bad = false, asym = false, notxfer = false;
     for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
         const uint16_t *row = A + i * lda;
         const int64_t si = sigma ? (int64_t)sigma[i] : 0;
+        WordMask wq = {0, 0, 0, 0};
+        if (words) wq = words[i];
         for (int64_t k0 = warp; k0 < nw; k0 += 4 * nwarps) { // 4 words' loads in flight
             uint16_t xv[4];
 #pragma unroll
@@ -2323,6 +2326,12 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
                 // symmetry hint: every finite entry must reappear at (sigma i, sigma j); sigma x
                 // sigma is a bijection, so the +inf entries then map onto +inf entries too
                 if (sigma && f) asym |= A[si * lda + sigma[c]] != x;
+                // transfer hint: A must be A(D_n) entry by entry (Alg. 1: label zeros(p) if p
+                // can follow q, else +inf)
+                if (words && c < N) {
+                    const WordMask wp = words[c];
+                    notxfer |= x != (can_follow_mask(wq, wp, full) ? (uint16_t)wp.zeros : (uint16_t)kBndInf);
+                }
                 const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
                 if (lane == 0) {
                     if (bits) bits[i * nw + k] = m;
@@ -2336,15 +2345,18 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
     }
     if (bad) *range_flag = 1;
     if (asym) *sym_flag = 1;
+    if (notxfer) *xfer_flag = 1;
 }
 
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
-                           const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s)
+                           const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s, const WordMask *words,
+                           int n, int *xfer_flag)
 {
     static_assert(kBK == 32, "occupancy tiles are the 32-column words");
     const int64_t Kt = Np / kBK;
     k_check_a<<<(unsigned)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
-        A, lda, N, Kt, occ, range_flag, sigma, sym_flag, bits, (N + 31) / 32);
+        A, lda, N, Kt, occ, range_flag, sigma, sym_flag, bits, (N + 31) / 32, words, words ? (1u << n) - 1u : 0u,
+        xfer_flag);
     return cudaGetLastError();
 }
 

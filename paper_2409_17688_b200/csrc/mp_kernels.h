@@ -125,9 +125,6 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
 cudaError_t launch_fold_stats(const RowDag &d, uint16_t *C, int64_t ld, int64_t N, const int32_t *gcol, int64_t c0,
                               const int32_t *sigma, const uint64_t *rw, const uint64_t *rwm, int64_t w,
                               unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s, int *launches);
-// *flag |= 1 unless A (row-major, boundary encoding) equals A(D_n)
-cudaError_t launch_verify_transfer(const uint16_t *A, int64_t lda, const WordMask *words, int64_t N, int n, int *flag,
-                                   cudaStream_t s);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
 // pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).
@@ -162,8 +159,11 @@ cudaError_t launch_row_weights(int64_t N, const int32_t *sigma, uint64_t *rw, ui
 // If sigma is not null, sym_flag is set when some finite A_ij != A_(sigma i, sigma j).
 // If bits is not null it receives A's support bitsets (bit b of bits[i * ceil(N/32) + k] =
 // A_(i, 32k + b) finite).
+// If words is not null, *xfer_flag is set unless A equals A(D_n) entry by entry (the transfer
+// hint, verified in the same pass).
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
-                           const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s);
+                           const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s,
+                           const WordMask *words = nullptr, int n = 0, int *xfer_flag = nullptr);
 cudaError_t launch_tile_occupancy(const uint32_t *AT2, int64_t Mp, int64_t Kp, uint8_t *occ, cudaStream_t s);
 
 } // namespace mp
