@@ -2310,10 +2310,12 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
         if (words) wq = words[i];
         for (int64_t k0 = warp; k0 < nw; k0 += 4 * nwarps) { // 4 words' loads in flight
             uint16_t xv[4];
+            WordMask wv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int64_t c = (k0 + (int64_t)u * nwarps) * 32 + lane;
                 xv[u] = c < N ? row[c] : kBndInf;
+                wv[u] = (words && c < N) ? words[c] : WordMask{0, 0, 0, 0};
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -2328,10 +2330,8 @@ __global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N
                 if (sigma && f) asym |= A[si * lda + sigma[c]] != x;
                 // transfer hint: A must be A(D_n) entry by entry (Alg. 1: label zeros(p) if p
                 // can follow q, else +inf)
-                if (words && c < N) {
-                    const WordMask wp = words[c];
-                    notxfer |= x != (can_follow_mask(wq, wp, full) ? (uint16_t)wp.zeros : (uint16_t)kBndInf);
-                }
+                if (words && c < N)
+                    notxfer |= x != (can_follow_mask(wq, wv[u], full) ? (uint16_t)wv[u].zeros : (uint16_t)kBndInf);
                 const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
                 if (lane == 0) {
                     if (bits) bits[i * nw + k] = m;
