@@ -57,6 +57,13 @@ std::vector<int32_t> g_sym;
 bool g_word_sym = true;
 bool g_small_off = false; // mp_set_small_path(0): always the general path
 int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be A(D_n)
+// MP_LOOKAHEAD=0: no lookahead in the large-N power loop (diagnostic)
+bool lookahead_on()
+{
+    const char *e = getenv("MP_LOOKAHEAD"); // read per run: tests switch it
+    return !(e && *e == '0');
+}
+
 // MP_FOLD_STATS=1: the fold passes also compute the statistics (k_fold_stats).  Off by default:
 // measured slower at n = 12 (6.95 ms per power against 2.43 + 1.42 ms for k_fold + k_stats_sym,
 // profiles/r2/README.md) -- a thread walks its column slice down the level's rows, so each row
@@ -64,12 +71,8 @@ int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be
 // (row, 8 columns) and hides that latency by sheer parallelism.
 bool fold_stats_on()
 {
-    static int on = -1;
-    if (on < 0) {
-        const char *e = getenv("MP_FOLD_STATS");
-        on = (e && *e == '1') ? 1 : 0;
-    }
-    return on == 1;
+    const char *e = getenv("MP_FOLD_STATS"); // read per run: tests switch it
+    return e && *e == '1';
 }
 bool g_row_reuse = true;   // mp_set_row_reuse: row-inclusion reuse for A(D_n)
 
@@ -227,6 +230,9 @@ struct PowerRun {
     // observer path: the whole power, unfolded on the device and copied to pinned host memory
     DBuf full_dev;
     DBuf small_hist, small_out, small_sig; // small-N path: power history, result, symmetry hint
+    int64_t *hstats = nullptr;             // lookahead: pinned host copy of the statistics
+    size_t hstats_n = 0;
+    std::vector<cudaEvent_t> events_la;    // lookahead: product done / statistics done, join
     cudaEvent_t small_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<long long> small_host; // the result's host copy
     uint16_t *full_host = nullptr;
@@ -238,6 +244,9 @@ struct PowerRun {
         if (full_host) cudaFreeHost(full_host);
         for (auto ev : small_ev)
             if (ev) cudaEventDestroy(ev);
+        for (auto ev : events_la)
+            if (ev) cudaEventDestroy(ev);
+        if (hstats) cudaFreeHost(hstats);
     }
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
@@ -246,6 +255,7 @@ struct PowerRun {
 struct DevState {
     cudaStream_t stream = nullptr;      // the library's own non-blocking stream
     cudaStream_t user_stream = nullptr; // mp_set_stream override for power runs
+    cudaStream_t stream2 = nullptr;     // second stream of the lookahead power loop
     DBuf at2, xb, cb, flag, stage_a, stage_b, stage_c, shard_c, gathered;
     // last use of the product scratch (at2, xb, cb, flag): the next user, on whatever stream,
     // waits on it, so a call on another stream cannot overwrite scratch still being read
@@ -948,7 +958,127 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     std::vector<const uint16_t *> buf((size_t)max_k + 1, nullptr);
     std::vector<int64_t> hsum(nst), hmin(nst);
     bool found = false;
-    for (int kb = 1; kb <= max_k && !found; kb += B) {
+    // Lookahead (large N, one rank, no observer): product k+1 runs on the library stream while
+    // the statistics of power k run on a second stream and the host searches for a repeat, so
+    // the statistics overlap the next product and the host round trip is hidden.  A power past
+    // the first repeat is computed and discarded (one product per run).
+    const bool lookahead = B == 1 && !cap && !g_dist.fn && !g_obs.fn && max_k >= 2 && R.ring.size() >= 3 &&
+                           lookahead_on();
+    if (lookahead) {
+        cudaStream_t s2 = st->stream2;
+        if (!s2) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&st->stream2, cudaStreamNonBlocking));
+            s2 = st->stream2;
+        }
+        if (!R.hstats || R.hstats_n < nst * 2) {
+            if (R.hstats) cudaFreeHost(R.hstats);
+            R.hstats = nullptr;
+            CUDA_TRY(cudaMallocHost((void **)&R.hstats, nst * 2 * 8));
+            R.hstats_n = nst * 2;
+        }
+        if ((int)R.events_la.size() < 2 * (max_k + 1) + 2) {
+            for (auto ev : R.events_la) cudaEventDestroy(ev);
+            R.events_la.assign((size_t)2 * (max_k + 1) + 2, nullptr);
+            for (auto &ev : R.events_la) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        int64_t *hsum_p = R.hstats, *hmin_p = R.hstats + nst;
+        cudaEvent_t *prod_done = R.events_la.data(), *stats_done = R.events_la.data() + (max_k + 1);
+        cudaEvent_t join = R.events_la[2 * (max_k + 1)], start2 = R.events_la[2 * (max_k + 1) + 1];
+        CUDA_TRY(cudaEventRecord(start2, s)); // the second stream starts after the setup
+        CUDA_TRY(cudaStreamWaitEvent(s2, start2, 0));
+        // enqueue power k: the product (or X_1) on s, its statistics and their copy to the host
+        // on s2 once the product is done
+        auto issue = [&](int k) -> mp_status {
+            const size_t q = (size_t)(k % (int)R.ring.size());
+            TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
+            uint16_t *dst = R.ring[q].as<uint16_t>();
+            R.slot_power[q] = k;
+            buf[(size_t)k] = dst;
+            if (k == 1) {
+                TRY(make_power1(R, dst, s));
+            } else {
+                CUDA_TRY(cudaEventRecord(R.events[2 * k], s));
+                TRY(product(R, buf[(size_t)k - 1], dst, s, R.events[4 * (max_k + 1) + k]));
+                CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
+                ++launches;
+            }
+            CUDA_TRY(cudaEventRecord(prod_done[k], s));
+            CUDA_TRY(cudaStreamWaitEvent(s2, prod_done[k], 0));
+            CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s2));
+            if (R.sym)
+                LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.drw.as<uint64_t>(),
+                                        R.drw.as<uint64_t>() + N, R.w,
+                                        reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
+                                        reinterpret_cast<unsigned long long *>(st_min + 2 * k), s2));
+            else
+                LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
+                                    reinterpret_cast<unsigned long long *>(st_min + 2 * k), s2));
+            CUDA_TRY(cudaEventRecord(R.events[3 * (max_k + 1) + k], s2));
+            COPY(hsum_p + 2 * k, st_sum + 2 * k, 16, cudaMemcpyDeviceToHost, s2);
+            COPY(hmin_p + 2 * k, st_min + 2 * k, 16, cudaMemcpyDeviceToHost, s2);
+            CUDA_TRY(cudaEventRecord(stats_done[k], s2));
+            return MP_OK;
+        };
+        TRY(issue(1));
+        int k_issued = 1;
+        for (int k = 1; k <= max_k && !found; ++k) {
+            if (k + 1 <= max_k) {
+                TRY(issue(k + 1));
+                k_issued = k + 1;
+            }
+            CUDA_TRY(cudaEventSynchronize(stats_done[k]));
+            tr.mark("power + statistics", k);
+            mp_power_stats &cs = hs[(size_t)k];
+            cs.fingerprint = hsum_p[2 * k];
+            cs.inf_count = hsum_p[2 * k + 1];
+            cs.diag_min = hmin_p[2 * k];
+            cs.ref = hmin_p[2 * k + 1];
+            res.diag_min[k] = (uint16_t)std::min<int64_t>(cs.diag_min, 0xFFFF);
+            res.fingerprint[k] = (uint64_t)cs.fingerprint;
+            if (!res.dense_from && cs.inf_count == 0) res.dense_from = k;
+            const uint16_t *cur = buf[(size_t)k];
+            // a5: forward first-repeat search, j = k-1 down to 1; the exact compare runs on s2
+            for (int j = k - 1; j >= 1 && !found; --j) {
+                int32_t c = 0;
+                if (!mp_repeat_candidate(&cs, &hs[(size_t)j], S, &c)) continue;
+                const uint16_t *Z = nullptr;
+                bool in_ring = false;
+                for (size_t q = 0; q < R.ring.size(); ++q)
+                    if (R.slot_power[q] == j) in_ring = true;
+                if (!in_ring) CUDA_TRY(cudaStreamSynchronize(s)); // the recompute runs on s
+                TRY(power_buffer(R, j, &Z, in_ring ? s2 : s));
+                if (!in_ring) CUDA_TRY(cudaStreamSynchronize(s));
+                int64_t *fl = R.flag.as<int64_t>();
+                CUDA_TRY(cudaMemsetAsync(fl, 0, 8, s2));
+                LAUNCH(launch_compare(cur, Z, R.ld, N, R.w, c, reinterpret_cast<unsigned long long *>(fl), s2));
+                int64_t bad = -1;
+                COPY(&bad, fl, 8, cudaMemcpyDeviceToHost, s2);
+                CUDA_TRY(cudaStreamSynchronize(s2));
+                if (bad == 0) {
+                    found = true;
+                    res.mu = j;
+                    res.lambda = k - j;
+                    res.offset = c;
+                    res.k_last = k;
+                }
+            }
+        }
+        CUDA_TRY(cudaEventRecord(join, s2)); // the library stream waits for the second one
+        CUDA_TRY(cudaStreamWaitEvent(s, join, 0));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (int k = 2; k <= k_issued; ++k) { // timings (the discarded lookahead power included)
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[2 * k + 1]));
+            prod_ms += ms;
+            if (R.spmm) {
+                CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * k], R.events[4 * (max_k + 1) + k]));
+                spmm_ms += ms;
+            }
+            CUDA_TRY(cudaEventElapsedTime(&ms, R.events[2 * (max_k + 1) + k], R.events[3 * (max_k + 1) + k]));
+            stats_ms += ms;
+        }
+    }
+    for (int kb = 1; kb <= max_k && !found && !lookahead; kb += B) {
         const int ke = std::min(max_k, kb + B - 1);
         for (int k = kb; k <= ke; ++k) {
             const size_t q = (size_t)(k % (int)R.ring.size());
@@ -1468,6 +1598,8 @@ void mp_shutdown(void)
         cudaSetDevice(kv.first);
         kv.second.pr.reset();
         if (kv.second.scratch_ev) cudaEventDestroy(kv.second.scratch_ev);
+        if (kv.second.stream2) cudaStreamDestroy(kv.second.stream2);
+        kv.second.stream2 = nullptr;
         kv.second.scratch_ev = nullptr;
         if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
         kv.second.stream = nullptr;

@@ -2294,45 +2294,52 @@ cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, c
 }
 
 // Range check of A (row-major, boundary encoding) and, if occ != null, the occupancy of its
-// 128 x 32 tiles (occ zeroed by the caller): one warp per (row, 32-column tile).
-__global__ void k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N, int64_t Kt, uint8_t *__restrict__ occ,
-                          int *__restrict__ range_flag, const int32_t *__restrict__ sigma, int *__restrict__ sym_flag,
-                          uint32_t *__restrict__ bits, int64_t nw, const WordMask *__restrict__ words, unsigned full,
-                          int *__restrict__ xfer_flag)
+// 128 x 32 tiles (occ zeroed by the caller); if sigma != null the symmetry hint (every finite
+// a_ij reappears at (sigma i, sigma j)); if bits != null the support bitsets; if words != null
+// the transfer hint (A = A(D_n) entry by entry: label zeros(p) if p can follow q, P:141-152,
+// else +inf).  Block (x, y) covers the 1024-column tile x of rows y, y + gridDim.y, ... with
+// the tile's word masks staged in shared memory; warp per row, 4 x 32 columns in flight.
+constexpr int kChkCols = 1024;
+__global__ void __launch_bounds__(256)
+    k_check_a(const uint16_t *__restrict__ A, int64_t lda, int64_t N, int64_t Kt, uint8_t *__restrict__ occ,
+              int *__restrict__ range_flag, const int32_t *__restrict__ sigma, int *__restrict__ sym_flag,
+              uint32_t *__restrict__ bits, int64_t nw, const WordMask *__restrict__ words, unsigned full,
+              int *__restrict__ xfer_flag)
 {
-    // blocks stride over rows, warps over the row's 32-column words (= the tile columns of occ)
+    __shared__ WordMask sw[kChkCols];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * kChkCols;
+    const int cols = (int)(N - c0 < kChkCols ? N - c0 : kChkCols);
+    if (words)
+        for (int t = threadIdx.x; t < cols; t += blockDim.x) sw[t] = words[c0 + t];
+    __syncthreads();
     bool bad = false, asym = false, notxfer = false;
-    for (int64_t i = blockIdx.x; i < N; i += gridDim.x) {
-        const uint16_t *row = A + i * lda;
+    for (int64_t i = (int64_t)blockIdx.y * nwarps + warp; i < N; i += (int64_t)gridDim.y * nwarps) {
+        const uint16_t *row = A + i * lda + c0;
         const int64_t si = sigma ? (int64_t)sigma[i] : 0;
         WordMask wq = {0, 0, 0, 0};
         if (words) wq = words[i];
-        for (int64_t k0 = warp; k0 < nw; k0 += 4 * nwarps) { // 4 words' loads in flight
+        for (int u0 = 0; u0 < kChkCols / 32; u0 += 4) {
             uint16_t xv[4];
-            WordMask wv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int64_t c = (k0 + (int64_t)u * nwarps) * 32 + lane;
-                xv[u] = c < N ? row[c] : kBndInf;
-                wv[u] = (words && c < N) ? words[c] : WordMask{0, 0, 0, 0};
+                const int c = (u0 + u) * 32 + lane;
+                xv[u] = c < cols ? row[c] : kBndInf;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int64_t k = k0 + (int64_t)u * nwarps;
-                if (k >= nw) break;
-                const int64_t c = k * 32 + lane;
+                const int c = (u0 + u) * 32 + lane;
+                if ((u0 + u) * 32 >= cols) break;
                 const uint16_t x = xv[u];
                 const bool f = x != kBndInf;
                 bad |= f && x > kFiniteMax;
                 // symmetry hint: every finite entry must reappear at (sigma i, sigma j); sigma x
                 // sigma is a bijection, so the +inf entries then map onto +inf entries too
-                if (sigma && f) asym |= A[si * lda + sigma[c]] != x;
-                // transfer hint: A must be A(D_n) entry by entry (Alg. 1: label zeros(p) if p
-                // can follow q, else +inf)
-                if (words && c < N)
-                    notxfer |= x != (can_follow_mask(wq, wv[u], full) ? (uint16_t)wv[u].zeros : (uint16_t)kBndInf);
+                if (sigma && f) asym |= A[si * lda + sigma[c0 + c]] != x;
+                if (words && c < cols)
+                    notxfer |= x != (can_follow_mask(wq, sw[c], full) ? (uint16_t)sw[c].zeros : (uint16_t)kBndInf);
                 const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+                const int64_t k = c0 / 32 + u0 + u;
                 if (lane == 0) {
                     if (bits) bits[i * nw + k] = m;
                     if (occ && m && k < Kt) {
@@ -2354,9 +2361,11 @@ cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np
 {
     static_assert(kBK == 32, "occupancy tiles are the 32-column words");
     const int64_t Kt = Np / kBK;
-    k_check_a<<<(unsigned)std::min<int64_t>(std::max<int64_t>(N, 1), (int64_t)num_sms() * 8), 256, 0, s>>>(
-        A, lda, N, Kt, occ, range_flag, sigma, sym_flag, bits, (N + 31) / 32, words, words ? (1u << n) - 1u : 0u,
-        xfer_flag);
+    const int64_t gx = std::max<int64_t>(1, (N + kChkCols - 1) / kChkCols);
+    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, ((int64_t)num_sms() * 8 + gx - 1) / gx));
+    k_check_a<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(A, lda, N, Kt, occ, range_flag, sigma, sym_flag, bits,
+                                                               (N + 31) / 32, words, words ? (1u << n) - 1u : 0u,
+                                                               xfer_flag);
     return cudaGetLastError();
 }
 

@@ -94,6 +94,22 @@ def run_config(mp, A, n, config):
             mp.set_row_reuse(True)
             mp.set_symmetry(None)
             mp.set_transfer_hint(0)
+    if config in ("nolookahead", "foldstats"):  # the benchmarked options, other power loops:
+        # no lookahead (statistics after each product on one stream) / the statistics fused
+        # into the fold passes (MP_FOLD_STATS=1, no lookahead)
+        env = {"MP_LOOKAHEAD": "0"}
+        if config == "foldstats":
+            env["MP_FOLD_STATS"] = "1"
+        os.environ.update(env)
+        mp.set_symmetry(mp.word_reversal(n))
+        mp.set_transfer_hint(n)
+        try:
+            return mp.minplus_power_until_periodic(A)
+        finally:
+            for v in env:
+                del os.environ[v]
+            mp.set_symmetry(None)
+            mp.set_transfer_hint(0)
     if config == "tiles":
         mp.set_options("tiles")
         try:
@@ -103,7 +119,7 @@ def run_config(mp, A, n, config):
     raise ValueError(config)
 
 
-@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse"])
+@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse", "nolookahead", "foldstats"])
 @pytest.mark.parametrize("n", SIZES)
 def test_power_records(mp, n, config):
     """Every power's fingerprint and diagonal minimum, (mu, lambda, b) and dense_from equal the
