@@ -161,22 +161,27 @@ __global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows,
             const int col = 256 * h + 8 * lane;
             v[h] = col < ncols ? *reinterpret_cast<const uint4 *>(row + col) : make_uint4(0, 0, 0, 0);
         }
-        for (int e = 0; e < np; ++e) {
-            const int64_t p = __shfl_sync(0xFFFFFFFFu, mine, e);
+        // parents two at a time: eight 16-byte loads per lane in flight
+        for (int e = 0; e < np; e += 2) {
+            const int64_t p0 = __shfl_sync(0xFFFFFFFFu, mine, e);
+            const int64_t p1 = __shfl_sync(0xFFFFFFFFu, mine, e + 1 < np ? e + 1 : e);
 #if MP_DEBUG_CHECKS
-            if (p < 0 || p == q) __trap();
+            if (p0 < 0 || p0 == q || p1 < 0 || p1 == q) __trap();
 #endif
-            const uint16_t *prow = C + p * ldc + seg * kFoldSeg;
+            const uint16_t *r0 = C + p0 * ldc + seg * kFoldSeg, *r1 = C + p1 * ldc + seg * kFoldSeg;
+            uint4 u0[4], u1[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
                 const int col = 256 * h + 8 * lane;
-                if (col < ncols) {
-                    const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(prow + col));
-                    v[h].x = __vminu2(v[h].x, u.x);
-                    v[h].y = __vminu2(v[h].y, u.y);
-                    v[h].z = __vminu2(v[h].z, u.z);
-                    v[h].w = __vminu2(v[h].w, u.w);
-                }
+                u0[h] = col < ncols ? __ldcg(reinterpret_cast<const uint4 *>(r0 + col)) : make_uint4(0, 0, 0, 0);
+                u1[h] = col < ncols ? __ldcg(reinterpret_cast<const uint4 *>(r1 + col)) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                v[h].x = __vminu2(v[h].x, __vminu2(u0[h].x, u1[h].x));
+                v[h].y = __vminu2(v[h].y, __vminu2(u0[h].y, u1[h].y));
+                v[h].z = __vminu2(v[h].z, __vminu2(u0[h].z, u1[h].z));
+                v[h].w = __vminu2(v[h].w, __vminu2(u0[h].w, u1[h].w));
             }
         }
 #pragma unroll
