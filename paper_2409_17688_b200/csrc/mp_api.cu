@@ -963,7 +963,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // the statistics overlap the next product and the host round trip is hidden.  A power past
     // the first repeat is computed and discarded (one product per run).
     const bool lookahead = B == 1 && !cap && !g_dist.fn && !g_obs.fn && max_k >= 2 && R.ring.size() >= 3 &&
-                           lookahead_on();
+                           lookahead_on() && !(R.spmm && R.dag_n && fold_stats_on());
     if (lookahead) {
         cudaStream_t s2 = st->stream2;
         if (!s2) {

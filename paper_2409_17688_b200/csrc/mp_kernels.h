@@ -105,6 +105,7 @@ struct RowDag {
     int32_t *idx = nullptr;     // parents
     int32_t *level = nullptr;   // [N] 0 without parents, else 1 + max level of the parents
     int32_t *lrows = nullptr;   // [N] rows grouped by level
+    int32_t *rec = nullptr;     // [N][16] per row in level order: row, #parents, parents
     int64_t *lptr_dev = nullptr;
     int *bad = nullptr;         // set by launch_extra_bits if a parent's support is not a subset
     std::vector<int64_t> lptr;  // [levels + 1] level offsets into lrows (host copy)
