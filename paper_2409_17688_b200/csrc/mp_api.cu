@@ -64,16 +64,6 @@ bool lookahead_on()
     return !(e && *e == '0');
 }
 
-// MP_FOLD_STATS=1: the fold passes also compute the statistics (k_fold_stats).  Off by default:
-// measured slower at n = 12 (6.95 ms per power against 2.43 + 1.42 ms for k_fold + k_stats_sym,
-// profiles/r2/README.md) -- a thread walks its column slice down the level's rows, so each row
-// is three dependent global loads the warp waits for, where k_fold runs one thread per
-// (row, 8 columns) and hides that latency by sheer parallelism.
-bool fold_stats_on()
-{
-    const char *e = getenv("MP_FOLD_STATS"); // read per run: tests switch it
-    return e && *e == '1';
-}
 bool g_row_reuse = true;   // mp_set_row_reuse: row-inclusion reuse for A(D_n)
 
 mp_profile g_prof{};
@@ -464,14 +454,8 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
 
 // C = A (x) X with the selected kernel.
 // mid (may be null): recorded between the SpMM and the fold passes of the row-inclusion reuse.
-// st_sum / st_min (may be null): with the reuse, the folds also compute the power's a4
-// statistics into these slots (one pass instead of fold + statistics); *stats_done tells the
-// caller.
-mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, cudaEvent_t mid = nullptr,
-                  unsigned long long *st_sum = nullptr, unsigned long long *st_min = nullptr,
-                  bool *stats_done = nullptr)
+mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, cudaEvent_t mid = nullptr)
 {
-    if (stats_done) *stats_done = false;
     if (R.spmm) {
         SparseA sa;
         sa.L = R.sp.L;
@@ -483,16 +467,7 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, c
         int nl = 0;
         cudaError_t e = launch_spmm(sa, R.plan, X, R.ld, C, R.ld, R.Np, s, &nl);
         if (e == cudaSuccess && mid) e = cudaEventRecord(mid, s);
-        if (e == cudaSuccess && R.dag_n) {
-            if (st_sum && fold_stats_on()) { // parents' rows and the statistics, level by level
-                e = launch_fold_stats(R.rdag, C, R.ld, R.N, R.sym ? R.dgcol.as<int32_t>() : nullptr, R.c0,
-                                      R.sym ? R.dsig.as<int32_t>() : nullptr, R.drw.as<uint64_t>(),
-                                      R.drw.as<uint64_t>() + R.N, R.w, st_sum, st_min, s, &nl);
-                if (stats_done) *stats_done = true;
-            } else {
-                e = launch_folds(R.rdag, C, R.ld, R.ld, s, &nl); // parents' rows
-            }
-        }
+        if (e == cudaSuccess && R.dag_n) e = launch_folds(R.rdag, C, R.ld, R.ld, s, &nl); // parents' rows
         g_launches.fetch_add(nl);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -844,10 +819,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     }
     // row-inclusion reuse needs the word structure and the grouped SpMM
     R.dag_n = (g_row_reuse && R.n_words && (g_opts.sparsity == 2 || g_opts.sparsity < 0)) ? R.n_words : 0;
-    if (R.dag_n && !R.sym) { // the fused fold + statistics pass reads the row weights
-        TRY(R.drw.ensure((size_t)N * 16, "row weights"));
-        LAUNCH(launch_row_weights(N, nullptr, R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, s));
-    }
+
     tr.mark("a2 stage A");
 
     // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
@@ -963,7 +935,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // the statistics overlap the next product and the host round trip is hidden.  A power past
     // the first repeat is computed and discarded (one product per run).
     const bool lookahead = B == 1 && !cap && !g_dist.fn && !g_obs.fn && max_k >= 2 && R.ring.size() >= 3 &&
-                           lookahead_on() && !(R.spmm && R.dag_n && fold_stats_on());
+                           lookahead_on();
     if (lookahead) {
         cudaStream_t s2 = st->stream2;
         if (!s2) {
@@ -1085,22 +1057,17 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             TRY(R.ring[q].ensure(R.slot_bytes(), "power store slot"));
             uint16_t *dst = R.ring[q].as<uint16_t>();
             R.slot_power[q] = k;
-            bool fused_stats = false;
             buf[(size_t)k] = dst;
             if (k == 1) {
                 TRY(make_power1(R, dst, s)); // X_1 = A[:, shard]
             } else {
                 CUDA_TRY(cudaEventRecord(R.events[2 * k], s));
-                TRY(product(R, prev, dst, s, R.events[4 * (max_k + 1) + k], // A^k = A (x) A^{k-1}
-                            reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
-                            reinterpret_cast<unsigned long long *>(st_min + 2 * k), &fused_stats));
+                TRY(product(R, prev, dst, s, R.events[4 * (max_k + 1) + k])); // A^k = A (x) A^{k-1}
                 CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
                 ++launches;
             }
             if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s)); // stats start
-            if (fused_stats) {
-                // computed by the fold passes (row-inclusion reuse)
-            } else if (R.sym)
+            if (R.sym)
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(),
                                         R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),

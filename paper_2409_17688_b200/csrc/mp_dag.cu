@@ -192,162 +192,6 @@ __global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows,
     }
 }
 
-// Fold and statistics of one DAG level in one pass (the a4 statistics fused into the reuse's
-// fold): a thread owns an 8-column slice of the power (its 8 column weights in registers, as in
-// k_stats_sym) and walks the level's rows two at a time; a row's record {row, #parents,
-// parents...} (one 64-byte load shared by the warp) gives every address up front, so the row's
-// own and parents' 16-byte loads are all in flight together.  Each row is finished (min with
-// its parents' rows, final: earlier levels; level 0 rows have no parents and are only read) and
-// then hashed exactly as k_stats / k_stats_sym do:
-//   H += s(2i) s(2g+1) x  (+ s(2 sigma i) s(2 sigma g + 1) x for a mirrored column, SYM),
-//   +inf count (x2 for a mirrored column), diagonal minimum over (g, g), first finite entry
-//   key (t << 16) | x over t = i N + g and (with SYM) t = sigma i N + sigma g.
-// Columns: local column jj stands for g = gcol[jj] (SYM) or g = c0 + jj.  The level launches
-// of one power accumulate into the same statistics slot (atomicAdd / atomicMin per block).
-constexpr int kRecInts = 16; // a row record: row, #parents, up to 14 parents
-template <bool SYM>
-__global__ void __launch_bounds__(128)
-    k_fold_stats(const int32_t *__restrict__ rec, int64_t nrows, uint16_t *__restrict__ C, int64_t ld, int64_t N,
-                 const int32_t *__restrict__ gcol, int64_t c0, const int32_t *__restrict__ sigma,
-                 const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t w, int64_t rpb, bool fold,
-                 unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
-{
-    unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
-    unsigned dmin = 0xFFFFu;
-    const int64_t j0 = (int64_t)blockIdx.x * 1024 + (int64_t)threadIdx.x * 8;
-    const int64_t r0 = (int64_t)blockIdx.y * rpb, r1 = min(nrows, r0 + rpb);
-    if (j0 < w && r0 < r1) {
-        const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
-        uint64_t b[8], bm[8];
-        int32_t g[8], m[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            g[e] = e < nc ? (SYM ? gcol[j0 + e] : (int32_t)(c0 + j0 + e)) : 0;
-            m[e] = (SYM && e < nc) ? sigma[g[e]] : g[e];
-            b[e] = e < nc ? mix64(2 * (uint64_t)g[e] + 1) : 0;
-            bm[e] = (SYM && e < nc && m[e] != g[e]) ? mix64(2 * (uint64_t)m[e] + 1) : 0;
-        }
-        auto finish = [&](const int4 (&rc)[4], uint4 &v) { // fold the parents into v, store
-            const int32_t pr[14] = {rc[0].z, rc[0].w, rc[1].x, rc[1].y, rc[1].z, rc[1].w, rc[2].x,
-                                    rc[2].y, rc[2].z, rc[2].w, rc[3].x, rc[3].y, rc[3].z, rc[3].w};
-            const int np = rc[0].y;
-#pragma unroll
-            for (int e0 = 0; e0 < 14; e0 += 4) { // four parents' loads in flight at a time
-                if (e0 >= np) break;
-                uint4 u[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (e0 + e < np && e0 + e < 14)
-                        u[e] = __ldcg(reinterpret_cast<const uint4 *>(C + (int64_t)pr[e0 + e] * ld + j0));
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (e0 + e < np && e0 + e < 14) {
-                        v.x = __vminu2(v.x, u[e].x);
-                        v.y = __vminu2(v.y, u[e].y);
-                        v.z = __vminu2(v.z, u[e].z);
-                        v.w = __vminu2(v.w, u[e].w);
-                    }
-            }
-            if (np > 0) *reinterpret_cast<uint4 *>(C + (int64_t)rc[0].x * ld + j0) = v;
-        };
-        auto hash = [&](int64_t i, const uint4 &v) {
-            const int64_t si = SYM ? (int64_t)sigma[i] : i;
-            const uint32_t words[4] = {v.x, v.y, v.z, v.w};
-            uint64_t rs = 0, rm = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                if (e >= nc) break;
-                uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                const bool two = SYM && m[e] != g[e];
-                if (x >= kDevInf) {
-                    x = kBndInf;
-                    infc += two ? 2 : 1;
-                } else {
-                    unsigned long long key = ((uint64_t)(i * N + g[e]) << 16) | x;
-                    if (key < ref) ref = key;
-                    if (SYM) {
-                        key = ((uint64_t)(si * N + m[e]) << 16) | x;
-                        if (key < ref) ref = key;
-                    }
-                }
-                rs += b[e] * x;
-                if (SYM) rm += bm[e] * x;
-                if (g[e] == i) dmin = min(dmin, x);
-            }
-            h += rw[i] * rs + (SYM ? rwm[i] * rm : 0ull);
-        };
-        int64_t r = r0;
-        for (; r + 2 <= r1; r += 2) {
-            int4 ra[4], rb[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                ra[u] = reinterpret_cast<const int4 *>(rec + r * kRecInts)[u];
-                rb[u] = reinterpret_cast<const int4 *>(rec + (r + 1) * kRecInts)[u];
-            }
-            uint4 va = *reinterpret_cast<const uint4 *>(C + (int64_t)ra[0].x * ld + j0);
-            uint4 vb = *reinterpret_cast<const uint4 *>(C + (int64_t)rb[0].x * ld + j0);
-            if (fold) {
-                finish(ra, va);
-                finish(rb, vb);
-            }
-            hash(ra[0].x, va);
-            hash(rb[0].x, vb);
-        }
-        if (r < r1) {
-            int4 ra[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) ra[u] = reinterpret_cast<const int4 *>(rec + r * kRecInts)[u];
-            uint4 va = *reinterpret_cast<const uint4 *>(C + (int64_t)ra[0].x * ld + j0);
-            if (fold) finish(ra, va);
-            hash(ra[0].x, va);
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
-        infc += __shfl_xor_sync(0xFFFFFFFFu, infc, o);
-        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
-        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, o));
-    }
-    __shared__ unsigned long long sh[4], sn[4], sr[4];
-    __shared__ unsigned sd[4];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        sh[warp] = h;
-        sn[warp] = infc;
-        sd[warp] = dmin;
-        sr[warp] = ref;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long H = 0, I = 0, Rf = 0x7FFFFFFFFFFFFFFFull;
-        unsigned D = 0xFFFFu;
-        for (int k = 0; k < 4; ++k) {
-            H += sh[k];
-            I += sn[k];
-            D = min(D, sd[k]);
-            Rf = min(Rf, sr[k]);
-        }
-        if (H) atomicAdd(out_sum + 0, H);
-        if (I) atomicAdd(out_sum + 1, I);
-        if (D < 0xFFFFu) atomicMin(out_min + 0, (unsigned long long)D);
-        if (Rf != 0x7FFFFFFFFFFFFFFFull) atomicMin(out_min + 1, Rf);
-    }
-}
-
-// rec[r] = {row, #parents, parents...} for the rows r in level order (lrows)
-__global__ void k_make_records(const int32_t *__restrict__ lrows, int64_t N, const int64_t *__restrict__ off,
-                               const int32_t *__restrict__ pidx, int32_t *__restrict__ rec)
-{
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t q = lrows[r], e0 = off[q], np = off[q + 1] - e0;
-        int32_t *o = rec + r * kRecInts;
-        o[0] = (int32_t)q;
-        o[1] = (int32_t)np;
-        for (int e = 0; e < kRecInts - 2; ++e) o[2 + e] = e < np ? pidx[e0 + e] : 0;
-    }
-}
-
 int grid_rows(int64_t work, int per_block)
 {
     const int64_t g = (work + per_block - 1) / per_block;
@@ -407,8 +251,7 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
         return e;
     if ((e = cudaMemsetAsync(hist, 0, 32 * 8, s)) != cudaSuccess) return e; // reused as the cursors
     k_level_scatter<<<gb, 256, 0, s>>>(d.level, N, d.lptr_dev, reinterpret_cast<unsigned long long *>(hist), d.lrows);
-    if ((e = A(d.rec, (size_t)N * kRecInts * 4)) != cudaSuccess) return e;
-    k_make_records<<<gb, 256, 0, s>>>(d.lrows, N, d.off, d.idx, d.rec);
+
     *launches += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaStreamSynchronize(s); // d.lptr (host) and ho go out of scope safely
@@ -430,32 +273,6 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
         // of items (the segment-major order above relies on it)
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, 148 * 8));
         k_fold<<<grid, 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc);
-        if (launches) ++*launches;
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-}
-
-cudaError_t launch_fold_stats(const RowDag &d, uint16_t *C, int64_t ld, int64_t N, const int32_t *gcol, int64_t c0,
-                              const int32_t *sigma, const uint64_t *rw, const uint64_t *rwm, int64_t w,
-                              unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s, int *launches)
-{
-    const int64_t gx = std::max<int64_t>(1, (w + 1023) / 1024);
-    for (int l = 0; l < d.levels; ++l) {
-        const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
-        // about 8 blocks of 128 threads per SM over the level, at least 32 rows per block (a
-        // thread's setup -- 16 column weights -- costs about as much as hashing a dozen rows)
-        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((148 * 8 + gx - 1) / gx, (nr + 31) / 32));
-        const int64_t rpb = (nr + gy - 1) / gy;
-        const dim3 grid((unsigned)gx, (unsigned)gy);
-        const int32_t *rec = d.rec + d.lptr[(size_t)l] * kRecInts;
-        if (sigma)
-            k_fold_stats<true><<<grid, 128, 0, s>>>(rec, nr, C, ld, N, gcol, c0, sigma, rw, rwm, w, rpb, l > 0, out_sum,
-                                                    out_min);
-        else
-            k_fold_stats<false><<<grid, 128, 0, s>>>(rec, nr, C, ld, N, gcol, c0, sigma, rw, rwm, w, rpb, l > 0,
-                                                     out_sum, out_min);
         if (launches) ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
