@@ -39,15 +39,25 @@ KERNEL_NAMES = {"dense": "k_minplus (dense tiles, VIADDMNMX.U16x2)",
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
-def traffic_bytes(kernel: str, n: int, world: int, sym: bool = False):
+def traffic_bytes(kernel: str, n: int, world: int, sym: bool = False, reuse: bool = False):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
     committed ncu --set full capture of the same configuration (profiles/ncu_traffic.json)."""
     try:
         table = json.load(open(TRAFFIC_PATH))
     except (OSError, ValueError):
         return None
-    rec = table.get(f"{kernel.split()[0]}:{kernel.split('(')[1].split(',')[0]}:n{n}:g{world}" + (":sym" if sym else ""))
+    rec = table.get(f"{kernel.split()[0]}:{kernel.split('(')[1].split(',')[0]}:n{n}:g{world}" + (":sym" if sym else "")
+                    + (":reuse" if reuse else ""))
     return rec["bytes_per_launch"] if rec else None
+
+
+def hbm_peak() -> float:
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the profiling
+    guide's B200 figure."""
+    try:
+        return float(json.load(open(PEAKS_PATH))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6450.0
 
 
 def parse():
@@ -423,6 +433,37 @@ def run_mine(args):
     achieved = issued_per_launch / (avg_kernel_ms * 1e-3) / 1e9 if issued_per_launch else None
     # the method's work (every finite A_il x every computed column) / the whole product's time
     useful_rate = useful_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    # The roofline of the dominant kernel.  With the row-inclusion reuse k_spmm issues few DPX
+    # steps and is bound by HBM: achieved = its ALGORITHMIC bytes per launch (read the X rows
+    # once, the sparse form's entries once, write C once: 2 N ld + 32 B x entries) / its
+    # duration, against the measured copy bandwidth; traffic = what ncu measured (the X rows
+    # staged once per tile that needs them).  Without the reuse it is DPX-issue-bound.
+    traffic = traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world, not args.no_symmetry, bool(row_levels))
+    alu = {"achieved": achieved, "peak": peak, "unit": "Gstep/s", "frac": (achieved / peak) if achieved else None,
+           "issued_steps_per_launch": issued_per_launch or None,
+           "work": "issued DPX steps per launch (4-row groups x entries x columns) / CUDA-event duration",
+           "peak_source": f"148 SM x 128 steps/clk/SM x {sm_mhz:.0f} MHz observed (DESIGN.md)"}
+    common = {"kernel": KERNEL_NAMES[kernel_used], "avg_kernel_ms": avg_kernel_ms, "traffic": traffic,
+              "useful_steps_per_product": useful_per_launch, "avg_product_ms": avg_launch_ms,
+              "useful_achieved": useful_rate, "useful_frac": useful_rate / peak,
+              "useful_note": "nnz(A) x computed columns per product / product time (kernel + fold passes); "
+                             "above 1 only when the row-inclusion reuse skips redundant terms",
+              "kernel_share_of_step": spmm_ms / max(ms, 1e-9), "product_share_of_step": prod_ms / max(ms, 1e-9)}
+    if row_levels and kernel_used == "spmm":
+        entries = issued_per_launch / (4.0 * ld) if ld else 0.0
+        alg_bytes = 2.0 * N * ld * 2 + 32.0 * entries
+        hbm = hbm_peak()
+        ach = alg_bytes / (avg_kernel_ms * 1e-3) / 1e9
+        roofline = dict(common, bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm,
+                        algorithmic_bytes_per_launch=alg_bytes,
+                        bytes_note="read X_{k-1} (N x ld u16) once + write A^k (N x ld) once + the sparse "
+                                   "form's 32-byte entries once", peak_source="MEASURED_PEAKS.json hbm_gbs",
+                        traffic_GBps=(traffic / (avg_kernel_ms * 1e-3) / 1e9) if traffic else None, alu=alu)
+    else:
+        if not achieved:  # the fused small-N run issues no separate product kernel
+            alu.update(achieved=useful_rate, frac=useful_rate / peak,
+                       work="useful steps per product / the fused run's time per product")
+        roofline = dict(common, bound="alu", **{k: v for k, v in alu.items()})
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = oracle_sample(args.n, args.cpu_seconds)
@@ -442,21 +483,7 @@ def run_mine(args):
         "seconds_to_gamma2": ms / args.steps / 1e3,
         "dense_equivalent_gops": dense_all / (ms * 1e-3) / 1e9,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
-        "roofline": {"bound": "alu", "kernel": KERNEL_NAMES[kernel_used],
-                     "achieved": achieved if achieved else useful_rate, "peak": peak, "unit": "Gstep/s",
-                     "frac": (achieved if achieved else useful_rate) / peak,
-                     "traffic": traffic_bytes(KERNEL_NAMES[kernel_used], args.n, world, not args.no_symmetry),
-                     "peak_source": f"148 SM x 128 steps/clk/SM x {sm_mhz:.0f} MHz observed (DESIGN.md)",
-                     "work": ("issued DPX steps of the product kernel per launch (4-row groups x extra/finite "
-                              "entries x columns) / its CUDA-event duration" if achieved else
-                              "useful steps / kernel duration (the fused small-N run)"),
-                     "avg_kernel_ms": avg_kernel_ms, "issued_steps_per_launch": issued_per_launch or None,
-                     "useful_steps_per_product": useful_per_launch, "avg_product_ms": avg_launch_ms,
-                     "useful_achieved": useful_rate, "useful_frac": useful_rate / peak,
-                     "useful_note": "nnz(A) x computed columns per product / product time (kernel + fold passes); "
-                                    "above 1 only when the row-inclusion reuse skips redundant terms",
-                     "kernel_share_of_step": spmm_ms / max(ms, 1e-9),
-                     "product_share_of_step": prod_ms / max(ms, 1e-9)},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": useful_all / args.steps * e2e_steps / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
                 "h2d_bytes_per_step": int(h2d / max(1, e2e_steps)), "d2h_bytes_per_step": int(d2h / max(1, e2e_steps)),
