@@ -1631,8 +1631,7 @@ cudaError_t launch_stats(const uint16_t *X, int64_t ld, int64_t N, int64_t c0, i
 #ifndef MP_ST_THREADS
 #define MP_ST_THREADS 128
 #endif
-constexpr int kSymThreads = MP_ST_THREADS;    // k_stats_sym block: kSymThreads x 8 columns
-constexpr int kSymCols = kSymThreads * 8;
+constexpr int kSymThreads = MP_ST_THREADS; // k_stats_sym block: kSymThreads x CT columns
 // Statistics of a power stored on a column list under a symmetry sigma (an involution with
 // A_(sigma i, sigma j) = A_ij, so every power has X_(sigma i, sigma j) = X_ij): local column jj
 // holds global column g = gcol[jj] (g <= sigma g) and stands for g and its mirror sigma g.
@@ -1640,58 +1639,74 @@ constexpr int kSymCols = kSymThreads * 8;
 // s(2i) s(2g+1) x + [sigma g != g] s(2 sigma i) s(2 sigma g + 1) x to H, one or two +inf
 // counts, the keys of (i, g) and (sigma i, sigma g), and the diagonal (g, g) (every diagonal
 // entry (r, r) of the full matrix equals (sigma r, sigma r), which some local column holds).
+// A thread owns CT = 8 or 16 consecutive columns (16: the per-row work -- row weights, the
+// +inf test, key tracking, the ring -- is shared by twice the entries).
+template <int CT>
 __global__ void __launch_bounds__(kSymThreads)
     k_stats_sym(const uint16_t *__restrict__ X, int64_t ld, int64_t N, const int32_t *__restrict__ gcol,
                 const int32_t *__restrict__ sigma, const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm,
                 int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
 {
+    constexpr int V = CT / 8; // uint4 per row and thread
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
-    const int64_t j0 = (int64_t)blockIdx.x * kSymCols + (int64_t)threadIdx.x * 8;
+    const int64_t j0 = (int64_t)blockIdx.x * kSymThreads * CT + (int64_t)threadIdx.x * CT;
     const int64_t i0 = (int64_t)blockIdx.y * rpb, i1 = min(N, i0 + rpb);
+    // the global columns and their mirrors (read only on the slow path: shared memory)
+    __shared__ int32_t sg[CT][kSymThreads], sm_[CT][kSymThreads];
     if (j0 < w) {
-        const int nc = (int)(w - j0 < 8 ? w - j0 : 8);
+        const int nc = (int)(w - j0 < CT ? w - j0 : CT);
         // column weights split in 32-bit halves: b * x = b.lo * x + (b.hi * x) << 32 (mod 2^64),
         // so an entry costs one IMAD.WIDE.U32 (64-bit accumulate) and one 32-bit IMAD per sum
-        uint32_t blo[8], bhi[8], bmlo[8], bmhi[8];
-        int32_t g[8], m[8];
+        uint32_t blo[CT], bhi[CT], bmlo[CT], bmhi[CT];
         unsigned two = 0; // bit e: column e stands for two global columns
-        int32_t mmin = INT32_MAX;
+        int32_t mmin = INT32_MAX, g0 = 0, glast = 0;
         int emin = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            g[e] = e < nc ? gcol[j0 + e] : 0;
-            m[e] = e < nc ? sigma[g[e]] : 0;
-            const uint64_t b = e < nc ? mix64(2 * (uint64_t)g[e] + 1) : 0;
-            const uint64_t bm = (e < nc && m[e] != g[e]) ? mix64(2 * (uint64_t)m[e] + 1) : 0;
+        for (int e = 0; e < CT; ++e) {
+            const int32_t g = e < nc ? gcol[j0 + e] : 0;
+            const int32_t m = e < nc ? sigma[g] : 0;
+            sg[e][threadIdx.x] = g;
+            sm_[e][threadIdx.x] = m;
+            const uint64_t b = e < nc ? mix64(2 * (uint64_t)g + 1) : 0;
+            const uint64_t bm = (e < nc && m != g) ? mix64(2 * (uint64_t)m + 1) : 0;
             blo[e] = (uint32_t)b;
             bhi[e] = (uint32_t)(b >> 32);
             bmlo[e] = (uint32_t)bm;
             bmhi[e] = (uint32_t)(bm >> 32);
-            if (e < nc && m[e] != g[e]) two |= 1u << e;
-            if (e < nc && m[e] < mmin) {
-                mmin = m[e];
+            if (e < nc && m != g) two |= 1u << e;
+            if (e < nc && m < mmin) {
+                mmin = m;
                 emin = e;
             }
+            if (e == 0) g0 = g;
+            if (e == nc - 1) glast = g;
         }
-        const int32_t glast = g[nc - 1];
         // Keys of the all-finite rows: among (i, g_e) the smallest is at the first such row and
         // e = 0 (gcol ascending); among the mirrors (sigma i, m_e) at the row of smallest
         // sigma i and e = emin.  Tracked here, folded into ref after the loop.
         int64_t fi = INT64_MAX, fsi = INT64_MAX;
         uint32_t fx = 0, fxm = 0;
-        auto row = [&](int64_t i, int64_t si, const uint4 &v) {
-            const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+        auto row = [&](int64_t i, int64_t si, const uint4 (&vv)[V]) {
+            uint32_t words[4 * V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                words[4 * q + 0] = vv[q].x;
+                words[4 * q + 1] = vv[q].y;
+                words[4 * q + 2] = vv[q].z;
+                words[4 * q + 3] = vv[q].w;
+            }
             // any half >= 0x7FFF (the device +inf; stored values never exceed it)
-            const uint32_t anyinf = (((v.x & 0x7FFF7FFFu) + 0x00010001u) | ((v.y & 0x7FFF7FFFu) + 0x00010001u) |
-                                     ((v.z & 0x7FFF7FFFu) + 0x00010001u) | ((v.w & 0x7FFF7FFFu) + 0x00010001u) |
-                                     v.x | v.y | v.z | v.w) & 0x80008000u;
+            uint32_t anyinf = 0;
+#pragma unroll
+            for (int q = 0; q < 4 * V; ++q) anyinf |= ((words[q] & 0x7FFF7FFFu) + 0x00010001u) | words[q];
+            anyinf &= 0x80008000u;
             uint64_t rs, rm;
-            if (nc == 8 && !anyinf) {
+            if (nc == CT && !anyinf) {
                 uint64_t lo = 0, lom = 0;
                 uint32_t hi = 0, him = 0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
+                for (int e = 0; e < CT; ++e) {
                     const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
                     lo = madw(blo[e], x, lo);
                     hi += bhi[e] * x;
@@ -1702,27 +1717,30 @@ __global__ void __launch_bounds__(kSymThreads)
                 rm = lom + ((uint64_t)him << 32);
                 if (i < fi) {
                     fi = i;
-                    fx = v.x & 0xFFFFu;
+                    fx = words[0] & 0xFFFFu;
                 }
                 if (si < fsi) {
                     fsi = si;
-                    const uint32_t wd = (emin & 4) ? ((emin & 2) ? v.w : v.z) : ((emin & 2) ? v.y : v.x);
+                    uint32_t wd = 0;
+#pragma unroll
+                    for (int q = 0; q < 4 * V; ++q)
+                        if (q == (emin >> 1)) wd = words[q]; // selects, no local-memory indexing
                     fxm = (wd >> ((emin & 1) * 16)) & 0xFFFFu;
                 }
             } else {
                 rs = 0;
                 rm = 0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
+                for (int e = 0; e < CT; ++e) {
                     if (e >= nc) break;
                     uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
                     if (x == kDevInf) {
                         x = kBndInf;
                         infc += 1 + ((two >> e) & 1u);
                     } else {
-                        unsigned long long key = ((uint64_t)(i * N + g[e]) << 16) | x;
+                        unsigned long long key = ((uint64_t)(i * N + sg[e][threadIdx.x]) << 16) | x;
                         if (key < ref) ref = key;
-                        key = ((uint64_t)(si * N + m[e]) << 16) | x;
+                        key = ((uint64_t)(si * N + sm_[e][threadIdx.x]) << 16) | x;
                         if (key < ref) ref = key;
                     }
                     const uint64_t b = ((uint64_t)bhi[e] << 32) | blo[e];
@@ -1732,55 +1750,48 @@ __global__ void __launch_bounds__(kSymThreads)
                 }
             }
             h += rw[i] * rs + rwm[i] * rm; // row weights s(2i), s(2 sigma i), precomputed
-            if (i >= g[0] && i <= glast) { // the diagonal entry (i, i), if this slice holds it
+            if (i >= g0 && i <= glast) { // the diagonal entry (i, i), if this slice holds it
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (e < nc && g[e] == i) {
+                for (int e = 0; e < CT; ++e)
+                    if (e < nc && sg[e][threadIdx.x] == i) {
                         const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
                         dmin = min(dmin, x == kDevInf ? (unsigned)kBndInf : x);
                     }
             }
         };
-#if MP_ST_DEPTH > 1
-        // kStDepth-deep per-thread cp.async ring: the thread's 16 bytes of rows i .. i+D-1 are
-        // in flight while row i is hashed (no block barrier: each thread reads only its slots)
-        __shared__ __align__(16) uint4 ring[kStDepth][kSymThreads];
-        const uint32_t slot0 = smem_addr(&ring[0][threadIdx.x]);
+        // kStDepth-deep per-thread cp.async ring: the thread's V x 16 bytes of rows i .. i+D-1
+        // are in flight while row i is hashed (no block barrier: each thread reads only its slots)
+        constexpr int D = CT == 16 ? 5 : kStDepth; // 16 columns: a shallower ring (48 KB of static smem)
+        __shared__ __align__(16) uint4 ring[D][V][kSymThreads];
+        const uint32_t slot0 = smem_addr(&ring[0][0][threadIdx.x]);
+        constexpr uint32_t kSlot = V * kSymThreads * 16, kPart = kSymThreads * 16;
         const uint16_t *src = X + i0 * ld + j0;
 #pragma unroll
-        for (int d = 0; d < kStDepth - 1; ++d) {
-            if (i0 + d < i1) cp_async16(slot0 + d * kSymThreads * 16, src + d * ld);
+        for (int d = 0; d < D - 1; ++d) {
+            if (i0 + d < i1)
+#pragma unroll
+                for (int q = 0; q < V; ++q) cp_async16(slot0 + d * kSlot + q * kPart, src + d * ld + 8 * q);
             cp_async_commit();
         }
         int slot = 0;
         for (int64_t i = i0; i < i1; ++i) {
-            const int64_t ip = i + kStDepth - 1; // refills the slot row i - 1 used
-            const int pslot = slot == 0 ? kStDepth - 1 : slot - 1;
-            if (ip < i1) cp_async16(slot0 + pslot * kSymThreads * 16, X + ip * ld + j0);
+            const int64_t ip = i + D - 1; // refills the slot row i - 1 used
+            const int pslot = slot == 0 ? D - 1 : slot - 1;
+            if (ip < i1)
+#pragma unroll
+                for (int q = 0; q < V; ++q) cp_async16(slot0 + pslot * kSlot + q * kPart, X + ip * ld + j0 + 8 * q);
             cp_async_commit();
             const int32_t si = sigma[i];
-            cp_async_wait<kStDepth - 1>();
-            row(i, si, lds128(slot0 + slot * kSymThreads * 16));
-            slot = slot == kStDepth - 1 ? 0 : slot + 1;
+            cp_async_wait<D - 1>();
+            uint4 vv[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) vv[q] = lds128(slot0 + slot * kSlot + q * kPart);
+            row(i, si, vv);
+            slot = slot == D - 1 ? 0 : slot + 1;
         }
         cp_async_wait<0>();
-#else
-        int64_t i = i0;
-        for (; i + kStRows <= i1; i += kStRows) { // kStRows rows' loads in flight
-            uint4 vv[kStRows];
-            int32_t ss[kStRows];
-#pragma unroll
-            for (int u = 0; u < kStRows; ++u) {
-                vv[u] = ldg_nc_v4(X + (i + u) * ld + j0);
-                ss[u] = sigma[i + u];
-            }
-#pragma unroll
-            for (int u = 0; u < kStRows; ++u) row(i + u, ss[u], vv[u]);
-        }
-        for (; i < i1; ++i) row(i, sigma[i], *reinterpret_cast<const uint4 *>(X + i * ld + j0));
-#endif
         if (fi != INT64_MAX) {
-            unsigned long long key = ((uint64_t)(fi * N + g[0]) << 16) | fx;
+            unsigned long long key = ((uint64_t)(fi * N + g0) << 16) | fx;
             if (key < ref) ref = key;
             key = ((uint64_t)(fsi * N + mmin) << 16) | fxm;
             if (key < ref) ref = key;
@@ -1823,16 +1834,25 @@ cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int
                              const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
                              unsigned long long *out_min, cudaStream_t s)
 {
-    const int64_t gx = std::max<int64_t>(1, (w + kSymCols - 1) / kSymCols);
+    static const int ct = [] { // MP_STATS_COLS=8 or 16 columns per thread (A/B knob)
+        const char *e = getenv("MP_STATS_COLS");
+        return (e && atoi(e) == 8) ? 8 : 16;
+    }();
+    const int64_t cols = (int64_t)kSymThreads * ct;
+    const int64_t gx = std::max<int64_t>(1, (w + cols - 1) / cols);
     // at least kStMinRows rows per block while that still leaves one block per SM: a thread's
-    // setup (16 column weights, gcol and sigma loads) costs about as much as hashing 10 rows
+    // setup (column weights, gcol and sigma loads) costs about as much as hashing 10 rows
     // (n = 9: 16 instead of 3 rows per block; n <= 6 keeps one or two rows per block)
     const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms() * 8 * (256 / kSymThreads) / gx);
     const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>((N + kStMinRows - 1) / kStMinRows,
                                                                                       std::min<int64_t>(N, num_sms()))));
     const int64_t rpb = (N + gy - 1) / gy;
-    k_stats_sym<<<dim3((unsigned)gx, (unsigned)gy), kSymThreads, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb, out_sum,
-                                                                 out_min);
+    if (ct == 16)
+        k_stats_sym<16><<<dim3((unsigned)gx, (unsigned)gy), kSymThreads, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb,
+                                                                                out_sum, out_min);
+    else
+        k_stats_sym<8><<<dim3((unsigned)gx, (unsigned)gy), kSymThreads, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb,
+                                                                               out_sum, out_min);
     return cudaGetLastError();
 }
 
