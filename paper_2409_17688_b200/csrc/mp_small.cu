@@ -86,6 +86,11 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     cg::cluster_group cluster = cg::this_cluster();
     const int nct = (int)cluster.num_blocks(), rk = (int)cluster.block_rank();
     const int R = nct / C, c = rk % C, r = rk / C;
+    // a cluster of one CTA needs only the block barrier
+    auto csync = [&]() {
+        if (nct > 1) cluster.sync();
+        else __syncthreads();
+    };
     const int rows_per = (N + R - 1) / R;
     const int r0 = min(N, r * rows_per), r1 = min(N, r0 + rows_per), nr = r1 - r0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -223,8 +228,6 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             if (v1 && j1 == i) st.dmin = min(st.dmin, (long long)b1);
             if (v0 && x0 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j0) << 16) | (long long)x0);
             if (v1 && x1 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j1) << 16) | (long long)x1);
-            // the row also goes to the history (exact compares of later powers read it)
-            reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)i * ldh + 64 * c)[lane] = p;
         }
         for (int m = 16; m; m >>= 1) {
             st.fp += shfl_xor_u64(st.fp, m);
@@ -244,7 +247,13 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             }
             if (lane == 0) xch[xi & 1] = s;
         }
-        cluster.sync(); // partials and the peers' rows of A^k visible cluster-wide
+        csync(); // partials and the peers' rows of A^k visible cluster-wide
+        // the own rows of A^k go to the history now, after the barrier: the stores complete while
+        // the next product runs instead of holding up this barrier's release (exact compares of
+        // later powers read them, ordered by the barriers in between)
+        for (int t = tid; t < nr * 32; t += nthreads)
+            reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)(r0 + (t >> 5)) * ldh + 64 * c)[t & 31] =
+                X[r0 * 32 + t];
         if (warp == 0) { // lane q < nct reads CTA q's partial; every lane ends with the sum
             Stats g = lane < nct ? cluster.map_shared_rank(xch, lane)[xi & 1]
                                  : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
                 for (int m = 16; m; m >>= 1) b += (long long)shfl_xor_u64((unsigned long long)b, m);
                 if (lane == 0) xmis[xi & 1] = b;
             }
-            cluster.sync();
+            csync();
             long long total = 0;
             for (int q = 0; q < nct; ++q) total += cluster.map_shared_rank(xmis, q)[xi & 1];
             ++xi;
@@ -331,7 +340,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             Xc = Xb;
         }
     }
-    cluster.sync(); // no CTA leaves while another may still read its shared memory
+    csync(); // no CTA leaves while another may still read its shared memory
     if (rk == 0 && tid == 0) {
         out[0] = found ? 0 : 4;
         out[1] = mu;
