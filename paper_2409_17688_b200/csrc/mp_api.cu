@@ -31,6 +31,7 @@ std::recursive_mutex g_mu;
 constexpr double kSpmmAdvantage = 0.6; // auto: SpMM if it issues < 60% of the tile kernel's steps
 constexpr int kBatch = 16;             // powers per host round trip when N <= kBatchMaxN
 constexpr int64_t kBatchMaxN = 4096;
+constexpr int64_t kLookaheadMaxN = 40000; // the lookahead power loop below this order
 constexpr double kDefaultRingBytes = 48.0 * 1024 * 1024 * 1024; // power-store cap unless set
 thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
@@ -483,6 +484,11 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, c
 // X_1 = A[:, c0:c0+w) in the device layout, from A, AT2 or straight from the word masks.
 mp_status make_power1(PowerRun &R, uint16_t *dst, cudaStream_t s)
 {
+    if (R.spmm && R.a_src && R.bits_ok && !R.sp.off) { // A's support bitsets from the range check
+        g_launches.fetch_add(1);
+        LAUNCH(launch_x1_bits(R.bits.as<uint32_t>(), R.N, R.a_src, R.a_ld, R.dloc.as<int32_t>(), dst, R.ld, R.Np, s));
+        return MP_OK;
+    }
     if (R.spmm && R.sp.off) { // row lists of A available (grouped path): fill + scatter
         LAUNCH(launch_x1_csr(R.sp.off, R.sp.idx, R.N, R.a_src, R.a_ld, R.a_src ? nullptr : R.words.as<WordMask>(),
                              R.dloc.as<int32_t>(), dst, R.ld, R.Np, s));
@@ -601,7 +607,7 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     }
     const int C = small_run_ctas(N);
     TRY(R.small_hist.ensure((size_t)(max_k + 1) * N * 64 * C * 2, "small-N power history"));
-    const size_t nout = 6 + 2 * (size_t)(max_k + 1);
+    const size_t nout = 6 + 2 * (size_t)(max_k + 1) + 4; // + 4 clock64 phase sums
     TRY(R.small_out.ensure(nout * 8, "small-N result"));
     const uint64_t S = mp_fingerprint_unit(N);
     const int32_t *dsig = nullptr;
@@ -620,6 +626,11 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     CUDA_TRY(cudaEventRecord(ev[3], s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (h[0] == -1) return MP_OK; // too many finite entries: the general path
+    if (getenv("MP_SMALL_PROFILE")) {
+        const long long *pf = h + 6 + 2 * (max_k + 1);
+        fprintf(stderr, "mp-small N=%lld k_last=%lld cycles: setup %lld, products+stats %lld, reductions %lld, search %lld\n",
+                (long long)N, h[4], pf[0], pf[1], pf[2], pf[3]);
+    }
     *handled = true;
     float kms = 0.f, all = 0.f, setup = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&kms, ev[1], ev[2]));
@@ -934,8 +945,10 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // the statistics of power k run on a second stream and the host searches for a repeat, so
     // the statistics overlap the next product and the host round trip is hidden.  A power past
     // the first repeat is computed and discarded (one product per run).
+    // (measured: n = 10 10.7 -> 9.8 ms, n = 11 36.4 -> 33.3 ms; at n = 12 the statistics slow the
+    // memory-bound product they overlap by more than the hidden round trip: 177.6 vs 179.6 ms)
     const bool lookahead = B == 1 && !cap && !g_dist.fn && !g_obs.fn && max_k >= 2 && R.ring.size() >= 3 &&
-                           lookahead_on();
+                           N < kLookaheadMaxN && lookahead_on();
     if (lookahead) {
         cudaStream_t s2 = st->stream2;
         if (!s2) {

@@ -2277,6 +2277,37 @@ __global__ void k_x1_scatter(const int64_t *__restrict__ off, const int32_t *__r
     }
 }
 
+// X_1 from A's support bitsets (nw words per row): the finite a_il with loc[l] >= 0 at
+// X1[i][loc[l]] (warp per row, lanes over the row's words); X1 filled with +inf first
+__global__ void k_x1_scatter_bits(const uint32_t *__restrict__ bits, int64_t nw, int64_t N,
+                                  const uint16_t *__restrict__ A, int64_t lda, const int32_t *__restrict__ loc,
+                                  uint16_t *__restrict__ X1, int64_t ldx)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        for (int64_t k = lane; k < nw; k += 32) {
+            uint32_t m = bits[i * nw + k];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int64_t l = k * 32 + b;
+                const int32_t j = loc[l];
+                if (j >= 0) X1[i * ldx + j] = A[i * lda + l]; // range-checked: finite <= 0x7FFE
+            }
+        }
+    }
+}
+
+cudaError_t launch_x1_bits(const uint32_t *bits, int64_t N, const uint16_t *A, int64_t lda, const int32_t *loc,
+                           uint16_t *X1, int64_t ldx, int64_t Np, cudaStream_t s)
+{
+    const int64_t n16 = Np * ldx / 8; // ldx is a multiple of 64
+    k_x1_fill<<<grid_for(n16, 256), 256, 0, s>>>(X1, n16);
+    k_x1_scatter_bits<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, (N + 31) / 32, N, A, lda, loc, X1, ldx);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_x1_csr(const int64_t *off, const int32_t *idx, int64_t N, const uint16_t *A, int64_t lda,
                           const WordMask *words, const int32_t *loc, uint16_t *X1, int64_t ldx, int64_t Np,
                           cudaStream_t s)

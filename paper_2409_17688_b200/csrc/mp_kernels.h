@@ -40,7 +40,7 @@ cudaError_t launch_decode(const uint16_t *src, int64_t lds, int64_t rows, int64_
 // out[]: status (0 ok, 1 hint violated, 2 range, 4 not periodic, -1 more than max_nnz finite
 // entries), mu, lambda,
 // offset, k_last, dense_from, then diag_min[k] at out[6 + k] and fingerprint[k] at
-// out[6 + (max_k + 1) + k].  hist: (max_k + 1) x N x (64 * ctas) u16 scratch.
+// out[6 + (max_k + 1) + k], then 4 clock64 phase sums.  hist: (max_k + 1) x N x (64 * ctas) u16.
 constexpr int kSmallMaxN = 256;
 int small_run_ctas(int64_t N);
 cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_k, int max_nnz, const int32_t *sigma,
@@ -137,6 +137,10 @@ cudaError_t launch_x1_from_words(const WordMask *words, int64_t N, int n, int64_
 cudaError_t launch_x1_csr(const int64_t *off, const int32_t *idx, int64_t N, const uint16_t *A, int64_t lda,
                           const WordMask *words, const int32_t *loc, uint16_t *X1, int64_t ldx, int64_t Np,
                           cudaStream_t s);
+// X_1 from A's support bitsets (from launch_check_a): +inf everywhere, then each finite a_il
+// with loc[l] >= 0 at X1[i][loc[l]] (two launches).
+cudaError_t launch_x1_bits(const uint32_t *bits, int64_t N, const uint16_t *A, int64_t lda, const int32_t *loc,
+                           uint16_t *X1, int64_t ldx, int64_t Np, cudaStream_t s);
 // X_1 on a column list: dst[i][j] = enc(src[i][gcol[j]]).
 cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, const int32_t *gcol, int64_t w,
                                uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s);

@@ -175,13 +175,18 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     }
     __syncthreads();
 
+    // MP_SMALL_PROFILE builds: clock64 phase sums of CTA 0 thread 0 (setup, product + statistics,
+    // reductions + barrier, search) appended to out[] for the host to print
+    long long t_setup = clock64(), t_prod = 0, t_red = 0, t_search = 0, t_mark = t_setup;
     uint32_t *Xp = Xa, *Xc = Xb; // X_{k-1}, X_k (X_1 is in Xa)
     int xi = 0;                  // cluster exchange count (parity buffer)
     int mu = 0, lam = 0, off = 0, k_last = 0, dense_from = 0;
     bool found = false;
     int k = 1;
     const uint32_t xlane = (uint32_t)__cvta_generic_to_shared(Xa) + 4 * lane; // this lane's column pair
+    t_setup = clock64() - t_setup;
     for (;; ++k) {
+        t_mark = clock64();
         uint32_t *X = (k == 1) ? Xa : Xc;
         const uint32_t xp_s = xlane + (uint32_t)((Xp - Xa) * 4);
         // ---- A^k = A (x) A^{k-1} on the own rows of this block (k >= 2) with the a4
@@ -247,6 +252,11 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             }
             if (lane == 0) xch[xi & 1] = s;
         }
+        {
+            const long long t = clock64();
+            t_prod += t - t_mark;
+            t_mark = t;
+        }
         csync(); // partials and the peers' rows of A^k visible cluster-wide
         // the own rows of A^k go to the history now, after the barrier: the stores complete while
         // the next product runs instead of holding up this barrier's release (exact compares of
@@ -268,6 +278,11 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         }
         ++xi;
         __syncthreads();
+        {
+            const long long t = clock64();
+            t_red += t - t_mark;
+            t_mark = t;
+        }
         // ---- a5: forward first-repeat search, j = k-1 down to 1 (identical in every CTA)
         int jn = k - 1;
         while (!found) {
@@ -331,6 +346,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             jn = j - 1;
             __syncthreads();
         }
+        t_search += clock64() - t_mark;
         if (found || k == max_k) break;
         if (k >= 2) { // the new power becomes X_{k-1}
             uint32_t *tmp = Xp;
@@ -353,6 +369,11 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             out[6 + q] = hs[q].dmin;
             out[6 + (max_k + 1) + q] = (long long)hs[q].fp;
         }
+        long long *prof = out + 6 + 2 * (max_k + 1);
+        prof[0] = t_setup;
+        prof[1] = t_prod;
+        prof[2] = t_red;
+        prof[3] = t_search;
     }
 }
 
