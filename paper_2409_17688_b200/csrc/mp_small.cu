@@ -49,6 +49,25 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
     return ((unsigned long long)hi << 32) | lo;
 }
 
+// Butterfly reduction of the statistics over the first `width` lanes (a power of two): the
+// fingerprint as 64 bits, the +inf count, diagonal minimum and first-finite key as 32 bits
+// (N <= 256: t = i N + j < 2^16, so a key (t << 16) | x < 2^32; no key = 0x7FFF..F maps to
+// 0xFFFFFFFF and back).
+__device__ __forceinline__ void reduce_stats(Stats &s, int width)
+{
+    uint32_t inf = (uint32_t)s.inf, dmin = (uint32_t)s.dmin;
+    uint32_t ref = s.ref == 0x7FFFFFFFFFFFFFFFll ? 0xFFFFFFFFu : (uint32_t)s.ref;
+    for (int m = width >> 1; m; m >>= 1) {
+        s.fp += shfl_xor_u64(s.fp, m);
+        inf += __shfl_xor_sync(0xFFFFFFFFu, inf, m);
+        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, m));
+        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, m));
+    }
+    s.inf = inf;
+    s.dmin = dmin;
+    s.ref = ref == 0xFFFFFFFFu ? 0x7FFFFFFFFFFFFFFFll : (long long)ref;
+}
+
 // Candidate test of the forward first-repeat search (the rule of mp_repeat_candidate in
 // mp_api.cu, restated for the device).
 __device__ bool candidate(const Stats &k, const Stats &j, unsigned long long S, int *c)
@@ -234,22 +253,12 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             if (v0 && x0 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j0) << 16) | (long long)x0);
             if (v1 && x1 < kDevInf) st.ref = min(st.ref, (((long long)i * N + j1) << 16) | (long long)x1);
         }
-        for (int m = 16; m; m >>= 1) {
-            st.fp += shfl_xor_u64(st.fp, m);
-            st.inf += shfl_xor_u64(st.inf, m);
-            st.dmin = min(st.dmin, (long long)shfl_xor_u64((unsigned long long)st.dmin, m));
-            st.ref = min(st.ref, (long long)shfl_xor_u64((unsigned long long)st.ref, m));
-        }
+        reduce_stats(st, 32);
         if (lane == 0) wred[warp] = st;
         __syncthreads();
         if (warp == 0) { // the CTA's partial: lanes < 16 hold the warps' partials
             Stats s = lane < nwarps ? wred[lane] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
-            for (int m = 16; m; m >>= 1) {
-                s.fp += shfl_xor_u64(s.fp, m);
-                s.inf += shfl_xor_u64(s.inf, m);
-                s.dmin = min(s.dmin, (long long)shfl_xor_u64((unsigned long long)s.dmin, m));
-                s.ref = min(s.ref, (long long)shfl_xor_u64((unsigned long long)s.ref, m));
-            }
+            reduce_stats(s, kSmWarps); // lanes >= nwarps hold the identity
             if (lane == 0) xch[xi & 1] = s;
         }
         {
@@ -267,12 +276,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         if (warp == 0) { // lane q < nct reads CTA q's partial; every lane ends with the sum
             Stats g = lane < nct ? cluster.map_shared_rank(xch, lane)[xi & 1]
                                  : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
-            for (int m = 16; m; m >>= 1) {
-                g.fp += shfl_xor_u64(g.fp, m);
-                g.inf += shfl_xor_u64(g.inf, m);
-                g.dmin = min(g.dmin, (long long)shfl_xor_u64((unsigned long long)g.dmin, m));
-                g.ref = min(g.ref, (long long)shfl_xor_u64((unsigned long long)g.ref, m));
-            }
+            reduce_stats(g, 16); // a cluster has at most 16 CTAs
             if (lane == 0) hs[k] = g;
             if (!dense_from && g.inf == 0) dense_from = k;
         }
@@ -419,9 +423,9 @@ cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(C * R));
-    // a warp per row at a time: about four rows per warp, 4 to 16 warps
+    // 4 to 16 warps: one row per warp where the rows allow
     const int64_t rows_per = (N + R - 1) / R;
-    const int warps = (int)std::max<int64_t>(4, std::min<int64_t>(kSmWarps, (rows_per + 3) / 4));
+    const int warps = (int)std::max<int64_t>(4, std::min<int64_t>(kSmWarps, rows_per)); // a row per warp if possible
     cfg.blockDim = dim3((unsigned)(32 * warps));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
