@@ -58,13 +58,6 @@ std::vector<int32_t> g_sym;
 bool g_word_sym = true;
 bool g_small_off = false; // mp_set_small_path(0): always the general path
 int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be A(D_n)
-// MP_FOLD_STATS=0: separate fold and statistics passes instead of k_fold_stats (diagnostic)
-bool fold_stats_on()
-{
-    const char *e = getenv("MP_FOLD_STATS"); // read per run: tests switch it
-    return !(e && *e == '0');
-}
-
 // MP_LOOKAHEAD=0: no lookahead in the large-N power loop (diagnostic)
 bool lookahead_on()
 {
@@ -462,13 +455,8 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
 
 // C = A (x) X with the selected kernel.
 // mid (may be null): recorded between the SpMM and the fold passes of the row-inclusion reuse.
-// st_sum / st_min (may be null): with the reuse, the fold passes also compute the power's a4
-// statistics into these slots (k_fold_stats); *stats_done says so.
-mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, cudaEvent_t mid = nullptr,
-                  unsigned long long *st_sum = nullptr, unsigned long long *st_min = nullptr,
-                  bool *stats_done = nullptr)
+mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, cudaEvent_t mid = nullptr)
 {
-    if (stats_done) *stats_done = false;
     if (R.spmm) {
         SparseA sa;
         sa.L = R.sp.L;
@@ -480,16 +468,7 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, c
         int nl = 0;
         cudaError_t e = launch_spmm(sa, R.plan, X, R.ld, C, R.ld, R.Np, s, &nl);
         if (e == cudaSuccess && mid) e = cudaEventRecord(mid, s);
-        if (e == cudaSuccess && R.dag_n) {
-            if (st_sum && fold_stats_on()) { // parents' rows and the statistics, level by level
-                e = launch_fold_stats(R.rdag, C, R.ld, R.N, R.sym ? R.dgcol.as<int32_t>() : nullptr, R.c0,
-                                      R.sym ? R.dsig.as<int32_t>() : nullptr, R.drw.as<uint64_t>(),
-                                      R.drw.as<uint64_t>() + R.N, R.w, st_sum, st_min, s, &nl);
-                if (stats_done) *stats_done = true;
-            } else {
-                e = launch_folds(R.rdag, C, R.ld, R.ld, s, &nl); // parents' rows
-            }
-        }
+        if (e == cudaSuccess && R.dag_n) e = launch_folds(R.rdag, C, R.ld, R.ld, s, &nl); // parents' rows
         g_launches.fetch_add(nl);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -851,10 +830,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     }
     // row-inclusion reuse needs the word structure and the grouped SpMM
     R.dag_n = (g_row_reuse && R.n_words && (g_opts.sparsity == 2 || g_opts.sparsity < 0)) ? R.n_words : 0;
-    if (R.dag_n && !R.sym) { // the fused fold + statistics pass reads the row weights
-        TRY(R.drw.ensure((size_t)N * 16, "row weights"));
-        LAUNCH(launch_row_weights(N, nullptr, R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, s));
-    }
+
 
     tr.mark("a2 stage A");
 
@@ -1007,21 +983,16 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             if (k == 1) {
                 TRY(make_power1(R, dst, s));
             }
-            bool fused = false;
             if (k >= 2) {
                 CUDA_TRY(cudaEventRecord(R.events[2 * k], s));
-                TRY(product(R, buf[(size_t)k - 1], dst, s, R.events[4 * (max_k + 1) + k],
-                            reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
-                            reinterpret_cast<unsigned long long *>(st_min + 2 * k), &fused));
+                TRY(product(R, buf[(size_t)k - 1], dst, s, R.events[4 * (max_k + 1) + k]));
                 CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
                 ++launches;
             }
             CUDA_TRY(cudaEventRecord(prod_done[k], s));
             CUDA_TRY(cudaStreamWaitEvent(s2, prod_done[k], 0));
             CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s2));
-            if (fused) {
-                // computed by the fold passes (k_fold_stats)
-            } else if (R.sym)
+            if (R.sym)
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.drw.as<uint64_t>(),
                                         R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
@@ -1102,21 +1073,16 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             uint16_t *dst = R.ring[q].as<uint16_t>();
             R.slot_power[q] = k;
             buf[(size_t)k] = dst;
-            bool fused_stats = false;
             if (k == 1) {
                 TRY(make_power1(R, dst, s)); // X_1 = A[:, shard]
             } else {
                 CUDA_TRY(cudaEventRecord(R.events[2 * k], s));
-                TRY(product(R, prev, dst, s, R.events[4 * (max_k + 1) + k], // A^k = A (x) A^{k-1}
-                            reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
-                            reinterpret_cast<unsigned long long *>(st_min + 2 * k), &fused_stats));
+                TRY(product(R, prev, dst, s, R.events[4 * (max_k + 1) + k])); // A^k = A (x) A^{k-1}
                 CUDA_TRY(cudaEventRecord(R.events[2 * k + 1], s));
                 ++launches;
             }
             if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s)); // stats start
-            if (fused_stats) {
-                // computed by the fold passes (k_fold_stats)
-            } else if (R.sym)
+            if (R.sym)
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(),
                                         R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),

@@ -26,14 +26,6 @@ namespace mp {
 
 namespace {
 
-// d = a * b + c with a 64-bit addend: one IMAD.WIDE.U32
-__device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c)
-{
-    uint64_t d;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
-    return d;
-}
-
 // Base-3 value of a word with letter 0 (the top row) most significant: the lexicographic order
 // of A(D_n) (G5) is the order of these keys.
 __device__ __forceinline__ uint32_t word_key(const WordMask &w, int n)
@@ -200,194 +192,6 @@ __global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows,
     }
 }
 
-// Fold and statistics of one DAG level in one pass.  Block (s, c) takes the 1024-column segment s
-// of the level's rows c*rpb ..; its eight warps walk those rows like k_fold (warp per row
-// segment, lane = 4 x 8 columns, parents two at a time) and then hash the finished row segment
-// exactly as k_stats / k_stats_sym do:
-//   H += s(2i) s(2g+1) x  (+ s(2 sigma i) s(2 sigma g + 1) x for a mirrored column, SYM),
-//   +inf count (x2 for a mirrored column), diagonal minimum over (g, g), first finite entry
-//   key (t << 16) | x over t = i N + g and (with SYM) t = sigma i N + sigma g.
-// The segment's column weights (split into 32-bit halves) sit in shared memory in a lane-major
-// layout (column 256h + 8 lane + e at [(8h + e) * 32 + lane]: one conflict-free LDS.128 per
-// column and lane).  Level 0 rows (no parents) are only hashed.  Columns: local column jj stands
-// for g = gcol[jj] (SYM) or g = c0 + jj; only jj < w counts.
-constexpr int kFsSeg = 1024;
-template <bool SYM>
-__global__ void __launch_bounds__(256)
-    k_fold_stats(const int32_t *__restrict__ lrows, int64_t nrows, const int64_t *__restrict__ off,
-                 const int32_t *__restrict__ pidx, uint16_t *__restrict__ C, int64_t ld, int64_t N,
-                 const int32_t *__restrict__ gcol, int64_t c0, const int32_t *__restrict__ sigma,
-                 const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t w, int64_t rpb, bool fold,
-                 unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
-{
-    __shared__ uint4 wt[kFsSeg];   // {b.lo, b.hi, bm.lo, bm.hi}
-    __shared__ int2 gm[kFsSeg];    // {g, m}
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t seg0 = (int64_t)blockIdx.x * kFsSeg;
-    const int ncols = (int)(w - seg0 < kFsSeg ? w - seg0 : kFsSeg);            // columns that count
-    const int ccols = (int)(ld - seg0 < kFsSeg ? ld - seg0 : kFsSeg);          // columns stored
-    for (int t = threadIdx.x; t < kFsSeg; t += blockDim.x) {
-        // t = (8h + e) * 32 + ln  <->  column 256h + 8 ln + e of the segment
-        const int he = t >> 5, ln = t & 31, col = 256 * (he >> 3) + 8 * ln + (he & 7);
-        uint64_t b = 0, bm = 0;
-        int32_t g = -1, m = -1;
-        if (col < ncols) {
-            g = SYM ? gcol[seg0 + col] : (int32_t)(c0 + seg0 + col);
-            m = SYM ? sigma[g] : g;
-            b = mix64(2 * (uint64_t)g + 1);
-            bm = (SYM && m != g) ? mix64(2 * (uint64_t)m + 1) : 0;
-        }
-        wt[t] = make_uint4((uint32_t)b, (uint32_t)(b >> 32), (uint32_t)bm, (uint32_t)(bm >> 32));
-        gm[t] = make_int2(g, m);
-    }
-    __syncthreads();
-    // the segment's global columns g run from gm at column 0 to gm at column ncols - 1
-    // (ascending): only rows q in that range can meet the diagonal here
-    const int32_t glo = ncols > 0 ? gm[0].x : 0;
-    const int lastc = ncols > 0 ? ncols - 1 : 0;
-    const int32_t ghi = ncols > 0 ? gm[((8 * (lastc >> 8) + (lastc & 7)) << 5) + ((lastc >> 3) & 31)].x : -1;
-    unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
-    unsigned dmin = 0xFFFFu;
-    const int64_t r0 = (int64_t)blockIdx.y * rpb, r1 = min(nrows, r0 + rpb);
-    for (int64_t r = r0 + warp; r < r1; r += 8) {
-        const int64_t q = lrows[r];
-        uint16_t *row = C + q * ld + seg0;
-        uint4 v[4];
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
-            const int col = 256 * hh + 8 * lane;
-            v[hh] = col < ccols ? *reinterpret_cast<const uint4 *>(row + col) : make_uint4(0, 0, 0, 0);
-        }
-        if (fold) {
-            const int64_t e0 = off[q], np = off[q + 1] - e0;
-            const int32_t mine = lane < np ? pidx[e0 + lane] : 0;
-            for (int e = 0; e < np; e += 2) {
-                const int64_t p0 = __shfl_sync(0xFFFFFFFFu, mine, e);
-                const int64_t p1 = __shfl_sync(0xFFFFFFFFu, mine, e + 1 < np ? e + 1 : e);
-                const uint16_t *ra = C + p0 * ld + seg0, *rb = C + p1 * ld + seg0;
-                uint4 u0[4], u1[4];
-#pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
-                    const int col = 256 * hh + 8 * lane;
-                    u0[hh] = col < ccols ? __ldcg(reinterpret_cast<const uint4 *>(ra + col)) : make_uint4(0, 0, 0, 0);
-                    u1[hh] = col < ccols ? __ldcg(reinterpret_cast<const uint4 *>(rb + col)) : make_uint4(0, 0, 0, 0);
-                }
-#pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
-                    v[hh].x = __vminu2(v[hh].x, __vminu2(u0[hh].x, u1[hh].x));
-                    v[hh].y = __vminu2(v[hh].y, __vminu2(u0[hh].y, u1[hh].y));
-                    v[hh].z = __vminu2(v[hh].z, __vminu2(u0[hh].z, u1[hh].z));
-                    v[hh].w = __vminu2(v[hh].w, __vminu2(u0[hh].w, u1[hh].w));
-                }
-            }
-            if (np > 0) {
-#pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
-                    const int col = 256 * hh + 8 * lane;
-                    if (col < ccols) *reinterpret_cast<uint4 *>(row + col) = v[hh];
-                }
-            }
-        }
-        // a4 statistics of the finished row segment
-        const int64_t si = SYM ? (int64_t)sigma[q] : q;
-        uint64_t lo = 0, lom = 0;
-        uint32_t hi = 0, him = 0;
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
-            const uint32_t words[4] = {v[hh].x, v[hh].y, v[hh].z, v[hh].w};
-            const int colb = 256 * hh + 8 * lane;
-            uint32_t anyinf = 0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) anyinf |= ((words[u] & 0x7FFF7FFFu) + 0x00010001u) | words[u];
-            const bool fast = !(anyinf & 0x80008000u) && colb + 8 <= ncols;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint4 b = wt[(8 * hh + e) * 32 + lane];
-                uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                if (!fast) {
-                    if (colb + e >= ncols) continue;
-                    const int2 g = gm[(8 * hh + e) * 32 + lane];
-                    if (x >= kDevInf) {
-                        x = kBndInf;
-                        infc += (SYM && g.y != g.x) ? 2 : 1;
-                    } else {
-                        unsigned long long key = ((uint64_t)(q * N + g.x) << 16) | x;
-                        if (key < ref) ref = key;
-                        if (SYM) {
-                            key = ((uint64_t)(si * N + g.y) << 16) | x;
-                            if (key < ref) ref = key;
-                        }
-                    }
-                }
-                lo = madw(b.x, x, lo);
-                hi += b.y * x;
-                if (SYM) {
-                    lom = madw(b.z, x, lom);
-                    him += b.w * x;
-                }
-            }
-            if (fast) { // the keys of an all-finite slice: its first column (g ascending)
-                const int2 g = gm[(8 * hh) * 32 + lane];
-                const uint32_t x0 = words[0] & 0xFFFFu;
-                unsigned long long key = ((uint64_t)(q * N + g.x) << 16) | x0;
-                if (key < ref) ref = key;
-                if (SYM) { // the mirrors: the smallest sigma g of the slice
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int2 ge = gm[(8 * hh + e) * 32 + lane];
-                        const uint32_t xe = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                        key = ((uint64_t)(si * N + ge.y) << 16) | xe;
-                        if (key < ref) ref = key;
-                    }
-                }
-            }
-            // the diagonal entry (q, q), if this slice holds it
-            if (q >= glo && q <= ghi) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if (colb + e >= ncols) break;
-                    if (gm[(8 * hh + e) * 32 + lane].x == q) {
-                        const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                        dmin = min(dmin, x >= kDevInf ? (unsigned)kBndInf : x);
-                    }
-                }
-            }
-        }
-        const uint64_t rs = lo + ((uint64_t)hi << 32), rm = lom + ((uint64_t)him << 32);
-        h += rw[q] * rs + (SYM ? rwm[q] * rm : 0ull);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
-        infc += __shfl_xor_sync(0xFFFFFFFFu, infc, o);
-        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
-        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, o));
-    }
-    __shared__ unsigned long long sh[8], sn[8], sr[8];
-    __shared__ unsigned sd[8];
-    if (lane == 0) {
-        sh[warp] = h;
-        sn[warp] = infc;
-        sd[warp] = dmin;
-        sr[warp] = ref;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long H = 0, I = 0, Rf = 0x7FFFFFFFFFFFFFFFull;
-        unsigned D = 0xFFFFu;
-        for (int k = 0; k < 8; ++k) {
-            H += sh[k];
-            I += sn[k];
-            D = min(D, sd[k]);
-            Rf = min(Rf, sr[k]);
-        }
-        if (H) atomicAdd(out_sum + 0, H);
-        if (I) atomicAdd(out_sum + 1, I);
-        if (D < 0xFFFFu) atomicMin(out_min + 0, (unsigned long long)D);
-        if (Rf != 0x7FFFFFFFFFFFFFFFull) atomicMin(out_min + 1, Rf);
-    }
-}
-
 int grid_rows(int64_t work, int per_block)
 {
     const int64_t g = (work + per_block - 1) / per_block;
@@ -469,33 +273,6 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
         // of items (the segment-major order above relies on it)
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, 148 * 8));
         k_fold<<<grid, 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc);
-        if (launches) ++*launches;
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-}
-
-cudaError_t launch_fold_stats(const RowDag &d, uint16_t *C, int64_t ld, int64_t N, const int32_t *gcol, int64_t c0,
-                              const int32_t *sigma, const uint64_t *rw, const uint64_t *rwm, int64_t w,
-                              unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s, int *launches)
-{
-    const int64_t gx = std::max<int64_t>(1, (w + kFsSeg - 1) / kFsSeg);
-    for (int l = 0; l < d.levels; ++l) {
-        const int64_t nr = d.lptr[(size_t)l + 1] - d.lptr[(size_t)l];
-        if (nr == 0) continue;
-        // about 8 blocks of 8 warps per SM; at least 64 rows per block (8 per warp) so the
-        // segment's weights, staged once per block, serve many rows
-        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((148 * 8 + gx - 1) / gx, (nr + 63) / 64));
-        const int64_t rpb = (nr + gy - 1) / gy;
-        const dim3 grid((unsigned)gx, (unsigned)gy);
-        const int32_t *lr = d.lrows + d.lptr[(size_t)l];
-        if (sigma)
-            k_fold_stats<true><<<grid, 256, 0, s>>>(lr, nr, d.off, d.idx, C, ld, N, gcol, c0, sigma, rw, rwm, w, rpb,
-                                                    l > 0, out_sum, out_min);
-        else
-            k_fold_stats<false><<<grid, 256, 0, s>>>(lr, nr, d.off, d.idx, C, ld, N, gcol, c0, sigma, rw, rwm, w, rpb,
-                                                     l > 0, out_sum, out_min);
         if (launches) ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

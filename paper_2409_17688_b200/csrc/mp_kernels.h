@@ -118,13 +118,6 @@ cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const
                               cudaStream_t s);
 // C_q = min(C_q, C_p) over the parents p, level by level (levels 1 .. levels-1), ncols columns
 cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncols, cudaStream_t s, int *launches);
-// The fold of every level with the a4 statistics of every row fused in (level 0 rows are only
-// hashed): w local columns, column jj = gcol[jj] under the symmetry sigma (sigma and gcol not
-// null) or c0 + jj; rw / rwm the row weights s(2i), s(2 sigma i); accumulates into out_sum /
-// out_min exactly like launch_stats(_sym).
-cudaError_t launch_fold_stats(const RowDag &d, uint16_t *C, int64_t ld, int64_t N, const int32_t *gcol, int64_t c0,
-                              const int32_t *sigma, const uint64_t *rw, const uint64_t *rwm, int64_t w,
-                              unsigned long long *out_sum, unsigned long long *out_min, cudaStream_t s, int *launches);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
 // pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).

@@ -136,9 +136,24 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     const bool v0 = j0 < N, v1 = j1 < N;
     const uint64_t cw0 = v0 ? mix64(2 * (uint64_t)j0 + 1) : 0, cw1 = v1 ? mix64(2 * (uint64_t)j1 + 1) : 0;
 
-    // ---- a2: row lists of the own rows, range and symmetry checks, X_1 block (every row)
+    // ---- a2: row lists of the own rows, range and symmetry checks, X_1 block (every row).
+    // A is read once with independent loads by every thread: the own rows into As (staged in
+    // the Xb buffer: nr <= 64 rows of N u16 fit in N x 128 bytes) and the CTA's column block of
+    // every row straight into Xa (X_1 in the device encoding); the passes below read shared memory.
+    long long t_start = clock64();
+    uint16_t *As = reinterpret_cast<uint16_t *>(Xb); // [nr][N]
     if (tid == 0) flags[0] = flags[1] = flags[4] = 0;
     for (int t = tid; t < nr; t += nthreads) rw[t] = mix64(2 * (uint64_t)(r0 + t));
+    for (int t = tid; t < nr * N; t += nthreads) {
+        const int ii = t / N, l = t - ii * N;
+        As[t] = A[(int64_t)(r0 + ii) * lda + l];
+    }
+    for (int t = tid; t < N * 32; t += nthreads) { // X_1 = A[:, block], packed pairs
+        const int i = t >> 5, ln = t & 31, ja = 64 * c + 2 * ln;
+        const uint16_t a0 = ja < N ? A[(int64_t)i * lda + ja] : (uint16_t)kBndInf;
+        const uint16_t a1 = ja + 1 < N ? A[(int64_t)i * lda + ja + 1] : (uint16_t)kBndInf;
+        Xa[t] = (uint32_t)(a0 == kBndInf ? kDevInf : a0) | ((uint32_t)(a1 == kBndInf ? kDevInf : a1) << 16);
+    }
     __syncthreads();
     for (int ii = warp; ii < nr; ii += nwarps) {
         const int i = r0 + ii;
@@ -146,7 +161,7 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         bool bad = false, asym = false;
         for (int l0 = 0; l0 < N; l0 += 32) {
             const int l = l0 + lane;
-            const uint16_t x = l < N ? A[(int64_t)i * lda + l] : (uint16_t)kBndInf;
+            const uint16_t x = l < N ? As[ii * N + l] : (uint16_t)kBndInf;
             bad |= x != kBndInf && x > kFiniteMax;
             if (sigma && x != kBndInf) asym |= A[(int64_t)sigma[i] * lda + sigma[l]] != x;
             cnt += __popc(__ballot_sync(0xFFFFFFFFu, x != kBndInf));
@@ -155,18 +170,13 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         if (__any_sync(0xFFFFFFFFu, asym) && lane == 0) flags[4] = 1;
         if (lane == 0) rptr[ii + 1] = cnt;
     }
-    for (int i = warp; i < N; i += nwarps) { // X_1 = A[:, block], device encoding, packed pairs
-        const uint16_t a0 = v0 ? A[(int64_t)i * lda + j0] : (uint16_t)kBndInf;
-        const uint16_t a1 = v1 ? A[(int64_t)i * lda + j1] : (uint16_t)kBndInf;
-        Xa[i * 32 + lane] = (uint32_t)(a0 == kBndInf ? kDevInf : a0) | ((uint32_t)(a1 == kBndInf ? kDevInf : a1) << 16);
-    }
     __syncthreads();
     if (tid == 0) {
         rptr[0] = 0;
         for (int ii = 0; ii < nr; ++ii) rptr[ii + 1] += rptr[ii];
         flags[1] = rptr[nr] > max_nnz;
     }
-    cluster.sync(); // every CTA's flags are final: one decision for the whole cluster
+    csync(); // every CTA's flags are final: one decision for the whole cluster
     bool stop = false;
     int status = 0;
     for (int q = 0; q < nct; ++q) {
@@ -176,27 +186,25 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         else if (f[1] && status == 0) status = -1;
     }
     stop = status != 0;
-    cluster.sync(); // nobody changes its flags before every CTA has read them
+    csync(); // nobody changes its flags before every CTA has read them
     if (stop) {
         if (rk == 0 && tid == 0) out[0] = status;
         return;
     }
     for (int ii = warp; ii < nr; ii += nwarps) {
-        const int i = r0 + ii;
         int e = rptr[ii];
         for (int l0 = 0; l0 < N; l0 += 32) {
             const int l = l0 + lane;
-            const uint16_t x = l < N ? A[(int64_t)i * lda + l] : (uint16_t)kBndInf;
+            const uint16_t x = l < N ? As[ii * N + l] : (uint16_t)kBndInf;
             const unsigned m = __ballot_sync(0xFFFFFFFFu, x != kBndInf);
             if (x != kBndInf) ent[e + __popc(m & ((1u << lane) - 1))] = make_uint2((uint32_t)l * 128u, (uint32_t)x * 0x10001u);
             e += __popc(m);
         }
     }
-    __syncthreads();
-
+    __syncthreads(); // As (in Xb) is free again: A^2 goes there
     // MP_SMALL_PROFILE builds: clock64 phase sums of CTA 0 thread 0 (setup, product + statistics,
     // reductions + barrier, search) appended to out[] for the host to print
-    long long t_setup = clock64(), t_prod = 0, t_red = 0, t_search = 0, t_mark = t_setup;
+    long long t_setup = t_start, t_prod = 0, t_red = 0, t_search = 0, t_mark = t_setup;
     uint32_t *Xp = Xa, *Xc = Xb; // X_{k-1}, X_k (X_1 is in Xa)
     int xi = 0;                  // cluster exchange count (parity buffer)
     int mu = 0, lam = 0, off = 0, k_last = 0, dense_from = 0;

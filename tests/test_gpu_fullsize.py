@@ -94,9 +94,8 @@ def run_config(mp, A, n, config):
             mp.set_row_reuse(True)
             mp.set_symmetry(None)
             mp.set_transfer_hint(0)
-    if config in ("nolookahead", "nofoldstats"):  # the benchmarked options, other power loops:
-        # no lookahead / the folds and the statistics as separate passes
-        env = {"nolookahead": {"MP_LOOKAHEAD": "0"}, "nofoldstats": {"MP_FOLD_STATS": "0"}}[config]
+    if config == "nolookahead":  # the benchmarked options, the power loop without lookahead
+        env = {"MP_LOOKAHEAD": "0"}
         os.environ.update(env)
         mp.set_symmetry(mp.word_reversal(n))
         mp.set_transfer_hint(n)
@@ -116,7 +115,7 @@ def run_config(mp, A, n, config):
     raise ValueError(config)
 
 
-@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse", "nolookahead", "nofoldstats"])
+@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse", "nolookahead"])
 @pytest.mark.parametrize("n", SIZES)
 def test_power_records(mp, n, config):
     """Every power's fingerprint and diagonal minimum, (mu, lambda, b) and dense_from equal the
