@@ -58,6 +58,13 @@ std::vector<int32_t> g_sym;
 bool g_word_sym = true;
 bool g_small_off = false; // mp_set_small_path(0): always the general path
 int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be A(D_n)
+// MP_FP_TC=0: the fingerprint on the CUDA cores (k_stats_sym) instead of the tensor cores
+bool fp_tc_on()
+{
+    const char *e = getenv("MP_FP_TC"); // read per run: tests switch it
+    return !(e && *e == '0');
+}
+
 // MP_LOOKAHEAD=0: no lookahead in the large-N power loop (diagnostic)
 bool lookahead_on()
 {
@@ -198,6 +205,8 @@ struct PowerRun {
     std::vector<int32_t> sigma, gcol, loc; // loc[g] = local column of domain column g (cap path)
     DBuf dsig, dgcol, dloc; // dloc[g] = local column of global column g, or -1
     DBuf drw;               // row weights s(2i), then s(2 sigma i) (symmetric statistics)
+    DBuf wfrag, tcs;        // tensor-core fingerprint: column-weight byte fragments, per-power {H, #inf}
+    bool fptc = false;
     int64_t cols_rep = 0;
     const uint16_t *a_src = nullptr; // matrix sources: A (boundary encoding; the caller's buffer or
     int64_t a_ld = 0;                // stage_raw), valid for the duration of the run
@@ -915,6 +924,15 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         }
         COPY(R.stats.p, init.data(), init.size() * 8, cudaMemcpyHostToDevice, s);
     }
+    // the fingerprint on the tensor cores for symmetric runs
+    R.fptc = R.sym && fp_tc_on() && R.w > 0;
+    if (R.fptc) {
+        TRY(R.tcs.ensure(nst * 8, "tensor-core fingerprints"));
+        CUDA_TRY(cudaMemsetAsync(R.tcs.p, 0, nst * 8, s));
+        TRY(R.wfrag.ensure((size_t)(R.ld / 32) * 32 * 16, "fingerprint weight fragments"));
+        LAUNCH(launch_fp_tc_weights(R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.w, R.ld, R.wfrag.as<uint4>(), s));
+    }
+    unsigned long long *tcs = R.fptc ? R.tcs.as<unsigned long long>() : nullptr;
     // Batch of powers between host synchronisations: products of small matrices take
     // microseconds, so up to kBatch of them are enqueued back to back and their statistics
     // read with one copy; powers computed past the first repeat are discarded.  The batch
@@ -992,11 +1010,16 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             CUDA_TRY(cudaEventRecord(prod_done[k], s));
             CUDA_TRY(cudaStreamWaitEvent(s2, prod_done[k], 0));
             CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s2));
-            if (R.sym)
+            if (R.sym) {
+                if (tcs)
+                    LAUNCH(launch_fp_tc(dst, R.ld, N, R.w, R.wfrag.as<uint4>(), R.drw.as<uint64_t>(),
+                                        R.drw.as<uint64_t>() + N, tcs + 2 * k, s2));
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.drw.as<uint64_t>(),
                                         R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
-                                        reinterpret_cast<unsigned long long *>(st_min + 2 * k), s2));
+                                        reinterpret_cast<unsigned long long *>(st_min + 2 * k), s2,
+                                        tcs ? tcs + 2 * k : nullptr));
+            }
             else
                 LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
                                     reinterpret_cast<unsigned long long *>(st_min + 2 * k), s2));
@@ -1082,11 +1105,16 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
                 ++launches;
             }
             if (k >= 2) CUDA_TRY(cudaEventRecord(R.events[2 * (max_k + 1) + k], s)); // stats start
-            if (R.sym)
+            if (R.sym) {
+                if (tcs)
+                    LAUNCH(launch_fp_tc(dst, R.ld, N, R.w, R.wfrag.as<uint4>(), R.drw.as<uint64_t>(),
+                                        R.drw.as<uint64_t>() + N, tcs + 2 * k, s));
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(),
                                         R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
-                                        reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));
+                                        reinterpret_cast<unsigned long long *>(st_min + 2 * k), s,
+                                        tcs ? tcs + 2 * k : nullptr));
+            }
             else
                 LAUNCH(launch_stats(dst, R.ld, N, R.c0, R.w, reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
                                     reinterpret_cast<unsigned long long *>(st_min + 2 * k), s));

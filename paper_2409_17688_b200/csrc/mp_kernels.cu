@@ -1645,9 +1645,43 @@ template <int CT>
 __global__ void __launch_bounds__(kSymThreads)
     k_stats_sym(const uint16_t *__restrict__ X, int64_t ld, int64_t N, const int32_t *__restrict__ gcol,
                 const int32_t *__restrict__ sigma, const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm,
-                int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min)
+                int64_t w, int64_t rpb, unsigned long long *__restrict__ out_sum, unsigned long long *__restrict__ out_min,
+                const unsigned long long *__restrict__ tcs)
 {
     constexpr int V = CT / 8; // uint4 per row and thread
+    if (tcs && tcs[1] == 0) {
+        // The tensor-core pass (k_fp_tc) found no +inf entry and holds the fingerprint: block
+        // (0, 0) adds it and finds the rest directly.  Diagonal: (g, g) for the local columns
+        // (the mirrors (sigma g, sigma g) are equal).  First finite key: every entry is finite,
+        // so it is (0, g_min) -- gcol is ascending -- or among the mirrors (sigma i, sigma g) the
+        // row i = sigma(0) (sigma i = 0) at the column of smallest sigma g.
+        if (blockIdx.x || blockIdx.y) return;
+        __shared__ unsigned long long sk[kSymThreads];
+        __shared__ unsigned sdm[kSymThreads];
+        unsigned dm = 0xFFFFu;
+        unsigned long long best = 0x7FFFFFFFFFFFFFFFull;
+        const int64_t s0 = sigma[0];
+        for (int64_t jj = threadIdx.x; jj < w; jj += blockDim.x) {
+            const int64_t g = gcol[jj], sg = sigma[g];
+            dm = min(dm, (unsigned)X[g * ld + jj]);
+            const unsigned long long key = ((uint64_t)sg << 16) | X[s0 * ld + jj];
+            if (key < best) best = key;
+        }
+        sk[threadIdx.x] = best;
+        sdm[threadIdx.x] = dm;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int t = 1; t < (int)blockDim.x; ++t) {
+                best = min(best, sk[t]);
+                dm = min(dm, sdm[t]);
+            }
+            if (w > 0) best = min(best, (unsigned long long)(((uint64_t)gcol[0] << 16) | X[0]));
+            atomicAdd(out_sum + 0, tcs[0]);
+            atomicMin(out_min + 0, (unsigned long long)dm);
+            atomicMin(out_min + 1, best);
+        }
+        return;
+    }
     unsigned long long h = 0, infc = 0, ref = 0x7FFFFFFFFFFFFFFFull;
     unsigned dmin = 0xFFFFu;
     const int64_t j0 = (int64_t)blockIdx.x * kSymThreads * CT + (int64_t)threadIdx.x * CT;
@@ -1832,7 +1866,7 @@ __global__ void __launch_bounds__(kSymThreads)
 
 cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
                              const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
-                             unsigned long long *out_min, cudaStream_t s)
+                             unsigned long long *out_min, cudaStream_t s, const unsigned long long *tcs)
 {
     static const int ct = [] { // MP_STATS_COLS=8 or 16 columns per thread (A/B knob)
         const char *e = getenv("MP_STATS_COLS");
@@ -1849,10 +1883,10 @@ cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int
     const int64_t rpb = (N + gy - 1) / gy;
     if (ct == 16)
         k_stats_sym<16><<<dim3((unsigned)gx, (unsigned)gy), kSymThreads, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb,
-                                                                                out_sum, out_min);
+                                                                                out_sum, out_min, tcs);
     else
         k_stats_sym<8><<<dim3((unsigned)gx, (unsigned)gy), kSymThreads, 0, s>>>(X, ld, N, gcol, sigma, rw, rwm, w, rpb,
-                                                                               out_sum, out_min);
+                                                                               out_sum, out_min, tcs);
     return cudaGetLastError();
 }
 

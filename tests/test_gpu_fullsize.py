@@ -94,8 +94,9 @@ def run_config(mp, A, n, config):
             mp.set_row_reuse(True)
             mp.set_symmetry(None)
             mp.set_transfer_hint(0)
-    if config == "nolookahead":  # the benchmarked options, the power loop without lookahead
-        env = {"MP_LOOKAHEAD": "0"}
+    if config in ("nolookahead", "nofptc"):  # the benchmarked options, other code paths: no
+        # lookahead power loop / the fingerprint on the CUDA cores instead of the tensor cores
+        env = {"nolookahead": {"MP_LOOKAHEAD": "0"}, "nofptc": {"MP_FP_TC": "0"}}[config]
         os.environ.update(env)
         mp.set_symmetry(mp.word_reversal(n))
         mp.set_transfer_hint(n)
@@ -115,7 +116,7 @@ def run_config(mp, A, n, config):
     raise ValueError(config)
 
 
-@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse", "nolookahead"])
+@pytest.mark.parametrize("config", ["bench", "allcols", "tiles", "noreuse", "nolookahead", "nofptc"])
 @pytest.mark.parametrize("n", SIZES)
 def test_power_records(mp, n, config):
     """Every power's fingerprint and diagonal minimum, (mu, lambda, b) and dense_from equal the
