@@ -12,9 +12,10 @@
 // where X_p B (rows x 32-column chunks of u8 times 32 x 8 byte matrices) is exact in 32 bits:
 // each term is at most 255^2 and a row has fewer than 66052 columns.  The products run as
 // mma.sync m16n8k32 u8 x u8 -> s32 (IMMA on sm_100a): one warp owns 16 rows, walks 32-column
-// chunks, loads its 4 x 4 u16 of X per chunk, maps +inf to 0xFFFF, splits the bytes with PRMT
-// and issues 4 MMAs (2 planes x {b, b'}).  The kernel is bound by reading X once; the issue
-// work per entry is about 0.1 instruction (the CUDA-core k_stats_sym needed about 20).
+// chunks two at a time, loads its 4 x 4 u16 of X per chunk, splits the bytes with PRMT and
+// issues 4 MMAs (2 planes x {b, b'}); about 1.5 instructions per entry (the CUDA-core
+// k_stats_sym needs about 20).  A power with +inf entries (only the first powers of A(D_n)) is
+// flagged and hashed again on the CUDA cores.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -63,62 +64,95 @@ __global__ void k_fp_tc_weights(const int32_t *__restrict__ gcol, const int32_t 
     }
 }
 
-// +inf (0x7FFF) -> 0xFFFF in both halves; counts the +inf halves into *cnt
-__device__ __forceinline__ uint32_t fix_inf(uint32_t v, uint32_t valid, int &cnt)
+// One 32-column chunk: the lane's 4 x 4 u16 of X (rows r0, r1; columns 4 tig .. and + 16),
+// the column weights' B fragments, and the chunk's 4 MMAs.  +inf entries are not remapped: a
+// power holding any (anyinf != 0) is hashed again on the CUDA cores (k_stats_sym), so only
+// their presence matters here.
+struct Chunk {
+    uint2 q00, q10, q01, q11;
+    uint4 wf;
+};
+
+__device__ __forceinline__ void load_chunk(Chunk &h, const uint16_t *x0, const uint16_t *x1, int64_t col,
+                                           const uint4 *wf)
 {
-    const uint32_t m = __vcmpeq2(v, 0x7FFF7FFFu) & valid; // 0xFFFF per +inf half
-    cnt += __popc(m) >> 4;
-    return (v | m) & valid;
+    h.q00 = *reinterpret_cast<const uint2 *>(x0 + col);
+    h.q10 = *reinterpret_cast<const uint2 *>(x1 + col);
+    h.q01 = *reinterpret_cast<const uint2 *>(x0 + col + 16);
+    h.q11 = *reinterpret_cast<const uint2 *>(x1 + col + 16);
+    h.wf = *wf;
 }
 
-// Work item = (16-row tile, column part): the part's chunks [c0, c1).
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void mma_chunk(int (&acc)[4][4], const Chunk &h, uint32_t &anyinf)
+{
+    anyinf |= __vcmpeq2(h.q00.x, 0x7FFF7FFFu) | __vcmpeq2(h.q00.y, 0x7FFF7FFFu) | __vcmpeq2(h.q10.x, 0x7FFF7FFFu) |
+              __vcmpeq2(h.q10.y, 0x7FFF7FFFu) | __vcmpeq2(h.q01.x, 0x7FFF7FFFu) | __vcmpeq2(h.q01.y, 0x7FFF7FFFu) |
+              __vcmpeq2(h.q11.x, 0x7FFF7FFFu) | __vcmpeq2(h.q11.y, 0x7FFF7FFFu);
+    // A fragments: a0 = (row n, cols 4 tig..), a1 = (row n + 8, ..), a2 / a3 = cols + 16
+    const uint32_t lo[4] = {__byte_perm(h.q00.x, h.q00.y, 0x6420), __byte_perm(h.q10.x, h.q10.y, 0x6420),
+                            __byte_perm(h.q01.x, h.q01.y, 0x6420), __byte_perm(h.q11.x, h.q11.y, 0x6420)};
+    const uint32_t hi[4] = {__byte_perm(h.q00.x, h.q00.y, 0x7531), __byte_perm(h.q10.x, h.q10.y, 0x7531),
+                            __byte_perm(h.q01.x, h.q01.y, 0x7531), __byte_perm(h.q11.x, h.q11.y, 0x7531)};
+    imma(acc[0], lo, h.wf.x, h.wf.y);
+    imma(acc[1], lo, h.wf.z, h.wf.w);
+    imma(acc[2], hi, h.wf.x, h.wf.y);
+    imma(acc[3], hi, h.wf.z, h.wf.w);
+}
+
+// Work item = (16-row tile, column part): the part's chunks [c0, c1).  Rows >= N and columns
+// >= w read as 0 (the last tile / chunk); the other chunks go two at a time (the next pair's
+// loads are in flight while the current pair's MMAs issue).
+__global__ void __launch_bounds__(256, 3)
     k_fp_tc(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t w, const uint4 *__restrict__ wfrag,
             const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t ntiles, int64_t nparts,
             int64_t chunks_per_part, int64_t nchunks, unsigned long long *__restrict__ tcs)
 {
     const int lane = threadIdx.x & 31, n = lane >> 2, tig = lane & 3;
     unsigned long long hacc = 0;
-    int infc = 0;
-    const int64_t items = ntiles * nparts;
+    uint32_t anyinf = 0;
+    const int64_t items = ntiles * nparts, nfull = w / 32; // chunks without padding columns
+    __shared__ __align__(16) uint16_t zero_row[32];
+    if (threadIdx.x < 32) zero_row[threadIdx.x] = 0;
+    __syncthreads();
     for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
          it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t tile = it / nparts, part = it - tile * nparts;
         const int64_t r0 = tile * 16 + n, r1 = r0 + 8; // this lane's two rows
         const bool v0 = r0 < N, v1 = r1 < N;
         const int64_t ca = part * chunks_per_part, cb = min(nchunks, ca + chunks_per_part);
+        const int64_t cfull = min(cb, nfull);
         int acc[4][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}}; // {p0 b, p0 b', p1 b, p1 b'}
-        const uint16_t *x0 = X + (v0 ? r0 : 0) * ld, *x1 = X + (v1 ? r1 : 0) * ld;
-        for (int64_t c = ca; c < cb; ++c) {
+        // rows past N read the zero row (shared memory, through generic pointers)
+        const uint16_t *x0 = v0 ? X + r0 * ld : zero_row, *x1 = v1 ? X + r1 * ld : zero_row;
+        const int64_t s0 = v0 ? 1 : 0, s1 = v1 ? 1 : 0; // column stride multiplier (0: the zero row)
+        int64_t c = ca;
+        if (tile * 16 + 16 <= N) { // warp-uniform (mma.sync needs the whole warp)
+            for (; c + 2 <= cfull; c += 2) {
+                Chunk h0, h1;
+                load_chunk(h0, x0, x1, c * 32 + 4 * tig, wfrag + c * 32 + lane);
+                load_chunk(h1, x0, x1, (c + 1) * 32 + 4 * tig, wfrag + (c + 1) * 32 + lane);
+                mma_chunk(acc, h0, anyinf);
+                mma_chunk(acc, h1, anyinf);
+            }
+        }
+        for (; c < cb; ++c) { // the rest: odd chunk, padding columns, rows past N
             const int64_t col = c * 32 + 4 * tig;
-            const uint2 q00 = *reinterpret_cast<const uint2 *>(x0 + col);      // row r0, cols +0..3
-            const uint2 q10 = *reinterpret_cast<const uint2 *>(x1 + col);      // row r1
-            const uint2 q01 = *reinterpret_cast<const uint2 *>(x0 + col + 16); // row r0, cols +16..19
-            const uint2 q11 = *reinterpret_cast<const uint2 *>(x1 + col + 16);
-            const uint4 wf = wfrag[c * 32 + lane];
-            // validity masks per u16 half: rows < N, columns < w
-            auto vm = [&](bool rowok, int64_t c0) -> uint2 {
-                uint32_t m0 = 0, m1 = 0;
-                if (rowok) {
-                    m0 = (c0 < w ? 0xFFFFu : 0u) | (c0 + 1 < w ? 0xFFFF0000u : 0u);
-                    m1 = (c0 + 2 < w ? 0xFFFFu : 0u) | (c0 + 3 < w ? 0xFFFF0000u : 0u);
-                }
-                return make_uint2(m0, m1);
-            };
-            const uint2 m00 = vm(v0, col), m10 = vm(v1, col), m01 = vm(v0, col + 16), m11 = vm(v1, col + 16);
-            const uint32_t y00x = fix_inf(q00.x, m00.x, infc), y00y = fix_inf(q00.y, m00.y, infc);
-            const uint32_t y10x = fix_inf(q10.x, m10.x, infc), y10y = fix_inf(q10.y, m10.y, infc);
-            const uint32_t y01x = fix_inf(q01.x, m01.x, infc), y01y = fix_inf(q01.y, m01.y, infc);
-            const uint32_t y11x = fix_inf(q11.x, m11.x, infc), y11y = fix_inf(q11.y, m11.y, infc);
-            // A fragments: a0 = (row n, cols 4 tig..), a1 = (row n + 8, ..), a2 / a3 = cols + 16
-            const uint32_t lo[4] = {__byte_perm(y00x, y00y, 0x6420), __byte_perm(y10x, y10y, 0x6420),
-                                    __byte_perm(y01x, y01y, 0x6420), __byte_perm(y11x, y11y, 0x6420)};
-            const uint32_t hi[4] = {__byte_perm(y00x, y00y, 0x7531), __byte_perm(y10x, y10y, 0x7531),
-                                    __byte_perm(y01x, y01y, 0x7531), __byte_perm(y11x, y11y, 0x7531)};
-            imma(acc[0], lo, wf.x, wf.y);
-            imma(acc[1], lo, wf.z, wf.w);
-            imma(acc[2], hi, wf.x, wf.y);
-            imma(acc[3], hi, wf.z, wf.w);
+            Chunk h;
+            h.q00 = *reinterpret_cast<const uint2 *>(x0 + col * s0);
+            h.q10 = *reinterpret_cast<const uint2 *>(x1 + col * s1);
+            h.q01 = *reinterpret_cast<const uint2 *>(x0 + (col + 16) * s0);
+            h.q11 = *reinterpret_cast<const uint2 *>(x1 + (col + 16) * s1);
+            h.wf = wfrag[c * 32 + lane];
+            if (c >= nfull) { // padding columns (+inf in X) read as 0
+                auto m = [&](int64_t c0) -> uint2 {
+                    return make_uint2((c0 < w ? 0xFFFFu : 0u) | (c0 + 1 < w ? 0xFFFF0000u : 0u),
+                                      (c0 + 2 < w ? 0xFFFFu : 0u) | (c0 + 3 < w ? 0xFFFF0000u : 0u));
+                };
+                const uint2 ma = m(col), mb = m(col + 16);
+                h.q00.x &= ma.x, h.q00.y &= ma.y, h.q10.x &= ma.x, h.q10.y &= ma.y;
+                h.q01.x &= mb.x, h.q01.y &= mb.y, h.q11.x &= mb.x, h.q11.y &= mb.y;
+            }
+            mma_chunk(acc, h, anyinf);
         }
         // D fragment: d0, d1 = (row n, bytes 2 tig, 2 tig + 1), d2, d3 = (row n + 8, same bytes).
         // u = sum_{p, t} 256^(p + t) D_p[t] over this lane's two bytes, then over the group's
@@ -148,11 +182,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         hacc += __shfl_xor_sync(0xFFFFFFFFu, hacc, o);
-        infc += __shfl_xor_sync(0xFFFFFFFFu, infc, o);
+        anyinf |= __shfl_xor_sync(0xFFFFFFFFu, anyinf, o);
     }
     if (lane == 0) {
         if (hacc) atomicAdd(tcs + 0, hacc);
-        if (infc) atomicAdd(tcs + 1, (unsigned long long)infc);
+        if (anyinf) atomicAdd(tcs + 1, 1ull);
     }
 }
 
@@ -171,12 +205,13 @@ cudaError_t launch_fp_tc(const uint16_t *X, int64_t ld, int64_t N, int64_t w, co
                          const uint64_t *rwm, unsigned long long *tcs, cudaStream_t s)
 {
     const int64_t nchunks = (w + 31) / 32, ntiles = (N + 15) / 16;
-    // about 16 warps per SM: split the columns when there are too few 16-row tiles
-    const int64_t want = 148 * 16;
-    const int64_t nparts = std::max<int64_t>(1, std::min<int64_t>(nchunks, (want + ntiles - 1) / ntiles));
+    // one wave of 3 x 8 resident warps per SM (76 registers): split the columns only when the
+    // 16-row tiles fill less than half of it
+    const int64_t want = 148 * 24;
+    const int64_t nparts = std::max<int64_t>(1, std::min<int64_t>(nchunks, want / ntiles));
     const int64_t cpp = (nchunks + nparts - 1) / nparts;
     const int64_t warps = ntiles * nparts;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 3));
     k_fp_tc<<<grid, 256, 0, s>>>(X, ld, N, w, wfrag, rw, rwm, ntiles, nparts, cpp, nchunks, tcs);
     return cudaGetLastError();
 }

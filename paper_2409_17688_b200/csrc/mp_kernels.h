@@ -146,14 +146,14 @@ cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, c
                                uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s);
 // Statistics of the full matrix from its columns gcol[0..w) under the symmetry sigma.
 // rw / rwm: the row weights of launch_row_weights.
-// tcs (may be null): {fingerprint, raw +inf count} of the tensor-core pass (launch_fp_tc) for this
+// tcs (may be null): {fingerprint, nonzero if the power holds +inf} of the tensor-core pass (launch_fp_tc) for this
 // power; if its +inf count is 0 the kernel adds that fingerprint and finds the diagonal minimum
 // and first finite key directly (one block), else it computes every field itself.
 cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
                              const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
                              unsigned long long *out_min, cudaStream_t s, const unsigned long long *tcs = nullptr);
 // The fingerprint of a power on its w local columns (column jj = gcol[jj], mirrors sigma) by
-// 8-bit integer tensor-core MMAs (mp_fptc.cu), plus the raw count of +inf entries, added into
+// 8-bit integer tensor-core MMAs (mp_fptc.cu), plus a nonzero count if it holds +inf, added into
 // tcs[0], tcs[1] (zeroed by the caller).  wfrag: the column weights' byte fragments from
 // launch_fp_tc_weights (ld / 32 chunks x 32 lanes x uint4).
 cudaError_t launch_fp_tc_weights(const int32_t *gcol, const int32_t *sigma, int64_t w, int64_t ld, uint4 *wfrag,
