@@ -321,7 +321,11 @@ def run_mine(args):
     A = mp.build_transition_matrix(args.n)
     N = A.shape[0]
     nnz = int(np.count_nonzero(A != mp.MP_INF))
-    dA = torch.from_numpy(A.view(np.int16)).cuda()  # resident input for the device-timed value
+    # resident input for the device-timed value; rows padded to 64 columns (128-byte aligned
+    # rows: the library's vectorised range / transfer-hint check reads them 16 bytes per lane)
+    ldA = -(-N // 64) * 64
+    dA = torch.full((N, ldA), -1, dtype=torch.int16, device="cuda")[:, :N]
+    dA.copy_(torch.from_numpy(A.view(np.int16)))
 
     def barrier():
         if world > 1:

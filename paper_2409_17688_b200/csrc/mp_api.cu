@@ -800,10 +800,14 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.a_src = src.dev;
         R.a_ld = src.lda;
         if (src.host) { // staging buffer kept with the workspace (no 2N^2-byte malloc per call)
-            TRY(R.stage_raw.ensure((size_t)N * N * 2, "A staging"));
-            COPY(R.stage_raw.p, src.host, (size_t)N * N * 2, cudaMemcpyHostToDevice, s);
+            // rows padded to 64 columns: 128-byte aligned rows for the vectorised range check
+            const int64_t pitch = round_up(N, 64);
+            TRY(R.stage_raw.ensure((size_t)N * pitch * 2, "A staging"));
+            CUDA_TRY(cudaMemcpy2DAsync(R.stage_raw.p, (size_t)pitch * 2, src.host, (size_t)N * 2, (size_t)N * 2,
+                                       (size_t)N, cudaMemcpyHostToDevice, s));
+            g_h2d.fetch_add((int64_t)N * N * 2);
             R.a_src = R.stage_raw.as<uint16_t>();
-            R.a_ld = N;
+            R.a_ld = pitch;
         }
         const bool need_occ = g_opts.sparsity != 0 && g_opts.sparsity != 2;
         if (need_occ) {
@@ -1013,7 +1017,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             if (R.sym) {
                 if (tcs)
                     LAUNCH(launch_fp_tc(dst, R.ld, N, R.w, R.wfrag.as<uint4>(), R.drw.as<uint64_t>(),
-                                        R.drw.as<uint64_t>() + N, tcs + 2 * k, s2));
+                                        R.drw.as<uint64_t>() + N, tcs + 2 * k, s2, k >= 2 ? tcs + 2 * (k - 1) : nullptr));
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(), R.drw.as<uint64_t>(),
                                         R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),
@@ -1108,7 +1112,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             if (R.sym) {
                 if (tcs)
                     LAUNCH(launch_fp_tc(dst, R.ld, N, R.w, R.wfrag.as<uint4>(), R.drw.as<uint64_t>(),
-                                        R.drw.as<uint64_t>() + N, tcs + 2 * k, s));
+                                        R.drw.as<uint64_t>() + N, tcs + 2 * k, s, k >= 2 ? tcs + 2 * (k - 1) : nullptr));
                 LAUNCH(launch_stats_sym(dst, R.ld, N, R.dgcol.as<int32_t>(), R.dsig.as<int32_t>(),
                                         R.drw.as<uint64_t>(), R.drw.as<uint64_t>() + N, R.w,
                                         reinterpret_cast<unsigned long long *>(st_sum + 2 * k),

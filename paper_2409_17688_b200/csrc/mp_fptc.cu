@@ -15,7 +15,7 @@
 // chunks two at a time, loads its 4 x 4 u16 of X per chunk, splits the bytes with PRMT and
 // issues 4 MMAs (2 planes x {b, b'}); about 1.5 instructions per entry (the CUDA-core
 // k_stats_sym needs about 20).  A power with +inf entries (only the first powers of A(D_n)) is
-// flagged and hashed again on the CUDA cores.
+// flagged: k_stats_sym then scans it for the other statistics, without hashing.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -65,9 +65,9 @@ __global__ void k_fp_tc_weights(const int32_t *__restrict__ gcol, const int32_t 
 }
 
 // One 32-column chunk: the lane's 4 x 4 u16 of X (rows r0, r1; columns 4 tig .. and + 16),
-// the column weights' B fragments, and the chunk's 4 MMAs.  +inf entries are not remapped: a
-// power holding any (anyinf != 0) is hashed again on the CUDA cores (k_stats_sym), so only
-// their presence matters here.
+// the column weights' B fragments, and the chunk's 4 MMAs.  +inf entries become 0xFFFF, and
+// their presence is flagged (k_stats_sym then still scans for the +inf count and the first
+// finite entry).
 struct Chunk {
     uint2 q00, q10, q01, q11;
     uint4 wf;
@@ -83,11 +83,22 @@ __device__ __forceinline__ void load_chunk(Chunk &h, const uint16_t *x0, const u
     h.wf = *wf;
 }
 
-__device__ __forceinline__ void mma_chunk(int (&acc)[4][4], const Chunk &h, uint32_t &anyinf)
+// +inf (0x7FFF) counts as 0xFFFF (FIX): q | (cmp & 0x80008000); without FIX the comparison
+// only flags the chunk
+template <bool FIX>
+__device__ __forceinline__ void fix_inf(uint32_t &q, uint32_t &any)
 {
-    anyinf |= __vcmpeq2(h.q00.x, 0x7FFF7FFFu) | __vcmpeq2(h.q00.y, 0x7FFF7FFFu) | __vcmpeq2(h.q10.x, 0x7FFF7FFFu) |
-              __vcmpeq2(h.q10.y, 0x7FFF7FFFu) | __vcmpeq2(h.q01.x, 0x7FFF7FFFu) | __vcmpeq2(h.q01.y, 0x7FFF7FFFu) |
-              __vcmpeq2(h.q11.x, 0x7FFF7FFFu) | __vcmpeq2(h.q11.y, 0x7FFF7FFFu);
+    const uint32_t c = __vcmpeq2(q, 0x7FFF7FFFu);
+    if (FIX) q |= c & 0x80008000u;
+    any |= c;
+}
+
+template <bool FIX>
+__device__ __forceinline__ void mma_chunk(int (&acc)[4][4], Chunk h, uint32_t &anyinf)
+{
+    fix_inf<FIX>(h.q00.x, anyinf), fix_inf<FIX>(h.q00.y, anyinf), fix_inf<FIX>(h.q10.x, anyinf);
+    fix_inf<FIX>(h.q10.y, anyinf), fix_inf<FIX>(h.q01.x, anyinf), fix_inf<FIX>(h.q01.y, anyinf);
+    fix_inf<FIX>(h.q11.x, anyinf), fix_inf<FIX>(h.q11.y, anyinf);
     // A fragments: a0 = (row n, cols 4 tig..), a1 = (row n + 8, ..), a2 / a3 = cols + 16
     const uint32_t lo[4] = {__byte_perm(h.q00.x, h.q00.y, 0x6420), __byte_perm(h.q10.x, h.q10.y, 0x6420),
                             __byte_perm(h.q01.x, h.q01.y, 0x6420), __byte_perm(h.q11.x, h.q11.y, 0x6420)};
@@ -102,18 +113,17 @@ __device__ __forceinline__ void mma_chunk(int (&acc)[4][4], const Chunk &h, uint
 // Work item = (16-row tile, column part): the part's chunks [c0, c1).  Rows >= N and columns
 // >= w read as 0 (the last tile / chunk); the other chunks go two at a time (the next pair's
 // loads are in flight while the current pair's MMAs issue).
-__global__ void __launch_bounds__(256, 3)
-    k_fp_tc(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t w, const uint4 *__restrict__ wfrag,
-            const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t ntiles, int64_t nparts,
-            int64_t chunks_per_part, int64_t nchunks, unsigned long long *__restrict__ tcs)
+template <bool FIX>
+__device__ __forceinline__ void fp_tc_body(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t w,
+                                           const uint4 *__restrict__ wfrag, const uint64_t *__restrict__ rw,
+                                           const uint64_t *__restrict__ rwm, int64_t ntiles, int64_t nparts,
+                                           int64_t chunks_per_part, int64_t nchunks, unsigned long long *__restrict__ tcs,
+                                           const uint16_t *zero_row)
 {
     const int lane = threadIdx.x & 31, n = lane >> 2, tig = lane & 3;
     unsigned long long hacc = 0;
     uint32_t anyinf = 0;
     const int64_t items = ntiles * nparts, nfull = w / 32; // chunks without padding columns
-    __shared__ __align__(16) uint16_t zero_row[32];
-    if (threadIdx.x < 32) zero_row[threadIdx.x] = 0;
-    __syncthreads();
     for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
          it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t tile = it / nparts, part = it - tile * nparts;
@@ -131,8 +141,8 @@ __global__ void __launch_bounds__(256, 3)
                 Chunk h0, h1;
                 load_chunk(h0, x0, x1, c * 32 + 4 * tig, wfrag + c * 32 + lane);
                 load_chunk(h1, x0, x1, (c + 1) * 32 + 4 * tig, wfrag + (c + 1) * 32 + lane);
-                mma_chunk(acc, h0, anyinf);
-                mma_chunk(acc, h1, anyinf);
+                mma_chunk<FIX>(acc, h0, anyinf);
+                mma_chunk<FIX>(acc, h1, anyinf);
             }
         }
         for (; c < cb; ++c) { // the rest: odd chunk, padding columns, rows past N
@@ -152,7 +162,7 @@ __global__ void __launch_bounds__(256, 3)
                 h.q00.x &= ma.x, h.q00.y &= ma.y, h.q10.x &= ma.x, h.q10.y &= ma.y;
                 h.q01.x &= mb.x, h.q01.y &= mb.y, h.q11.x &= mb.x, h.q11.y &= mb.y;
             }
-            mma_chunk(acc, h, anyinf);
+            mma_chunk<FIX>(acc, h, anyinf);
         }
         // D fragment: d0, d1 = (row n, bytes 2 tig, 2 tig + 1), d2, d3 = (row n + 8, same bytes).
         // u = sum_{p, t} 256^(p + t) D_p[t] over this lane's two bytes, then over the group's
@@ -186,8 +196,30 @@ __global__ void __launch_bounds__(256, 3)
     }
     if (lane == 0) {
         if (hacc) atomicAdd(tcs + 0, hacc);
-        if (anyinf) atomicAdd(tcs + 1, 1ull);
+        // +inf present: count the warp; without the remapping the fingerprint is void (bit 63)
+        if (anyinf) {
+            atomicAdd(tcs + 1, 1ull);
+            if (!FIX) atomicOr(tcs + 1, 1ull << 63); // (the counts never reach bit 63)
+        }
     }
+}
+
+// FIX (the +inf remapping) only where it can matter: the first power, and any power after one
+// that held +inf (prev: the previous power's {H, flags}); a power of A(D_n) after an all-finite
+// one is all-finite.  A power that holds +inf anyway is flagged void (k_stats_sym then hashes it).
+__global__ void __launch_bounds__(256, 3)
+    k_fp_tc(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t w, const uint4 *__restrict__ wfrag,
+            const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t ntiles, int64_t nparts,
+            int64_t chunks_per_part, int64_t nchunks, unsigned long long *__restrict__ tcs,
+            const unsigned long long *__restrict__ prev)
+{
+    __shared__ __align__(16) uint16_t zero_row[32];
+    if (threadIdx.x < 32) zero_row[threadIdx.x] = 0;
+    __syncthreads();
+    if (!prev || prev[1] != 0)
+        fp_tc_body<true>(X, ld, N, w, wfrag, rw, rwm, ntiles, nparts, chunks_per_part, nchunks, tcs, zero_row);
+    else
+        fp_tc_body<false>(X, ld, N, w, wfrag, rw, rwm, ntiles, nparts, chunks_per_part, nchunks, tcs, zero_row);
 }
 
 } // namespace
@@ -202,7 +234,7 @@ cudaError_t launch_fp_tc_weights(const int32_t *gcol, const int32_t *sigma, int6
 }
 
 cudaError_t launch_fp_tc(const uint16_t *X, int64_t ld, int64_t N, int64_t w, const uint4 *wfrag, const uint64_t *rw,
-                         const uint64_t *rwm, unsigned long long *tcs, cudaStream_t s)
+                         const uint64_t *rwm, unsigned long long *tcs, cudaStream_t s, const unsigned long long *prev)
 {
     const int64_t nchunks = (w + 31) / 32, ntiles = (N + 15) / 16;
     // one wave of 3 x 8 resident warps per SM (76 registers): split the columns only when the
@@ -212,7 +244,7 @@ cudaError_t launch_fp_tc(const uint16_t *X, int64_t ld, int64_t N, int64_t w, co
     const int64_t cpp = (nchunks + nparts - 1) / nparts;
     const int64_t warps = ntiles * nparts;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 3));
-    k_fp_tc<<<grid, 256, 0, s>>>(X, ld, N, w, wfrag, rw, rwm, ntiles, nparts, cpp, nchunks, tcs);
+    k_fp_tc<<<grid, 256, 0, s>>>(X, ld, N, w, wfrag, rw, rwm, ntiles, nparts, cpp, nchunks, tcs, prev);
     return cudaGetLastError();
 }
 

@@ -776,23 +776,38 @@ __global__ void k_bits_csr(const uint32_t *__restrict__ bits, int64_t nw, int64_
     }
 }
 
-// bitsT = the transpose of the N x N bit matrix bits (one warp per 32 x 32 block).
-__global__ void k_bits_transpose(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, uint32_t *__restrict__ bitsT)
+// bitsT = the transpose of the N x N bit matrix bits (N rows of nw words).  A block transposes
+// 512 rows x 8 words (256 columns) through shared memory: coalesced 32-byte row segments in,
+// 32 ballots per (32-row block, word), 64-byte segments of bitsT rows out.
+constexpr int kTrRows = 512, kTrWords = 8;
+__global__ void __launch_bounds__(256) k_bits_transpose(const uint32_t *__restrict__ bits, int64_t nw, int64_t N,
+                                                        uint32_t *__restrict__ bitsT)
 {
-    const int lane = threadIdx.x & 31;
-    const int64_t total = nw * nw;
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t bi = t / nw, bk = t - bi * nw; // rows 32bi.., word bk
-        const int64_t i = bi * 32 + lane;
-        const uint32_t w = i < N ? bits[i * nw + bk] : 0u; // lane r: row 32bi + r
-        uint32_t out = 0;                                   // lane b: column 32bk + b over rows
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t m = __ballot_sync(0xFFFFFFFFu, (w >> b) & 1u);
-            if (lane == b) out = m;
+    __shared__ uint32_t in[kTrRows][kTrWords + 1];          // [row][word]
+    __shared__ uint32_t out[kTrWords * 32][kTrRows / 32 + 1]; // [column][32-row block]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * kTrRows, k0 = (int64_t)blockIdx.y * kTrWords;
+    for (int q = threadIdx.x; q < kTrRows * kTrWords; q += blockDim.x) {
+        const int r = q / kTrWords, kk = q % kTrWords;
+        in[r][kk] = (i0 + r < N && k0 + kk < nw) ? bits[(i0 + r) * nw + k0 + kk] : 0u;
+    }
+    __syncthreads();
+    for (int wc = warp; wc < kTrWords; wc += blockDim.x / 32)
+        for (int rb = 0; rb < kTrRows / 32; ++rb) {
+            const uint32_t x = in[rb * 32 + lane][wc]; // lane r: row 32 rb + r
+            uint32_t mine = 0;                        // lane b: column 32 (k0 + wc) + b over the 32 rows
+            for (int bit = 0; bit < 32; ++bit) {
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, (x >> bit) & 1u);
+                if (lane == bit) mine = m;
+            }
+            out[wc * 32 + lane][rb] = mine;
         }
-        const int64_t l = bk * 32 + lane;
-        if (l < N) bitsT[l * nw + bi] = out;
+    __syncthreads();
+    const int64_t b0 = i0 / 32, nb = (N + 31) / 32;
+    for (int q = threadIdx.x; q < kTrWords * 32 * (kTrRows / 32); q += blockDim.x) {
+        const int c = q / (kTrRows / 32), rb = q % (kTrRows / 32);
+        const int64_t l = k0 * 32 + c;
+        if (l < N && b0 + rb < nb) bitsT[l * nw + b0 + rb] = out[c][rb];
     }
 }
 
@@ -1073,26 +1088,74 @@ __device__ int64_t block_compact(int64_t n, FlagF flag, EmitF emit)
     return base_sh;
 }
 
-// Per 32-row tile t: the ordered union U_t of its 4 groups' l.  Count pass (L == nullptr)
-// writes tcnt[t]; fill pass writes L[tptr[t] + rank] = l.
-__global__ void k_tile_union(const uint8_t *__restrict__ m8, int64_t Np, const int64_t *__restrict__ tptr,
-                             int32_t *__restrict__ tcnt, int32_t *__restrict__ L)
+// Per 32-row tile t: the ordered union U_t of its kSpGroups groups' l.  Count pass (L ==
+// nullptr) writes tcnt[t]; fill pass writes L[tptr[t] + rank] = l.  A thread takes 16
+// consecutive l (one 16-byte load per group row of m8; Np is a multiple of 128), a block-wide
+// exclusive scan of the per-thread counts gives the ranks.
+constexpr int kUnThreads = 1024, kUnPer = 16;
+__global__ void __launch_bounds__(kUnThreads) k_tile_union(const uint8_t *__restrict__ m8, int64_t Np,
+                                                          const int64_t *__restrict__ tptr,
+                                                          int32_t *__restrict__ tcnt, int32_t *__restrict__ L)
 {
+    __shared__ int wsum[kUnThreads / 32];
+    __shared__ int64_t base_sh;
     const int64_t t = blockIdx.x;
     const uint8_t *m = m8 + t * kSpGroups * Np;
-    auto flag = [&](int64_t l) {
-        unsigned any = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t *Lt = L ? L + tptr[t] : nullptr;
+    if (threadIdx.x == 0) base_sh = 0;
+    __syncthreads();
+    for (int64_t l0 = 0; l0 < Np; l0 += (int64_t)kUnThreads * kUnPer) {
+        const int64_t l = l0 + (int64_t)threadIdx.x * kUnPer;
+        uint4 any = make_uint4(0, 0, 0, 0);
+        if (l < Np)
 #pragma unroll
-        for (int j = 0; j < kSpGroups; ++j) any |= m[j * Np + l];
-        return any != 0;
-    };
-    if (!L) {
-        const int64_t c = block_compact(Np, flag, [](int64_t, int64_t) {});
-        if (threadIdx.x == 0) tcnt[t] = (int32_t)c;
-        return;
+            for (int j = 0; j < kSpGroups; ++j) {
+                const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(m + j * Np + l));
+                any.x |= v.x, any.y |= v.y, any.z |= v.z, any.w |= v.w;
+            }
+        // bit e: byte e of any is nonzero
+        uint32_t f = 0;
+        const uint32_t wv[4] = {any.x, any.y, any.z, any.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t nz = (((wv[q] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | wv[q]) & 0x80808080u; // 0x80 per nonzero byte
+            f |= ((nz >> 7) & 1u | (nz >> 14) & 2u | (nz >> 21) & 4u | (nz >> 28) & 8u) << (4 * q);
+        }
+        const int c = __popc(f);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const int v = lane < kUnThreads / 32 ? wsum[lane] : 0;
+            int x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane < kUnThreads / 32) wsum[lane] = x - v; // exclusive
+        }
+        __syncthreads();
+        const int64_t base = base_sh;
+        if (Lt) {
+            int64_t r = base + wsum[warp] + incl - c;
+            while (f) {
+                const int e = __ffs(f) - 1;
+                f &= f - 1;
+                Lt[r++] = (int32_t)(l + e);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == kUnThreads - 1) base_sh = base + wsum[warp] + incl;
+        __syncthreads();
     }
-    int32_t *Lt = L + tptr[t];
-    block_compact(Np, flag, [&](int64_t l, int64_t rank) { Lt[rank] = (int32_t)l; });
+    if (!Lt && threadIdx.x == 0) tcnt[t] = (int32_t)base_sh;
 }
 
 // Reorders each tile's union list L_t so that every chunk of kSpChunk l's carries about the
@@ -1650,35 +1713,45 @@ __global__ void __launch_bounds__(kSymThreads)
 {
     constexpr int V = CT / 8; // uint4 per row and thread
     if (tcs && tcs[1] == 0) {
-        // The tensor-core pass (k_fp_tc) found no +inf entry and holds the fingerprint: block
-        // (0, 0) adds it and finds the rest directly.  Diagonal: (g, g) for the local columns
-        // (the mirrors (sigma g, sigma g) are equal).  First finite key: every entry is finite,
-        // so it is (0, g_min) -- gcol is ascending -- or among the mirrors (sigma i, sigma g) the
-        // row i = sigma(0) (sigma i = 0) at the column of smallest sigma g.
-        if (blockIdx.x || blockIdx.y) return;
-        __shared__ unsigned long long sk[kSymThreads];
-        __shared__ unsigned sdm[kSymThreads];
+        // The tensor-core pass (k_fp_tc) found no +inf entry and holds the fingerprint: the
+        // grid finds the rest directly, one column per thread (scattered 2-byte reads, so all
+        // blocks share them).  Diagonal: (g, g) for the local columns (the mirrors (sigma g,
+        // sigma g) are equal).  First finite key: every entry is finite, so it is (0, g_min) --
+        // gcol is ascending -- or among the mirrors (sigma i, sigma g) the row i = sigma(0)
+        // (sigma i = 0) at the column of smallest sigma g.
+        __shared__ unsigned long long sk[kSymThreads / 32];
+        __shared__ unsigned sdm[kSymThreads / 32];
         unsigned dm = 0xFFFFu;
         unsigned long long best = 0x7FFFFFFFFFFFFFFFull;
         const int64_t s0 = sigma[0];
-        for (int64_t jj = threadIdx.x; jj < w; jj += blockDim.x) {
+        const int64_t nthreads = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+        for (int64_t jj = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; jj < w;
+             jj += nthreads) {
             const int64_t g = gcol[jj], sg = sigma[g];
             dm = min(dm, (unsigned)X[g * ld + jj]);
             const unsigned long long key = ((uint64_t)sg << 16) | X[s0 * ld + jj];
             if (key < best) best = key;
         }
-        sk[threadIdx.x] = best;
-        sdm[threadIdx.x] = dm;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            dm = min(dm, __shfl_xor_sync(0xFFFFFFFFu, dm, o));
+            best = min(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            sk[threadIdx.x >> 5] = best;
+            sdm[threadIdx.x >> 5] = dm;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int t = 1; t < (int)blockDim.x; ++t) {
+            for (int t = 1; t < (int)blockDim.x / 32; ++t) {
                 best = min(best, sk[t]);
                 dm = min(dm, sdm[t]);
             }
-            if (w > 0) best = min(best, (unsigned long long)(((uint64_t)gcol[0] << 16) | X[0]));
-            atomicAdd(out_sum + 0, tcs[0]);
-            atomicMin(out_min + 0, (unsigned long long)dm);
-            atomicMin(out_min + 1, best);
+            const bool first = blockIdx.x == 0 && blockIdx.y == 0;
+            if (first && w > 0) best = min(best, (unsigned long long)(((uint64_t)gcol[0] << 16) | X[0]));
+            if (first) atomicAdd(out_sum + 0, tcs[0]);
+            if (dm != 0xFFFFu) atomicMin(out_min + 0, (unsigned long long)dm);
+            if (best != 0x7FFFFFFFFFFFFFFFull) atomicMin(out_min + 1, best);
         }
         return;
     }
@@ -1694,8 +1767,7 @@ __global__ void __launch_bounds__(kSymThreads)
         // so an entry costs one IMAD.WIDE.U32 (64-bit accumulate) and one 32-bit IMAD per sum
         uint32_t blo[CT], bhi[CT], bmlo[CT], bmhi[CT];
         unsigned two = 0; // bit e: column e stands for two global columns
-        int32_t mmin = INT32_MAX, g0 = 0, glast = 0;
-        int emin = 0;
+        int32_t g0 = 0, glast = 0;
 #pragma unroll
         for (int e = 0; e < CT; ++e) {
             const int32_t g = e < nc ? gcol[j0 + e] : 0;
@@ -1709,18 +1781,26 @@ __global__ void __launch_bounds__(kSymThreads)
             bmlo[e] = (uint32_t)bm;
             bmhi[e] = (uint32_t)(bm >> 32);
             if (e < nc && m != g) two |= 1u << e;
-            if (e < nc && m < mmin) {
-                mmin = m;
-                emin = e;
-            }
             if (e == 0) g0 = g;
             if (e == nc - 1) glast = g;
         }
-        // Keys of the all-finite rows: among (i, g_e) the smallest is at the first such row and
-        // e = 0 (gcol ascending); among the mirrors (sigma i, m_e) at the row of smallest
-        // sigma i and e = emin.  Tracked here, folded into ref after the loop.
+        // First finite keys: among (i, g_e) the smallest is at the first row with a finite
+        // entry in these columns, at its first finite e (gcol ascending); among the mirrors
+        // (sigma i, m_e) at the row of smallest sigma i with a finite entry, at its finite e of
+        // smallest m_e.  Tracked here (a new minimum of sigma i is rare), folded into ref after
+        // the loop.
         int64_t fi = INT64_MAX, fsi = INT64_MAX;
         uint32_t fx = 0, fxm = 0;
+        int32_t fg = 0, fm = 0;
+        const uint32_t validm = nc >= 32 ? 0xFFFFFFFFu : (1u << nc) - 1u;
+        const bool hash = tcs == nullptr || (tcs[1] >> 63); // else k_fp_tc holds the fingerprint
+        auto half = [&](const uint32_t (&words)[4 * V], int e) { // x of column e (selects only)
+            uint32_t wd = 0;
+#pragma unroll
+            for (int q = 0; q < 4 * V; ++q)
+                if (q == (e >> 1)) wd = words[q];
+            return (wd >> ((e & 1) * 16)) & 0xFFFFu;
+        };
         auto row = [&](int64_t i, int64_t si, const uint4 (&vv)[V]) {
             uint32_t words[4 * V];
 #pragma unroll
@@ -1730,60 +1810,67 @@ __global__ void __launch_bounds__(kSymThreads)
                 words[4 * q + 2] = vv[q].z;
                 words[4 * q + 3] = vv[q].w;
             }
-            // any half >= 0x7FFF (the device +inf; stored values never exceed it)
-            uint32_t anyinf = 0;
+            // bit e: column e holds the device +inf (stored values never exceed it)
+            uint32_t infm = 0;
 #pragma unroll
-            for (int q = 0; q < 4 * V; ++q) anyinf |= ((words[q] & 0x7FFF7FFFu) + 0x00010001u) | words[q];
-            anyinf &= 0x80008000u;
-            uint64_t rs, rm;
-            if (nc == CT && !anyinf) {
-                uint64_t lo = 0, lom = 0;
-                uint32_t hi = 0, him = 0;
+            for (int q = 0; q < 4 * V; ++q) {
+                const uint32_t m = __vcmpeq2(words[q], 0x7FFF7FFFu);
+                infm |= ((m & 1u) | ((m >> 15) & 2u)) << (2 * q);
+            }
+            infm &= validm;
+            if (hash) {
+                uint64_t rs, rm;
+                if (nc == CT && !infm) {
+                    uint64_t lo = 0, lom = 0;
+                    uint32_t hi = 0, him = 0;
 #pragma unroll
-                for (int e = 0; e < CT; ++e) {
-                    const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                    lo = madw(blo[e], x, lo);
-                    hi += bhi[e] * x;
-                    lom = madw(bmlo[e], x, lom);
-                    him += bmhi[e] * x;
+                    for (int e = 0; e < CT; ++e) {
+                        const uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                        lo = madw(blo[e], x, lo);
+                        hi += bhi[e] * x;
+                        lom = madw(bmlo[e], x, lom);
+                        him += bmhi[e] * x;
+                    }
+                    rs = lo + ((uint64_t)hi << 32);
+                    rm = lom + ((uint64_t)him << 32);
+                } else { // +inf counted as 0xFFFF; columns past nc have zero weights
+                    rs = 0;
+                    rm = 0;
+#pragma unroll
+                    for (int e = 0; e < CT; ++e) {
+                        uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                        if (x == kDevInf) x = kBndInf;
+                        const uint64_t b = ((uint64_t)bhi[e] << 32) | blo[e];
+                        const uint64_t bm = ((uint64_t)bmhi[e] << 32) | bmlo[e];
+                        rs += b * x;
+                        rm += bm * x;
+                    }
                 }
-                rs = lo + ((uint64_t)hi << 32);
-                rm = lom + ((uint64_t)him << 32);
-                if (i < fi) {
+                h += rw[i] * rs + rwm[i] * rm; // row weights s(2i), s(2 sigma i), precomputed
+            }
+            if (infm) infc += __popc(infm) + __popc(infm & two);
+            const uint32_t fin = validm & ~infm;
+            if (fin) {
+                if (i < fi) { // the first such row of this thread (rows ascend)
+                    const int e = __ffs(fin) - 1;
                     fi = i;
-                    fx = words[0] & 0xFFFFu;
+                    fx = half(words, e);
+                    fg = sg[e][threadIdx.x];
                 }
                 if (si < fsi) {
+                    int32_t mb = INT32_MAX;
+                    int eb = 0;
+#pragma unroll
+                    for (int e = 0; e < CT; ++e)
+                        if (((fin >> e) & 1u) && sm_[e][threadIdx.x] < mb) {
+                            mb = sm_[e][threadIdx.x];
+                            eb = e;
+                        }
                     fsi = si;
-                    uint32_t wd = 0;
-#pragma unroll
-                    for (int q = 0; q < 4 * V; ++q)
-                        if (q == (emin >> 1)) wd = words[q]; // selects, no local-memory indexing
-                    fxm = (wd >> ((emin & 1) * 16)) & 0xFFFFu;
-                }
-            } else {
-                rs = 0;
-                rm = 0;
-#pragma unroll
-                for (int e = 0; e < CT; ++e) {
-                    if (e >= nc) break;
-                    uint32_t x = (words[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                    if (x == kDevInf) {
-                        x = kBndInf;
-                        infc += 1 + ((two >> e) & 1u);
-                    } else {
-                        unsigned long long key = ((uint64_t)(i * N + sg[e][threadIdx.x]) << 16) | x;
-                        if (key < ref) ref = key;
-                        key = ((uint64_t)(si * N + sm_[e][threadIdx.x]) << 16) | x;
-                        if (key < ref) ref = key;
-                    }
-                    const uint64_t b = ((uint64_t)bhi[e] << 32) | blo[e];
-                    const uint64_t bm = ((uint64_t)bmhi[e] << 32) | bmlo[e];
-                    rs += b * x;
-                    rm += bm * x;
+                    fm = mb;
+                    fxm = half(words, eb);
                 }
             }
-            h += rw[i] * rs + rwm[i] * rm; // row weights s(2i), s(2 sigma i), precomputed
             if (i >= g0 && i <= glast) { // the diagonal entry (i, i), if this slice holds it
 #pragma unroll
                 for (int e = 0; e < CT; ++e)
@@ -1825,12 +1912,14 @@ __global__ void __launch_bounds__(kSymThreads)
         }
         cp_async_wait<0>();
         if (fi != INT64_MAX) {
-            unsigned long long key = ((uint64_t)(fi * N + g0) << 16) | fx;
+            unsigned long long key = ((uint64_t)(fi * N + fg) << 16) | fx;
             if (key < ref) ref = key;
-            key = ((uint64_t)(fsi * N + mmin) << 16) | fxm;
+            key = ((uint64_t)(fsi * N + fm) << 16) | fxm;
             if (key < ref) ref = key;
         }
     }
+    if (tcs && !(tcs[1] >> 63) && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        h += tcs[0]; // k_fp_tc's fingerprint
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
@@ -2165,7 +2254,8 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
         SP_ALLOC(bitsT, (size_t)N * nw * 4);
         SP_ALLOC(coff, (size_t)(N + 1) * 8);
         SP_ALLOC(cidx, (size_t)std::max<int64_t>(nnz, 1) * 4);
-        SP_LAUNCH((k_bits_transpose<<<grid_for(nw * nw * 32, 256), 256, 0, s>>>(bits, nw, N, bitsT)));
+        SP_LAUNCH((k_bits_transpose<<<dim3((unsigned)((N + kTrRows - 1) / kTrRows), (unsigned)((nw + kTrWords - 1) / kTrWords)),
+                                       256, 0, s>>>(bits, nw, N, bitsT)));
         SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, cnt)));
         SP_SCAN(cnt, N, coff);
         const int64_t nwin = (N + kGrpWin - 1) / kGrpWin;
@@ -2440,11 +2530,128 @@ __global__ void __launch_bounds__(256)
     if (notxfer) *xfer_flag = 1;
 }
 
+// The transfer-hint check (A = A(D_n) entry by entry) with the range check and the
+// support bitsets (and the tile occupancy if occ), for 16-byte aligned rows (lda % 8 == 0) and
+// no symmetry check (the bench path).  Block (x, y): the 512-column tile x, rows y, y + gridDim.y, ... (warp per
+// row, two rows in flight).  A lane owns columns 8 lane + 256 u + e (u < 2, e < 8) of the tile
+// and keeps their masks in registers as column pairs (two 16-bit masks per 32-bit word), so the
+// can-follow rule (mp_internal.h) runs on two columns per instruction:
+//   fail = (q.t & ~p.z) | (p.t & ~exactly_one) | (p.o & ~at_least_two),
+//   exactly_one = (U ^ q.z) & ~(B & q.z), at_least_two = B | (U & q.z),
+// U = up ^ dn, B = up & dn of p's zero neighbours, q.z and q.t duplicated in both halves.
+constexpr int kXfCols = 512;
+__global__ void __launch_bounds__(128)
+    k_check_xfer(const uint16_t *__restrict__ A, int64_t lda, int64_t N, const WordMask *__restrict__ words,
+                 unsigned full, uint32_t *__restrict__ bits, int64_t nw, uint8_t *__restrict__ occ, int64_t Kt,
+                 int *__restrict__ range_flag, int *__restrict__ xfer_flag)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * kXfCols;
+    // column-pair masks: pair j = 4 u + k holds columns 8 lane + 256 u + 2k, + 1
+    uint32_t pz[8], pu[8], pb[8], pt[8], po[8], pl[8], vm[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        uint32_t h[7][2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int64_t c = c0 + 8 * lane + 256 * (j / 4) + 2 * (j % 4) + hh;
+            WordMask p = {0, 0, 0, 0};
+            const bool ok = c < N;
+            if (ok) p = words[c];
+            const unsigned up = ((unsigned)p.z << 1) & full, dn = (unsigned)p.z >> 1;
+            h[0][hh] = p.z;
+            h[1][hh] = up ^ dn;
+            h[2][hh] = up & dn;
+            h[3][hh] = p.t;
+            h[4][hh] = p.o;
+            h[5][hh] = p.zeros;
+            h[6][hh] = ok ? 0xFFFFu : 0u;
+        }
+        pz[j] = h[0][0] | h[0][1] << 16;
+        pu[j] = h[1][0] | h[1][1] << 16;
+        pb[j] = h[2][0] | h[2][1] << 16;
+        pt[j] = h[3][0] | h[3][1] << 16;
+        po[j] = h[4][0] | h[4][1] << 16;
+        pl[j] = h[5][0] | h[5][1] << 16;
+        vm[j] = h[6][0] | h[6][1] << 16;
+    }
+    uint32_t notx = 0, bad = 0;
+    const int64_t stride = (int64_t)gridDim.y * nwarps;
+    auto load = [&](int64_t i, uint4 (&x)[2]) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t c = c0 + 8 * lane + 256 * u;
+            x[u] = (i < N && c < lda) ? __ldcs(reinterpret_cast<const uint4 *>(A + i * lda + c)) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    auto check = [&](int64_t i, const uint4 (&x)[2]) {
+        const WordMask q = words[i];
+        const uint32_t qz = (uint32_t)q.z | (uint32_t)q.z << 16, qt = (uint32_t)q.t | (uint32_t)q.t << 16;
+        uint32_t m8[2] = {0, 0};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint4 &xv = x[j / 4];
+            const uint32_t xx = (j % 4 == 0) ? xv.x : (j % 4 == 1) ? xv.y : (j % 4 == 2) ? xv.z : xv.w;
+            const uint32_t ex1 = (pu[j] ^ qz) & ~(pb[j] & qz);
+            const uint32_t at2 = pb[j] | (pu[j] & qz);
+            const uint32_t f = (qt & ~pz[j]) | (pt[j] & ~ex1) | (po[j] & ~at2);
+            const uint32_t M = __vcmpeq2(f, 0u);         // 0xFFFF: p can follow q
+            const uint32_t expect = ~M | pl[j];          // label zeros(p), else 0xFFFF (+inf)
+            const uint32_t d = (expect ^ xx) & vm[j];
+            if (d) { // not A(D_n); a value in (0x7FFE, 0xFFFF) is a range error first
+                notx = 1;
+                bad |= __vcmpgtu2(xx, 0x7FFE7FFEu) & ~__vcmpeq2(xx, 0xFFFFFFFFu) & vm[j];
+            }
+            const uint32_t fin = M & vm[j];
+            m8[j / 4] |= ((fin & 1u) | ((fin >> 15) & 2u)) << (2 * (j % 4));
+        }
+        // support bitsets: 4 lanes x 8 bits per 32-column word
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            uint32_t v = m8[u];
+            v |= __shfl_down_sync(0xFFFFFFFFu, v, 1) << 8;
+            v |= __shfl_down_sync(0xFFFFFFFFu, v, 2) << 16;
+            const int64_t k = (c0 + 256 * u + 8 * lane) / 32;
+            if ((lane & 3) == 0 && k < nw) {
+                bits[i * nw + k] = v;
+                if (occ && v && k < Kt) {
+                    uint8_t *o = occ + (i / kBM) * Kt + k;
+                    if (!*o) *o = 1;
+                }
+            }
+        }
+    };
+    int64_t i = (int64_t)blockIdx.y * nwarps + warp;
+    for (; i + stride < N; i += 2 * stride) {
+        uint4 xa[2], xb[2];
+        load(i, xa);
+        load(i + stride, xb);
+        check(i, xa);
+        check(i + stride, xb);
+    }
+    if (i < N) {
+        uint4 xa[2];
+        load(i, xa);
+        check(i, xa);
+    }
+    if (bad) *range_flag = 1;
+    if (notx) *xfer_flag = 1;
+}
+
 cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np, uint8_t *occ, int *range_flag,
                            const int32_t *sigma, int *sym_flag, uint32_t *bits, cudaStream_t s, const WordMask *words,
                            int n, int *xfer_flag)
 {
     static_assert(kBK == 32, "occupancy tiles are the 32-column words");
+    if (words && !sigma && bits && lda % 8 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 && n <= 16) {
+        const int64_t gx = std::max<int64_t>(1, (N + kXfCols - 1) / kXfCols);
+        // one wave: 104 registers -> 4 blocks of 4 warps per SM
+        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, (int64_t)num_sms() * 4 / gx));
+        k_check_xfer<<<dim3((unsigned)gx, (unsigned)gy), 128, 0, s>>>(A, lda, N, words, (1u << n) - 1u, bits,
+                                                                     (N + 31) / 32, occ, Np / kBK, range_flag,
+                                                                     xfer_flag);
+        return cudaGetLastError();
+    }
     const int64_t Kt = Np / kBK;
     const int64_t gx = std::max<int64_t>(1, (N + kChkCols - 1) / kChkCols);
     const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, ((int64_t)num_sms() * 8 + gx - 1) / gx));

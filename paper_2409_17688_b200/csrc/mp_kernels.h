@@ -146,20 +146,23 @@ cudaError_t launch_encode_cols(const uint16_t *src, int64_t lds, int64_t rows, c
                                uint16_t *dst, int64_t ldd, int64_t rows_p, cudaStream_t s);
 // Statistics of the full matrix from its columns gcol[0..w) under the symmetry sigma.
 // rw / rwm: the row weights of launch_row_weights.
-// tcs (may be null): {fingerprint, nonzero if the power holds +inf} of the tensor-core pass (launch_fp_tc) for this
-// power; if its +inf count is 0 the kernel adds that fingerprint and finds the diagonal minimum
-// and first finite key directly (one block), else it computes every field itself.
+// tcs (may be null): {fingerprint, nonzero if the power holds +inf} of the tensor-core pass
+// (launch_fp_tc) for this power; the kernel adds that fingerprint instead of hashing, and
+// without +inf finds the diagonal minimum and first finite key directly (one column per
+// thread), else it scans the power for them and the +inf count.
 cudaError_t launch_stats_sym(const uint16_t *X, int64_t ld, int64_t N, const int32_t *gcol, const int32_t *sigma,
                              const uint64_t *rw, const uint64_t *rwm, int64_t w, unsigned long long *out_sum,
                              unsigned long long *out_min, cudaStream_t s, const unsigned long long *tcs = nullptr);
 // The fingerprint of a power on its w local columns (column jj = gcol[jj], mirrors sigma) by
 // 8-bit integer tensor-core MMAs (mp_fptc.cu), plus a nonzero count if it holds +inf, added into
-// tcs[0], tcs[1] (zeroed by the caller).  wfrag: the column weights' byte fragments from
-// launch_fp_tc_weights (ld / 32 chunks x 32 lanes x uint4).
+// tcs[0], tcs[1] (zeroed by the caller).  prev: the previous power's tcs (null for the first
+// power): +inf is remapped to 0xFFFF only if prev is null or held +inf; otherwise a power with
+// +inf gets bit 63 of tcs[1] (fingerprint void).  wfrag: the column weights' byte fragments
+// from launch_fp_tc_weights (ld / 32 chunks x 32 lanes x uint4).
 cudaError_t launch_fp_tc_weights(const int32_t *gcol, const int32_t *sigma, int64_t w, int64_t ld, uint4 *wfrag,
                                  cudaStream_t s);
 cudaError_t launch_fp_tc(const uint16_t *X, int64_t ld, int64_t N, int64_t w, const uint4 *wfrag, const uint64_t *rw,
-                         const uint64_t *rwm, unsigned long long *tcs, cudaStream_t s);
+                         const uint64_t *rwm, unsigned long long *tcs, cudaStream_t s, const unsigned long long *prev);
 // rw[i] = s(2i), rwm[i] = s(2 sigma i) for i < N.
 cudaError_t launch_row_weights(int64_t N, const int32_t *sigma, uint64_t *rw, uint64_t *rwm, cudaStream_t s);
 // Range check of a row-major A (flag set if an entry lies in (0x7FFE, 0xFFFF)) and, if occ is

@@ -550,3 +550,72 @@ def test_n13_record(mp):
     f = r.formula()
     for m in range(r.mu, r.mu + 200):
         assert r.gamma2(m) == -(-f["b"] * m // f["a"]) + f["alpha"][m % f["a"]]
+
+
+@pytest.mark.parametrize("pitch", ["host", "dense", "padded"])
+@pytest.mark.parametrize("n", [7, 9])
+def test_transfer_check_layouts(mp, oracle_mod, n, pitch):
+    """The range / transfer-hint check of A on both of its kernels: the vectorised one (rows
+    16-byte aligned: host sources are staged with a padded pitch, and a padded device tensor)
+    and the general one (a device tensor with lda = N).  A(D_n) passes with the oracle's record;
+    a changed label, a dropped arc and an added arc are MP_ERR_DOMAIN; a value in (0x7FFE,
+    0xFFFF) is MP_ERR_RANGE."""
+    import torch
+    A = mp.build_transition_matrix(n)
+    N = A.shape[0]
+    o = oracle_mod.power_until_periodic(A)
+    fin = np.argwhere(A != INF)
+    inf = np.argwhere(A == INF)
+    cases = []
+    for (i, j), v in [(fin[len(fin) // 2], None), (fin[-1], INF), (inf[len(inf) // 3], 3), (fin[1], 0x8000)]:
+        B = A.copy()
+        B[i, j] = (int(A[i, j]) + 1) if v is None else v
+        cases.append((B, "MP_ERR_RANGE" if v == 0x8000 else "MP_ERR_DOMAIN"))
+
+    def run(M):
+        if pitch == "host":
+            return mp.minplus_power_until_periodic(M)
+        ld = N if pitch == "dense" else -(-N // 64) * 64
+        d = torch.full((N, ld), -1, dtype=torch.int16, device="cuda")[:, :N]
+        d.copy_(torch.from_numpy(M.view(np.int16)))
+        return mp.minplus_power_until_periodic_device(d)
+
+    mp.set_transfer_hint(n)
+    mp.set_symmetry(mp.word_reversal(n))
+    try:
+        g = run(A)
+        for B, name in cases:
+            with pytest.raises(mp.MinplusError) as e:
+                run(B)
+            assert e.value.name == name
+    finally:
+        mp.set_symmetry(None)
+        mp.set_transfer_hint(0)
+    assert (g.mu, g.lam, g.offset) == (o.mu, o.lam, o.offset)
+    assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
+
+
+@pytest.mark.parametrize("kernel", ["tiles", "spmm"])
+def test_fingerprint_saturating_powers(mp, oracle_mod, kernel):
+    """Every power after the first is all-finite here until the sums saturate (G6): A^3 is
+    all-finite, A^4 onwards hold +inf.  The tensor-core fingerprint remaps +inf only after a
+    power that held +inf, so at A^4 it flags itself void and the statistics kernel hashes that
+    power on the CUDA cores: every fingerprint still equals the oracle's."""
+    rng = np.random.default_rng(77)
+    N = 300
+    A = rng.integers(0x2000, 0x2C00, size=(N, N)).astype(np.uint16)
+    A[rng.random((N, N)) < 0.002] = INF  # a few +inf in A^1 (remapped: the first power)
+    use_kernel(mp, kernel)
+    mp.set_symmetry(np.arange(N, dtype=np.int32))  # the identity: every column computed, symmetric path
+    try:
+        g = mp.minplus_power_until_periodic(A, max_k=16)
+    finally:
+        mp.set_symmetry(None)
+        reset_kernel(mp)
+    o = oracle_mod.power_until_periodic(A, max_k=16)
+    assert o.rc == 0
+    P2 = oracle_mod.minplus(A, A)
+    P3 = oracle_mod.minplus(A, P2)
+    assert (P3 != INF).all() and (oracle_mod.minplus(A, P3) == INF).any()
+    assert (g.mu, g.lam, g.offset, g.k_last, g.dense_from) == (o.mu, o.lam, o.offset, o.k_last, o.dense_from)
+    assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
