@@ -95,20 +95,23 @@ bool trace_on()
     return on == 1;
 }
 
+// MP_TRACE=1: stream-synchronised phase times on stderr (each mark: time since the previous
+// mark of any tracer on this thread, and since this tracer's creation)
+thread_local std::chrono::steady_clock::time_point t_trace_last = std::chrono::steady_clock::now();
 struct Tracer {
     cudaStream_t s;
-    std::chrono::steady_clock::time_point t0, t;
-    explicit Tracer(cudaStream_t st) : s(st), t0(std::chrono::steady_clock::now()), t(t0) {}
+    std::chrono::steady_clock::time_point t0;
+    explicit Tracer(cudaStream_t st) : s(st), t0(std::chrono::steady_clock::now()) {}
     void mark(const char *what, int k = -1)
     {
         if (!trace_on()) return;
         cudaStreamSynchronize(s);
         const auto now = std::chrono::steady_clock::now();
-        const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+        const double ms = std::chrono::duration<double, std::milli>(now - t_trace_last).count();
         const double tot = std::chrono::duration<double, std::milli>(now - t0).count();
         if (k >= 0) fprintf(stderr, "mp-trace %-26s k=%-3d %10.3f ms  (%10.3f ms)\n", what, k, ms, tot);
         else fprintf(stderr, "mp-trace %-32s %10.3f ms  (%10.3f ms)\n", what, ms, tot);
-        t = now;
+        t_trace_last = now;
     }
 };
 
@@ -205,6 +208,7 @@ struct PowerRun {
     std::vector<int32_t> sigma, gcol, loc; // loc[g] = local column of domain column g (cap path)
     DBuf dsig, dgcol, dloc; // dloc[g] = local column of global column g, or -1
     DBuf drw;               // row weights s(2i), then s(2 sigma i) (symmetric statistics)
+    int words_n = 0;        // words holds the word masks of D_(words_n) (0: none)
     DBuf wfrag, tcs;        // tensor-core fingerprint: column-weight byte fragments, per-power {H, #inf}
     bool fptc = false;
     int64_t cols_rep = 0;
@@ -423,6 +427,19 @@ cudaError_t sp_alloc(void **p, size_t bytes, void *ctx)
     return cudaSuccess;
 }
 
+// The word masks of D_n on the device (kept across runs of the same n)
+mp_status stage_words(PowerRun &R, int n, cudaStream_t s)
+{
+    if (R.words_n == n && R.words.p) return MP_OK;
+    const std::vector<WordMask> words = enumerate_words(n);
+    R.words_n = 0;
+    TRY(R.words.ensure(words.size() * sizeof(WordMask), "word masks"));
+    COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
+    CUDA_TRY(cudaStreamSynchronize(s)); // the host vector goes out of scope
+    R.words_n = n;
+    return MP_OK;
+}
+
 mp_status build_sparse(PowerRun &R, cudaStream_t s)
 {
     R.sp_next = 0;
@@ -435,6 +452,7 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
     if (R.dag_n && group) { // row-inclusion reuse: parents and levels
         R.rdag = RowDag();
         e = build_row_dag(R.words.as<WordMask>(), R.N, R.dag_n, R.rdag, s, sp_alloc, &R, &launches);
+        if (trace_on()) Tracer(s).mark("  row DAG (since a2)");
         dag = &R.rdag;
     } else {
         R.dag_n = 0;
@@ -445,6 +463,7 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
                                         &launches, dag)
                     : build_sparse_form_words(R.words.as<WordMask>(), R.N, R.n_words, R.Np, group, R.sp, s, sp_alloc,
                                               &R, &launches, dag);
+    if (trace_on()) Tracer(s).mark("  sparse form");
     g_launches.fetch_add(launches);
     g_d2h.fetch_add(24);
     if (e == cudaErrorMemoryAllocation) return MP_ERR_RESOURCE; // message set by DBuf::alloc
@@ -793,9 +812,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     TRY(R.flag.ensure(16, "range flag"));
     const int64_t Mt = R.Np / kBM, Kt = R.Np / kBK;
     if (words_src) {
-        std::vector<WordMask> words = enumerate_words(src.n);
-        TRY(R.words.ensure(words.size() * sizeof(WordMask), "word masks"));
-        COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
+        TRY(stage_words(R, src.n, s));
     } else {
         R.a_src = src.dev;
         R.a_ld = src.lda;
@@ -809,7 +826,11 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
             R.a_src = R.stage_raw.as<uint16_t>();
             R.a_ld = pitch;
         }
-        const bool need_occ = g_opts.sparsity != 0 && g_opts.sparsity != 2;
+        // a transfer-matrix hint (mp_set_transfer_hint) brings the word masks along, verified below
+        const bool hint = g_transfer_n >= 2 && count_words(g_transfer_n) == N;
+        // the tile occupancy only feeds the tile kernels' choice: A(D_n) (a verified hint) takes
+        // the grouped SpMM directly, as the words source does
+        const bool need_occ = g_opts.sparsity != 0 && g_opts.sparsity != 2 && !hint;
         if (need_occ) {
             TRY(R.occ.ensure((size_t)(Mt * Kt), "tile occupancy"));
             CUDA_TRY(cudaMemsetAsync(R.occ.p, 0, (size_t)(Mt * Kt), s));
@@ -818,13 +839,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         R.bits_ok = (g_opts.sparsity == 2 || g_opts.sparsity < 0) &&
                     (g_opts.grouping == 1 || (g_opts.grouping < 0 && N >= kGroupMinN));
         if (R.bits_ok) TRY(R.bits.ensure((size_t)N * ((N + 31) / 32) * 4, "support bitsets"));
-        // a transfer-matrix hint (mp_set_transfer_hint) brings the word masks along, verified below
-        const bool hint = g_transfer_n >= 2 && count_words(g_transfer_n) == N;
-        if (hint) {
-            std::vector<WordMask> words = enumerate_words(g_transfer_n);
-            TRY(R.words.ensure(words.size() * sizeof(WordMask), "word masks"));
-            COPY(R.words.p, words.data(), words.size() * sizeof(WordMask), cudaMemcpyHostToDevice, s);
-        }
+        if (hint) TRY(stage_words(R, g_transfer_n, s));
         CUDA_TRY(cudaMemsetAsync(R.flag.p, 0, 3 * sizeof(int), s));
         // A verified equal to A(D_n) is reflection-symmetric (DESIGN.md section 4 "Symmetry"):
         // a symmetry hint that IS the word reversal then needs no separate check
@@ -840,6 +855,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
         if (hflag[1]) return fail(MP_ERR_DOMAIN, "symmetry hint: A[sigma i][sigma j] != A[i][j] for some i, j");
         if (hflag[2]) return fail(MP_ERR_DOMAIN, "transfer hint: A is not A(D_%d)", g_transfer_n);
         if (hint) R.n_words = g_transfer_n; // the rows' word structure is now known
+        tr.mark("a2 check A");
     }
     // row-inclusion reuse needs the word structure and the grouped SpMM
     R.dag_n = (g_row_reuse && R.n_words && (g_opts.sparsity == 2 || g_opts.sparsity < 0)) ? R.n_words : 0;
@@ -850,7 +866,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // kernel choice: dense tiles, block-sparse tiles, grouped SpMM
     R.sparse = R.spmm = false;
     R.has_at2 = false;
-    if (g_opts.sparsity == 2 || (g_opts.sparsity < 0 && words_src)) {
+    if (g_opts.sparsity == 2 || (g_opts.sparsity < 0 && (words_src || R.n_words))) {
         TRY(build_sparse(R, s));
         R.spmm = true;
         R.issued_per_product = R.issued_spmm;

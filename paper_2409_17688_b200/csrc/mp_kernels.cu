@@ -2,6 +2,7 @@
 // with its roofline; the citations name the paper passage each one implements.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -2178,6 +2179,22 @@ cudaError_t launch_spmm(const SparseA &sa, const SpmmPlan &P, const uint16_t *X,
     return cudaSuccess;
 }
 
+// MP_TRACE=1: stream-synchronised step times of the sparse-form builder on stderr
+static void sp_trace(cudaStream_t s, const char *what)
+{
+    static const bool on = [] {
+        const char *e = getenv("MP_TRACE");
+        return e && *e && *e != '0';
+    }();
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "mp-trace     sparse: %-22s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 // Builds the grouped sparse form (all device work; two host reads of totals).
 template <class Acc>
 cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, const uint32_t *pre_bits, SparseWork &w,
@@ -2186,6 +2203,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
 {
     const int64_t G = Np / kG, Mt = Np / kSpRows;
     cudaError_t e;
+    sp_trace(s, "start");
 #define SP_LAUNCH(x)                                                                                                    \
     do {                                                                                                                \
         x;                                                                                                              \
@@ -2237,6 +2255,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
             ++*launches;
             bits = ebits;
         }
+        sp_trace(s, "extra bits");
         w.bits = bits;
         SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, cnt)));
         SP_SCAN(cnt, N, off);
@@ -2247,6 +2266,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
         SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bits, nw, N, off, idx, nullptr, 0)));
         w.off = off;
         w.idx = idx;
+        sp_trace(s, "row lists");
         // column lists: the transposed bits through the same two kernels (bits is reused)
         uint32_t *bitsT = nullptr;
         int64_t *coff = nullptr;
@@ -2262,11 +2282,13 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
         int32_t *cwst = nullptr;
         SP_ALLOC(cwst, (size_t)N * nwin * 4);
         SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, coff, cidx, cwst, nwin)));
+        sp_trace(s, "column lists");
         const int smem_g = (int)(nw * 4);
         if ((e = cudaFuncSetAttribute(k_tile_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g)) != cudaSuccess)
             return e;
         SP_LAUNCH((k_tile_greedy<<<(unsigned)((N + kGrpWin - 1) / kGrpWin), kGrpWin, smem_g, s>>>(
             off, idx, coff, cidx, cwst, nwin, nw, N, w.rows)));
+        sp_trace(s, "greedy");
         // pass 3: shared memory = max(G + P + R staging, R + Um); tile unions up to 12288 l
         // (n = 12: consecutive tiles reach 9600 at most, greedy tiles fewer)
         const int64_t uw_max = 384;
@@ -2280,6 +2302,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
         }
         if (Np > N) SP_LAUNCH((k_iota_rows<<<grid_for(Np - N, 256), 256, 0, s>>>(w.rows, N, Np)));
         AT2.rows = w.rows;
+        sp_trace(s, "refine");
     }
     SP_ALLOC(w.m8, (size_t)(G * Np));
     SP_ALLOC(w.tcnt, (size_t)Mt * 4);
@@ -2295,12 +2318,14 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     SP_SCAN(w.tcnt, Mt, w.tptr);
     SP_LAUNCH((k_chunk_counts<<<grid_for(Mt, 256), 256, 0, s>>>(w.tcnt, Mt, w.nch)));
     SP_SCAN(w.nch, Mt, w.tch);
+    sp_trace(s, "masks+unions");
     int64_t tot[2] = {0, 0};
     if ((e = cudaMemcpyAsync(&tot[0], w.tptr + Mt, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(&tot[1], w.tch + Mt, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     w.total_union = tot[0];
     w.total_chunks = tot[1];
+    sp_trace(s, "totals read");
     const int64_t TC = std::max<int64_t>(tot[1], 1);
     SP_ALLOC(w.L, (size_t)std::max<int64_t>(tot[0], 1) * 4);
     SP_ALLOC(w.chunk_tile, (size_t)TC * 4);
@@ -2315,6 +2340,7 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     }
 #endif
     SP_LAUNCH((k_chunk_tiles<<<grid_for(Mt, 256), 256, 0, s>>>(w.tch, Mt, w.chunk_tile)));
+    sp_trace(s, "union lists");
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], w.ecnt, nullptr, nullptr, 0u)));
     SP_SCAN(w.ecnt, tot[1] * kSpGroups, w.eoff);
@@ -2322,11 +2348,13 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
     if ((e = cudaMemcpyAsync(&ne, w.eoff + tot[1] * kSpGroups, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     w.entries = ne;
+    sp_trace(s, "entry counts");
     SP_ALLOC(w.E, (size_t)std::max<int64_t>(ne, 1) * kEntBytes);
     w.group_rows = kG;
     SP_LAUNCH((k_chunk_entries<<<grid_for(tot[1] * kSpGroups, 256), 256, 0, s>>>(
         w.m8, AT2, Np, w.L, w.tptr, w.tch, w.chunk_tile, tot[1], nullptr, w.eoff, w.E, 0u)));
     if (dag) w.off = nullptr, w.idx = nullptr; // row lists of the extra entries only: not A's
+    sp_trace(s, "entries");
 #undef SP_SCAN
 #undef SP_LAUNCH
 #undef SP_ALLOC
