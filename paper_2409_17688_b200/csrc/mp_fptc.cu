@@ -110,6 +110,55 @@ __device__ __forceinline__ void mma_chunk(int (&acc)[4][4], Chunk h, uint32_t &a
     imma(acc[3], hi, h.wf.z, h.wf.w);
 }
 
+// D fragment: d0, d1 = (row n, bytes 2 tig, 2 tig + 1), d2, d3 = (row n + 8, same bytes).
+// u = sum_{p, t} 256^(p + t) D_p[t] over this lane's two bytes, then over the group's four
+// lanes (all eight bytes): sums of 32-bit values as unsigned, mod 2^64; times the row weights.
+__device__ __forceinline__ void tile_hash(const int (&acc)[4][4], int tig, int64_t r0, int64_t r1, bool v0, bool v1,
+                                          const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm,
+                                          unsigned long long &hacc)
+{
+    uint64_t u[2] = {0, 0}, um[2] = {0, 0};
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int t = 2 * tig + e;
+            const int d = 2 * rr + e;
+            u[rr] += ((uint64_t)(uint32_t)acc[0][d] << (8 * t)) + ((uint64_t)(uint32_t)acc[2][d] << (8 * t + 8));
+            um[rr] += ((uint64_t)(uint32_t)acc[1][d] << (8 * t)) + ((uint64_t)(uint32_t)acc[3][d] << (8 * t + 8));
+        }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            u[rr] += __shfl_xor_sync(0xFFFFFFFFu, u[rr], o);
+            um[rr] += __shfl_xor_sync(0xFFFFFFFFu, um[rr], o);
+        }
+    if (tig == 0) {
+        if (v0) hacc += rw[r0] * u[0] + rwm[r0] * um[0];
+        if (v1) hacc += rw[r1] * u[1] + rwm[r1] * um[1];
+    }
+}
+
+// The warp's fingerprint part and +inf flag into tcs: +inf present counts the warp; without the
+// remapping (FIX) the fingerprint is void (bit 63; the counts never reach it)
+template <bool FIX>
+__device__ __forceinline__ void warp_flush(unsigned long long hacc, uint32_t anyinf, unsigned long long *tcs)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        hacc += __shfl_xor_sync(0xFFFFFFFFu, hacc, o);
+        anyinf |= __shfl_xor_sync(0xFFFFFFFFu, anyinf, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (hacc) atomicAdd(tcs + 0, hacc);
+        if (anyinf) {
+            atomicAdd(tcs + 1, 1ull);
+            if (!FIX) atomicOr(tcs + 1, 1ull << 63);
+        }
+    }
+}
+
 // Work item = (16-row tile, column part): the part's chunks [c0, c1).  Rows >= N and columns
 // >= w read as 0 (the last tile / chunk); the other chunks go two at a time (the next pair's
 // loads are in flight while the current pair's MMAs issue).
@@ -164,44 +213,9 @@ __device__ __forceinline__ void fp_tc_body(const uint16_t *__restrict__ X, int64
             }
             mma_chunk<FIX>(acc, h, anyinf);
         }
-        // D fragment: d0, d1 = (row n, bytes 2 tig, 2 tig + 1), d2, d3 = (row n + 8, same bytes).
-        // u = sum_{p, t} 256^(p + t) D_p[t] over this lane's two bytes, then over the group's
-        // four lanes (all eight bytes): sums of 32-bit values as unsigned, mod 2^64.
-        uint64_t u[2] = {0, 0}, um[2] = {0, 0};
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int t = 2 * tig + e;
-                const int d = 2 * rr + e;
-                u[rr] += ((uint64_t)(uint32_t)acc[0][d] << (8 * t)) + ((uint64_t)(uint32_t)acc[2][d] << (8 * t + 8));
-                um[rr] += ((uint64_t)(uint32_t)acc[1][d] << (8 * t)) + ((uint64_t)(uint32_t)acc[3][d] << (8 * t + 8));
-            }
-#pragma unroll
-        for (int o = 1; o < 4; o <<= 1)
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                u[rr] += __shfl_xor_sync(0xFFFFFFFFu, u[rr], o);
-                um[rr] += __shfl_xor_sync(0xFFFFFFFFu, um[rr], o);
-            }
-        if (tig == 0) {
-            if (v0) hacc += rw[r0] * u[0] + rwm[r0] * um[0];
-            if (v1) hacc += rw[r1] * u[1] + rwm[r1] * um[1];
-        }
+        tile_hash(acc, tig, r0, r1, v0, v1, rw, rwm, hacc);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        hacc += __shfl_xor_sync(0xFFFFFFFFu, hacc, o);
-        anyinf |= __shfl_xor_sync(0xFFFFFFFFu, anyinf, o);
-    }
-    if (lane == 0) {
-        if (hacc) atomicAdd(tcs + 0, hacc);
-        // +inf present: count the warp; without the remapping the fingerprint is void (bit 63)
-        if (anyinf) {
-            atomicAdd(tcs + 1, 1ull);
-            if (!FIX) atomicOr(tcs + 1, 1ull << 63); // (the counts never reach bit 63)
-        }
-    }
+    warp_flush<FIX>(hacc, anyinf, tcs);
 }
 
 // FIX (the +inf remapping) only where it can matter: the first power, and any power after one
