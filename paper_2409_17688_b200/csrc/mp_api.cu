@@ -65,11 +65,16 @@ bool fp_tc_on()
     return !(e && *e == '0');
 }
 
-// MP_LOOKAHEAD=0: no lookahead in the large-N power loop (diagnostic)
+// MP_LOOKAHEAD=0: no lookahead in the large-N power loop (diagnostic); =2: lookahead at every N
 bool lookahead_on()
 {
     const char *e = getenv("MP_LOOKAHEAD"); // read per run: tests switch it
     return !(e && *e == '0');
+}
+bool lookahead_forced()
+{
+    const char *e = getenv("MP_LOOKAHEAD");
+    return e && *e == '2';
 }
 
 bool g_row_reuse = true;   // mp_set_row_reuse: row-inclusion reuse for A(D_n)
@@ -987,7 +992,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     // (measured: n = 10 10.7 -> 9.8 ms, n = 11 36.4 -> 33.3 ms; at n = 12 the statistics slow the
     // memory-bound product they overlap by more than the hidden round trip: 177.6 vs 179.6 ms)
     const bool lookahead = B == 1 && !cap && !g_dist.fn && !g_obs.fn && max_k >= 2 && R.ring.size() >= 3 &&
-                           N < kLookaheadMaxN && lookahead_on();
+                           (N < kLookaheadMaxN || lookahead_forced()) && lookahead_on();
     if (lookahead) {
         cudaStream_t s2 = st->stream2;
         if (!s2) {
