@@ -2567,7 +2567,12 @@ __global__ void __launch_bounds__(256)
 //   fail = (q.t & ~p.z) | (p.t & ~exactly_one) | (p.o & ~at_least_two),
 //   exactly_one = (U ^ q.z) & ~(B & q.z), at_least_two = B | (U & q.z),
 // U = up ^ dn, B = up & dn of p's zero neighbours, q.z and q.t duplicated in both halves.
-constexpr int kXfCols = 512;
+#ifndef MP_XF_U
+#define MP_XF_U 1
+#endif
+constexpr int kXfU = MP_XF_U;          // 256-column slices per lane
+constexpr int kXfCols = 256 * kXfU;    // columns per block
+constexpr int kXfP = 4 * kXfU;         // column pairs per lane
 __global__ void __launch_bounds__(128)
     k_check_xfer(const uint16_t *__restrict__ A, int64_t lda, int64_t N, const WordMask *__restrict__ words,
                  unsigned full, uint32_t *__restrict__ bits, int64_t nw, uint8_t *__restrict__ occ, int64_t Kt,
@@ -2576,9 +2581,9 @@ __global__ void __launch_bounds__(128)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int64_t c0 = (int64_t)blockIdx.x * kXfCols;
     // column-pair masks: pair j = 4 u + k holds columns 8 lane + 256 u + 2k, + 1
-    uint32_t pz[8], pu[8], pb[8], pt[8], po[8], pl[8], vm[8];
+    uint32_t pz[kXfP], pu[kXfP], pb[kXfP], pt[kXfP], po[kXfP], pl[kXfP], vm[kXfP];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < kXfP; ++j) {
         uint32_t h[7][2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -2605,37 +2610,45 @@ __global__ void __launch_bounds__(128)
     }
     uint32_t notx = 0, bad = 0;
     const int64_t stride = (int64_t)gridDim.y * nwarps;
-    auto load = [&](int64_t i, uint4 (&x)[2]) {
+    auto load = [&](int64_t i, uint4 (&x)[kXfU]) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kXfU; ++u) {
             const int64_t c = c0 + 8 * lane + 256 * u;
             x[u] = (i < N && c < lda) ? __ldcs(reinterpret_cast<const uint4 *>(A + i * lda + c)) : make_uint4(0, 0, 0, 0);
         }
     };
-    auto check = [&](int64_t i, const uint4 (&x)[2]) {
+    auto check = [&](int64_t i, const uint4 (&x)[kXfU]) {
         const WordMask q = words[i];
         const uint32_t qz = (uint32_t)q.z | (uint32_t)q.z << 16, qt = (uint32_t)q.t | (uint32_t)q.t << 16;
-        uint32_t m8[2] = {0, 0};
+        uint32_t m8[kXfU] = {}, err = 0;
+        // bit 15 / 31: the low / high half of v is nonzero ((v & 0x7FFF) + 0x7FFF carries into
+        // bit 15 unless it is 0; no carry crosses the halves)
+        auto nz2 = [](uint32_t v) { return (((v & 0x7FFF7FFFu) + 0x7FFF7FFFu) | v) & 0x80008000u; };
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < kXfP; ++j) {
             const uint4 &xv = x[j / 4];
             const uint32_t xx = (j % 4 == 0) ? xv.x : (j % 4 == 1) ? xv.y : (j % 4 == 2) ? xv.z : xv.w;
             const uint32_t ex1 = (pu[j] ^ qz) & ~(pb[j] & qz);
             const uint32_t at2 = pb[j] | (pu[j] & qz);
-            const uint32_t f = (qt & ~pz[j]) | (pt[j] & ~ex1) | (po[j] & ~at2);
-            const uint32_t M = __vcmpeq2(f, 0u);         // 0xFFFF: p can follow q
-            const uint32_t expect = ~M | pl[j];          // label zeros(p), else 0xFFFF (+inf)
-            const uint32_t d = (expect ^ xx) & vm[j];
-            if (d) { // not A(D_n); a value in (0x7FFE, 0xFFFF) is a range error first
-                notx = 1;
+            const uint32_t F = nz2((qt & ~pz[j]) | (pt[j] & ~ex1) | (po[j] & ~at2)); // p cannot follow q
+            const uint32_t FIN = nz2(~xx);                                            // x finite
+            const uint32_t D = nz2(xx ^ pl[j]);                                       // x != zeros(p)
+            // A(D_n): finite exactly where p can follow q, and there equal to the label
+            err |= (~(FIN ^ F) | (FIN & D)) & vm[j] & 0x80008000u;
+            m8[j / 4] |= (((FIN & vm[j]) >> 15) & 1u | ((FIN & vm[j]) >> 30) & 2u) << (2 * (j % 4));
+        }
+        if (err) { // not A(D_n); a value in (0x7FFE, 0xFFFF) is a range error first
+            notx = 1;
+#pragma unroll
+            for (int j = 0; j < kXfP; ++j) {
+                const uint4 &xv = x[j / 4];
+                const uint32_t xx = (j % 4 == 0) ? xv.x : (j % 4 == 1) ? xv.y : (j % 4 == 2) ? xv.z : xv.w;
                 bad |= __vcmpgtu2(xx, 0x7FFE7FFEu) & ~__vcmpeq2(xx, 0xFFFFFFFFu) & vm[j];
             }
-            const uint32_t fin = M & vm[j];
-            m8[j / 4] |= ((fin & 1u) | ((fin >> 15) & 2u)) << (2 * (j % 4));
         }
         // support bitsets: 4 lanes x 8 bits per 32-column word
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kXfU; ++u) {
             uint32_t v = m8[u];
             v |= __shfl_down_sync(0xFFFFFFFFu, v, 1) << 8;
             v |= __shfl_down_sync(0xFFFFFFFFu, v, 2) << 16;
@@ -2651,14 +2664,14 @@ __global__ void __launch_bounds__(128)
     };
     int64_t i = (int64_t)blockIdx.y * nwarps + warp;
     for (; i + stride < N; i += 2 * stride) {
-        uint4 xa[2], xb[2];
+        uint4 xa[kXfU], xb[kXfU];
         load(i, xa);
         load(i + stride, xb);
         check(i, xa);
         check(i + stride, xb);
     }
     if (i < N) {
-        uint4 xa[2];
+        uint4 xa[kXfU];
         load(i, xa);
         check(i, xa);
     }
@@ -2673,8 +2686,8 @@ cudaError_t launch_check_a(const uint16_t *A, int64_t lda, int64_t N, int64_t Np
     static_assert(kBK == 32, "occupancy tiles are the 32-column words");
     if (words && !sigma && bits && lda % 8 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 && n <= 16) {
         const int64_t gx = std::max<int64_t>(1, (N + kXfCols - 1) / kXfCols);
-        // one wave: 104 registers -> 4 blocks of 4 warps per SM
-        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, (int64_t)num_sms() * 4 / gx));
+        // about one wave: 69 registers -> 7 blocks of 4 warps per SM
+        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, (int64_t)num_sms() * 7 / gx));
         k_check_xfer<<<dim3((unsigned)gx, (unsigned)gy), 128, 0, s>>>(A, lda, N, words, (1u << n) - 1u, bits,
                                                                      (N + 31) / 32, occ, Np / kBK, range_flag,
                                                                      xfer_flag);
