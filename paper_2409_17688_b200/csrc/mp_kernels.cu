@@ -779,7 +779,8 @@ __global__ void k_bits_csr(const uint32_t *__restrict__ bits, int64_t nw, int64_
 
 // bitsT = the transpose of the N x N bit matrix bits (N rows of nw words).  A block transposes
 // 512 rows x 8 words (256 columns) through shared memory: coalesced 32-byte row segments in,
-// 32 ballots per (32-row block, word), 64-byte segments of bitsT rows out.
+// an in-register 32 x 32 bit transpose per (32-row block, word), 64-byte segments of bitsT
+// rows out.
 constexpr int kTrRows = 512, kTrWords = 8;
 __global__ void __launch_bounds__(256) k_bits_transpose(const uint32_t *__restrict__ bits, int64_t nw, int64_t N,
                                                         uint32_t *__restrict__ bitsT)
@@ -795,13 +796,18 @@ __global__ void __launch_bounds__(256) k_bits_transpose(const uint32_t *__restri
     __syncthreads();
     for (int wc = warp; wc < kTrWords; wc += blockDim.x / 32)
         for (int rb = 0; rb < kTrRows / 32; ++rb) {
-            const uint32_t x = in[rb * 32 + lane][wc]; // lane r: row 32 rb + r
-            uint32_t mine = 0;                        // lane b: column 32 (k0 + wc) + b over the 32 rows
-            for (int bit = 0; bit < 32; ++bit) {
-                const uint32_t m = __ballot_sync(0xFFFFFFFFu, (x >> bit) & 1u);
-                if (lane == bit) mine = m;
+            // lane r: row 32 rb + r; after the 32 x 32 bit transpose (five block-swap stages:
+            // the off-diagonal j x j blocks of every 2j x 2j block change places), lane b holds
+            // column 32 (k0 + wc) + b over the 32 rows
+            uint32_t x = in[rb * 32 + lane][wc];
+#pragma unroll
+            for (int j = 16; j >= 1; j >>= 1) {
+                const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                                                      : j == 2 ? 0x33333333u : 0x55555555u;
+                const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+                x = (lane & j) ? (x & ~m) | ((y >> j) & m) : (x & m) | ((y << j) & ~m);
             }
-            out[wc * 32 + lane][rb] = mine;
+            out[wc * 32 + lane][rb] = x;
         }
     __syncthreads();
     const int64_t b0 = i0 / 32, nb = (N + 31) / 32;
