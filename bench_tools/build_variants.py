@@ -1,5 +1,5 @@
 """Builds libminplus.so variants with -D overrides into bench_tools/variants/<name>.so
-(for gpu_variants.sh).  Usage: build_variants.py name=-DA=1,-DB=2 ..."""
+(for bench_tools/r2/gpu_ab.sh).  Usage: build_variants.py name=-DA=1,-DB=2 ..."""
 import os
 import subprocess
 import sys
