@@ -9,7 +9,7 @@ h = rows[0]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
 agg = {}
 for r in rows[1:]:
-    name = r[ki].split("(")[0].split("<")[0].replace("void ", "")
+    name = r[ki].replace("<unnamed>::", "").replace("void ", "").split("(")[0].split("<")[0]
     v = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1e-6)
     a = agg.setdefault(name, [0.0, 0])
     a[0] += v
