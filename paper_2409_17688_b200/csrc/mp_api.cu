@@ -55,6 +55,7 @@ constexpr int64_t kGroupMinN = 8192; // below this the grouping pass costs more 
 // Symmetry hint for matrix sources (mp_set_symmetry) and the word-reversal switch for the
 // words source.
 std::vector<int32_t> g_sym;
+uint64_t g_sym_version = 1; // bumped by every mp_set_symmetry (device copies keyed by it)
 bool g_word_sym = true;
 bool g_small_off = false; // mp_set_small_path(0): always the general path
 int g_transfer_n = 0;      // mp_set_transfer_hint: matrix sources claimed to be A(D_n)
@@ -243,7 +244,9 @@ struct PowerRun {
     size_t hstats_n = 0;
     std::vector<cudaEvent_t> events_la;    // lookahead: product done / statistics done, join
     cudaEvent_t small_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    std::vector<long long> small_host; // the result's host copy
+    long long *small_host = nullptr;   // the result's host copy (pinned)
+    size_t small_host_n = 0;
+    uint64_t small_sig_version = 0;    // g_sym_version of the symmetry hint in small_sig
     uint16_t *full_host = nullptr;
     size_t full_host_bytes = 0;
     ~PowerRun()
@@ -256,6 +259,7 @@ struct PowerRun {
         for (auto ev : events_la)
             if (ev) cudaEventDestroy(ev);
         if (hstats) cudaFreeHost(hstats);
+        if (small_host) cudaFreeHost(small_host);
     }
     size_t slot_bytes() const { return (size_t)Np * ld * 2; }
 };
@@ -645,16 +649,26 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     const uint64_t S = mp_fingerprint_unit(N);
     const int32_t *dsig = nullptr;
     if ((src.dev || src.host) && (int64_t)g_sym.size() == N) { // a matrix source's symmetry hint
-        TRY(R.small_sig.ensure((size_t)N * 4, "symmetry"));
-        COPY(R.small_sig.p, g_sym.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s);
+        if (R.small_sig_version != g_sym_version || R.small_sig.bytes < (size_t)N * 4) { // copied once per hint
+            R.small_sig_version = 0;
+            TRY(R.small_sig.ensure((size_t)N * 4, "symmetry"));
+            COPY(R.small_sig.p, g_sym.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s);
+            R.small_sig_version = g_sym_version;
+        }
         dsig = R.small_sig.as<int32_t>();
     }
     CUDA_TRY(cudaEventRecord(ev[1], s));
     LAUNCH(launch_small_run(dA, lda, N, max_k, kSmallMaxNnz, dsig, R.small_hist.as<uint16_t>(), S,
                             R.small_out.as<long long>(), s));
     CUDA_TRY(cudaEventRecord(ev[2], s));
-    if (R.small_host.size() < nout) R.small_host.assign(nout, 0);
-    long long *h = R.small_host.data();
+    if (R.small_host_n < nout) {
+        if (R.small_host) cudaFreeHost(R.small_host);
+        R.small_host = nullptr;
+        R.small_host_n = 0;
+        CUDA_TRY(cudaMallocHost((void **)&R.small_host, nout * 8));
+        R.small_host_n = nout;
+    }
+    long long *h = R.small_host;
     COPY(h, R.small_out.p, nout * 8, cudaMemcpyDeviceToHost, s);
     CUDA_TRY(cudaEventRecord(ev[3], s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1684,12 +1698,14 @@ mp_status mp_set_symmetry(const int32_t *sigma, int64_t N)
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!sigma || N <= 0) {
         g_sym.clear();
+        ++g_sym_version;
         return MP_OK;
     }
     for (int64_t i = 0; i < N; ++i)
         if (sigma[i] < 0 || sigma[i] >= N || sigma[sigma[i]] != i)
             return fail(MP_ERR_DOMAIN, "mp_set_symmetry: sigma is not an involution of [0, %lld)", (long long)N);
     g_sym.assign(sigma, sigma + N);
+    ++g_sym_version;
     return MP_OK;
 }
 

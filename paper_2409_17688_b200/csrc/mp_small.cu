@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mp_internal.h"
 #include "mp_kernels.h"
@@ -433,7 +434,9 @@ cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_
     cfg.gridDim = dim3((unsigned)(C * R));
     // 4 to 16 warps: one row per warp where the rows allow
     const int64_t rows_per = (N + R - 1) / R;
-    const int warps = (int)std::max<int64_t>(4, std::min<int64_t>(kSmWarps, rows_per)); // a row per warp if possible
+    int warps = (int)std::max<int64_t>(4, std::min<int64_t>(kSmWarps, rows_per)); // a row per warp if possible
+    if (const char *e = getenv("MP_SMALL_WARPS")) // experiments: a fixed warp count (1 .. 16)
+        warps = std::max(1, std::min(kSmWarps, atoi(e)));
     cfg.blockDim = dim3((unsigned)(32 * warps));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
