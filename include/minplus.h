@@ -349,7 +349,9 @@ mp_status mp_last_profile(mp_profile *out);
 
 /* Stream for the power runs on the current device (a cudaStream_t, e.g. torch's current
  * stream, so that caller-side CUDA events bracket a run); NULL restores the library's own
- * non-blocking stream.  Errors: MP_ERR_CUDA if no device. */
+ * non-blocking stream, so the legacy default stream is passed as cudaStreamLegacy ((void *)1;
+ * the Python binding maps torch's default stream, handle 0, to it).  Errors: MP_ERR_CUDA if
+ * no device. */
 mp_status mp_set_stream(void *stream);
 
 /* Tuning knobs (process-wide; defaults in DESIGN.md).  sparsity selects the product kernel

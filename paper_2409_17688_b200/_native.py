@@ -260,9 +260,8 @@ class PeriodicResult:
 
 
 def _result(r: _PeriodicResult) -> PeriodicResult:
-    return PeriodicResult(r.mu, r.lambda_, r.offset, r.k_last, r.dense_from,
-                          [int(r.diag_min[k]) for k in range(r.k_last + 1)],
-                          [int(r.fingerprint[k]) for k in range(r.k_last + 1)], r)
+    k = r.k_last + 1
+    return PeriodicResult(r.mu, r.lambda_, r.offset, r.k_last, r.dense_from, r.diag_min[:k], r.fingerprint[:k], r)
 
 
 def minplus_power_until_periodic(A, max_k: int = 64) -> PeriodicResult:
@@ -284,12 +283,16 @@ def minplus_power_until_periodic_device(dA, max_k: int = 64) -> PeriodicResult:
     r = _PeriodicResult()
     # the run is enqueued on the library stream of this device: unless that is torch's current
     # stream (set_stream), wait for whatever torch still has in flight on dA
-    cur = torch.cuda.current_stream(dA.device)
-    if _lib_stream.get(dA.device.index) != cur.cuda_stream:
+    dev = dA.device.index
+    cur = torch.cuda.current_stream(dev)
+    if _lib_stream.get(dev) != cur.cuda_stream:
         cur.synchronize()
-    with torch.cuda.device(dA.device):
-        _check(lib.minplus_power_until_periodic_device(dA.data_ptr(), dA.stride(0), dA.shape[0],
-                                                       max_k, ctypes.byref(r)))
+    args = (dA.data_ptr(), dA.stride(0), dA.shape[0], max_k, ctypes.byref(r))
+    if torch.cuda.current_device() == dev:  # (the device switch costs microseconds at small n)
+        _check(lib.minplus_power_until_periodic_device(*args))
+    else:
+        with torch.cuda.device(dev):
+            _check(lib.minplus_power_until_periodic_device(*args))
     return _result(r)
 
 
@@ -300,8 +303,14 @@ def set_stream(stream) -> None:
     """Run power sequences on `stream` (torch.cuda.Stream or None for the library's own),
     on the current device."""
     import torch
-    _check(lib.mp_set_stream(None if stream is None else stream.cuda_stream))
-    _lib_stream[torch.cuda.current_device()] = None if stream is None else stream.cuda_stream
+    handle = None if stream is None else stream.cuda_stream
+    # torch's default stream is the legacy default stream (handle 0), which the ABI takes as
+    # cudaStreamLegacy: NULL would mean "the library's own stream"
+    _check(lib.mp_set_stream(None if handle is None else (handle or _CUDA_STREAM_LEGACY)))
+    _lib_stream[torch.cuda.current_device()] = handle
+
+
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
 
 
 def minplus_power_rows(A, rows, kmax: int) -> np.ndarray:

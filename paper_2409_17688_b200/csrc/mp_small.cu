@@ -56,14 +56,18 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
 // 0xFFFFFFFF and back).
 __device__ __forceinline__ void reduce_stats(Stats &s, int width)
 {
-    uint32_t inf = (uint32_t)s.inf, dmin = (uint32_t)s.dmin;
-    uint32_t ref = s.ref == 0x7FFFFFFFFFFFFFFFll ? 0xFFFFFFFFu : (uint32_t)s.ref;
-    for (int m = width >> 1; m; m >>= 1) {
-        s.fp += shfl_xor_u64(s.fp, m);
-        inf += __shfl_xor_sync(0xFFFFFFFFu, inf, m);
-        dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, m));
-        ref = min(ref, __shfl_xor_sync(0xFFFFFFFFu, ref, m));
-    }
+    // whole-warp reductions (redux.sync); lanes outside `width` hold the identity, so the
+    // result is the same.  The 64-bit sum in 16/16/32-bit limbs: at most 32 terms, no limb sum
+    // overflows except the top one, which is taken mod 2^32 as the sum is mod 2^64.
+    (void)width;
+    const uint32_t inf = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)s.inf);
+    const uint32_t dmin = __reduce_min_sync(0xFFFFFFFFu, (uint32_t)s.dmin);
+    const uint32_t ref =
+        __reduce_min_sync(0xFFFFFFFFu, s.ref == 0x7FFFFFFFFFFFFFFFll ? 0xFFFFFFFFu : (uint32_t)s.ref);
+    const uint32_t l0 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(s.fp & 0xFFFFu));
+    const uint32_t l1 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)((s.fp >> 16) & 0xFFFFu));
+    const uint32_t hi = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(s.fp >> 32));
+    s.fp = ((unsigned long long)hi << 32) + ((unsigned long long)l1 << 16) + (unsigned long long)l0;
     s.inf = inf;
     s.dmin = dmin;
     s.ref = ref == 0xFFFFFFFFu ? 0x7FFFFFFFFFFFFFFFll : (long long)ref;
