@@ -28,6 +28,14 @@ namespace mp {
 
 namespace {
 
+#ifndef MP_FPTC_CHUNKS
+#define MP_FPTC_CHUNKS 2
+#endif
+#ifndef MP_FPTC_MINB
+#define MP_FPTC_MINB 3
+#endif
+constexpr int kFpChunks = MP_FPTC_CHUNKS; // 32-column chunks in flight per warp
+
 __device__ __forceinline__ void imma(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
 {
     asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -186,12 +194,13 @@ __device__ __forceinline__ void fp_tc_body(const uint16_t *__restrict__ X, int64
         const int64_t s0 = v0 ? 1 : 0, s1 = v1 ? 1 : 0; // column stride multiplier (0: the zero row)
         int64_t c = ca;
         if (tile * 16 + 16 <= N) { // warp-uniform (mma.sync needs the whole warp)
-            for (; c + 2 <= cfull; c += 2) {
-                Chunk h0, h1;
-                load_chunk(h0, x0, x1, c * 32 + 4 * tig, wfrag + c * 32 + lane);
-                load_chunk(h1, x0, x1, (c + 1) * 32 + 4 * tig, wfrag + (c + 1) * 32 + lane);
-                mma_chunk<FIX>(acc, h0, anyinf);
-                mma_chunk<FIX>(acc, h1, anyinf);
+            for (; c + kFpChunks <= cfull; c += kFpChunks) {
+                Chunk h[kFpChunks];
+#pragma unroll
+                for (int q = 0; q < kFpChunks; ++q)
+                    load_chunk(h[q], x0, x1, (c + q) * 32 + 4 * tig, wfrag + (c + q) * 32 + lane);
+#pragma unroll
+                for (int q = 0; q < kFpChunks; ++q) mma_chunk<FIX>(acc, h[q], anyinf);
             }
         }
         for (; c < cb; ++c) { // the rest: odd chunk, padding columns, rows past N
@@ -221,7 +230,7 @@ __device__ __forceinline__ void fp_tc_body(const uint16_t *__restrict__ X, int64
 // FIX (the +inf remapping) only where it can matter: the first power, and any power after one
 // that held +inf (prev: the previous power's {H, flags}); a power of A(D_n) after an all-finite
 // one is all-finite.  A power that holds +inf anyway is flagged void (k_stats_sym then hashes it).
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, MP_FPTC_MINB)
     k_fp_tc(const uint16_t *__restrict__ X, int64_t ld, int64_t N, int64_t w, const uint4 *__restrict__ wfrag,
             const uint64_t *__restrict__ rw, const uint64_t *__restrict__ rwm, int64_t ntiles, int64_t nparts,
             int64_t chunks_per_part, int64_t nchunks, unsigned long long *__restrict__ tcs,
@@ -251,13 +260,13 @@ cudaError_t launch_fp_tc(const uint16_t *X, int64_t ld, int64_t N, int64_t w, co
                          const uint64_t *rwm, unsigned long long *tcs, cudaStream_t s, const unsigned long long *prev)
 {
     const int64_t nchunks = (w + 31) / 32, ntiles = (N + 15) / 16;
-    // one wave of 3 x 8 resident warps per SM (76 registers): split the columns only when the
+    // one wave of MP_FPTC_MINB x 8 resident warps per SM: split the columns only when the
     // 16-row tiles fill less than half of it
-    const int64_t want = 148 * 24;
+    const int64_t want = 148 * 8 * MP_FPTC_MINB;
     const int64_t nparts = std::max<int64_t>(1, std::min<int64_t>(nchunks, want / ntiles));
     const int64_t cpp = (nchunks + nparts - 1) / nparts;
     const int64_t warps = ntiles * nparts;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 3));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * MP_FPTC_MINB));
     k_fp_tc<<<grid, 256, 0, s>>>(X, ld, N, w, wfrag, rw, rwm, ntiles, nparts, cpp, nchunks, tcs, prev);
     return cudaGetLastError();
 }
