@@ -1661,9 +1661,10 @@ void mp_shutdown(void)
 
 const char *mp_version(void)
 {
-    return "minplus-b200 0.3 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse, 4-stage "
+    return "minplus-b200 0.4 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse, 4-stage "
            "cp.async) and warp-specialised grouped SpMM (4-row groups, greedy row grouping, bulk copies + mbarrier "
-           "ring); column symmetry";
+           "ring); column symmetry; row-inclusion reuse (SpMM on the extra entries + fold passes); u8 IMMA "
+           "fingerprint; one-cluster small-N kernel";
 }
 
 int64_t mp_kernel_launches(void) { return g_launches.load(); }
