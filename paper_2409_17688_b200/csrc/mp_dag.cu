@@ -213,6 +213,10 @@ __global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows,
 constexpr int kWaveSeg = 256;
 constexpr int kWaveRows = 4;
 constexpr int kWaveThreads = 256;
+#ifndef MP_WAVE_MINB
+#define MP_WAVE_MINB 3
+#endif
+constexpr int kWaveMinBlocks = MP_WAVE_MINB;
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p)
 {
@@ -238,44 +242,51 @@ __global__ void k_fold_rec(const int32_t *__restrict__ lrows, int64_t N, const i
     }
 }
 
-__global__ void __launch_bounds__(kWaveThreads) k_fold_wave(const int4 *__restrict__ pairs,
-                                                            const int64_t *__restrict__ item0, int npairs,
-                                                            int64_t items, const int64_t *__restrict__ lptr,
-                                                            const int4 *__restrict__ frec,
-                                                            const int32_t *__restrict__ pidx, uint16_t *C, int64_t ldc,
-                                                            unsigned *cnt)
+__device__ __forceinline__ unsigned ld_volatile(const unsigned *p)
+{
+    return *reinterpret_cast<const volatile unsigned *>(p);
+}
+
+// flush_every: completions are published (one fence, then one atomic per pending pair) after
+// this many items, or before any wait -- a warp never waits while it holds unpublished items.
+__global__ void __launch_bounds__(kWaveThreads, kWaveMinBlocks)
+    k_fold_wave(const int4 *__restrict__ pairs, const int64_t *__restrict__ item0, int npairs, int64_t items,
+                const int64_t *__restrict__ lptr, const int4 *__restrict__ frec, const int32_t *__restrict__ pidx,
+                uint16_t *C, int64_t ldc, unsigned *cnt, int flush_every)
 {
     const int lane = threadIdx.x & 31, g = lane >> 3, sub = lane & 7;
     const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    int pi = 0, ready = -1, pend = -1;
-    unsigned pending = 0;
+    // pending completions, lane-distributed: lane j < npend holds (pair mp, count mc)
+    int npend = 0, mp = -1;
+    unsigned mc = 0;
     auto flush = [&]() {
-        __threadfence(); // this lane's stores of the pair's items, visible GPU-wide
+        __threadfence(); // this lane's stores of the pending items, visible GPU-wide
         __syncwarp();
-        if (lane == 0) {
+        if (lane < npend) {
             __threadfence();
-            atomicAdd(cnt + pend, pending);
+            atomicAdd(cnt + mp, mc);
         }
+        npend = 0;
+        mp = -1;
+        mc = 0;
     };
-    for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += W) {
-        while (pi + 1 < npairs && item0[pi + 1] <= it) ++pi;
-        if (pi != pend) {
-            if (pending) flush();
-            pend = pi;
-            pending = 0;
-        }
+    int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int pi = 0;
+    while (pi + 1 < npairs && item0[pi + 1] <= it) ++pi;
+    unsigned depv = it < items && pairs[pi].z >= 0 ? ld_volatile(cnt + pairs[pi].z) : 0u;
+    while (it < items) {
         const int4 P = pairs[pi];
-        if (pi != ready) {
-            if (P.z >= 0 && lane == 0) {
+        if (P.z >= 0 && depv < (unsigned)P.w) { // not yet known complete: publish, then wait
+            if (__any_sync(0xFFFFFFFFu, npend > 0)) flush();
+            if (lane == 0) {
                 const uint64_t t0 = global_ns();
-                while (ld_acquire_gpu(cnt + P.z) < (unsigned)P.w) {
-                    __nanosleep(100);
+                while (ld_volatile(cnt + P.z) < (unsigned)P.w) {
+                    __nanosleep(64);
                     if (global_ns() - t0 > 2000000000ull) __trap(); // never: see above
                 }
             }
             __syncwarp();
-            ready = pi;
         }
         const int64_t r0 = lptr[P.y] + (it - item0[pi]) * kWaveRows;
         const int64_t nrow = lptr[P.y + 1] - r0;
@@ -326,9 +337,24 @@ __global__ void __launch_bounds__(kWaveThreads) k_fold_wave(const int4 *__restri
             const int col = 64 * h + 8 * sub;
             if (active && col < ncols) *reinterpret_cast<uint4 *>(row + col) = v[h];
         }
-        ++pending;
+        // this item is pending on pair pi (lane-distributed list, pairs ascending)
+        const int last = __shfl_sync(0xFFFFFFFFu, mp, npend > 0 ? npend - 1 : 0);
+        if (npend > 0 && last == pi) {
+            if (lane == npend - 1) ++mc;
+        } else {
+            if (lane == npend) {
+                mp = pi;
+                mc = 1;
+            }
+            ++npend;
+        }
+        // the next item, and its dependency's counter read ahead (consumed at the loop top)
+        it += W;
+        while (pi + 1 < npairs && item0[pi + 1] <= it) ++pi;
+        depv = it < items && pairs[pi].z >= 0 ? ld_volatile(cnt + pairs[pi].z) : 0u;
+        if (npend >= flush_every || npend == 32) flush();
     }
-    if (pending) flush();
+    if (__any_sync(0xFFFFFFFFu, npend > 0)) flush();
 }
 
 int grid_rows(int64_t work, int per_block)
@@ -431,9 +457,12 @@ cudaError_t prepare_fold_wave(RowDag &d, int64_t ldc, cudaStream_t s, cudaError_
     std::vector<int> at((size_t)nseg * (size_t)d.levels, -1);                // pair index of (s, L)
     d.wp_host.clear();
     d.wi_host.assign(1, 0);
-    for (int diag = 0; diag < nseg + nl - 1; ++diag)
-        for (int sg = std::max(0, diag - nl + 1); sg <= std::min(nseg - 1, diag); ++sg) {
-            const int L = diag - sg + 1;
+    int c = 2; // diagonal spacing: (s, L) on diagonal s + c (L - 1); MP_WAVE_C overrides (experiments)
+    if (const char *ev = getenv("MP_WAVE_C")) c = std::max(1, std::min(16, atoi(ev)));
+    for (int diag = 0; diag < nseg + c * (nl - 1); ++diag)
+        for (int sg = std::max(0, diag - c * (nl - 1)); sg <= std::min(nseg - 1, diag); ++sg) {
+            if ((diag - sg) % c) continue;
+            const int L = (diag - sg) / c + 1;
             const int64_t rows = d.lptr[(size_t)L + 1] - d.lptr[(size_t)L];
             const int64_t its = (rows + kWaveRows - 1) / kWaveRows;
             const int dep = L >= 2 ? at[(size_t)sg * d.levels + (L - 1)] : -1;
@@ -476,6 +505,13 @@ static bool fold_levels()
     return e && e[0] == 'l';
 }
 
+// completions published every 4 items (MP_WAVE_F overrides: experiments)
+static int wave_flush_every()
+{
+    const char *e = getenv("MP_WAVE_F");
+    return e ? std::max(1, std::min(32, atoi(e))) : 4;
+}
+
 cudaError_t launch_folds_wave(const RowDag &d, uint16_t *C, int64_t ldc, cudaStream_t s, int *launches)
 {
     if (fold_levels() || d.wave_ld != ldc) return launch_folds(d, C, ldc, ldc, s, launches);
@@ -483,7 +519,7 @@ cudaError_t launch_folds_wave(const RowDag &d, uint16_t *C, int64_t ldc, cudaStr
     cudaError_t e = cudaMemsetAsync(d.wcnt, 0, (size_t)d.npairs * 4, s);
     if (e != cudaSuccess) return e;
     k_fold_wave<<<d.wave_grid, kWaveThreads, 0, s>>>(d.wpairs, d.witem0, d.npairs, d.wave_items, d.lptr_dev, d.frec,
-                                                     d.idx, C, ldc, d.wcnt);
+                                                     d.idx, C, ldc, d.wcnt, wave_flush_every());
     if (launches) ++*launches;
     return cudaGetLastError();
 }
