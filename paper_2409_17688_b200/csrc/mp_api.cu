@@ -463,7 +463,6 @@ mp_status build_sparse(PowerRun &R, cudaStream_t s)
     if (R.dag_n && group) { // row-inclusion reuse: parents and levels
         R.rdag = RowDag();
         e = build_row_dag(R.words.as<WordMask>(), R.N, R.dag_n, R.rdag, s, sp_alloc, &R, &launches);
-        if (e == cudaSuccess) e = prepare_fold_wave(R.rdag, R.ld, s, sp_alloc, &R, &launches);
         if (trace_on()) Tracer(s).mark("  row DAG (since a2)");
         dag = &R.rdag;
     } else {
@@ -508,7 +507,7 @@ mp_status product(PowerRun &R, const uint16_t *X, uint16_t *C, cudaStream_t s, c
         int nl = 0;
         cudaError_t e = launch_spmm(sa, R.plan, X, R.ld, C, R.ld, R.Np, s, &nl);
         if (e == cudaSuccess && mid) e = cudaEventRecord(mid, s);
-        if (e == cudaSuccess && R.dag_n) e = launch_folds_wave(R.rdag, C, R.ld, s, &nl); // parents' rows
+        if (e == cudaSuccess && R.dag_n) e = launch_folds(R.rdag, C, R.ld, R.ld, s, &nl); // parents' rows
         g_launches.fetch_add(nl);
         if (e != cudaSuccess) {
             cudaGetLastError();

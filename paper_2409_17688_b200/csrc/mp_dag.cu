@@ -18,8 +18,6 @@
 
 #include <algorithm>
 #include <cstdint>
-#include <cstdlib>
-#include <vector>
 
 #include "mp_internal.h"
 #include "mp_kernels.h"
@@ -194,169 +192,6 @@ __global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows,
     }
 }
 
-// ---- The folds of all levels in ONE persistent launch (k_fold_wave).
-// The columns are cut into kWaveSeg-column segments; the fold of level L in segment s -- the
-// pair (s, L) -- needs only the pairs (s, L') with L' < L finished (a fold reads the parents'
-// rows in its own columns).  Pairs go in wavefront order: diagonal d = s + L - 1, s ascending
-// inside a diagonal, so the pair a fold depends on, (s, L - 1), sits one diagonal earlier at the
-// same place in it -- finished by the time its dependents start (no waiting in the common case),
-// and written only about one diagonal (~N x 512 B of rows) ago, so the parents' rows come from L2
-// instead of DRAM (the per-level launches stream every level over all columns: ~37 % of the
-// parent reads missed L2 at n = 12).  An item = kWaveRows consecutive rows of one level in one
-// segment (8 lanes per row, 4 x 16 B per lane); warp w takes items w, w + W, ... in schedule
-// order, so every warp moves forward through the pairs.  Completion: a counter per pair, added
-// to when a warp leaves the pair (fence first); a warp entering pair (s, L) waits (acquire) until
-// (s, L - 1) has all its items -- and each of those started only after (s, L - 2) had all of its,
-// so every lower level of the segment is final.  Deadlock-free because every warp holding an
-// item is resident (grid = co-resident blocks) and only waits on items earlier in the order; a
-// wait longer than 2 s traps (a bug, never a hang).
-constexpr int kWaveSeg = 256;
-constexpr int kWaveRows = 4;
-constexpr int kWaveThreads = 256;
-#ifndef MP_WAVE_MINB
-#define MP_WAVE_MINB 3
-#endif
-constexpr int kWaveMinBlocks = MP_WAVE_MINB;
-
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p)
-{
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ uint64_t global_ns()
-{
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
-    return t;
-}
-
-__global__ void k_fold_rec(const int32_t *__restrict__ lrows, int64_t N, const int64_t *__restrict__ off,
-                           int4 *__restrict__ frec)
-{
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t q = lrows[r];
-        const int64_t e0 = off[q];
-        frec[r] = make_int4(q, (int)(off[q + 1] - e0), (int)(uint32_t)(uint64_t)e0, (int)(uint32_t)((uint64_t)e0 >> 32));
-    }
-}
-
-__device__ __forceinline__ unsigned ld_volatile(const unsigned *p)
-{
-    return *reinterpret_cast<const volatile unsigned *>(p);
-}
-
-// flush_every: completions are published (one fence, then one atomic per pending pair) after
-// this many items, or before any wait -- a warp never waits while it holds unpublished items.
-__global__ void __launch_bounds__(kWaveThreads, kWaveMinBlocks)
-    k_fold_wave(const int4 *__restrict__ pairs, const int64_t *__restrict__ item0, int npairs, int64_t items,
-                const int64_t *__restrict__ lptr, const int4 *__restrict__ frec, const int32_t *__restrict__ pidx,
-                uint16_t *C, int64_t ldc, unsigned *cnt, int flush_every)
-{
-    const int lane = threadIdx.x & 31, g = lane >> 3, sub = lane & 7;
-    const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    // pending completions, lane-distributed: lane j < npend holds (pair mp, count mc)
-    int npend = 0, mp = -1;
-    unsigned mc = 0;
-    auto flush = [&]() {
-        __threadfence(); // this lane's stores of the pending items, visible GPU-wide
-        __syncwarp();
-        if (lane < npend) {
-            __threadfence();
-            atomicAdd(cnt + mp, mc);
-        }
-        npend = 0;
-        mp = -1;
-        mc = 0;
-    };
-    int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int pi = 0;
-    while (pi + 1 < npairs && item0[pi + 1] <= it) ++pi;
-    unsigned depv = it < items && pairs[pi].z >= 0 ? ld_volatile(cnt + pairs[pi].z) : 0u;
-    while (it < items) {
-        const int4 P = pairs[pi];
-        if (P.z >= 0 && depv < (unsigned)P.w) { // not yet known complete: publish, then wait
-            if (__any_sync(0xFFFFFFFFu, npend > 0)) flush();
-            if (lane == 0) {
-                const uint64_t t0 = global_ns();
-                while (ld_volatile(cnt + P.z) < (unsigned)P.w) {
-                    __nanosleep(64);
-                    if (global_ns() - t0 > 2000000000ull) __trap(); // never: see above
-                }
-            }
-            __syncwarp();
-        }
-        const int64_t r0 = lptr[P.y] + (it - item0[pi]) * kWaveRows;
-        const int64_t nrow = lptr[P.y + 1] - r0;
-        const int64_t cbase = (int64_t)P.x * kWaveSeg;
-        const int64_t ncols = ldc - cbase < kWaveSeg ? ldc - cbase : kWaveSeg;
-        const bool active = g < nrow;
-        const int4 fr = active ? frec[r0 + g] : make_int4(0, 0, 0, 0);
-        const int np = fr.y;
-        const int64_t e0 = (int64_t)(((uint64_t)(uint32_t)fr.w << 32) | (uint32_t)fr.z);
-        const int32_t m0 = (active && sub < np) ? pidx[e0 + sub] : 0;
-        const int32_t m1 = (active && sub + 8 < np) ? pidx[e0 + 8 + sub] : 0;
-        const int npmax = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)np);
-#if MP_DEBUG_CHECKS
-        if (active && (fr.x < 0 || np < 1 || np > 16)) __trap();
-#endif
-        uint16_t *row = C + (int64_t)fr.x * ldc + cbase;
-        uint4 v[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int col = 64 * h + 8 * sub;
-            v[h] = (active && col < ncols) ? __ldcg(reinterpret_cast<const uint4 *>(row + col)) : ones;
-        }
-        for (int e = 0; e < npmax; e += 2) {
-            const int32_t a0 = __shfl_sync(0xFFFFFFFFu, e < 8 ? m0 : m1, e & 7, 8);
-            const int32_t a1 = __shfl_sync(0xFFFFFFFFu, e + 1 < 8 ? m0 : m1, (e + 1) & 7, 8);
-            const bool h0 = active && e < np, h1 = active && e + 1 < np;
-#if MP_DEBUG_CHECKS
-            if ((h0 && (a0 < 0 || a0 == fr.x)) || (h1 && (a1 < 0 || a1 == fr.x))) __trap();
-#endif
-            const uint16_t *p0 = C + (int64_t)a0 * ldc + cbase, *p1 = C + (int64_t)a1 * ldc + cbase;
-            uint4 u0[4], u1[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int col = 64 * h + 8 * sub;
-                u0[h] = (h0 && col < ncols) ? __ldcg(reinterpret_cast<const uint4 *>(p0 + col)) : ones;
-                u1[h] = (h1 && col < ncols) ? __ldcg(reinterpret_cast<const uint4 *>(p1 + col)) : ones;
-            }
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                v[h].x = __vminu2(v[h].x, __vminu2(u0[h].x, u1[h].x));
-                v[h].y = __vminu2(v[h].y, __vminu2(u0[h].y, u1[h].y));
-                v[h].z = __vminu2(v[h].z, __vminu2(u0[h].z, u1[h].z));
-                v[h].w = __vminu2(v[h].w, __vminu2(u0[h].w, u1[h].w));
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int col = 64 * h + 8 * sub;
-            if (active && col < ncols) *reinterpret_cast<uint4 *>(row + col) = v[h];
-        }
-        // this item is pending on pair pi (lane-distributed list, pairs ascending)
-        const int last = __shfl_sync(0xFFFFFFFFu, mp, npend > 0 ? npend - 1 : 0);
-        if (npend > 0 && last == pi) {
-            if (lane == npend - 1) ++mc;
-        } else {
-            if (lane == npend) {
-                mp = pi;
-                mc = 1;
-            }
-            ++npend;
-        }
-        // the next item, and its dependency's counter read ahead (consumed at the loop top)
-        it += W;
-        while (pi + 1 < npairs && item0[pi + 1] <= it) ++pi;
-        depv = it < items && pairs[pi].z >= 0 ? ld_volatile(cnt + pairs[pi].z) : 0u;
-        if (npend >= flush_every || npend == 32) flush();
-    }
-    if (__any_sync(0xFFFFFFFFu, npend > 0)) flush();
-}
-
 int grid_rows(int64_t work, int per_block)
 {
     const int64_t g = (work + per_block - 1) / per_block;
@@ -443,85 +278,6 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
-}
-
-cudaError_t prepare_fold_wave(RowDag &d, int64_t ldc, cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *),
-                              void *actx, int64_t *launches)
-{
-    d.npairs = 0;
-    d.wave_items = 0;
-    d.wave_ld = ldc;
-    if (d.levels <= 1) return cudaSuccess;
-    const int64_t N = d.lptr.back();
-    const int nseg = (int)((ldc + kWaveSeg - 1) / kWaveSeg), nl = d.levels - 1; // levels 1 .. levels - 1
-    std::vector<int> at((size_t)nseg * (size_t)d.levels, -1);                // pair index of (s, L)
-    d.wp_host.clear();
-    d.wi_host.assign(1, 0);
-    int c = 2; // diagonal spacing: (s, L) on diagonal s + c (L - 1); MP_WAVE_C overrides (experiments)
-    if (const char *ev = getenv("MP_WAVE_C")) c = std::max(1, std::min(16, atoi(ev)));
-    for (int diag = 0; diag < nseg + c * (nl - 1); ++diag)
-        for (int sg = std::max(0, diag - c * (nl - 1)); sg <= std::min(nseg - 1, diag); ++sg) {
-            if ((diag - sg) % c) continue;
-            const int L = (diag - sg) / c + 1;
-            const int64_t rows = d.lptr[(size_t)L + 1] - d.lptr[(size_t)L];
-            const int64_t its = (rows + kWaveRows - 1) / kWaveRows;
-            const int dep = L >= 2 ? at[(size_t)sg * d.levels + (L - 1)] : -1;
-            const int64_t dep_items = dep >= 0 ? d.wi_host[(size_t)dep + 1] - d.wi_host[(size_t)dep] : 0;
-            at[(size_t)sg * d.levels + L] = (int)d.wp_host.size();
-            d.wp_host.push_back(make_int4(sg, L, dep, (int)dep_items));
-            d.wi_host.push_back(d.wi_host.back() + its);
-        }
-    d.npairs = (int)d.wp_host.size();
-    d.wave_items = d.wi_host.back();
-    cudaError_t e;
-    auto A = [&](auto *&p, size_t bytes) { return alloc((void **)&p, std::max<size_t>(bytes, 16), actx); };
-    if ((e = A(d.frec, (size_t)N * sizeof(int4))) != cudaSuccess) return e;
-    if ((e = A(d.wpairs, d.wp_host.size() * sizeof(int4))) != cudaSuccess) return e;
-    if ((e = A(d.witem0, d.wi_host.size() * 8)) != cudaSuccess) return e;
-    if ((e = A(d.wcnt, d.wp_host.size() * 4)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(d.wpairs, d.wp_host.data(), d.wp_host.size() * sizeof(int4), cudaMemcpyHostToDevice,
-                             s)) != cudaSuccess)
-        return e;
-    if ((e = cudaMemcpyAsync(d.witem0, d.wi_host.data(), d.wi_host.size() * 8, cudaMemcpyHostToDevice, s)) !=
-        cudaSuccess)
-        return e;
-    k_fold_rec<<<grid_rows(N, 256), 256, 0, s>>>(d.lrows, N, d.off, d.frec);
-    *launches += 1;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    // a persistent grid: exactly the blocks that fit on the device at once
-    int dev = 0, sms = 0, per_sm = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_wave, kWaveThreads, 0)) != cudaSuccess)
-        return e;
-    d.wave_grid = std::max(1, sms * per_sm);
-    return cudaSuccess;
-}
-
-// MP_FOLD=levels: one k_fold launch per level (the round-2 fold) instead of k_fold_wave
-static bool fold_levels()
-{
-    const char *e = getenv("MP_FOLD"); // read per call: tests switch it
-    return e && e[0] == 'l';
-}
-
-// completions published every 4 items (MP_WAVE_F overrides: experiments)
-static int wave_flush_every()
-{
-    const char *e = getenv("MP_WAVE_F");
-    return e ? std::max(1, std::min(32, atoi(e))) : 4;
-}
-
-cudaError_t launch_folds_wave(const RowDag &d, uint16_t *C, int64_t ldc, cudaStream_t s, int *launches)
-{
-    if (fold_levels() || d.wave_ld != ldc) return launch_folds(d, C, ldc, ldc, s, launches);
-    if (d.npairs == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(d.wcnt, 0, (size_t)d.npairs * 4, s);
-    if (e != cudaSuccess) return e;
-    k_fold_wave<<<d.wave_grid, kWaveThreads, 0, s>>>(d.wpairs, d.witem0, d.npairs, d.wave_items, d.lptr_dev, d.frec,
-                                                     d.idx, C, ldc, d.wcnt, wave_flush_every());
-    if (launches) ++*launches;
-    return cudaGetLastError();
 }
 
 } // namespace mp

@@ -110,16 +110,6 @@ struct RowDag {
     std::vector<int64_t> lptr;  // [levels + 1] level offsets into lrows (host copy)
     int levels = 0;
     int64_t parents = 0;
-    // one-launch fold (k_fold_wave, prepare_fold_wave): per level-ordered row {q, #parents,
-    // first parent}, the (segment, level) pairs in wavefront order, their completion counters
-    int4 *frec = nullptr;       // [N] {q, np, e0 lo, e0 hi}
-    int4 *wpairs = nullptr;     // [npairs] {s, L, dep pair (-1: none), dep items}
-    int64_t *witem0 = nullptr;  // [npairs + 1] first item of each pair
-    unsigned *wcnt = nullptr;   // [npairs] items finished (zeroed before each launch)
-    std::vector<int4> wp_host;
-    std::vector<int64_t> wi_host;
-    int64_t wave_ld = -1, wave_items = 0;
-    int npairs = 0, wave_grid = 0;
 };
 cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cudaStream_t s,
                           cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);
@@ -128,13 +118,6 @@ cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const
                               cudaStream_t s);
 // C_q = min(C_q, C_p) over the parents p, level by level (levels 1 .. levels-1), ncols columns
 cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncols, cudaStream_t s, int *launches);
-// The same folds in ONE persistent launch (k_fold_wave): 256-column segments, (segment, level)
-// pairs in wavefront order with device-side completion counters.  prepare_fold_wave builds the
-// schedule for pitch ldc (once per run); launch_folds_wave falls back to launch_folds (the
-// per-level launches) when MP_FOLD=levels.
-cudaError_t prepare_fold_wave(RowDag &d, int64_t ldc, cudaStream_t s, cudaError_t (*alloc)(void **, size_t, void *),
-                              void *actx, int64_t *launches);
-cudaError_t launch_folds_wave(const RowDag &d, uint16_t *C, int64_t ldc, cudaStream_t s, int *launches);
 // group: form the row groups with k_group_greedy (else groups are consecutive rows).
 // A: the matrix source itself (row-major, boundary encoding, range-checked by launch_check_a).
 // pre_bits (may be null): A's support bitsets from launch_check_a (N x ceil(N/32) words).
