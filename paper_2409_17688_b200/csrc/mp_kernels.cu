@@ -9,6 +9,7 @@
 #include <mutex>
 #include <set>
 #include <utility>
+#include <vector>
 
 #include "mp_internal.h"
 #include "mp_kernels.h"
@@ -732,6 +733,25 @@ __global__ void k_support_bits(Acc acc, int64_t N, int64_t nw, uint32_t *__restr
 }
 
 // cnt[i] = |support of row i| (warp per row)
+// Sort key of a row for the extras ordering (row-inclusion reuse): its first two columns
+// (ascending CSR lists; N where absent), packed (c1, c2).
+__global__ void k_first_cols(const int64_t *__restrict__ off, const int32_t *__restrict__ idx, int64_t N,
+                             uint64_t *__restrict__ keys)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = off[q], z = off[q + 1];
+        const uint64_t c1 = a < z ? (uint64_t)idx[a] : (uint64_t)N, c2 = a + 1 < z ? (uint64_t)idx[a + 1] : (uint64_t)N;
+        keys[q] = (c1 << 32) | c2;
+    }
+}
+
+// MP_GROUP_ORDER=greedy: the windowed greedy tiles also for the extras (diagnostic / A-B)
+static bool extras_sorted_order()
+{
+    const char *e = getenv("MP_GROUP_ORDER"); // read per build: tests switch it
+    return !(e && e[0] == 'g');
+}
+
 __global__ void k_row_popc(const uint32_t *__restrict__ bits, int64_t nw, int64_t N, int32_t *__restrict__ cnt)
 {
     const int lane = threadIdx.x & 31;
@@ -2273,28 +2293,59 @@ cudaError_t build_sparse_form_t(Acc AT2, int64_t N, int64_t Np, bool group, cons
         w.off = off;
         w.idx = idx;
         sp_trace(s, "row lists");
-        // column lists: the transposed bits through the same two kernels (bits is reused)
-        uint32_t *bitsT = nullptr;
-        int64_t *coff = nullptr;
-        int32_t *cidx = nullptr;
-        SP_ALLOC(bitsT, (size_t)N * nw * 4);
-        SP_ALLOC(coff, (size_t)(N + 1) * 8);
-        SP_ALLOC(cidx, (size_t)std::max<int64_t>(nnz, 1) * 4);
-        SP_LAUNCH((k_bits_transpose<<<dim3((unsigned)((N + kTrRows - 1) / kTrRows), (unsigned)((nw + kTrWords - 1) / kTrWords)),
-                                       256, 0, s>>>(bits, nw, N, bitsT)));
-        SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, cnt)));
-        SP_SCAN(cnt, N, coff);
-        const int64_t nwin = (N + kGrpWin - 1) / kGrpWin;
-        int32_t *cwst = nullptr;
-        SP_ALLOC(cwst, (size_t)N * nwin * 4);
-        SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, coff, cidx, cwst, nwin)));
-        sp_trace(s, "column lists");
-        const int smem_g = (int)(nw * 4);
-        if ((e = cudaFuncSetAttribute(k_tile_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g)) != cudaSuccess)
-            return e;
-        SP_LAUNCH((k_tile_greedy<<<(unsigned)((N + kGrpWin - 1) / kGrpWin), kGrpWin, smem_g, s>>>(
-            off, idx, coff, cidx, cwst, nwin, nw, N, w.rows)));
-        sp_trace(s, "greedy");
+        if (dag && extras_sorted_order()) {
+            // Extras ordering: rows sorted by their first two extra columns
+            // (ties in row order).  A row's extras are a few columns close together, so sorted
+            // neighbours share most of them: n = 12 tile unions 147 k X rows against 218 k for
+            // the windowed greedy tiles (host model), without the column lists.
+            uint64_t *keys = nullptr;
+            SP_ALLOC(keys, (size_t)N * 8);
+            SP_LAUNCH((k_first_cols<<<grid_for(N, 256), 256, 0, s>>>(off, idx, N, keys)));
+            std::vector<uint64_t> hk((size_t)N);
+            if ((e = cudaMemcpyAsync(hk.data(), keys, (size_t)N * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+            // two stable counting passes (c2, then c1): order by (c1, c2, row)
+            std::vector<int32_t> a((size_t)N), b((size_t)N);
+            std::vector<int64_t> cnt2((size_t)N + 2);
+            for (int64_t q = 0; q < N; ++q) a[(size_t)q] = (int32_t)q;
+            for (int pass = 0; pass < 2; ++pass) {
+                const int sh = pass == 0 ? 0 : 32;
+                std::fill(cnt2.begin(), cnt2.end(), 0);
+                for (int64_t q = 0; q < N; ++q) ++cnt2[(size_t)((hk[(size_t)q] >> sh) & 0xFFFFFFFFu) + 1];
+                for (int64_t c = 0; c <= N; ++c) cnt2[(size_t)c + 1] += cnt2[(size_t)c];
+                for (int64_t t = 0; t < N; ++t) {
+                    const int32_t q = a[(size_t)t];
+                    b[(size_t)cnt2[(size_t)((hk[(size_t)q] >> sh) & 0xFFFFFFFFu)]++] = q;
+                }
+                a.swap(b);
+            }
+            if ((e = cudaMemcpyAsync(w.rows, a.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e; // a goes out of scope
+            sp_trace(s, "extras order");
+        } else {
+            // column lists: the transposed bits through the same two kernels (bits is reused)
+            uint32_t *bitsT = nullptr;
+            int64_t *coff = nullptr;
+            int32_t *cidx = nullptr;
+            SP_ALLOC(bitsT, (size_t)N * nw * 4);
+            SP_ALLOC(coff, (size_t)(N + 1) * 8);
+            SP_ALLOC(cidx, (size_t)std::max<int64_t>(nnz, 1) * 4);
+            SP_LAUNCH((k_bits_transpose<<<dim3((unsigned)((N + kTrRows - 1) / kTrRows), (unsigned)((nw + kTrWords - 1) / kTrWords)),
+                                           256, 0, s>>>(bits, nw, N, bitsT)));
+            SP_LAUNCH((k_row_popc<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, cnt)));
+            SP_SCAN(cnt, N, coff);
+            const int64_t nwin = (N + kGrpWin - 1) / kGrpWin;
+            int32_t *cwst = nullptr;
+            SP_ALLOC(cwst, (size_t)N * nwin * 4);
+            SP_LAUNCH((k_bits_csr<<<grid_for(N * 32, 256), 256, 0, s>>>(bitsT, nw, N, coff, cidx, cwst, nwin)));
+            sp_trace(s, "column lists");
+            const int smem_g = (int)(nw * 4);
+            if ((e = cudaFuncSetAttribute(k_tile_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g)) != cudaSuccess)
+                return e;
+            SP_LAUNCH((k_tile_greedy<<<(unsigned)((N + kGrpWin - 1) / kGrpWin), kGrpWin, smem_g, s>>>(
+                off, idx, coff, cidx, cwst, nwin, nw, N, w.rows)));
+            sp_trace(s, "greedy");
+        }
         // pass 3: shared memory = max(G + P + R staging, R + Um); tile unions up to 12288 l
         // (n = 12: consecutive tiles reach 9600 at most, greedy tiles fewer)
         const int64_t uw_max = 384;

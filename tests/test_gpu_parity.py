@@ -223,13 +223,18 @@ def test_spmm_width_power_until_periodic(mp, oracle_mod, n, width):
     assert g.diag_min == o.diag_min and g.fingerprint == o.fingerprint
 
 
+@pytest.mark.parametrize("order", ["sorted", "greedy"])
 @pytest.mark.parametrize("sym", [False, True])
 @pytest.mark.parametrize("n", [4, 6, 7, 8, 9])
-def test_row_reuse_transfer_hint(mp, oracle_mod, n, sym):
+def test_row_reuse_transfer_hint(mp, oracle_mod, n, sym, order, monkeypatch):
     """Row-inclusion reuse (SpMM on each row's extra entries, then one fold pass per level of
     the parent DAG) on A(D_n) announced by the transfer hint, greedy grouping forced so the
-    grouped SpMM runs at these sizes: every entry of A^1..A^8 and the whole periodic record
-    equal the oracle's; a matrix that is not A(D_n) is refused."""
+    grouped SpMM runs at these sizes, with the rows in the extras order (sorted by their first
+    extra columns, the default) or in the windowed greedy tiles (MP_GROUP_ORDER=greedy): every
+    entry of A^1..A^8 and the whole periodic record equal the oracle's; a matrix that is not
+    A(D_n) is refused."""
+    if order == "greedy":
+        monkeypatch.setenv("MP_GROUP_ORDER", "greedy")
     A = mp.build_transition_matrix(n)
     o = oracle_mod.power_until_periodic(A)
     use_kernel(mp, "spmm-greedy")
