@@ -282,13 +282,16 @@ def minplus_power_until_periodic_device(dA, max_k: int = 64) -> PeriodicResult:
     import torch
     r = _PeriodicResult()
     # the run is enqueued on the library stream of this device: unless that is torch's current
-    # stream (set_stream), wait for whatever torch still has in flight on dA
+    # stream (set_stream), wait for whatever torch still has in flight on dA.  (The raw-handle
+    # and device getters cost a fraction of the public wrappers: microseconds at small n.)
     dev = dA.device.index
-    cur = torch.cuda.current_stream(dev)
-    if _lib_stream.get(dev) != cur.cuda_stream:
-        cur.synchronize()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    handle = raw(dev) if raw else torch.cuda.current_stream(dev).cuda_stream
+    if _lib_stream.get(dev) != handle:
+        torch.cuda.current_stream(dev).synchronize()
     args = (dA.data_ptr(), dA.stride(0), dA.shape[0], max_k, ctypes.byref(r))
-    if torch.cuda.current_device() == dev:  # (the device switch costs microseconds at small n)
+    getdev = getattr(torch._C, "_cuda_getDevice", torch.cuda.current_device)
+    if getdev() == dev:  # (the device switch costs microseconds at small n)
         _check(lib.minplus_power_until_periodic_device(*args))
     else:
         with torch.cuda.device(dev):

@@ -82,6 +82,7 @@ bool g_row_reuse = true;   // mp_set_row_reuse: row-inclusion reuse for A(D_n)
 
 mp_profile g_prof{};
 cudaEvent_t *g_small_prof_ev = nullptr; // small-N run whose event times g_prof still lacks
+bool g_small_prof_staged = false;        // ... and whether it recorded ev[0], ev[3] (host staging)
 
 // Parity observer (mp_set_power_observer): sees every power of every run in full.
 struct Observer {
@@ -627,7 +628,10 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     cudaEvent_t *ev = R.small_ev;
     if (!ev[0])
         for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&ev[i]));
-    CUDA_TRY(cudaEventRecord(ev[0], s));
+    // events: ev[1], ev[2] around the kernel; ev[0], ev[3] around the whole call only when a
+    // host matrix is staged (each record costs the caller about a microsecond at n = 3)
+    const bool staged = !src.dev;
+    if (staged) CUDA_TRY(cudaEventRecord(ev[0], s));
     const uint16_t *dA = src.dev;
     int64_t lda = src.lda;
     if (!dA) { // host matrix, or A(D_n) from the word masks (at most 256 x 256 here)
@@ -676,7 +680,7 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     CUDA_TRY(cudaEventRecord(ev[2], s));
     long long *h = R.small_host;
     g_d2h.fetch_add((int64_t)nout * 8); // written over the bus by the kernel
-    CUDA_TRY(cudaEventRecord(ev[3], s));
+    if (staged) CUDA_TRY(cudaEventRecord(ev[3], s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (h[0] == -1) return MP_OK; // too many finite entries: the general path
     if (getenv("MP_SMALL_PROFILE")) {
@@ -690,6 +694,7 @@ mp_status run_small(DevState &st, const ASource &src, int64_t N, int max_k, mp_p
     // the event times are read by mp_last_profile (three cudaEventElapsedTime calls cost more
     // than a tenth of an n = 3 run)
     g_small_prof_ev = ev;
+    g_small_prof_staged = staged;
     g_prof.product_launches = products;
     g_prof.dense_steps = (double)products * (double)N * (double)N * (double)N;
     g_prof.issued_steps = 0.0; // the row lists of A against 64 C columns; counted by the caller as nnz * 64 C
@@ -1677,8 +1682,11 @@ mp_status mp_last_profile(mp_profile *out)
         cudaEvent_t *ev = g_small_prof_ev;
         float kms = 0.f, all = 0.f, setup = 0.f;
         CUDA_TRY(cudaEventElapsedTime(&kms, ev[1], ev[2]));
-        CUDA_TRY(cudaEventElapsedTime(&all, ev[0], ev[3]));
-        CUDA_TRY(cudaEventElapsedTime(&setup, ev[0], ev[1]));
+        all = kms;
+        if (g_small_prof_staged) {
+            CUDA_TRY(cudaEventElapsedTime(&all, ev[0], ev[3]));
+            CUDA_TRY(cudaEventElapsedTime(&setup, ev[0], ev[1]));
+        }
         g_prof.product_ms = kms;
         g_prof.spmm_ms = kms;
         g_prof.total_ms = all;

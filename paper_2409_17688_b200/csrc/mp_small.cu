@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kSmThreads, 1)
     Stats *wred = hs + (max_k + 1);                                       // [kSmWarps]
     Stats *xch = wred + kSmWarps;                                         // [2]: this CTA's partials
     long long *xmis = reinterpret_cast<long long *>(xch + 2);             // [2]: mismatch partials
-    int *flags = reinterpret_cast<int *>(xmis + 2); // [0] range, [1] nnz, [2] candidate j, [3] c, [4] asym
+    int *flags = reinterpret_cast<int *>(xmis + 2); // [0] range, [1] nnz, [2] candidate j, [3] c, [4] asym,
+                                                    // [5] dense_from (at the end)
 
     const int j0 = 64 * c + 2 * lane, j1 = j0 + 1; // this lane's global columns
     const bool v0 = j0 < N, v1 = j1 < N;
@@ -272,29 +273,39 @@ __global__ void __launch_bounds__(kSmThreads, 1)
         if (warp == 0) { // the CTA's partial: lanes < 16 hold the warps' partials
             Stats s = lane < nwarps ? wred[lane] : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
             reduce_stats(s, kSmWarps); // lanes >= nwarps hold the identity
-            if (lane == 0) xch[xi & 1] = s;
+            if (nct == 1) { // a single CTA: its partial is the power's statistics
+                if (lane == 0) hs[k] = s;
+                if (!dense_from && s.inf == 0) dense_from = k;
+                __syncwarp(); // hs[k] visible to warp 0's lanes (the search)
+            } else if (lane == 0) {
+                xch[xi & 1] = s;
+            }
         }
         {
             const long long t = clock64();
             t_prod += t - t_mark;
             t_mark = t;
         }
-        csync(); // partials and the peers' rows of A^k visible cluster-wide
-        // the own rows of A^k go to the history now, after the barrier: the stores complete while
-        // the next product runs instead of holding up this barrier's release (exact compares of
-        // later powers read them, ordered by the barriers in between)
+        if (nct > 1) {
+            csync(); // partials and the peers' rows of A^k visible cluster-wide
+            if (warp == 0) { // lane q < nct reads CTA q's partial; every lane ends with the sum
+                Stats g = lane < nct ? cluster.map_shared_rank(xch, lane)[xi & 1]
+                                     : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
+                reduce_stats(g, 16); // a cluster has at most 16 CTAs
+                if (lane == 0) hs[k] = g;
+                if (!dense_from && g.inf == 0) dense_from = k;
+            }
+            ++xi;
+            __syncthreads();
+        }
+        // (one CTA: only warp 0 reads hs[], in the search below; the other warps' rows of A^k
+        // are published by the search's barrier before anyone reads them)
+        // the own rows of A^k go to the history after the barrier: the stores complete while the
+        // next product runs (exact compares of later powers read them, ordered by the barriers
+        // in between)
         for (int t = tid; t < nr * 32; t += nthreads)
             reinterpret_cast<uint32_t *>(hist + (int64_t)k * hsz + (int64_t)(r0 + (t >> 5)) * ldh + 64 * c)[t & 31] =
                 X[r0 * 32 + t];
-        if (warp == 0) { // lane q < nct reads CTA q's partial; every lane ends with the sum
-            Stats g = lane < nct ? cluster.map_shared_rank(xch, lane)[xi & 1]
-                                 : Stats{0ull, 0ull, 0xFFFFll, 0x7FFFFFFFFFFFFFFFll};
-            reduce_stats(g, 16); // a cluster has at most 16 CTAs
-            if (lane == 0) hs[k] = g;
-            if (!dense_from && g.inf == 0) dense_from = k;
-        }
-        ++xi;
-        __syncthreads();
         {
             const long long t = clock64();
             t_red += t - t_mark;
@@ -373,19 +384,25 @@ __global__ void __launch_bounds__(kSmThreads, 1)
             Xc = Xb;
         }
     }
+    if (warp == 0 && lane == 0) flags[5] = dense_from; // (kept by warp 0 only)
     csync(); // no CTA leaves while another may still read its shared memory
-    if (rk == 0 && tid == 0) {
-        out[0] = found ? 0 : 4;
-        out[1] = mu;
-        out[2] = lam;
-        out[3] = off;
-        out[4] = found ? k_last : k;
-        out[5] = dense_from;
+    if (rk == 0) { // the result, one element per thread (mapped host memory: one burst of writes)
         const int kk = found ? k_last : k;
-        for (int q = 1; q <= kk; ++q) {
-            out[6 + q] = hs[q].dmin;
-            out[6 + (max_k + 1) + q] = (long long)hs[q].fp;
+        for (int t = tid; t <= kk; t += nthreads) {
+            if (t == 0) {
+                out[0] = found ? 0 : 4;
+                out[1] = mu;
+                out[2] = lam;
+                out[3] = off;
+                out[4] = kk;
+                out[5] = flags[5];
+            } else {
+                out[6 + t] = hs[t].dmin;
+                out[6 + (max_k + 1) + t] = (long long)hs[t].fp;
+            }
         }
+    }
+    if (rk == 0 && tid == 0) {
         long long *prof = out + 6 + 2 * (max_k + 1);
         prof[0] = t_setup;
         prof[1] = t_prod;
@@ -450,7 +467,7 @@ cudaError_t launch_small_run(const uint16_t *A, int64_t lda, int64_t N, int max_
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = C * R > 1 ? 1 : 0; // one CTA: a plain launch (its implicit cluster of one)
     return cudaLaunchKernelEx(&cfg, k_small_run, A, lda, (int)N, C, max_k, max_nnz, sigma, hist,
                               (unsigned long long)S, out);
 }
