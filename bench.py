@@ -37,6 +37,7 @@ KERNEL_NAMES = {"dense": "k_minplus (dense tiles, VIADDMNMX.U16x2)",
                 "spmm": "k_spmm (grouped SpMM, VIADDMNMX.U16x2)",
                 "small": "k_small_run (the whole run in one thread-block-cluster launch, VIADDMNMX.U16x2)"}
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+FOLD_NAME = "k_fold (row-inclusion fold, one launch per DAG level)"
 
 
 def traffic_bytes(kernel: str, n: int, world: int, sym: bool = False, reuse: bool = False):
@@ -360,6 +361,7 @@ def run_mine(args):
         spmm_cols = p["spmm_cols"]
         local_cols, ld = p["local_cols"], p["ld"]
         row_levels, row_parents = p["row_levels"], p["row_parents"]
+        fold_bytes = p["fold_bytes"]
         dense += p["dense_steps"]
         issued += p["issued_steps"]
         setup_ms = p["setup_ms"]
@@ -454,6 +456,7 @@ def run_mine(args):
               "useful_note": "nnz(A) x computed columns per product / product time (kernel + fold passes); "
                              "above 1 only when the row-inclusion reuse skips redundant terms",
               "kernel_share_of_step": spmm_ms / max(ms, 1e-9), "product_share_of_step": prod_ms / max(ms, 1e-9)}
+    others = []
     if row_levels and kernel_used == "spmm":
         entries = issued_per_launch / (4.0 * ld) if ld else 0.0
         alg_bytes = 2.0 * N * ld * 2 + 32.0 * entries
@@ -464,6 +467,27 @@ def run_mine(args):
                         bytes_note="read X_{k-1} (N x ld u16) once + write A^k (N x ld) once + the sparse "
                                    "form's 32-byte entries once", peak_source="MEASURED_PEAKS.json hbm_gbs",
                         traffic_GBps=(traffic / (avg_kernel_ms * 1e-3) / 1e9) if traffic else None, alu=alu)
+        # The fold passes of the reuse (k_fold, one launch per DAG level) take as long as the SpMM
+        # or longer: the roofline object names whichever of the two took more of the step, the
+        # other goes to roofline_others.  k_fold's algorithmic bytes per product (summed over its
+        # levels' launches): every folded row read and written once, each distinct parent row of
+        # a level read once by that level's launch (library-computed from the DAG).
+        fold_ms = (prod_ms - spmm_ms) / max(1, prod_launches)  # per product, all its levels
+        if fold_bytes and fold_ms > 0:
+            fach = fold_bytes / (fold_ms * 1e-3) / 1e9
+            ftraffic = traffic_bytes(FOLD_NAME, args.n, world, not args.no_symmetry, True)
+            fold = {"kernel": FOLD_NAME, "bound": "hbm", "achieved": fach, "peak": hbm, "unit": "GB/s",
+                    "frac": fach / hbm, "traffic": ftraffic, "avg_kernel_ms": fold_ms,
+                    "launches_per_product": row_levels - 1, "algorithmic_bytes_per_product": fold_bytes,
+                    "bytes_note": "per product over its row_levels - 1 launches: every folded row read + written "
+                                  "once, each distinct parent row of a level read once (x ld x 2 B)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "traffic_GBps": (ftraffic / (fold_ms * 1e-3) / 1e9) if ftraffic else None,
+                    "kernel_share_of_step": (prod_ms - spmm_ms) / max(ms, 1e-9)}
+            if fold_ms > avg_kernel_ms:
+                roofline, others = fold, [roofline]
+            else:
+                others = [fold]
     else:
         if not achieved:  # the fused small-N run issues no separate product kernel
             alu.update(achieved=useful_rate, frac=useful_rate / peak,
@@ -489,6 +513,7 @@ def run_mine(args):
         "dense_equivalent_gops": dense_all / (ms * 1e-3) / 1e9,
         "issued_gops": issued_all / (ms * 1e-3) / 1e9,
         "roofline": roofline,
+        "roofline_others": others or None,
         "cpu_baseline": cpu,
         "e2e": {"value": useful_all / args.steps * e2e_steps / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
                 "h2d_bytes_per_step": int(h2d / max(1, e2e_steps)), "d2h_bytes_per_step": int(d2h / max(1, e2e_steps)),

@@ -344,6 +344,9 @@ typedef struct {
                                  passes of the row-inclusion reuse)                          */
     int32_t row_levels;       /* row-inclusion reuse: levels of the parent DAG (0 = not used)   */
     int64_t row_parents;      /*   and its number of parent links                               */
+    double fold_bytes;        /*   algorithmic bytes of one product's fold passes: every folded
+                                   row read and written once, each distinct parent row of a
+                                   level read once by that level's pass (x ld x 2 bytes)         */
 } mp_profile;
 mp_status mp_last_profile(mp_profile *out);
 

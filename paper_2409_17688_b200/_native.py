@@ -70,7 +70,8 @@ class _Profile(ctypes.Structure):
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("kernel", ctypes.c_int32), ("spmm_cols", ctypes.c_int32),
                 ("local_cols", ctypes.c_int64), ("ld", ctypes.c_int64),
-                ("spmm_ms", ctypes.c_double), ("row_levels", ctypes.c_int32), ("row_parents", ctypes.c_int64)]
+                ("spmm_ms", ctypes.c_double), ("row_levels", ctypes.c_int32), ("row_parents", ctypes.c_int64),
+                ("fold_bytes", ctypes.c_double)]
 
 
 OBSERVER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64)
@@ -492,7 +493,7 @@ def last_profile() -> dict:
             "setup_ms": p.setup_ms, "stats_ms": p.stats_ms, "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
             "kernel": {0: "dense", 1: "tiles", 2: "spmm", 3: "small"}.get(p.kernel, "?"), "spmm_cols": p.spmm_cols,
             "local_cols": p.local_cols, "ld": p.ld, "row_levels": p.row_levels, "row_parents": p.row_parents,
-            "spmm_ms": p.spmm_ms}
+            "spmm_ms": p.spmm_ms, "fold_bytes": p.fold_bytes}
 
 
 SPARSITY = {"auto": -1, "dense": 0, "tiles": 1, "spmm": 2}

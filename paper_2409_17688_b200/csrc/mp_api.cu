@@ -1291,6 +1291,7 @@ mp_status run_powers(const ASource &src, int64_t N, int max_k, mp_periodic_resul
     g_prof.spmm_ms = R.spmm ? spmm_ms : prod_ms;
     g_prof.row_levels = R.spmm && R.dag_n ? R.rdag.levels : 0;
     g_prof.row_parents = R.spmm && R.dag_n ? R.rdag.parents : 0;
+    g_prof.fold_bytes = R.spmm && R.dag_n ? (double)R.rdag.fold_rows * (double)R.ld * 2.0 : 0.0;
 
     if (!found) return fail(MP_ERR_NOT_PERIODIC, "no repeat A^k = c (x) A^j with k <= %d", max_k);
     *out = res;
@@ -1666,10 +1667,10 @@ void mp_shutdown(void)
 
 const char *mp_version(void)
 {
-    return "minplus-b200 0.4 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse, 4-stage "
-           "cp.async) and warp-specialised grouped SpMM (4-row groups, greedy row grouping, bulk copies + mbarrier "
-           "ring); column symmetry; row-inclusion reuse (SpMM on the extra entries + fold passes); u8 IMMA "
-           "fingerprint; one-cluster small-N kernel";
+    return "minplus-b200 0.5 sm_100a: DPX VIADDMNMX.U16x2; 128x256x32 tile kernel (dense / block-sparse, 4-stage "
+           "cp.async) and warp-specialised grouped SpMM (4-row groups, greedy row grouping; extras order under the "
+           "reuse, bulk copies + mbarrier ring); column symmetry; row-inclusion reuse (SpMM on the extra entries + "
+           "fold passes); u8 IMMA fingerprint; one-cluster small-N kernel";
 }
 
 int64_t mp_kernel_launches(void) { return g_launches.load(); }

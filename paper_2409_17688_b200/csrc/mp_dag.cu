@@ -249,6 +249,28 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
     if (d.lptr.back() != N) return cudaErrorUnknown; // levels are contiguous from 0
     if ((e = cudaMemcpyAsync(d.lptr_dev, d.lptr.data(), d.lptr.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return e;
+    {   // fold_rows = sum over levels >= 1 of (2 x rows + distinct parents): levels and parent
+        // lists to the host once per DAG (N + #parents ints)
+        std::vector<int32_t> lv((size_t)N), pi((size_t)std::max<int64_t>(d.parents, 1));
+        if ((e = cudaMemcpyAsync(lv.data(), d.level, (size_t)N * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+        if (d.parents > 0 &&
+            (e = cudaMemcpyAsync(pi.data(), d.idx, (size_t)d.parents * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+            return e;
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+        std::vector<std::vector<int32_t>> by((size_t)d.levels);
+        for (int64_t q = 0; q < N; ++q) by[(size_t)lv[(size_t)q]].push_back((int32_t)q);
+        std::vector<int32_t> seen((size_t)N, -1);
+        d.fold_rows = 0;
+        for (int l = 1; l < d.levels; ++l)
+            for (const int32_t q : by[(size_t)l]) {
+                d.fold_rows += 2;
+                for (int64_t k = ho[(size_t)q]; k < ho[(size_t)q + 1]; ++k)
+                    if (seen[(size_t)pi[(size_t)k]] != l) {
+                        seen[(size_t)pi[(size_t)k]] = l;
+                        ++d.fold_rows;
+                    }
+            }
+    }
     if ((e = cudaMemsetAsync(hist, 0, 32 * 8, s)) != cudaSuccess) return e; // reused as the cursors
     k_level_scatter<<<gb, 256, 0, s>>>(d.level, N, d.lptr_dev, reinterpret_cast<unsigned long long *>(hist), d.lrows);
 

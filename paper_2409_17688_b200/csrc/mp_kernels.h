@@ -110,6 +110,9 @@ struct RowDag {
     std::vector<int64_t> lptr;  // [levels + 1] level offsets into lrows (host copy)
     int levels = 0;
     int64_t parents = 0;
+    // the folds' algorithmic traffic in rows per product: every folded row read and written once,
+    // each distinct parent row of a level read once by that level's launch
+    int64_t fold_rows = 0;
 };
 cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cudaStream_t s,
                           cudaError_t (*alloc)(void **, size_t, void *), void *actx, int64_t *launches);

@@ -266,6 +266,44 @@ def test_row_reuse_transfer_hint(mp, oracle_mod, n, sym, order, monkeypatch):
         assert np.array_equal(got[k - 1], X), k
 
 
+def _fold_rows_model(oracle_mod, n):
+    """sum over DAG levels >= 1 of (2 x rows + distinct parents of the level): the parents of a
+    word are the words with one letter 0 or 1 turned into a 2, the level
+    is 0 without parents, else 1 + the parents' maximum"""
+    W = [tuple(w) for w in oracle_mod.words(n).tolist()]
+    pos = {w: i for i, w in enumerate(W)}
+    par = [[pos[w[:b] + (2,) + w[b + 1:]] for b in range(n) if w[b] != 2 and w[:b] + (2,) + w[b + 1:] in pos]
+           for w in W]
+    level = [0] * len(W)
+    for q in sorted(range(len(W)), key=lambda q: -W[q].count(2)):  # parents have one more 2
+        level[q] = 1 + max(level[p] for p in par[q]) if par[q] else 0
+    total = 0
+    for lv in range(1, max(level) + 1):
+        rows = [q for q in range(len(W)) if level[q] == lv]
+        total += 2 * len(rows) + len({p for q in rows for p in par[q]})
+    return total, max(level) + 1
+
+
+@pytest.mark.parametrize("n", [5, 7, 8])
+def test_fold_bytes_profile(mp, oracle_mod, n):
+    """The folds' algorithmic bytes the library reports (mp_profile.fold_bytes, bench.py's k_fold
+    roofline numerator) equal the count from a host model of the parent DAG x ld x 2 bytes."""
+    A = mp.build_transition_matrix(n)
+    use_kernel(mp, "spmm-greedy")
+    mp.set_transfer_hint(n)
+    mp.set_small_path(False)
+    try:
+        mp.minplus_power_until_periodic(A)
+        p = mp.last_profile()
+    finally:
+        mp.set_transfer_hint(0)
+        mp.set_small_path(True)
+        reset_kernel(mp)
+    rows, levels = _fold_rows_model(oracle_mod, n)
+    assert p["row_levels"] == levels
+    assert p["fold_bytes"] == rows * p["ld"] * 2
+
+
 @pytest.mark.parametrize("main", [-1024, -512, -256, 0])
 @pytest.mark.parametrize("N", [100, 700, 960, 1500, 1800])
 def test_spmm_remainder_columns(mp, oracle_mod, N, main):
