@@ -249,6 +249,11 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
     if (d.lptr.back() != N) return cudaErrorUnknown; // levels are contiguous from 0
     if ((e = cudaMemcpyAsync(d.lptr_dev, d.lptr.data(), d.lptr.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return e;
+    // the level lists in a fixed order (MP_FOLD_ORDER: q = ascending row, the default; p = by
+    // first parent, then row; s = the order of the device scatter's atomics)
+    const char *fo = getenv("MP_FOLD_ORDER");
+    const char order = fo && (fo[0] == 'p' || fo[0] == 's') ? fo[0] : 'q';
+    std::vector<int32_t> hl;
     {   // fold_rows = sum over levels >= 1 of (2 x rows + distinct parents): levels and parent
         // lists to the host once per DAG (N + #parents ints)
         std::vector<int32_t> lv((size_t)N), pi((size_t)std::max<int64_t>(d.parents, 1));
@@ -270,11 +275,27 @@ cudaError_t build_row_dag(const WordMask *words, int64_t N, int n, RowDag &d, cu
                         ++d.fold_rows;
                     }
             }
+        if (order != 's') {
+            hl.reserve((size_t)N);
+            for (auto &rows : by) {
+                if (order == 'p')
+                    std::stable_sort(rows.begin(), rows.end(), [&](int32_t a, int32_t b) {
+                        const int32_t pa = ho[(size_t)a] < ho[(size_t)a + 1] ? pi[(size_t)ho[(size_t)a]] : -1;
+                        const int32_t pb = ho[(size_t)b] < ho[(size_t)b + 1] ? pi[(size_t)ho[(size_t)b]] : -1;
+                        return pa < pb;
+                    });
+                hl.insert(hl.end(), rows.begin(), rows.end());
+            }
+        }
     }
-    if ((e = cudaMemsetAsync(hist, 0, 32 * 8, s)) != cudaSuccess) return e; // reused as the cursors
-    k_level_scatter<<<gb, 256, 0, s>>>(d.level, N, d.lptr_dev, reinterpret_cast<unsigned long long *>(hist), d.lrows);
-
-    *launches += 1;
+    if (order != 's') {
+        if ((e = cudaMemcpyAsync(d.lrows, hl.data(), (size_t)N * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    } else {
+        if ((e = cudaMemsetAsync(hist, 0, 32 * 8, s)) != cudaSuccess) return e; // reused as the cursors
+        k_level_scatter<<<gb, 256, 0, s>>>(d.level, N, d.lptr_dev, reinterpret_cast<unsigned long long *>(hist),
+                                           d.lrows);
+        *launches += 1;
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaStreamSynchronize(s); // d.lptr (host) and ho go out of scope safely
 }
