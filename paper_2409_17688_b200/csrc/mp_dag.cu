@@ -137,8 +137,19 @@ __global__ void k_extra_bits(const uint32_t *__restrict__ bits, int64_t nw, int6
 // instructions per 1 KB of data.  Work items go segment-major (every row of the level for
 // segment 0, then segment 1, ...), so the warps running at one time read the parents' rows of
 // one segment column, which L2 then serves to the parents' other children.
-constexpr int kFoldSeg = 1024; // columns per warp item (ld is a multiple of 64: the last is partial)
-__global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows, int64_t nrows,
+#ifndef MP_FOLD_SEG
+#define MP_FOLD_SEG 1024
+#endif
+#ifndef MP_FOLD_PAR
+#define MP_FOLD_PAR 2
+#endif
+#ifndef MP_FOLD_MINB
+#define MP_FOLD_MINB 4
+#endif
+constexpr int kFoldSeg = MP_FOLD_SEG; // columns per warp item (ld is a multiple of 64: the last is partial)
+constexpr int kFoldQ = kFoldSeg / 256; // 16-byte loads per lane and row
+constexpr int kFoldPar = MP_FOLD_PAR;  // parents loaded per step
+__global__ void __launch_bounds__(256, MP_FOLD_MINB) k_fold(const int32_t *__restrict__ lrows, int64_t nrows,
                                               const int64_t *__restrict__ off, const int32_t *__restrict__ pidx,
                                               uint16_t *__restrict__ C, int64_t ldc)
 {
@@ -155,37 +166,41 @@ __global__ void __launch_bounds__(256) k_fold(const int32_t *__restrict__ lrows,
 #if MP_DEBUG_CHECKS
         if (q < 0 || np > 32) __trap();
 #endif
-        uint4 v[4];
+        uint4 v[kFoldQ];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < kFoldQ; ++h) {
             const int col = 256 * h + 8 * lane;
             v[h] = col < ncols ? *reinterpret_cast<const uint4 *>(row + col) : make_uint4(0, 0, 0, 0);
         }
-        // parents two at a time: eight 16-byte loads per lane in flight
-        for (int e = 0; e < np; e += 2) {
-            const int64_t p0 = __shfl_sync(0xFFFFFFFFu, mine, e);
-            const int64_t p1 = __shfl_sync(0xFFFFFFFFu, mine, e + 1 < np ? e + 1 : e);
+        // parents kFoldPar at a time: kFoldPar x kFoldQ 16-byte loads per lane in flight (a
+        // missing parent repeats the last one: min is idempotent)
+        for (int e = 0; e < np; e += kFoldPar) {
+            uint4 u[kFoldPar][kFoldQ];
+#pragma unroll
+            for (int j = 0; j < kFoldPar; ++j) {
+                const int64_t pj = __shfl_sync(0xFFFFFFFFu, mine, e + j < np ? e + j : (int)np - 1);
 #if MP_DEBUG_CHECKS
-            if (p0 < 0 || p0 == q || p1 < 0 || p1 == q) __trap();
+                if (pj < 0 || pj == q) __trap();
 #endif
-            const uint16_t *r0 = C + p0 * ldc + seg * kFoldSeg, *r1 = C + p1 * ldc + seg * kFoldSeg;
-            uint4 u0[4], u1[4];
+                const uint16_t *rj = C + pj * ldc + seg * kFoldSeg;
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int col = 256 * h + 8 * lane;
-                u0[h] = col < ncols ? __ldcg(reinterpret_cast<const uint4 *>(r0 + col)) : make_uint4(0, 0, 0, 0);
-                u1[h] = col < ncols ? __ldcg(reinterpret_cast<const uint4 *>(r1 + col)) : make_uint4(0, 0, 0, 0);
+                for (int h = 0; h < kFoldQ; ++h) {
+                    const int col = 256 * h + 8 * lane;
+                    u[j][h] = col < ncols ? __ldcg(reinterpret_cast<const uint4 *>(rj + col)) : make_uint4(0, 0, 0, 0);
+                }
             }
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                v[h].x = __vminu2(v[h].x, __vminu2(u0[h].x, u1[h].x));
-                v[h].y = __vminu2(v[h].y, __vminu2(u0[h].y, u1[h].y));
-                v[h].z = __vminu2(v[h].z, __vminu2(u0[h].z, u1[h].z));
-                v[h].w = __vminu2(v[h].w, __vminu2(u0[h].w, u1[h].w));
-            }
+            for (int j = 0; j < kFoldPar; ++j)
+#pragma unroll
+                for (int h = 0; h < kFoldQ; ++h) {
+                    v[h].x = __vminu2(v[h].x, u[j][h].x);
+                    v[h].y = __vminu2(v[h].y, u[j][h].y);
+                    v[h].z = __vminu2(v[h].z, u[j][h].z);
+                    v[h].w = __vminu2(v[h].w, u[j][h].w);
+                }
         }
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < kFoldQ; ++h) {
             const int col = 256 * h + 8 * lane;
             if (col < ncols) *reinterpret_cast<uint4 *>(row + col) = v[h];
         }
