@@ -104,6 +104,25 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
+// MP_SP_L2 (experiments): bit 0 = the SpMM's C rows stored evict-first (st.global.cs), bit 1 =
+// its X-row bulk copies with an L2 evict_last policy
+#ifndef MP_SP_L2
+#define MP_SP_L2 0
+#endif
+__device__ __forceinline__ void bulk_g2s_keep(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                                              uint64_t pol)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+
 // ---------------------------------------------------------------------------------------
 // a3: C = A (x) X on one column tile set.  P:53 "(A x B)_ij = min_k(a_ik + b_kj)";
 // Algorithm 2 line 2 "A^i = A x A^{i-1}".
@@ -1527,7 +1546,11 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
             if (lane == 0) mbar_arrive_expect_tx(bar_full + st * 8, (uint32_t)nrows * kSpRowBytes + ebytes + kSpOffBytes);
             __syncwarp();
             if (lane < nrows)
-                bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
+                if constexpr ((MP_SP_L2 & 2) != 0)
+                    bulk_g2s_keep(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8,
+                                  policy_evict_last());
+                else
+                    bulk_g2s(sX + lane * kSpRowBytes, X + (int64_t)l * ldx + col0, kSpRowBytes, bar_full + st * 8);
             if (lane == 0 && ebytes) bulk_g2s(sX + XB, E + kEntU4 * e0, ebytes, bar_full + st * 8);
             if (lane == 1) bulk_g2s(sX + XB + EB, eoff + gc * kSpGroups, kSpOffBytes, bar_full + st * 8);
         }
@@ -1643,7 +1666,10 @@ __global__ void __launch_bounds__(kSpThreads, SpCfg<PPL>::Ctas)
             v.y = __vminu2(acc[gg][r][4 * h + 1], 0x7FFF7FFFu);
             v.z = __vminu2(acc[gg][r][4 * h + 2], 0x7FFF7FFFu);
             v.w = __vminu2(acc[gg][r][4 * h + 3], 0x7FFF7FFFu);
-            *reinterpret_cast<uint4 *>(crow + 256 * h) = v;
+            if constexpr ((MP_SP_L2 & 1) != 0)
+                __stcs(reinterpret_cast<uint4 *>(crow + 256 * h), v);
+            else
+                *reinterpret_cast<uint4 *>(crow + 256 * h) = v;
         }
     }
 }
