@@ -153,6 +153,9 @@ __global__ void __launch_bounds__(256, MP_FOLD_MINB) k_fold(const int32_t *__res
                                               const int64_t *__restrict__ off, const int32_t *__restrict__ pidx,
                                               uint16_t *__restrict__ C, int64_t ldc)
 {
+    // launched as a programmatic dependent: the previous kernel's writes (the SpMM's rows, the
+    // lower levels' folds) are complete and visible after this wait
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const int lane = threadIdx.x & 31;
     const int64_t nseg = (ldc + kFoldSeg - 1) / kFoldSeg, items = nrows * nseg;
     for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
@@ -322,6 +325,12 @@ cudaError_t launch_extra_bits(const uint32_t *bits, int64_t nw, int64_t N, const
     return cudaGetLastError();
 }
 
+static bool fold_pdl()
+{
+    const char *e = getenv("MP_FOLD_PDL"); // read per call: experiments switch it
+    return !(e && e[0] == '0');
+}
+
 cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncols, cudaStream_t s, int *launches)
 {
     for (int l = 1; l < d.levels; ++l) {
@@ -330,7 +339,21 @@ cudaError_t launch_folds(const RowDag &d, uint16_t *C, int64_t ldc, int64_t ncol
         // a grid of at most 148 x 8 blocks of 8 warps: the running warps are a contiguous range
         // of items (the segment-major order above relies on it)
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, 148 * 8));
-        k_fold<<<grid, 256, 0, s>>>(d.lrows + d.lptr[(size_t)l], nr, d.off, d.idx, C, ldc);
+        // programmatic dependent launch: this level's grid is set up while the previous kernel
+        // (the SpMM or the level before) drains; k_fold waits for that kernel's completion
+        // (griddepcontrol.wait) before its first load.  MP_FOLD_PDL=0: plain launches.
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = fold_pdl() ? 1 : 0;
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, k_fold, (const int32_t *)(d.lrows + d.lptr[(size_t)l]), nr,
+                                                  (const int64_t *)d.off, (const int32_t *)d.idx, C, ldc);
+        if (le != cudaSuccess) return le;
         if (launches) ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
